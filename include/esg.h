@@ -1,0 +1,164 @@
+/* esg.h -- C ABI of the B200-native esgnn hot path (libesg_b200.so).
+ *
+ * Drop-in boundary for the reference's C++20 library API (no FFI exists in
+ * the reference; these are the entry points its façade would bind).  Every
+ * function returns an ESG_* status; esg_last_error() gives the message.  The
+ * C++ façade in paper_2507_03840_b200/csrc/esgnn_b200.hpp rethrows the
+ * matching esgnn::Error subclass (core/error.h:11-51), mirroring the CLI's
+ * exit-code mapping usage->2, data->3, divergence->4 (esgnn_main.cpp:221-233).
+ *
+ * Conventions: host arrays are caller-owned; device buffers are owned by the
+ * context / handle that created them.  A context drives one GPU and is not
+ * thread-safe (one host thread or process per context, like one rank of the
+ * reference's DistributedRunner).  Collectives are issued in the same order
+ * on every rank (transport.h:17-20 lockstep contract).
+ */
+#ifndef ESG_H_
+#define ESG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ESG_OK = 0,
+  ESG_ERR_OTHER = 1,
+  ESG_ERR_USAGE = 2,      /* esgnn::UsageError */
+  ESG_ERR_DATA = 3,       /* esgnn::DataError / ShapeError / ParseError */
+  ESG_ERR_DIVERGENCE = 4, /* esgnn::DivergenceError */
+  ESG_ERR_NCCL = 5,       /* esgnn::TransportError */
+  ESG_ERR_CUDA = 6,
+  ESG_ERR_OOM = 7
+};
+
+/* precision of the SO(2) linears (everything else is fp32 state with fp64
+ * geometry): FP32 = CUDA-core fp32 (parity mode), BF16 = tcgen05 kind::f16
+ * with fp32 accumulation in TMEM (throughput mode). */
+enum { ESG_LINEAR_FP32 = 0, ESG_LINEAR_BF16 = 1 };
+
+typedef struct esg_ctx esg_ctx;
+typedef struct esg_graph esg_graph;
+typedef struct esg_plan esg_plan;
+typedef struct esg_model esg_model;
+
+typedef struct esg_timing {
+  double forward_ms;      /* first init kernel -> last head kernel (CUDA events) */
+  double message_ms;      /* message passing only (all 2*M blocks) */
+  double halo_ms;         /* sum over the 2*M exchanges: pack start -> last recv */
+  double heads_ms;
+  int64_t exchanges;      /* exactly 2*M per forward (acceptance.cpp:298) */
+  int64_t gpu_launches;   /* kernels this library launched in the call */
+} esg_timing;
+
+const char* esg_last_error(void);
+int esg_version(void);
+
+/* ---- context (one GPU, optional NCCL communicator) ------------------- */
+int esg_nccl_unique_id_size(void);
+int esg_nccl_get_unique_id(void* out /* esg_nccl_unique_id_size() bytes */);
+/* world > 1 requires nccl_id (the same bytes on every rank). */
+int esg_ctx_create(int device, int rank, int world, const void* nccl_id, esg_ctx** out);
+int esg_ctx_destroy(esg_ctx* ctx);
+int esg_ctx_synchronize(esg_ctx* ctx);
+
+/* ---- structures (structure.h:12-36, synthetic.h:17-41) ---------------- */
+/* AtomicStructure::wrap (structure.cpp:26-38), host. */
+int esg_wrap_positions(int n_atoms, double* pos /* n*3, in place */, const double cell[9],
+                       const uint8_t pbc[3]);
+/* model::make_jittered_lattice (synthetic.cpp:17-41), host input generator. */
+int esg_jittered_lattice(int n_atoms, double spacing, double jitter, int n_cycle, const int* cycle,
+                         uint64_t seed, double* pos_out, double cell_out[9], int* species_out);
+/* structures::tile (structure.cpp:40-63), host. */
+int esg_tile(int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
+             const int* species, const int reps[3], double* pos_out, double cell_out[9],
+             int* species_out);
+
+/* ---- graph: structures::build_graph (graph.h:37, graph.cpp:55-131) ---- */
+/* Builds the periodic cutoff graph on the GPU: a destination-major CSR
+ * whose edges are ordered by (dst, src, shift) exactly like Graph::edges. */
+int esg_build_graph(esg_ctx* ctx, int n_atoms, const double* pos, const double cell[9],
+                    const uint8_t pbc[3], double r_cut, esg_graph** out);
+int esg_graph_destroy(esg_graph* g);
+int esg_graph_info(const esg_graph* g, int* n_nodes, int64_t* n_edges);
+/* Copies Graph::edges to host SoA arrays (any pointer may be NULL). */
+int esg_graph_export(const esg_graph* g, int32_t* src, int32_t* dst, int32_t* shift /* E*3 */,
+                     double* disp /* E*3 */, double* dist);
+/* Graph::in_degrees (graph.cpp:49-53) and incoming_ranges offsets (N+1). */
+int esg_graph_in_degrees(const esg_graph* g, int32_t* deg);
+int esg_graph_offsets(const esg_graph* g, int64_t* dst_off /* N+1 */);
+
+/* ---- partition::lownn_partition (partition.h:24, lownn.cpp:105-133) --- */
+/* pos are the UNWRAPPED input positions (model_run.cpp:68 passes in.s). */
+int esg_lownn_partition(int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
+                        const int32_t* in_degree, int depth, double r_cut, int32_t* node_to_part);
+
+/* ---- runtime::build_comm_plan (comm_plan.h:35, comm_plan.cpp:11-106) -- */
+int esg_plan_build(const esg_graph* g, const int32_t* species, const int32_t* node_to_part,
+                   int n_parts, int rank, esg_plan** out);
+/* Same plan from host CSR arrays (dst_off[N+1], src[E]); needs no GPU. */
+int esg_plan_build_host(int n_nodes, const int64_t* dst_off, const int32_t* src, const int32_t* species,
+                        const int32_t* node_to_part, int n_parts, int rank, esg_plan** out);
+int esg_plan_destroy(esg_plan* p);
+/* info[0..4] = n_rows, n_owned, n_edges, n_neighbors, total_send_rows */
+int esg_plan_info(const esg_plan* p, int64_t info[5]);
+/* Any pointer may be NULL.  edge_index maps view edges to global edges. */
+int esg_plan_export(const esg_plan* p, int32_t* row_global, int32_t* row_species,
+                    int32_t* edge_index, int32_t* src_row, int32_t* dst_row, int32_t* nbr_peer,
+                    int32_t* nbr_recv_row, int32_t* nbr_recv_count, int32_t* nbr_send_count,
+                    int32_t* send_rows /* concatenated in neighbour order */);
+
+/* ---- model::Network<float> (network.h:77-228) ------------------------- */
+typedef struct esg_model_config {
+  int l_max, e_width, layers, n_radial; /* ModelConfig (network.h:16-35) */
+  double r_cut;
+  uint64_t seed;
+  int gate_enabled;
+  int linear_precision; /* ESG_LINEAR_* */
+} esg_model_config;
+
+/* basis: species Z ascending or not; shells concatenated per species.  ctx
+ * may be NULL for a host-only model (parameter registration / init / hash). */
+int esg_model_create(esg_ctx* ctx, const esg_model_config* cfg, int n_species, const int* z,
+                     const int* n_shells, const int* shells, esg_model** out);
+int esg_model_destroy(esg_model* m);
+int esg_model_set_precision(esg_model* m, int linear_precision);
+/* ParamStore (params.h:40-107): entries in registration order. */
+int esg_model_init_params(esg_model* m); /* ParamStore::init(seed) */
+int64_t esg_model_param_count(const esg_model* m);
+int esg_model_n_entries(const esg_model* m);
+int esg_model_entry(const esg_model* m, int i, const char** name, int* rows, int* cols,
+                    int64_t* offset);
+int esg_model_get_params(const esg_model* m, float* out);
+int esg_model_set_params(esg_model* m, const float* in); /* uploads + repacks */
+uint64_t esg_model_param_hash(const esg_model* m); /* ParamStore::value_hash */
+int esg_model_out_len(const esg_model* m);           /* HeadLayout::out_len */
+
+/* Network::prepare (network.h:98-105) on a rank view: plan may be NULL for the
+ * serial view of g (serial_view, graph_view.h:37-56). */
+int esg_prepare(esg_model* m, const esg_graph* g, const esg_plan* plan, const int32_t* species);
+int esg_prepared_info(const esg_model* m, int64_t info[3]); /* n_rows, n_owned, n_edges */
+
+/* DistributedRunner::forward + heads (distributed.h:193, network.h:115-164).
+ * Host outputs may be NULL (results stay on the device). */
+int esg_forward(esg_model* m, float* node_out /* n_owned*out_len */,
+                float* edge_out /* n_edges*out_len */, esg_timing* timing);
+/* Device pointers of the last forward's outputs / features (valid until the
+ * next forward or destroy). */
+int esg_forward_outputs(const esg_model* m, const float** node_out, const float** edge_out,
+                        const float** node_features, const float** edge_features);
+/* Node / edge feature tables (n_rows*H*E / n_edges*H*E) to host. */
+int esg_features_export(const esg_model* m, float* nodes, float* edges);
+
+/* model::blocks_to_uncoupled (block_matrix.cpp:66-88) of the last forward:
+ * per item a dense n_orb(za) x n_orb(zb) block, concatenated in item order
+ * (nodes first, then edges).  sizes: esg_blocks_size. */
+int esg_blocks_size(const esg_model* m, int64_t* n_values);
+int esg_blocks_uncoupled(esg_model* m, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESG_H_ */

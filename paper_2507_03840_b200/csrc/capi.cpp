@@ -1,0 +1,573 @@
+// capi.cpp -- the extern "C" boundary (include/esg.h).  Every entry point
+// catches and maps exceptions to ESG_* codes; the message is kept per thread
+// for esg_last_error().
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <random>
+
+#include "esg_internal.h"
+
+namespace esg {
+esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos, const M3& cell, const bool pbc[3], double r_cut);
+void model_device_create(esg_model* M);
+void model_device_destroy(esg_model* M);
+void model_upload_params(esg_model* M);
+void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const int32_t* species);
+void model_forward(esg_model* M, esg_timing* tm);
+void model_outputs(const esg_model* M, const float** no, const float** eo, const float** nf, const float** ef);
+void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
+void model_copy_features(const esg_model* M, float* nodes, float* edges);
+void model_prepared_info(const esg_model* M, int64_t info[3]);
+int64_t model_blocks_size(const esg_model* M);
+void model_blocks(esg_model* M, double* out);
+
+namespace {
+thread_local std::string g_last;
+M3 to_m3(const double c[9]) {
+  M3 m;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) m[i][j] = c[3 * i + j];
+  return m;
+}
+}  // namespace
+void set_error(const std::string& m) { g_last = m; }
+const char* last_error() { return g_last.c_str(); }
+}  // namespace esg
+
+using namespace esg;
+
+#define ESG_API_BEGIN try {
+#define ESG_API_END                       \
+  return ESG_OK;                          \
+  }                                       \
+  catch (const esg::Error& e) {           \
+    esg::set_error(e.what());             \
+    return e.code;                        \
+  }                                       \
+  catch (const std::bad_alloc& e) {       \
+    esg::set_error("host out of memory"); \
+    return ESG_ERR_OOM;                   \
+  }                                       \
+  catch (const std::exception& e) {       \
+    esg::set_error(e.what());             \
+    return ESG_ERR_OTHER;                 \
+  }
+
+#define NEED(p, what) \
+  if (!(p)) esg::usage(std::string("null ") + what)
+
+extern "C" {
+
+const char* esg_last_error(void) { return esg::last_error(); }
+int esg_version(void) { return 1; }
+
+int esg_nccl_unique_id_size(void) { return (int)sizeof(ncclUniqueId); }
+int esg_nccl_get_unique_id(void* out) {
+  ESG_API_BEGIN
+  NEED(out, "out");
+  ncclUniqueId id;
+  ESG_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  ESG_API_END
+}
+
+int esg_ctx_create(int device, int rank, int world, const void* nccl_id, esg_ctx** out) {
+  ESG_API_BEGIN
+  NEED(out, "out");
+  if (world < 1 || rank < 0 || rank >= world) usage("rank outside the world");
+  int ndev = 0;
+  ESG_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) usage("no CUDA device " + std::to_string(device));
+  ESG_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop{};
+  ESG_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) usage("libesg_b200 targets sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+                              std::to_string(prop.minor));
+  auto* c = new esg_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  ESG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  if (world > 1) {
+    if (!nccl_id) {
+      delete c;
+      usage("world > 1 needs an NCCL unique id");
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ESG_NCCL(ncclCommInitRank(&c->comm, world, id, rank));
+  }
+  *out = c;
+  ESG_API_END
+}
+
+int esg_ctx_destroy(esg_ctx* ctx) {
+  ESG_API_BEGIN
+  if (!ctx) return ESG_OK;
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  ESG_API_END
+}
+
+int esg_ctx_synchronize(esg_ctx* ctx) {
+  ESG_API_BEGIN
+  NEED(ctx, "ctx");
+  ESG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ESG_API_END
+}
+
+int esg_wrap_positions(int n, double* pos, const double cell[9], const uint8_t pbc[3]) {
+  ESG_API_BEGIN
+  NEED(pos, "pos");
+  bool p[3] = {pbc[0] != 0, pbc[1] != 0, pbc[2] != 0};
+  wrap_positions(n, pos, to_m3(cell), p);
+  ESG_API_END
+}
+
+// synthetic.cpp:17-41
+int esg_jittered_lattice(int n_atoms, double spacing, double jitter, int n_cycle, const int* cycle, uint64_t seed,
+                         double* pos_out, double cell_out[9], int* species_out) {
+  ESG_API_BEGIN
+  if (n_atoms < 1) usage("need at least one atom");
+  if (n_cycle < 1) usage("species cycle is empty");
+  if (!(spacing > 0.0)) usage("lattice spacing must be positive");
+  int n = 1;
+  while (n * n * n < n_atoms) ++n;
+  for (int i = 0; i < 9; ++i) cell_out[i] = (i % 4 == 0) ? 1.0 * (n * spacing) : 0.0 * (n * spacing);
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(-jitter, jitter);
+  int placed = 0;
+  for (int ix = 0; ix < n && placed < n_atoms; ++ix)
+    for (int iy = 0; iy < n && placed < n_atoms; ++iy)
+      for (int iz = 0; iz < n && placed < n_atoms; ++iz) {
+        double p[3] = {(ix + 0.5) * spacing, (iy + 0.5) * spacing, (iz + 0.5) * spacing};
+        for (int d = 0; d < 3; ++d) p[d] += u(rng);
+        for (int d = 0; d < 3; ++d) pos_out[3 * placed + d] = p[d];
+        species_out[placed] = cycle[placed % n_cycle];
+        ++placed;
+      }
+  ESG_API_END
+}
+
+// structure.cpp:40-63
+int esg_tile(int n, const double* pos, const double cell[9], const uint8_t pbc[3], const int* species,
+             const int reps[3], double* pos_out, double cell_out[9], int* species_out) {
+  ESG_API_BEGIN
+  for (int d = 0; d < 3; ++d) {
+    if (reps[d] < 1) usage("tile factors must be positive");
+    if (reps[d] > 1 && !pbc[d]) usage("cannot tile along aperiodic dimension");
+  }
+  for (int d = 0; d < 3; ++d)
+    for (int k = 0; k < 3; ++k) cell_out[3 * d + k] = cell[3 * d + k] * reps[d];
+  int64_t at = 0;
+  for (int ix = 0; ix < reps[0]; ++ix)
+    for (int iy = 0; iy < reps[1]; ++iy)
+      for (int iz = 0; iz < reps[2]; ++iz) {
+        double off[3];
+        for (int k = 0; k < 3; ++k) off[k] = (ix * cell[k] + iy * cell[3 + k]) + iz * cell[6 + k];
+        for (int a = 0; a < n; ++a, ++at) {
+          for (int k = 0; k < 3; ++k) pos_out[3 * at + k] = pos[3 * a + k] + off[k];
+          species_out[at] = species[a];
+        }
+      }
+  ESG_API_END
+}
+
+int esg_build_graph(esg_ctx* ctx, int n, const double* pos, const double cell[9], const uint8_t pbc[3], double r_cut,
+                    esg_graph** out) {
+  ESG_API_BEGIN
+  NEED(ctx, "ctx");
+  NEED(out, "out");
+  ESG_CUDA(cudaSetDevice(ctx->device));
+  bool p[3] = {pbc[0] != 0, pbc[1] != 0, pbc[2] != 0};
+  *out = build_graph_gpu(ctx, n, pos, to_m3(cell), p, r_cut);
+  ESG_API_END
+}
+
+int esg_graph_destroy(esg_graph* g) {
+  ESG_API_BEGIN
+  if (!g) return ESG_OK;
+  for (void* p : {(void*)g->d_off, (void*)g->d_src, (void*)g->d_shift, (void*)g->d_disp, (void*)g->d_dist})
+    if (p) cudaFree(p);
+  delete g;
+  ESG_API_END
+}
+
+int esg_graph_info(const esg_graph* g, int* n_nodes, int64_t* n_edges) {
+  ESG_API_BEGIN
+  NEED(g, "graph");
+  if (n_nodes) *n_nodes = g->n;
+  if (n_edges) *n_edges = g->E;
+  ESG_API_END
+}
+
+int esg_graph_export(const esg_graph* g, int32_t* src, int32_t* dst, int32_t* shift, double* disp, double* dist) {
+  ESG_API_BEGIN
+  NEED(g, "graph");
+  ESG_CUDA(cudaSetDevice(g->ctx->device));
+  const int64_t E = g->E;
+  g->host_sync();
+  if (src) std::copy(g->h_src.begin(), g->h_src.end(), src);
+  if (dst)
+    for (int j = 0; j < g->n; ++j)
+      for (int64_t k = g->h_off[j]; k < g->h_off[j + 1]; ++k) dst[k] = j;
+  if (shift && E) {
+    std::vector<uint32_t> s(E);
+    ESG_CUDA(cudaMemcpy(s.data(), g->d_shift, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < E; ++k) {
+      shift[3 * k] = int((s[k] >> 20) & 1023) - 512;
+      shift[3 * k + 1] = int((s[k] >> 10) & 1023) - 512;
+      shift[3 * k + 2] = int(s[k] & 1023) - 512;
+    }
+  }
+  if (disp && E) ESG_CUDA(cudaMemcpy(disp, g->d_disp, sizeof(double) * 3 * E, cudaMemcpyDeviceToHost));
+  if (dist && E) ESG_CUDA(cudaMemcpy(dist, g->d_dist, sizeof(double) * E, cudaMemcpyDeviceToHost));
+  ESG_API_END
+}
+
+int esg_graph_in_degrees(const esg_graph* g, int32_t* deg) {
+  ESG_API_BEGIN
+  NEED(g, "graph");
+  NEED(deg, "deg");
+  g->host_sync();
+  for (int j = 0; j < g->n; ++j) deg[j] = (int32_t)(g->h_off[j + 1] - g->h_off[j]);
+  ESG_API_END
+}
+
+int esg_graph_offsets(const esg_graph* g, int64_t* off) {
+  ESG_API_BEGIN
+  NEED(g, "graph");
+  NEED(off, "off");
+  g->host_sync();
+  std::copy(g->h_off.begin(), g->h_off.end(), off);
+  ESG_API_END
+}
+
+int esg_lownn_partition(int n, const double* pos, const double cell[9], const uint8_t pbc[3], const int32_t* deg,
+                        int depth, double r_cut, int32_t* part) {
+  ESG_API_BEGIN
+  NEED(pos, "pos");
+  NEED(deg, "in_degree");
+  NEED(part, "node_to_part");
+  bool p[3] = {pbc[0] != 0, pbc[1] != 0, pbc[2] != 0};
+  auto a = lownn(n, pos, to_m3(cell), p, deg, depth, r_cut);
+  std::copy(a.begin(), a.end(), part);
+  ESG_API_END
+}
+
+// comm_plan.cpp:11-106: owned rows ascending by global id, halo rows for
+// remote sources of owned edges grouped by (owner, id), owned edges in the
+// global (dst, src, shift) order, send lists ascending by global id.
+static esg_plan* plan_from_csr(int n, const int64_t* off, const int32_t* src, const int32_t* species,
+                               const int32_t* part, int n_parts, int rank) {
+  if (rank < 0 || rank >= n_parts) usage("rank outside the assignment");
+  for (int i = 0; i < n; ++i)
+    if (part[i] < 0 || part[i] >= n_parts) data("assignment part out of range");
+  auto* P = new esg_plan();
+  P->rank = rank;
+  P->world = n_parts;
+  std::vector<int> owned_row(n, -1);
+  for (int i = 0; i < n; ++i)
+    if (part[i] == rank) {
+      owned_row[i] = P->n_owned++;
+      P->row_global.push_back(i);
+    }
+  std::vector<std::pair<int, int>> halo;
+  for (int j = 0; j < n; ++j) {
+    if (part[j] != rank) continue;
+    for (int64_t k = off[j]; k < off[j + 1]; ++k) {
+      const int s = src[k];
+      if (part[s] != rank) halo.emplace_back(part[s], s);
+    }
+  }
+  std::sort(halo.begin(), halo.end());
+  halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+  std::vector<int> halo_row(n, -1);
+  for (size_t q = 0; q < halo.size(); ++q) {
+    halo_row[halo[q].second] = P->n_owned + (int)q;
+    P->row_global.push_back(halo[q].second);
+  }
+  P->n_rows = P->n_owned + (int)halo.size();
+  if (species)
+    for (int r = 0; r < P->n_rows; ++r) P->row_species.push_back(species[P->row_global[r]]);
+  for (int j = 0; j < n; ++j) {
+    if (part[j] != rank) continue;
+    for (int64_t k = off[j]; k < off[j + 1]; ++k) {
+      const int s = src[k];
+      P->edge_index.push_back((int32_t)k);
+      P->src_row.push_back(owned_row[s] >= 0 ? owned_row[s] : halo_row[s]);
+      P->dst_row.push_back(owned_row[j]);
+    }
+  }
+  std::map<int, std::vector<int>> sends;
+  for (int j = 0; j < n; ++j) {
+    if (part[j] == rank) continue;
+    for (int64_t k = off[j]; k < off[j + 1]; ++k) {
+      const int s = src[k];
+      if (part[s] == rank) sends[part[j]].push_back(s);
+    }
+  }
+  std::map<int, Neighbor> nb;
+  for (auto& kv : sends) {
+    std::sort(kv.second.begin(), kv.second.end());
+    kv.second.erase(std::unique(kv.second.begin(), kv.second.end()), kv.second.end());
+    Neighbor& x = nb[kv.first];
+    x.peer = kv.first;
+    for (int id : kv.second) x.send_rows.push_back(owned_row[id]);
+  }
+  int at = P->n_owned;
+  for (size_t q = 0; q < halo.size();) {
+    size_t r = q;
+    while (r < halo.size() && halo[r].first == halo[q].first) ++r;
+    Neighbor& x = nb[halo[q].first];
+    x.peer = halo[q].first;
+    x.recv_row = at;
+    x.recv_count = (int)(r - q);
+    at += x.recv_count;
+    q = r;
+  }
+  for (auto& kv : nb) P->nbrs.push_back(kv.second);
+  return P;
+}
+
+int esg_plan_build(const esg_graph* g, const int32_t* species, const int32_t* part, int n_parts, int rank,
+                   esg_plan** out) {
+  ESG_API_BEGIN
+  NEED(g, "graph");
+  NEED(part, "node_to_part");
+  NEED(out, "out");
+  g->host_sync();
+  *out = plan_from_csr(g->n, g->h_off.data(), g->h_src.data(), species, part, n_parts, rank);
+  ESG_API_END
+}
+
+int esg_plan_build_host(int n, const int64_t* dst_off, const int32_t* src, const int32_t* species,
+                        const int32_t* part, int n_parts, int rank, esg_plan** out) {
+  ESG_API_BEGIN
+  NEED(dst_off, "dst_off");
+  NEED(src, "src");
+  NEED(part, "node_to_part");
+  NEED(out, "out");
+  *out = plan_from_csr(n, dst_off, src, species, part, n_parts, rank);
+  ESG_API_END
+}
+
+int esg_plan_destroy(esg_plan* p) {
+  delete p;
+  return ESG_OK;
+}
+
+int esg_plan_info(const esg_plan* p, int64_t info[5]) {
+  ESG_API_BEGIN
+  NEED(p, "plan");
+  info[0] = p->n_rows;
+  info[1] = p->n_owned;
+  info[2] = (int64_t)p->src_row.size();
+  info[3] = (int64_t)p->nbrs.size();
+  int64_t s = 0;
+  for (const auto& nb : p->nbrs) s += (int64_t)nb.send_rows.size();
+  info[4] = s;
+  ESG_API_END
+}
+
+int esg_plan_export(const esg_plan* p, int32_t* row_global, int32_t* row_species, int32_t* edge_index,
+                    int32_t* src_row, int32_t* dst_row, int32_t* nbr_peer, int32_t* nbr_recv_row,
+                    int32_t* nbr_recv_count, int32_t* nbr_send_count, int32_t* send_rows) {
+  ESG_API_BEGIN
+  NEED(p, "plan");
+  if (row_global) std::copy(p->row_global.begin(), p->row_global.end(), row_global);
+  if (row_species) std::copy(p->row_species.begin(), p->row_species.end(), row_species);
+  if (edge_index) std::copy(p->edge_index.begin(), p->edge_index.end(), edge_index);
+  if (src_row) std::copy(p->src_row.begin(), p->src_row.end(), src_row);
+  if (dst_row) std::copy(p->dst_row.begin(), p->dst_row.end(), dst_row);
+  int at = 0;
+  for (size_t q = 0; q < p->nbrs.size(); ++q) {
+    if (nbr_peer) nbr_peer[q] = p->nbrs[q].peer;
+    if (nbr_recv_row) nbr_recv_row[q] = p->nbrs[q].recv_row;
+    if (nbr_recv_count) nbr_recv_count[q] = p->nbrs[q].recv_count;
+    if (nbr_send_count) nbr_send_count[q] = (int)p->nbrs[q].send_rows.size();
+    if (send_rows)
+      for (int r : p->nbrs[q].send_rows) send_rows[at++] = r;
+  }
+  ESG_API_END
+}
+
+int esg_model_create(esg_ctx* ctx, const esg_model_config* cfg, int n_species, const int* z, const int* n_shells,
+                     const int* shells, esg_model** out) {
+  ESG_API_BEGIN
+  NEED(cfg, "cfg");
+  NEED(out, "out");
+  // ModelConfig::validate (network.h:29-35)
+  if (cfg->l_max < 0 || cfg->l_max > 6) usage("l_max must be in 0..6");
+  if (cfg->e_width < 1) usage("embedding width must be >= 1");
+  if (cfg->layers < 0) usage("layer count must be >= 0");
+  if (cfg->n_radial < 2) usage("radial basis needs at least 2 Gaussians");
+  if (!(cfg->r_cut > 0)) usage("cutoff must be positive");
+  if (n_species < 1) data("basis defines no species");
+  auto* M = new esg_model();
+  M->ctx = ctx;
+  M->cfg = *cfg;
+  int at = 0;
+  for (int s = 0; s < n_species; ++s) {
+    if (n_shells[s] < 1) {
+      delete M;
+      data("basis for " + element_symbol(z[s]) + " has no shells");
+    }
+    std::vector<int> ls(shells + at, shells + at + n_shells[s]);
+    for (int l : ls)
+      if (l < 0 || l > 6) {
+        delete M;
+        data("shell angular momentum out of range: " + std::to_string(l));
+      }
+    at += n_shells[s];
+    M->basis.shells[z[s]] = ls;
+  }
+  M->heads = head_layout(M->basis);
+  if (cfg->l_max < M->heads.max_l) {
+    const int need = M->heads.max_l;
+    delete M;
+    usage("l_max " + std::to_string(cfg->l_max) + " cannot couple the basis shells; need at least " +
+          std::to_string(need));
+  }
+  M->lay = m_layout(cfg->l_max);
+  for (const auto& kv : M->basis.shells) M->species_list.push_back(kv.first);
+  M->params = register_params(*cfg, M->basis, M->heads);
+  M->host_params.assign(M->params.total, 0.0f);
+  if (ctx) try {
+      model_device_create(M);
+    } catch (...) {
+      delete M;
+      throw;
+    }
+  *out = M;
+  ESG_API_END
+}
+
+int esg_model_destroy(esg_model* m) {
+  ESG_API_BEGIN
+  if (!m) return ESG_OK;
+  model_device_destroy(m);
+  delete m;
+  ESG_API_END
+}
+
+int esg_model_set_precision(esg_model* m, int prec) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (prec != ESG_LINEAR_FP32 && prec != ESG_LINEAR_BF16) usage("unknown linear precision");
+  m->cfg.linear_precision = prec;
+  ESG_API_END
+}
+
+int esg_model_init_params(esg_model* m) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  init_params(m->params, m->cfg.seed, m->host_params);
+  if (m->ctx) {
+    ESG_CUDA(cudaSetDevice(m->ctx->device));
+    model_upload_params(m);
+  }
+  ESG_API_END
+}
+
+int64_t esg_model_param_count(const esg_model* m) { return m ? m->params.total : -1; }
+int esg_model_n_entries(const esg_model* m) { return m ? (int)m->params.entries.size() : -1; }
+int esg_model_entry(const esg_model* m, int i, const char** name, int* rows, int* cols, int64_t* offset) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (i < 0 || i >= (int)m->params.entries.size()) usage("entry index out of range");
+  const auto& e = m->params.entries[i];
+  if (name) *name = e.name.c_str();
+  if (rows) *rows = e.rows;
+  if (cols) *cols = e.cols;
+  if (offset) *offset = e.offset;
+  ESG_API_END
+}
+int esg_model_get_params(const esg_model* m, float* out) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  std::copy(m->host_params.begin(), m->host_params.end(), out);
+  ESG_API_END
+}
+int esg_model_set_params(esg_model* m, const float* in) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  std::copy(in, in + m->host_params.size(), m->host_params.begin());
+  if (m->ctx) {
+    ESG_CUDA(cudaSetDevice(m->ctx->device));
+    model_upload_params(m);
+  }
+  ESG_API_END
+}
+uint64_t esg_model_param_hash(const esg_model* m) { return m ? param_hash(m->params, m->host_params) : 0; }
+int esg_model_out_len(const esg_model* m) { return m ? m->heads.out_len : -1; }
+
+int esg_prepare(esg_model* m, const esg_graph* g, const esg_plan* plan, const int32_t* species) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  NEED(g, "graph");
+  NEED(species, "species");
+  if (plan && (plan->world != m->ctx->world || plan->rank != m->ctx->rank) && m->ctx->world > 1)
+    usage("plan rank/world does not match the context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_prepare(m, g, plan, species);
+  ESG_API_END
+}
+
+int esg_prepared_info(const esg_model* m, int64_t info[3]) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  model_prepared_info(m, info);
+  ESG_API_END
+}
+
+int esg_forward(esg_model* m, float* node_out, float* edge_out, esg_timing* timing) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_forward(m, timing);
+  if (node_out || edge_out) model_copy_outputs(m, node_out, edge_out);
+  ESG_API_END
+}
+
+int esg_forward_outputs(const esg_model* m, const float** no, const float** eo, const float** nf, const float** ef) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  model_outputs(m, no, eo, nf, ef);
+  ESG_API_END
+}
+
+int esg_features_export(const esg_model* m, float* nodes, float* edges) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_copy_features(m, nodes, edges);
+  ESG_API_END
+}
+
+int esg_blocks_size(const esg_model* m, int64_t* n) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  *n = model_blocks_size(m);
+  ESG_API_END
+}
+
+int esg_blocks_uncoupled(esg_model* m, double* out) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  NEED(out, "out");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_blocks(m, out);
+  ESG_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// esg_internal.h -- shared internal declarations of libesg_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/esg.h"
+
+namespace esg {
+
+// ---- error taxonomy (core/error.h:11-51) mapped to ESG_* codes ----------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void usage(const std::string& m) { throw Error(ESG_ERR_USAGE, m); }
+[[noreturn]] inline void data(const std::string& m) { throw Error(ESG_ERR_DATA, m); }
+void set_error(const std::string& m);
+
+#define ESG_CUDA(x)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::esg::Error(e_ == cudaErrorMemoryAllocation ? ESG_ERR_OOM : ESG_ERR_CUDA,  \
+                         std::string(#x) + ": " + cudaGetErrorString(e_));              \
+  } while (0)
+#define ESG_NCCL(x)                                                                     \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess)                                                              \
+      throw ::esg::Error(ESG_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// ---- host structures (structure.cpp) ------------------------------------
+using M3 = std::array<std::array<double, 3>, 3>;
+void wrap_positions(int n, double* pos, const M3& cell, const bool pbc[3]);
+double face_spacing(const M3& cell, int d);
+
+// ---- partition / plan ----------------------------------------------------
+std::vector<int> lownn(int n, const double* pos, const M3& cell, const bool pbc[3],
+                       const int32_t* deg, int depth, double r_cut);
+
+struct Neighbor {
+  int peer = -1;
+  std::vector<int> send_rows;
+  int recv_row = 0, recv_count = 0;
+};
+
+// ---- basis / layouts (basis.cpp, layout.h) ------------------------------
+struct Basis {
+  std::map<int, std::vector<int>> shells;  // Z ascending
+  int n_orb(int z) const;
+  int off(int z, int sh) const;
+  int n_slots() const;
+  int slot_l(int s) const;
+};
+struct HeadKey {
+  int sa, sb, L;
+};
+struct HeadLayout {
+  std::vector<HeadKey> keys;
+  std::vector<int> offsets;
+  int out_len = 0, max_l = 0;
+  int segment(int a, int b, int L) const;
+};
+HeadLayout head_layout(const Basis& b);
+
+struct MLayout {
+  int l_max = 0, h = 0;
+  std::vector<int> to_m, to_l, m_offset;
+  int nd(int m) const { return l_max - m + 1; }
+};
+MLayout m_layout(int l_max);
+
+std::string element_symbol(int z);
+
+struct ParamEntry {
+  std::string name;
+  int rows, cols, fan_in;
+  int64_t offset;
+};
+struct ParamSet {
+  std::vector<ParamEntry> entries;
+  std::map<std::string, int> index;
+  int64_t total = 0;
+  void add(const std::string& n, int r, int c, int f);
+  const ParamEntry& at(const std::string& n) const;
+};
+ParamSet register_params(const esg_model_config& cfg, const Basis& b, const HeadLayout& h);
+void init_params(const ParamSet& p, uint64_t seed, std::vector<float>& out);
+uint64_t param_hash(const ParamSet& p, const std::vector<float>& v);
+
+// Real-basis coupling matrix C(la, lb, L): (2L+1) x ((2la+1)(2lb+1)) row-major
+// (clebsch_gordan.h:19), computed by the Racah closed form.
+std::vector<double> coupling_matrix(int la, int lb, int L);
+
+}  // namespace esg
+
+// ---- opaque handle bodies -----------------------------------------------
+struct esg_ctx {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int64_t launches = 0;  // kernels launched by this library
+};
+
+struct esg_graph {
+  esg_ctx* ctx = nullptr;
+  int n = 0;
+  int64_t E = 0;
+  int nimg[3] = {0, 0, 0};
+  // device CSR (dst-major): offsets, src, packed shift, fp64 geometry
+  int64_t* d_off = nullptr;
+  int32_t* d_src = nullptr;
+  uint32_t* d_shift = nullptr;  // (sx+512)<<20 | (sy+512)<<10 | (sz+512)
+  double* d_disp = nullptr;     // E*3
+  double* d_dist = nullptr;
+  // host mirrors filled lazily
+  mutable std::vector<int64_t> h_off;
+  mutable std::vector<int32_t> h_src;
+  void host_sync() const;
+};
+
+struct esg_plan {
+  int rank = 0, world = 1;
+  int n_rows = 0, n_owned = 0;
+  std::vector<int32_t> row_global, row_species;
+  std::vector<int32_t> edge_index, src_row, dst_row;
+  std::vector<esg::Neighbor> nbrs;
+};
+
+namespace esg {
+struct DeviceModel;  // defined in model.cu
+}
+
+struct esg_model {
+  esg_ctx* ctx = nullptr;
+  esg_model_config cfg{};
+  esg::Basis basis;
+  esg::HeadLayout heads;
+  esg::MLayout lay;
+  esg::ParamSet params;
+  std::vector<int> species_list;  // ascending Z
+  std::vector<float> host_params;
+  esg::DeviceModel* dev = nullptr;
+};

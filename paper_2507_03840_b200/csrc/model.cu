@@ -1,0 +1,1034 @@
+// model.cu -- the eGNN forward on the GPU (network.h:115-164 composition).
+//
+// Per block (layer x {node, edge}), over destination-aligned edge chunks:
+//   k_rotate_in   gather [src | dst | edge] rows, Wigner-D of the edge
+//                 direction (recomputed, never stored), rotate into the edge
+//                 frame, scatter to the order-major A1 operand     (a8-a10)
+//   SO(2) linears lin1 -> gate -> lin2 per order m                  (a11-a12)
+//                 fp32 CUDA cores (k_so2_simt) or tcgen05 bf16 (so2_tc.cu)
+//   k_rotate_out_edge   rotate back (D^T) and residual-add in place (a13 edge)
+//   k_node_update       segment softmax over the dst CSR segment, weighted
+//                       sum of rotated-back messages, one store per node
+//                       (a13 node; deterministic, partition-invariant order)
+// followed by the output heads (a16) and the uncoupled block assembly (a17).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "esg_internal.h"
+#include "model_kernels.cuh"
+
+namespace esg {
+
+// Coupling tables for the uncoupled block kernel: per (la, lb) pair with
+// la, lb <= 2 (basis shells), C_L stacked for L = |la-lb|..la+lb.
+struct CgTable {
+  int off[3][3];     // start of the (la, lb) table in vals
+  float vals[3000];  // sum over pairs of (da*db)^2
+};
+__constant__ CgTable c_cg;
+
+void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2,
+                   float* Y, int gate, cudaStream_t st);  // so2_tc.cu
+bool so2_tc_available(int L, int E);
+
+namespace {
+
+__device__ __forceinline__ int64_t cmin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+template <typename T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (n) ESG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+__device__ __forceinline__ void store_out(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_out(uint16_t* p, float v) {
+  // round-to-nearest-even fp32 -> bf16
+  uint32_t u = __float_as_uint(v);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  *p = uint16_t(u >> 16);
+}
+
+// -------------------------------------------------------------- init
+// ops.h:18-36 embed_nodes, network.h:41-50 radial_features (fp64 exp, cast),
+// ops.h:40-63 lift_radial (sequential fp32 sum over Gaussians).
+template <int H, int E>
+__global__ void k_init_nodes(const int* __restrict__ row_slot, int n_rows, const float* __restrict__ embed,
+                             float* __restrict__ nodes) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n_rows * H * E) return;
+  const int i = int(t / (H * E)), q = int(t % (H * E));
+  nodes[t] = q < E ? embed[row_slot[i] * E + q] : 0.f;
+}
+
+template <int H, int E>
+__global__ void k_init_edges(const double* __restrict__ dist, int64_t n_e, const float* __restrict__ lift, int ng,
+                             double spacing, float* __restrict__ edges) {
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x / E) + threadIdx.x / E;
+  const int c = threadIdx.x % E;
+  if (k >= n_e) return;
+  const double d0 = dist[k];
+  float acc = 0.f;
+  for (int g = 0; g < ng; ++g) {
+    const double d = d0 - g * spacing;
+    const float rbf = (float)exp(-d * d / (2.0 * spacing * spacing));
+    acc = __fadd_rn(acc, __fmul_rn(lift[c * ng + g], rbf));
+  }
+  float* row = edges + k * (H * E);
+  row[c] = acc;
+  for (int q = E + c; q < H * E; q += E) row[q] = 0.f;
+}
+
+// ----------------------------------------------------------- rotate in
+template <int L, int E, int KPAD, typename OutT>
+__global__ void __launch_bounds__(256) k_rotate_in(const float* __restrict__ nodes, const float* __restrict__ edges,
+                                                   const int* __restrict__ src_row, const int* __restrict__ dst_row,
+                                                   const float* __restrict__ dir, int64_t e0, int64_t n_e,
+                                                   OutT* __restrict__ A1) {
+  using G = Geo<L>;
+  using Y = Lay1<L, E, KPAD>;
+  constexpr int TE = 16, DSP = G::DS + 1, H = G::H, C3 = 3 * E;
+  __shared__ float sD[TE * DSP];
+  __shared__ float sdir[TE * 3];
+  const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
+  const int ne = (int)cmin64(TE, e0 + n_e - t0);
+  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
+  __syncthreads();
+  wigner_tile<L, DSP>(sdir, ne, sD);
+  for (int idx = threadIdx.x; idx < ne * C3; idx += blockDim.x) {
+    const int e = idx / C3, c = idx % C3, p = c / E, cc = c % E;
+    const int64_t k = t0 + e;
+    const float* base = p == 0 ? nodes + (int64_t)src_row[k] * H * E
+                               : (p == 1 ? nodes + (int64_t)dst_row[k] * H * E : edges + k * H * E);
+    float x[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) x[h] = base[h * E + cc];
+    const float* D = sD + e * DSP;
+    OutT* out = A1 + (k - e0) * Y::KTOT;
+#pragma unroll
+    for (int l = 0; l <= L; ++l) {
+      const int dd = 2 * l + 1;
+#pragma unroll
+      for (int a = -l; a <= l; ++a) {
+        float acc = 0.f;
+#pragma unroll
+        for (int b = -l; b <= l; ++b) acc = fmaf(D[G::doff(l) + (a + l) * dd + (b + l)], x[l * l + l + b], acc);
+        const int m = a < 0 ? -a : a;
+        const int r = G::mrow(l, a) - G::moff(m);
+        store_out(out + Y::kofs(m) + r * C3 + c, acc);
+      }
+    }
+  }
+  // zero the K padding of each order block
+  for (int idx = threadIdx.x; idx < ne * (L + 1) * KPAD; idx += blockDim.x) {
+    const int e = idx / ((L + 1) * KPAD), rem = idx % ((L + 1) * KPAD), m = rem / KPAD, q = rem % KPAD;
+    const int k = Y::K(m) + q;
+    if (k < Y::KP(m)) store_out(A1 + (t0 + e - e0) * Y::KTOT + Y::kofs(m) + k, 0.f);
+  }
+}
+
+// ------------------------------------------------- SO(2) linears, fp32
+// kernels.h:133-161 (lin1 3E->2E), :210-226 (gate), lin2 2E->E, per order m
+// with the expanded weight [[Wr, Wi], [-Wi, Wr]] so ym = Wr xm + Wi xp and
+// yp = Wr xp - Wi xm come out of one product.  W1T/W2T are the expanded
+// matrices transposed (K x N, N contiguous) and concatenated over m.
+template <int L, int E>
+__global__ void __launch_bounds__(256) k_so2_simt(const float* __restrict__ A1, int64_t n_e,
+                                                  const float* __restrict__ W1T, const float* __restrict__ W2T,
+                                                  float* __restrict__ Yout, int gate) {
+  using G = Geo<L>;
+  using Y = Lay1<L, E, 1>;
+  constexpr int TE = 16, C2 = 2 * E;
+  constexpr int KMAX = Y::K(L > 0 ? 1 : 0) > Y::K(0) ? Y::K(1) : Y::K(0);
+  constexpr int NMAX = Y::N1(L > 0 ? 1 : 0) > Y::N1(0) ? Y::N1(1) : Y::N1(0);
+  __shared__ float sA[TE * KMAX];
+  __shared__ float sH[TE * NMAX];
+  __shared__ float sS[TE * C2];
+  const int64_t t0 = (int64_t)blockIdx.x * TE;
+  const int ne = (int)cmin64(TE, n_e - t0);
+  int64_t w1 = 0, w2 = 0;
+#pragma unroll 1
+  for (int m = 0; m <= L; ++m) {
+    const int K = Y::K(m), N = Y::N1(m), N2 = Y::N2(m);
+    for (int i = threadIdx.x; i < TE * K; i += blockDim.x) {
+      const int e = i / K, k = i % K;
+      sA[i] = e < ne ? A1[(t0 + e) * Y::KTOT + Y::kofs(m) + k] : 0.f;
+    }
+    __syncthreads();
+    float acc[TE];
+    const int o = threadIdx.x;
+    if (o < N) {
+#pragma unroll
+      for (int e = 0; e < TE; ++e) acc[e] = 0.f;
+      for (int k = 0; k < K; ++k) {
+        const float w = W1T[w1 + (int64_t)k * N + o];
+#pragma unroll
+        for (int e = 0; e < TE; ++e) acc[e] = fmaf(sA[e * K + k], w, acc[e]);
+      }
+      if (m == 0 && o < C2) {
+#pragma unroll
+        for (int e = 0; e < TE; ++e) sS[e * C2 + o] = gate ? 1.f / (1.f + expf(-acc[e])) : 1.f;
+      }
+    }
+    __syncthreads();
+    if (o < N) {
+#pragma unroll
+      for (int e = 0; e < TE; ++e) sH[e * N + o] = acc[e] * sS[e * C2 + (o % C2)];
+    }
+    __syncthreads();
+    if (o < N2) {
+#pragma unroll
+      for (int e = 0; e < TE; ++e) acc[e] = 0.f;
+      for (int k = 0; k < N; ++k) {
+        const float w = W2T[w2 + (int64_t)k * N2 + o];
+#pragma unroll
+        for (int e = 0; e < TE; ++e) acc[e] = fmaf(sH[e * N + k], w, acc[e]);
+      }
+      for (int e = 0; e < ne; ++e) Yout[(t0 + e) * (G::H * E) + G::moff(m) * E + o] = acc[e];
+    }
+    __syncthreads();
+    w1 += (int64_t)K * N;
+    w2 += (int64_t)N * N2;
+  }
+}
+
+// --------------------------------------------------- rotate out (edge)
+// ops.h:115-117 rotate with D^T, then ops.h:265-283 residual add in place.
+template <int L, int E>
+__global__ void __launch_bounds__(256) k_rotate_out_edge(const float* __restrict__ Yin, const float* __restrict__ dir,
+                                                         int64_t e0, int64_t n_e, float* __restrict__ edges) {
+  using G = Geo<L>;
+  constexpr int TE = 16, DSP = G::DS + 1, H = G::H;
+  __shared__ float sD[TE * DSP];
+  __shared__ float sdir[TE * 3];
+  const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
+  const int ne = (int)cmin64(TE, e0 + n_e - t0);
+  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
+  __syncthreads();
+  wigner_tile<L, DSP>(sdir, ne, sD);
+  for (int idx = threadIdx.x; idx < ne * E; idx += blockDim.x) {
+    const int e = idx / E, c = idx % E;
+    const int64_t k = t0 + e;
+    const float* y = Yin + (k - e0) * H * E;
+    const float* D = sD + e * DSP;
+    float* row = edges + k * H * E;
+#pragma unroll
+    for (int l = 0; l <= L; ++l) {
+      const int dd = 2 * l + 1;
+      float yl[2 * L + 1];
+#pragma unroll
+      for (int b = -l; b <= l; ++b) yl[b + l] = y[G::mrow(l, b) * E + c];
+#pragma unroll
+      for (int a = -l; a <= l; ++a) {
+        float acc = 0.f;
+#pragma unroll
+        for (int b = -l; b <= l; ++b) acc = fmaf(D[G::doff(l) + (b + l) * dd + (a + l)], yl[b + l], acc);
+        row[(l * l + l + a) * E + c] += acc;
+      }
+    }
+  }
+}
+
+// --------------------------------------------------- node update
+// ops.h:192-263: logits from the l=0 channels, max-subtracted softmax per
+// destination segment, out_j = node_j + sum_k alpha_k msg_k in edge order.
+// One CTA per owned row; thread t <-> output (h, c); sequential over edges,
+// so the result depends only on the segment (partition-invariant).
+template <int L, int E>
+__global__ void __launch_bounds__(512) k_node_update(const float* __restrict__ Yin, const float* __restrict__ dir,
+                                                     const int64_t* __restrict__ seg, int j0, int64_t e0,
+                                                     const float* __restrict__ att, const float* __restrict__ nodes_in,
+                                                     float* __restrict__ nodes_out, float* __restrict__ logit_scratch) {
+  using G = Geo<L>;
+  constexpr int TE = 16, DSP = G::DS + 1, H = G::H;
+  __shared__ float sD[TE * DSP];
+  __shared__ float sdir[TE * 3];
+  __shared__ float sred[32];
+  __shared__ float sA[TE];
+  const int j = j0 + blockIdx.x;
+  const int64_t b = seg[j], e = seg[j + 1];
+  const int t = threadIdx.x;
+  const int h = t / E, c = t % E;
+  float out = 0.f;
+  if (t < H * E) out = nodes_in[(int64_t)j * H * E + t];
+  if (b == e) {
+    if (t < H * E) nodes_out[(int64_t)j * H * E + t] = out;
+    return;
+  }
+  float* lg = logit_scratch + (b - e0);
+  // pass 1: logits (msg row 0 == y row 0 because D_0 = 1) and the max
+  float mx = -INFINITY;
+  for (int64_t k = b + t; k < e; k += blockDim.x) {
+    const float* y = Yin + (k - e0) * H * E;
+    float s = 0.f;
+    for (int q = 0; q < E; ++q) s = fmaf(att[q], y[q], s);
+    lg[k - b] = s;
+    mx = fmaxf(mx, s);
+  }
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((t & 31) == 0) sred[t >> 5] = mx;
+  __syncthreads();
+  if (t < 32) {
+    float v = t < (int)(blockDim.x >> 5) ? sred[t] : -INFINITY;
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (t == 0) sred[0] = v;
+  }
+  __syncthreads();
+  mx = sred[0];
+  __syncthreads();
+  float z = 0.f;
+  for (int64_t k = b + t; k < e; k += blockDim.x) {
+    const float a = expf(lg[k - b] - mx);
+    lg[k - b] = a;
+    z += a;
+  }
+  for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+  if ((t & 31) == 0) sred[t >> 5] = z;
+  __syncthreads();
+  if (t < 32) {
+    float v = t < (int)(blockDim.x >> 5) ? sred[t] : 0.f;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (t == 0) sred[0] = v;
+  }
+  __syncthreads();
+  z = sred[0];
+  // pass 2: weighted sum of rotated-back messages
+  int l = 0;
+  while ((l + 1) * (l + 1) <= h) ++l;
+  const int a = h - l * l - l;
+  for (int64_t k0 = b; k0 < e; k0 += TE) {
+    const int ne = (int)cmin64(TE, e - k0);
+    __syncthreads();
+    for (int i = t; i < ne * 3; i += blockDim.x) sdir[i] = dir[(k0 - e0) * 3 + i];
+    for (int i = t; i < ne; i += blockDim.x) sA[i] = lg[k0 - b + i] / z;
+    __syncthreads();
+    wigner_tile<L, DSP>(sdir, ne, sD);
+    if (t < H * E) {
+      const int dd = 2 * l + 1;
+      for (int i = 0; i < ne; ++i) {
+        const float* y = Yin + (k0 + i - e0) * H * E;
+        const float* D = sD + i * DSP + G::doff(l);
+        float msg = 0.f;
+        for (int bb = -l; bb <= l; ++bb) msg = fmaf(D[(bb + l) * dd + (a + l)], y[G::mrow(l, bb) * E + c], msg);
+        out = fmaf(sA[i], msg, out);
+      }
+    }
+  }
+  if (t < H * E) nodes_out[(int64_t)j * H * E + t] = out;
+}
+
+__global__ void k_copy_rows(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------- heads
+// ops.h:287-335: out[i][off_k + r] = sum_c w_k[c] x[i][L^2 + r][c].
+__global__ void k_heads(const float* __restrict__ x, int64_t n_items, int HE, int E, const float* __restrict__ W,
+                        const int* __restrict__ key_of, const int* __restrict__ row_of, int out_len,
+                        float* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_items * out_len) return;
+  const int64_t i = t / out_len;
+  const int jj = int(t % out_len);
+  const float* plane = x + i * HE + row_of[jj] * E;
+  const float* w = W + key_of[jj] * E;
+  float acc = 0.f;
+  for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[c], plane[c]));
+  out[t] = acc;
+}
+
+// ------------------------------------------------ uncoupled blocks
+// network.h:296-315 fill_block + block_matrix.cpp:66-88 to_block: per item
+// and shell pair, flat = sum_L C_L^T c_L, written row-major into the
+// n_orb(za) x n_orb(zb) block.  Work items are (item, shell pair).
+struct PairDesc {
+  int la, lb, oa, ob, nb;  // shell degrees, orbital offsets, block width
+  int seg[5];              // head offsets for L = |la-lb|.. (up to 5)
+};
+__global__ void k_blocks(const float* __restrict__ heads, int out_len, const int64_t* __restrict__ item_pair0,
+                         const int* __restrict__ item_npairs, const int64_t* __restrict__ item_off,
+                         const PairDesc* __restrict__ pairs, const int* __restrict__ pair_of_item_species,
+                         int64_t n_items, double* __restrict__ out) {
+  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  const float* row = heads + it * out_len;
+  const int p0 = pair_of_item_species[it];
+  const int np = item_npairs[it];
+  double* ob = out + item_off[it];
+  for (int q = 0; q < np; ++q) {
+    const PairDesc pd = pairs[p0 + q];
+    const int da = 2 * pd.la + 1, db = 2 * pd.lb + 1, dim = da * db;
+    const float* C = c_cg.vals + c_cg.off[pd.la][pd.lb];
+    for (int p = 0; p < dim; ++p) {
+      double flat = 0.0;
+      int r0 = 0, si = 0;
+      for (int L = abs(pd.la - pd.lb); L <= pd.la + pd.lb; ++L, ++si) {
+        const int dL = 2 * L + 1;
+        double acc = 0.0;
+        for (int r = 0; r < dL; ++r) acc += (double)C[(r0 + r) * dim + p] * (double)row[pd.seg[si] + r];
+        flat += acc;
+        r0 += dL;
+      }
+      ob[(pd.oa + p / db) * pd.nb + pd.ob + p % db] = flat;
+    }
+  }
+  (void)item_pair0;
+}
+
+__global__ void k_pack_rows(const float* __restrict__ nodes, const int* __restrict__ rows, int64_t n_rows, int row_len,
+                            float* __restrict__ buf) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_rows * row_len) return;
+  const int64_t r = t / row_len;
+  buf[t] = nodes[(int64_t)rows[r] * row_len + (t % row_len)];
+}
+
+__global__ void k_gather_dirs(const double* __restrict__ disp, const int* __restrict__ eidx, int64_t n,
+                              float* __restrict__ dir, double* __restrict__ dist_in, double* __restrict__ dist_out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t g = eidx ? eidx[k] : k;
+  dir[3 * k] = (float)disp[3 * g];
+  dir[3 * k + 1] = (float)disp[3 * g + 1];
+  dir[3 * k + 2] = (float)disp[3 * g + 2];
+  dist_out[k] = dist_in[g];
+}
+
+}  // namespace
+
+// =================================================================== host
+struct DeviceModel {
+  int L = 0, E = 0, H = 0;
+  // weights (device)
+  float* params = nullptr;  // raw flat parameters
+  std::vector<float*> w1t, w2t;      // per block (2*layers): SIMT packed
+  std::vector<uint16_t*> w1b, w2b;   // per block: tcgen05 bf16 packed
+  std::vector<int64_t> att_off;      // per layer offset into params
+  float* embed = nullptr;            // per species slot x E
+  float* head_w[2] = {nullptr, nullptr};  // node / edge: n_keys x E
+  int* head_key = nullptr;
+  int* head_row = nullptr;
+  int64_t lift_off = 0;
+  // prepared view
+  bool prepared = false;
+  int n_rows = 0, n_owned = 0;
+  int64_t n_edges = 0;
+  int* row_slot = nullptr;
+  std::vector<int> row_species;
+  int* src_row = nullptr;
+  int* dst_row = nullptr;
+  float* dir = nullptr;
+  double* dist = nullptr;
+  int64_t* seg = nullptr;  // n_owned + 1
+  std::vector<int64_t> h_seg;
+  std::vector<std::pair<int, int>> chunks;  // owned-row ranges, dst aligned
+  // halo
+  std::vector<esg::Neighbor> nbrs;
+  int* send_rows = nullptr;
+  int64_t n_send = 0;
+  float* send_buf = nullptr;
+  // tables / scratch
+  float* nodes = nullptr;
+  float* nodes_alt = nullptr;
+  float* edges = nullptr;
+  void* A1 = nullptr;
+  float* Y = nullptr;
+  float* logits = nullptr;
+  int64_t chunk_cap = 0;
+  float* node_out = nullptr;
+  float* edge_out = nullptr;
+  // uncoupled block bookkeeping
+  std::vector<int> h_item_species_a, h_item_species_b;
+  int64_t block_values = 0;
+  cudaEvent_t ev[8];
+  int precision = ESG_LINEAR_FP32;
+  size_t a1_elem = 4;
+};
+
+namespace {
+
+void free_ptr(void* p) {
+  if (p) cudaFree(p);
+}
+
+void upload_wigner_coef(int L) {
+  static bool done = false;
+  if (done) return;
+  WignerCoef wc{};
+  auto delta = [](int a, int b) { return a == b ? 1.0 : 0.0; };
+  int off = 0;
+  for (int l = 0; l <= L && l <= 4; ++l) {
+    const int d = 2 * l + 1;
+    if (l >= 2)
+      for (int m = -l; m <= l; ++m)
+        for (int n = -l; n <= l; ++n) {
+          const double denom = (std::abs(n) == l) ? (2.0 * l) * (2.0 * l - 1.0) : double(l + n) * double(l - n);
+          const int q = off + (m + l) * d + (n + l);
+          wc.u[q] = (float)std::sqrt(double(l + m) * double(l - m) / denom);
+          wc.v[q] = (float)(0.5 * std::sqrt((1.0 + delta(m, 0)) * (l + std::abs(m) - 1.0) * (l + std::abs(m)) / denom) *
+                            (1.0 - 2.0 * delta(m, 0)));
+          wc.w[q] = (float)(-0.5 * std::sqrt((l - std::abs(m) - 1.0) * (l - std::abs(m)) / denom) * (1.0 - delta(m, 0)));
+        }
+    off += d * d;
+  }
+  ESG_CUDA(cudaMemcpyToSymbol(c_wig, &wc, sizeof(wc)));
+  done = true;
+}
+
+void upload_cg_tables() {
+  static bool done = false;
+  if (done) return;
+  CgTable t{};
+  int at = 0;
+  for (int la = 0; la <= 2; ++la)
+    for (int lb = 0; lb <= 2; ++lb) {
+      t.off[la][lb] = at;
+      for (int L = std::abs(la - lb); L <= la + lb; ++L) {
+        const auto C = coupling_matrix(la, lb, L);
+        for (double v : C) t.vals[at++] = (float)v;
+      }
+    }
+  ESG_CUDA(cudaMemcpyToSymbol(c_cg, &t, sizeof(t)));
+  done = true;
+}
+
+bool supported(int L, int E) { return (L == 4 || L == 2) && (E == 16 || E == 8); }
+
+// Expanded SO(2) weight of order m in (N x K) row-major form:
+// m = 0: W0 ; m >= 1: [[Wr, Wi], [-Wi, Wr]].
+std::vector<float> expanded(const esg_model* M, const std::string& base, int m, int cin, int cout) {
+  const int nd = M->lay.nd(m);
+  if (m == 0) {
+    const auto& e = M->params.at(base + "/m0");
+    return std::vector<float>(M->host_params.begin() + e.offset,
+                              M->host_params.begin() + e.offset + (int64_t)e.rows * e.cols);
+  }
+  const auto& er = M->params.at(base + "/m" + std::to_string(m) + "r");
+  const auto& ei = M->params.at(base + "/m" + std::to_string(m) + "i");
+  const int R = nd * cout, C = nd * cin;
+  std::vector<float> W((size_t)4 * R * C);
+  const float* wr = M->host_params.data() + er.offset;
+  const float* wi = M->host_params.data() + ei.offset;
+  for (int o = 0; o < R; ++o)
+    for (int k = 0; k < C; ++k) {
+      W[(size_t)o * 2 * C + k] = wr[o * C + k];
+      W[(size_t)o * 2 * C + C + k] = wi[o * C + k];
+      W[(size_t)(R + o) * 2 * C + k] = -wi[o * C + k];
+      W[(size_t)(R + o) * 2 * C + C + k] = wr[o * C + k];
+    }
+  return W;
+}
+
+uint16_t to_bf16(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+}  // namespace
+
+void model_upload_params(esg_model* M) {
+  DeviceModel* D = M->dev;
+  cudaStream_t st = M->ctx->stream;
+  const int L = M->cfg.l_max, E = M->cfg.e_width;
+  free_ptr(D->params);
+  D->params = dalloc<float>(M->host_params.size());
+  ESG_CUDA(cudaMemcpyAsync(D->params, M->host_params.data(), sizeof(float) * M->host_params.size(),
+                           cudaMemcpyHostToDevice, st));
+  for (auto p : D->w1t) free_ptr(p);
+  for (auto p : D->w2t) free_ptr(p);
+  for (auto p : D->w1b) free_ptr(p);
+  for (auto p : D->w2b) free_ptr(p);
+  D->w1t.clear();
+  D->w2t.clear();
+  D->w1b.clear();
+  D->w2b.clear();
+  D->att_off.clear();
+  auto pad64 = [](int x) { return (x + 63) / 64 * 64; };
+  for (int layer = 0; layer < M->cfg.layers; ++layer) {
+    for (const char* blk : {"node", "edge"}) {
+      const std::string base = "layer" + std::to_string(layer) + "/" + blk;
+      std::vector<float> t1, t2;
+      std::vector<uint16_t> b1, b2;
+      for (int m = 0; m <= L; ++m) {
+        const int rows = m == 0 ? M->lay.nd(0) : 2 * M->lay.nd(m);
+        const int K1 = rows * 3 * E, N1 = rows * 2 * E, N2 = rows * E;
+        const auto W1 = expanded(M, base + "/lin1", m, 3 * E, 2 * E);  // N1 x K1
+        const auto W2 = expanded(M, base + "/lin2", m, 2 * E, E);      // N2 x N1
+        for (int k = 0; k < K1; ++k)
+          for (int o = 0; o < N1; ++o) t1.push_back(W1[(size_t)o * K1 + k]);
+        for (int k = 0; k < N1; ++k)
+          for (int o = 0; o < N2; ++o) t2.push_back(W2[(size_t)o * N1 + k]);
+        // tcgen05 operands: K-major (N rows, K contiguous), K padded to 64
+        const int K1p = pad64(K1), N1p = pad64(N1);
+        for (int o = 0; o < N1; ++o)
+          for (int k = 0; k < K1p; ++k) b1.push_back(k < K1 ? to_bf16(W1[(size_t)o * K1 + k]) : 0);
+        for (int o = 0; o < N2; ++o)
+          for (int k = 0; k < N1p; ++k) b2.push_back(k < N1 ? to_bf16(W2[(size_t)o * N1 + k]) : 0);
+      }
+      float* d1 = dalloc<float>(t1.size());
+      float* d2 = dalloc<float>(t2.size());
+      uint16_t* e1 = dalloc<uint16_t>(b1.size());
+      uint16_t* e2 = dalloc<uint16_t>(b2.size());
+      ESG_CUDA(cudaMemcpy(d1, t1.data(), sizeof(float) * t1.size(), cudaMemcpyHostToDevice));
+      ESG_CUDA(cudaMemcpy(d2, t2.data(), sizeof(float) * t2.size(), cudaMemcpyHostToDevice));
+      ESG_CUDA(cudaMemcpy(e1, b1.data(), sizeof(uint16_t) * b1.size(), cudaMemcpyHostToDevice));
+      ESG_CUDA(cudaMemcpy(e2, b2.data(), sizeof(uint16_t) * b2.size(), cudaMemcpyHostToDevice));
+      D->w1t.push_back(d1);
+      D->w2t.push_back(d2);
+      D->w1b.push_back(e1);
+      D->w2b.push_back(e2);
+    }
+    D->att_off.push_back(M->params.at("layer" + std::to_string(layer) + "/att").offset);
+  }
+  // embeddings per species slot (ascending Z), lift, heads
+  std::vector<float> emb;
+  for (int z : M->species_list) {
+    const auto& e = M->params.at("embed/" + element_symbol(z));
+    emb.insert(emb.end(), M->host_params.begin() + e.offset, M->host_params.begin() + e.offset + E);
+  }
+  free_ptr(D->embed);
+  D->embed = dalloc<float>(emb.size());
+  ESG_CUDA(cudaMemcpy(D->embed, emb.data(), sizeof(float) * emb.size(), cudaMemcpyHostToDevice));
+  D->lift_off = M->params.at("radial/lift").offset;
+  std::vector<int> key_of, row_of;
+  for (size_t k = 0; k < M->heads.keys.size(); ++k) {
+    const int Lk = M->heads.keys[k].L;
+    for (int r = 0; r < 2 * Lk + 1; ++r) {
+      key_of.push_back((int)k);
+      row_of.push_back(Lk * Lk + r);
+    }
+  }
+  for (int s = 0; s < 2; ++s) {
+    std::vector<float> hw;
+    for (const auto& k : M->heads.keys) {
+      const auto& e = M->params.at(std::string("head/") + (s == 0 ? "node" : "edge") + "/s" + std::to_string(k.sa) +
+                                   "s" + std::to_string(k.sb) + "L" + std::to_string(k.L));
+      hw.insert(hw.end(), M->host_params.begin() + e.offset, M->host_params.begin() + e.offset + E);
+    }
+    free_ptr(D->head_w[s]);
+    D->head_w[s] = dalloc<float>(hw.size());
+    ESG_CUDA(cudaMemcpy(D->head_w[s], hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice));
+  }
+  free_ptr(D->head_key);
+  free_ptr(D->head_row);
+  D->head_key = dalloc<int>(key_of.size());
+  D->head_row = dalloc<int>(row_of.size());
+  ESG_CUDA(cudaMemcpy(D->head_key, key_of.data(), sizeof(int) * key_of.size(), cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpy(D->head_row, row_of.data(), sizeof(int) * row_of.size(), cudaMemcpyHostToDevice));
+}
+
+void model_device_create(esg_model* M) {
+  const int L = M->cfg.l_max, E = M->cfg.e_width;
+  if (!supported(L, E))
+    usage("the B200 kernels are instantiated for l_max in {2,4} and e_width in {8,16}; got l_max " +
+          std::to_string(L) + ", e_width " + std::to_string(E));
+  M->dev = new DeviceModel();
+  M->dev->L = L;
+  M->dev->E = E;
+  M->dev->H = (L + 1) * (L + 1);
+  M->dev->precision = M->cfg.linear_precision;
+  for (auto& e : M->dev->ev) ESG_CUDA(cudaEventCreate(&e));
+  ESG_CUDA(cudaSetDevice(M->ctx->device));
+  upload_wigner_coef(L);
+  upload_cg_tables();
+}
+
+void model_device_destroy(esg_model* M) {
+  DeviceModel* D = M->dev;
+  if (!D) return;
+  for (void* p : {(void*)D->params, (void*)D->embed, (void*)D->head_w[0], (void*)D->head_w[1], (void*)D->head_key,
+                  (void*)D->head_row, (void*)D->row_slot, (void*)D->src_row, (void*)D->dst_row, (void*)D->dir,
+                  (void*)D->dist, (void*)D->seg, (void*)D->send_rows, (void*)D->send_buf, (void*)D->nodes,
+                  (void*)D->nodes_alt, (void*)D->edges, D->A1, (void*)D->Y, (void*)D->logits, (void*)D->node_out,
+                  (void*)D->edge_out})
+    free_ptr(p);
+  for (auto p : D->w1t) free_ptr(p);
+  for (auto p : D->w2t) free_ptr(p);
+  for (auto p : D->w1b) free_ptr(p);
+  for (auto p : D->w2b) free_ptr(p);
+  for (auto& e : D->ev) cudaEventDestroy(e);
+  delete D;
+  M->dev = nullptr;
+}
+
+// Network::prepare on a rank view (comm_plan.cpp layout; plan == nullptr is
+// the serial view of the whole graph).
+void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const int32_t* species) {
+  DeviceModel* D = M->dev;
+  cudaStream_t st = M->ctx->stream;
+  g->host_sync();
+  const int E = D->E, H = D->H;
+  std::vector<int32_t> row_global, src_row, dst_row, eidx;
+  int n_rows, n_owned;
+  if (plan) {
+    n_rows = plan->n_rows;
+    n_owned = plan->n_owned;
+    row_global = plan->row_global;
+    src_row = plan->src_row;
+    dst_row = plan->dst_row;
+    eidx = plan->edge_index;
+  } else {
+    n_rows = n_owned = g->n;
+    row_global.resize(g->n);
+    for (int i = 0; i < g->n; ++i) row_global[i] = i;
+    src_row = g->h_src;
+    dst_row.resize(g->E);
+    for (int j = 0; j < g->n; ++j)
+      for (int64_t k = g->h_off[j]; k < g->h_off[j + 1]; ++k) dst_row[k] = j;
+  }
+  const int64_t ne = (int64_t)src_row.size();
+  std::vector<int> slot(n_rows);
+  D->row_species.resize(n_rows);
+  for (int i = 0; i < n_rows; ++i) {
+    const int z = species[row_global[i]];
+    D->row_species[i] = z;
+    auto it = std::find(M->species_list.begin(), M->species_list.end(), z);
+    if (it == M->species_list.end()) data("species " + element_symbol(z) + " missing from the model's basis");
+    slot[i] = int(it - M->species_list.begin());
+  }
+  std::vector<int64_t> seg(n_owned + 1, 0);
+  for (int64_t k = 0; k < ne; ++k) seg[dst_row[k] + 1]++;
+  for (int j = 0; j < n_owned; ++j) seg[j + 1] += seg[j];
+  for (void* p : {(void*)D->row_slot, (void*)D->src_row, (void*)D->dst_row, (void*)D->dir, (void*)D->dist,
+                  (void*)D->seg, (void*)D->nodes, (void*)D->nodes_alt, (void*)D->edges, D->A1, (void*)D->Y,
+                  (void*)D->logits, (void*)D->node_out, (void*)D->edge_out, (void*)D->send_rows, (void*)D->send_buf})
+    free_ptr(p);
+  D->n_rows = n_rows;
+  D->n_owned = n_owned;
+  D->n_edges = ne;
+  D->h_seg = seg;
+  D->row_slot = dalloc<int>(n_rows);
+  D->src_row = dalloc<int>(ne);
+  D->dst_row = dalloc<int>(ne);
+  D->dir = dalloc<float>(3 * ne);
+  D->dist = dalloc<double>(ne);
+  D->seg = dalloc<int64_t>(n_owned + 1);
+  ESG_CUDA(cudaMemcpy(D->row_slot, slot.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpy(D->src_row, src_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpy(D->dst_row, dst_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpy(D->seg, seg.data(), sizeof(int64_t) * (n_owned + 1), cudaMemcpyHostToDevice));
+  int* d_eidx = nullptr;
+  if (plan) {
+    d_eidx = dalloc<int>(ne);
+    ESG_CUDA(cudaMemcpy(d_eidx, eidx.data(), sizeof(int) * ne, cudaMemcpyHostToDevice));
+  }
+  if (ne) {
+    k_gather_dirs<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(g->d_disp, d_eidx, ne, D->dir, g->d_dist, D->dist);
+    ++M->ctx->launches;
+  }
+  ESG_CUDA(cudaStreamSynchronize(st));
+  free_ptr(d_eidx);
+  // destination-aligned chunks of about chunk_cap edges
+  const int64_t cap = std::max<int64_t>(std::min<int64_t>(ne, 2 << 20), 1);
+  int64_t maxseg = 0;
+  for (int j = 0; j < n_owned; ++j) maxseg = std::max(maxseg, seg[j + 1] - seg[j]);
+  D->chunk_cap = std::max(cap, maxseg);
+  D->chunks.clear();
+  for (int j = 0; j < n_owned;) {
+    int j1 = j;
+    while (j1 < n_owned && (j1 == j || seg[j1 + 1] - seg[j] <= D->chunk_cap)) ++j1;
+    D->chunks.push_back({j, j1});
+    j = j1;
+  }
+  // tables and scratch
+  const int64_t row = (int64_t)H * E;
+  D->nodes = dalloc<float>((size_t)n_rows * row);
+  D->nodes_alt = dalloc<float>((size_t)n_rows * row);
+  D->edges = dalloc<float>((size_t)std::max<int64_t>(ne, 1) * row);
+  const int K1T = [&] {
+    int t = 0;
+    for (int m = 0; m <= D->L; ++m) t += ((m == 0 ? D->L + 1 : 2 * (D->L - m + 1)) * 3 * E + 63) / 64 * 64;
+    return t;
+  }();
+  D->A1 = (void*)dalloc<float>((size_t)D->chunk_cap * K1T);  // sized for fp32 (bf16 uses half)
+  D->Y = dalloc<float>((size_t)D->chunk_cap * row);
+  D->logits = dalloc<float>((size_t)D->chunk_cap);
+  D->node_out = dalloc<float>((size_t)std::max(n_owned, 1) * M->heads.out_len);
+  D->edge_out = dalloc<float>((size_t)std::max<int64_t>(ne, 1) * M->heads.out_len);
+  // halo
+  D->nbrs.clear();
+  D->n_send = 0;
+  if (plan) {
+    D->nbrs = plan->nbrs;
+    std::vector<int> all;
+    for (const auto& nb : plan->nbrs) all.insert(all.end(), nb.send_rows.begin(), nb.send_rows.end());
+    D->n_send = (int64_t)all.size();
+    D->send_rows = dalloc<int>(all.size());
+    D->send_buf = dalloc<float>(all.size() * row);
+    if (!all.empty()) ESG_CUDA(cudaMemcpy(D->send_rows, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice));
+  }
+  // per-item species for block assembly (nodes: owned rows, edges: view edges)
+  D->h_item_species_a.assign(n_owned + ne, 0);
+  D->h_item_species_b.assign(n_owned + ne, 0);
+  for (int i = 0; i < n_owned; ++i) D->h_item_species_a[i] = D->h_item_species_b[i] = D->row_species[i];
+  for (int64_t k = 0; k < ne; ++k) {
+    D->h_item_species_a[n_owned + k] = D->row_species[src_row[k]];
+    D->h_item_species_b[n_owned + k] = D->row_species[dst_row[k]];
+  }
+  D->prepared = true;
+}
+
+namespace {
+
+template <int L, int E>
+void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
+  DeviceModel* D = M->dev;
+  esg_ctx* ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  constexpr int H = (L + 1) * (L + 1);
+  const int bidx = 2 * layer + (node_block ? 0 : 1);
+  // halo exchange (distributed.h:51-130): pack, grouped send/recv straight
+  // into the contiguous halo rows of each peer.
+  if (ctx->world > 1) {
+    ESG_CUDA(cudaEventRecord(D->ev[4], st));
+    const int row = H * E;
+    if (D->n_send) {
+      k_pack_rows<<<(unsigned)((D->n_send * row + 255) / 256), 256, 0, st>>>(D->nodes, D->send_rows, D->n_send, row,
+                                                                             D->send_buf);
+      ++ctx->launches;
+    }
+    ESG_NCCL(ncclGroupStart());
+    int64_t so = 0;
+    for (const auto& nb : D->nbrs) {
+      const int64_t cnt = (int64_t)nb.send_rows.size() * row;
+      ESG_NCCL(ncclSend(D->send_buf + so * row, cnt, ncclFloat, nb.peer, ctx->comm, st));
+      so += (int64_t)nb.send_rows.size();
+      ESG_NCCL(ncclRecv(D->nodes + (int64_t)nb.recv_row * row, (int64_t)nb.recv_count * row, ncclFloat, nb.peer,
+                        ctx->comm, st));
+    }
+    ESG_NCCL(ncclGroupEnd());
+    ESG_CUDA(cudaEventRecord(D->ev[5], st));
+    ESG_CUDA(cudaEventSynchronize(D->ev[5]));
+    float ms = 0.f;
+    ESG_CUDA(cudaEventElapsedTime(&ms, D->ev[4], D->ev[5]));
+    *halo_ms += ms;
+  }
+  if (node_block) {  // halo rows pass through (ops.h:200 copies all rows)
+    const int64_t n = (int64_t)D->n_rows * H * E;
+    k_copy_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->nodes, D->nodes_alt, n);
+    ++ctx->launches;
+  }
+  const bool tc = D->precision == ESG_LINEAR_BF16 && so2_tc_available(L, E);
+  const float* att = D->params + D->att_off[layer];
+  for (const auto& ch : D->chunks) {
+    const int64_t e0 = D->h_seg[ch.first], e1 = D->h_seg[ch.second];
+    const int64_t n = e1 - e0;
+    if (n > 0) {
+      const unsigned tiles = (unsigned)((n + 15) / 16);
+      if (tc) {
+        k_rotate_in<L, E, 64, uint16_t><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir, e0,
+                                                                n, (uint16_t*)D->A1);
+        ++ctx->launches;
+        so2_tc_launch(L, E, (const uint16_t*)D->A1, n, D->w1b[bidx], D->w2b[bidx], D->Y, M->cfg.gate_enabled, st);
+        ++ctx->launches;
+      } else {
+        k_rotate_in<L, E, 1, float><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir, e0, n,
+                                                           (float*)D->A1);
+        k_so2_simt<L, E><<<tiles, 256, 0, st>>>((const float*)D->A1, n, D->w1t[bidx], D->w2t[bidx], D->Y,
+                                                M->cfg.gate_enabled);
+        ctx->launches += 2;
+      }
+      if (!node_block) {
+        k_rotate_out_edge<L, E><<<tiles, 256, 0, st>>>(D->Y, D->dir, e0, n, D->edges);
+        ++ctx->launches;
+      }
+    }
+    if (node_block && ch.second > ch.first) {
+      const int threads = ((H * E + 31) / 32) * 32;
+      k_node_update<L, E><<<ch.second - ch.first, threads, 0, st>>>(D->Y, D->dir + 0, D->seg, ch.first, e0, att,
+                                                                   D->nodes, D->nodes_alt, D->logits);
+      ++ctx->launches;
+    }
+  }
+  ESG_CUDA(cudaGetLastError());
+  if (node_block) std::swap(D->nodes, D->nodes_alt);
+}
+
+template <int L, int E>
+void forward_impl(esg_model* M, esg_timing* tm) {
+  DeviceModel* D = M->dev;
+  esg_ctx* ctx = M->ctx;
+  cudaStream_t st = ctx->stream;
+  constexpr int H = (L + 1) * (L + 1);
+  const int64_t launches0 = ctx->launches;
+  ESG_CUDA(cudaEventRecord(D->ev[0], st));
+  {
+    const int64_t n = (int64_t)D->n_rows * H * E;
+    k_init_nodes<H, E><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->row_slot, D->n_rows, D->embed, D->nodes);
+    ++ctx->launches;
+    if (D->n_edges) {
+      const int per = 256 / E;
+      k_init_edges<H, E><<<(unsigned)((D->n_edges + per - 1) / per), per * E, 0, st>>>(
+          D->dist, D->n_edges, D->params + D->lift_off, M->cfg.n_radial, M->cfg.r_cut / (M->cfg.n_radial - 1),
+          D->edges);
+      ++ctx->launches;
+    }
+  }
+  ESG_CUDA(cudaEventRecord(D->ev[1], st));
+  float halo_ms = 0.f;
+  int64_t exchanges = 0;
+  for (int layer = 0; layer < M->cfg.layers; ++layer)
+    for (bool nb : {true, false}) {
+      run_block<L, E>(M, layer, nb, &halo_ms);
+      ++exchanges;
+    }
+  ESG_CUDA(cudaEventRecord(D->ev[2], st));
+  const int out_len = M->heads.out_len;
+  if (D->n_owned) {
+    const int64_t n = (int64_t)D->n_owned * out_len;
+    k_heads<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->nodes, D->n_owned, H * E, E, D->head_w[0], D->head_key,
+                                                         D->head_row, out_len, D->node_out);
+    ++ctx->launches;
+  }
+  if (D->n_edges) {
+    const int64_t n = D->n_edges * out_len;
+    k_heads<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->edges, D->n_edges, H * E, E, D->head_w[1], D->head_key,
+                                                         D->head_row, out_len, D->edge_out);
+    ++ctx->launches;
+  }
+  ESG_CUDA(cudaEventRecord(D->ev[3], st));
+  ESG_CUDA(cudaGetLastError());
+  ESG_CUDA(cudaEventSynchronize(D->ev[3]));
+  if (tm) {
+    float a = 0, b = 0, c = 0;
+    ESG_CUDA(cudaEventElapsedTime(&a, D->ev[0], D->ev[3]));
+    ESG_CUDA(cudaEventElapsedTime(&b, D->ev[1], D->ev[2]));
+    ESG_CUDA(cudaEventElapsedTime(&c, D->ev[2], D->ev[3]));
+    tm->forward_ms = a;
+    tm->message_ms = b;
+    tm->heads_ms = c;
+    tm->halo_ms = halo_ms;
+    tm->exchanges = ctx->world > 1 ? exchanges : 0;
+    tm->gpu_launches = ctx->launches - launches0;
+  }
+}
+
+}  // namespace
+
+void model_forward(esg_model* M, esg_timing* tm) {
+  DeviceModel* D = M->dev;
+  if (!D->prepared) usage("forward before prepare");
+  D->precision = M->cfg.linear_precision;
+  const int L = D->L, E = D->E;
+  if (L == 4 && E == 16)
+    forward_impl<4, 16>(M, tm);
+  else if (L == 4 && E == 8)
+    forward_impl<4, 8>(M, tm);
+  else if (L == 2 && E == 16)
+    forward_impl<2, 16>(M, tm);
+  else
+    forward_impl<2, 8>(M, tm);
+}
+
+void model_outputs(const esg_model* M, const float** no, const float** eo, const float** nf, const float** ef) {
+  const DeviceModel* D = M->dev;
+  if (no) *no = D->node_out;
+  if (eo) *eo = D->edge_out;
+  if (nf) *nf = D->nodes;
+  if (ef) *ef = D->edges;
+}
+
+void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out) {
+  const DeviceModel* D = M->dev;
+  const int ol = M->heads.out_len;
+  if (node_out && D->n_owned)
+    ESG_CUDA(cudaMemcpy(node_out, D->node_out, sizeof(float) * (size_t)D->n_owned * ol, cudaMemcpyDeviceToHost));
+  if (edge_out && D->n_edges)
+    ESG_CUDA(cudaMemcpy(edge_out, D->edge_out, sizeof(float) * (size_t)D->n_edges * ol, cudaMemcpyDeviceToHost));
+}
+
+void model_copy_features(const esg_model* M, float* nodes, float* edges) {
+  const DeviceModel* D = M->dev;
+  const size_t row = (size_t)D->H * D->E;
+  if (nodes) ESG_CUDA(cudaMemcpy(nodes, D->nodes, sizeof(float) * D->n_rows * row, cudaMemcpyDeviceToHost));
+  if (edges && D->n_edges)
+    ESG_CUDA(cudaMemcpy(edges, D->edges, sizeof(float) * D->n_edges * row, cudaMemcpyDeviceToHost));
+}
+
+void model_prepared_info(const esg_model* M, int64_t info[3]) {
+  info[0] = M->dev->n_rows;
+  info[1] = M->dev->n_owned;
+  info[2] = M->dev->n_edges;
+}
+
+// Uncoupled blocks of the last forward, items = owned nodes then view edges.
+int64_t model_blocks_size(const esg_model* M) {
+  const DeviceModel* D = M->dev;
+  int64_t n = 0;
+  for (size_t i = 0; i < D->h_item_species_a.size(); ++i)
+    n += (int64_t)M->basis.n_orb(D->h_item_species_a[i]) * M->basis.n_orb(D->h_item_species_b[i]);
+  return n;
+}
+
+void model_blocks(esg_model* M, double* out_host) {
+  DeviceModel* D = M->dev;
+  cudaStream_t st = M->ctx->stream;
+  if (M->basis.shells.empty()) return;
+  for (const auto& kv : M->basis.shells)
+    for (int l : kv.second)
+      if (l > 2) usage("uncoupled block kernel supports shells up to l = 2");
+  // pair descriptors per (za, zb) species pair
+  std::map<std::pair<int, int>, std::pair<int, int>> pair_range;  // -> (first, count)
+  std::vector<PairDesc> pairs;
+  for (const auto& ka : M->basis.shells)
+    for (const auto& kb : M->basis.shells) {
+      const int first = (int)pairs.size();
+      for (size_t a = 0; a < ka.second.size(); ++a)
+        for (size_t b = 0; b < kb.second.size(); ++b) {
+          PairDesc pd{};
+          pd.la = ka.second[a];
+          pd.lb = kb.second[b];
+          pd.oa = M->basis.off(ka.first, (int)a);
+          pd.ob = M->basis.off(kb.first, (int)b);
+          pd.nb = M->basis.n_orb(kb.first);
+          int si = 0;
+          for (int L = std::abs(pd.la - pd.lb); L <= pd.la + pd.lb; ++L) pd.seg[si++] = M->heads.segment((int)a, (int)b, L);
+          pairs.push_back(pd);
+        }
+      pair_range[{ka.first, kb.first}] = {first, (int)pairs.size() - first};
+    }
+  const int64_t n_items = (int64_t)D->h_item_species_a.size();
+  std::vector<int> pfirst(n_items), pcount(n_items);
+  std::vector<int64_t> off(n_items);
+  int64_t at = 0;
+  for (int64_t i = 0; i < n_items; ++i) {
+    const auto& pr = pair_range.at({D->h_item_species_a[i], D->h_item_species_b[i]});
+    pfirst[i] = pr.first;
+    pcount[i] = pr.second;
+    off[i] = at;
+    at += (int64_t)M->basis.n_orb(D->h_item_species_a[i]) * M->basis.n_orb(D->h_item_species_b[i]);
+  }
+  PairDesc* d_pairs = dalloc<PairDesc>(pairs.size());
+  int* d_first = dalloc<int>(n_items);
+  int* d_count = dalloc<int>(n_items);
+  int64_t* d_off = dalloc<int64_t>(n_items);
+  double* d_out = dalloc<double>(at);
+  ESG_CUDA(cudaMemcpy(d_pairs, pairs.data(), sizeof(PairDesc) * pairs.size(), cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpy(d_first, pfirst.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpy(d_count, pcount.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpy(d_off, off.data(), sizeof(int64_t) * n_items, cudaMemcpyHostToDevice));
+  const int ol = M->heads.out_len;
+  if (D->n_owned) {
+    k_blocks<<<(D->n_owned + 127) / 128, 128, 0, st>>>(D->node_out, ol, nullptr, d_count, d_off, d_pairs, d_first,
+                                                       D->n_owned, d_out);
+    ++M->ctx->launches;
+  }
+  if (D->n_edges) {
+    k_blocks<<<(unsigned)((D->n_edges + 127) / 128), 128, 0, st>>>(D->edge_out, ol, nullptr, d_count + D->n_owned,
+                                                                  d_off + D->n_owned, d_pairs, d_first + D->n_owned,
+                                                                  D->n_edges, d_out);
+    ++M->ctx->launches;
+  }
+  ESG_CUDA(cudaGetLastError());
+  ESG_CUDA(cudaMemcpy(out_host, d_out, sizeof(double) * at, cudaMemcpyDeviceToHost));
+  for (void* p : {(void*)d_pairs, (void*)d_first, (void*)d_count, (void*)d_off, (void*)d_out}) free_ptr(p);
+}
+
+}  // namespace esg

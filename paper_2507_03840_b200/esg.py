@@ -1,0 +1,444 @@
+"""ctypes binding of libesg_b200.so (include/esg.h).
+
+This mirrors the reference's C++ API names and argument meaning
+(structures::build_graph, partition::lownn_partition, runtime::build_comm_plan,
+model::Network<float>) so tests and the bench read like the reference's own
+tests.  It is plumbing only: every computation runs inside the CUDA library,
+and importing this module fails loudly if the library was not built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libesg_b200.so")
+
+OK, ERR_OTHER, ERR_USAGE, ERR_DATA, ERR_DIVERGENCE, ERR_NCCL, ERR_CUDA, ERR_OOM = range(8)
+LINEAR_FP32, LINEAR_BF16 = 0, 1
+
+
+class EsgError(RuntimeError):
+    """Base of the mirrored esgnn::Error taxonomy (core/error.h:11-51)."""
+
+    code = ERR_OTHER
+
+
+class UsageError(EsgError):
+    code = ERR_USAGE
+
+
+class DataError(EsgError):
+    code = ERR_DATA
+
+
+class DivergenceError(EsgError):
+    code = ERR_DIVERGENCE
+
+
+class TransportError(EsgError):
+    code = ERR_NCCL
+
+
+class CudaError(EsgError):
+    code = ERR_CUDA
+
+
+class OutOfMemory(EsgError):
+    code = ERR_OOM
+
+
+_ERRORS = {c.code: c for c in (UsageError, DataError, DivergenceError, TransportError, CudaError, OutOfMemory)}
+
+_lib_handle = None
+
+
+class _Timing(C.Structure):
+    _fields_ = [
+        ("forward_ms", C.c_double),
+        ("message_ms", C.c_double),
+        ("halo_ms", C.c_double),
+        ("heads_ms", C.c_double),
+        ("exchanges", C.c_int64),
+        ("gpu_launches", C.c_int64),
+    ]
+
+
+class _ModelConfig(C.Structure):
+    _fields_ = [
+        ("l_max", C.c_int),
+        ("e_width", C.c_int),
+        ("layers", C.c_int),
+        ("n_radial", C.c_int),
+        ("r_cut", C.c_double),
+        ("seed", C.c_uint64),
+        ("gate_enabled", C.c_int),
+        ("linear_precision", C.c_int),
+    ]
+
+
+def lib() -> C.CDLL:
+    """Loads libesg_b200.so; raises if it is missing (no fallback path)."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C csrc)")
+        L = C.CDLL(LIB_PATH)
+        L.esg_last_error.restype = C.c_char_p
+        L.esg_model_param_count.restype = C.c_int64
+        L.esg_model_param_hash.restype = C.c_uint64
+        _lib_handle = L
+    return _lib_handle
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _check(rc: int) -> None:
+    if rc != OK:
+        msg = lib().esg_last_error().decode()
+        raise _ERRORS.get(rc, EsgError)(msg)
+
+
+# --------------------------------------------------------------- structures
+@dataclasses.dataclass
+class AtomicStructure:
+    """structures::AtomicStructure (structure.h:12-36): rows of `cell` are the
+    lattice vectors, positions are Cartesian."""
+
+    positions: np.ndarray  # (n, 3) float64
+    species: np.ndarray  # (n,) int32 atomic numbers
+    cell: np.ndarray  # (3, 3) float64
+    pbc: np.ndarray  # (3,) bool
+
+    @property
+    def n_atoms(self) -> int:
+        return int(self.positions.shape[0])
+
+    def _pbc8(self) -> np.ndarray:
+        return np.ascontiguousarray(self.pbc, dtype=np.uint8)
+
+
+def make_jittered_lattice(n_atoms: int, spacing: float, jitter: float, species_cycle: Sequence[int],
+                          seed: int) -> AtomicStructure:
+    """model::make_jittered_lattice (synthetic.cpp:17-41)."""
+    cyc = np.ascontiguousarray(species_cycle, dtype=np.int32)
+    pos = np.zeros((n_atoms, 3))
+    cell = np.zeros(9)
+    sp = np.zeros(n_atoms, dtype=np.int32)
+    _check(lib().esg_jittered_lattice(C.c_int(n_atoms), C.c_double(spacing), C.c_double(jitter), C.c_int(len(cyc)),
+                                      _p(cyc), C.c_uint64(seed), _p(pos), _p(cell), _p(sp)))
+    return AtomicStructure(pos, sp, cell.reshape(3, 3), np.ones(3, dtype=bool))
+
+
+def tile(s: AtomicStructure, reps: Sequence[int]) -> AtomicStructure:
+    """structures::tile (structure.cpp:40-63)."""
+    r = np.ascontiguousarray(reps, dtype=np.int32)
+    n = s.n_atoms * int(np.prod(r))
+    pos = np.zeros((n, 3))
+    cell = np.zeros(9)
+    sp = np.zeros(n, dtype=np.int32)
+    _check(lib().esg_tile(C.c_int(s.n_atoms), _p(np.ascontiguousarray(s.positions)), _p(np.ascontiguousarray(s.cell)),
+                          _p(s._pbc8()), _p(np.ascontiguousarray(s.species, dtype=np.int32)), _p(r), _p(pos), _p(cell),
+                          _p(sp)))
+    return AtomicStructure(pos, sp, cell.reshape(3, 3), np.array(s.pbc, dtype=bool))
+
+
+def wrap_positions(s: AtomicStructure) -> np.ndarray:
+    """AtomicStructure::wrap (structure.cpp:26-38) on a copy of the positions."""
+    pos = np.ascontiguousarray(s.positions, dtype=np.float64).copy()
+    _check(lib().esg_wrap_positions(C.c_int(s.n_atoms), _p(pos), _p(np.ascontiguousarray(s.cell)), _p(s._pbc8())))
+    return pos
+
+
+# ------------------------------------------------------------------ context
+def nccl_unique_id() -> bytes:
+    n = lib().esg_nccl_unique_id_size()
+    buf = (C.c_char * n)()
+    _check(lib().esg_nccl_get_unique_id(buf))
+    return bytes(buf)
+
+
+class Context:
+    """One GPU (and, for world > 1, one NCCL rank)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        self._h = C.c_void_p()
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (C.c_char * len(nccl_id)).from_buffer_copy(nccl_id)
+        _check(lib().esg_ctx_create(C.c_int(device), C.c_int(rank), C.c_int(world), idbuf, C.byref(self._h)))
+        self.device, self.rank, self.world = device, rank, world
+
+    def synchronize(self) -> None:
+        _check(lib().esg_ctx_synchronize(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            lib().esg_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# -------------------------------------------------------------------- graph
+class Graph:
+    """structures::Graph built by esg_build_graph (graph.h:22-37)."""
+
+    def __init__(self, ctx: Context, s: AtomicStructure, r_cut: float):
+        self.ctx = ctx
+        self._h = C.c_void_p()
+        _check(lib().esg_build_graph(ctx._h, C.c_int(s.n_atoms), _p(np.ascontiguousarray(s.positions, np.float64)),
+                                     _p(np.ascontiguousarray(s.cell, np.float64)), _p(s._pbc8()), C.c_double(r_cut),
+                                     C.byref(self._h)))
+        n = C.c_int()
+        e = C.c_int64()
+        _check(lib().esg_graph_info(self._h, C.byref(n), C.byref(e)))
+        self.n_nodes, self.n_edges = n.value, e.value
+
+    def export(self) -> Dict[str, np.ndarray]:
+        E = self.n_edges
+        out = dict(src=np.zeros(E, np.int32), dst=np.zeros(E, np.int32), shift=np.zeros((E, 3), np.int32),
+                   disp=np.zeros((E, 3)), dist=np.zeros(E))
+        _check(lib().esg_graph_export(self._h, _p(out["src"]), _p(out["dst"]), _p(out["shift"]), _p(out["disp"]),
+                                      _p(out["dist"])))
+        return out
+
+    def in_degrees(self) -> np.ndarray:
+        d = np.zeros(self.n_nodes, np.int32)
+        _check(lib().esg_graph_in_degrees(self._h, _p(d)))
+        return d
+
+    def offsets(self) -> np.ndarray:
+        o = np.zeros(self.n_nodes + 1, np.int64)
+        _check(lib().esg_graph_offsets(self._h, _p(o)))
+        return o
+
+    def close(self) -> None:
+        if self._h:
+            lib().esg_graph_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_graph(ctx: Context, s: AtomicStructure, r_cut: float) -> Graph:
+    return Graph(ctx, s, r_cut)
+
+
+def lownn_partition(s: AtomicStructure, in_degrees: np.ndarray, depth: int, r_cut: float) -> np.ndarray:
+    """partition::lownn_partition (partition.h:24); positions are the unwrapped input."""
+    part = np.zeros(s.n_atoms, np.int32)
+    _check(lib().esg_lownn_partition(C.c_int(s.n_atoms), _p(np.ascontiguousarray(s.positions, np.float64)),
+                                     _p(np.ascontiguousarray(s.cell, np.float64)), _p(s._pbc8()),
+                                     _p(np.ascontiguousarray(in_degrees, np.int32)), C.c_int(depth),
+                                     C.c_double(r_cut), _p(part)))
+    return part
+
+
+class CommPlan:
+    """runtime::CommPlan (comm_plan.h:15-35)."""
+
+    def __init__(self, g: Optional[Graph], species: np.ndarray, part: np.ndarray, n_parts: int, rank: int,
+                 csr: Optional[tuple] = None):
+        """From a device graph, or (csr=(dst_off, src)) from host arrays."""
+        self._h = C.c_void_p()
+        self._species = np.ascontiguousarray(species, np.int32)
+        part = np.ascontiguousarray(part, np.int32)
+        if g is not None:
+            _check(lib().esg_plan_build(g._h, _p(self._species), _p(part), C.c_int(n_parts), C.c_int(rank),
+                                        C.byref(self._h)))
+        else:
+            off = np.ascontiguousarray(csr[0], np.int64)
+            src = np.ascontiguousarray(csr[1], np.int32)
+            _check(lib().esg_plan_build_host(C.c_int(len(off) - 1), _p(off), _p(src), _p(self._species), _p(part),
+                                             C.c_int(n_parts), C.c_int(rank), C.byref(self._h)))
+        info = np.zeros(5, np.int64)
+        _check(lib().esg_plan_info(self._h, _p(info)))
+        self.n_rows, self.n_owned, self.n_edges, self.n_neighbors, self.n_send = (int(x) for x in info)
+        self.rank, self.world = rank, n_parts
+
+    def export(self) -> Dict[str, np.ndarray]:
+        z = lambda n: np.zeros(n, np.int32)
+        o = dict(row_global=z(self.n_rows), row_species=z(self.n_rows), edge_index=z(self.n_edges),
+                 src_row=z(self.n_edges), dst_row=z(self.n_edges), nbr_peer=z(self.n_neighbors),
+                 nbr_recv_row=z(self.n_neighbors), nbr_recv_count=z(self.n_neighbors),
+                 nbr_send_count=z(self.n_neighbors), send_rows=z(self.n_send))
+        _check(lib().esg_plan_export(self._h, *[_p(o[k]) for k in ("row_global", "row_species", "edge_index",
+                                                                   "src_row", "dst_row", "nbr_peer",
+                                                                   "nbr_recv_row", "nbr_recv_count",
+                                                                   "nbr_send_count", "send_rows")]))
+        return o
+
+    def close(self) -> None:
+        if self._h:
+            lib().esg_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_comm_plan(g: Graph, species, part, n_parts: int, rank: int) -> CommPlan:
+    return CommPlan(g, species, part, n_parts, rank)
+
+
+# -------------------------------------------------------------------- model
+@dataclasses.dataclass
+class ModelConfig:
+    """model::ModelConfig (network.h:16-35) + the linear precision knob."""
+
+    l_max: int = 2
+    e_width: int = 8
+    layers: int = 2
+    n_radial: int = 32
+    r_cut: float = 4.0
+    seed: int = 1
+    gate_enabled: bool = True
+    linear_precision: int = LINEAR_FP32
+
+
+@dataclasses.dataclass
+class Timing:
+    forward_ms: float
+    message_ms: float
+    halo_ms: float
+    heads_ms: float
+    exchanges: int
+    gpu_launches: int
+
+
+class Network:
+    """model::Network<float> (network.h:77-228) driven through the C ABI."""
+
+    def __init__(self, ctx: Optional[Context], cfg: ModelConfig, basis: Dict[int, List[int]]):
+        """ctx=None gives a host-only model (parameters, layouts, hash)."""
+        self.ctx, self.cfg = ctx, cfg
+        zs = sorted(basis)
+        z = np.array(zs, np.int32)
+        ns = np.array([len(basis[k]) for k in zs], np.int32)
+        sh = np.array([l for k in zs for l in basis[k]], np.int32)
+        c = _ModelConfig(cfg.l_max, cfg.e_width, cfg.layers, cfg.n_radial, cfg.r_cut, cfg.seed,
+                         int(cfg.gate_enabled), cfg.linear_precision)
+        self._h = C.c_void_p()
+        _check(lib().esg_model_create(ctx._h if ctx is not None else None, C.byref(c), C.c_int(len(z)), _p(z), _p(ns), _p(sh), C.byref(self._h)))
+        self.out_len = lib().esg_model_out_len(self._h)
+        self.n_params = lib().esg_model_param_count(self._h)
+
+    def set_precision(self, prec: int) -> None:
+        _check(lib().esg_model_set_precision(self._h, C.c_int(prec)))
+        self.cfg.linear_precision = prec
+
+    def init_params(self) -> None:
+        _check(lib().esg_model_init_params(self._h))
+
+    def entries(self):
+        out = []
+        for i in range(lib().esg_model_n_entries(self._h)):
+            name = C.c_char_p()
+            r, c, off = C.c_int(), C.c_int(), C.c_int64()
+            _check(lib().esg_model_entry(self._h, C.c_int(i), C.byref(name), C.byref(r), C.byref(c), C.byref(off)))
+            out.append((name.value.decode(), r.value, c.value, off.value))
+        return out
+
+    def params(self) -> np.ndarray:
+        p = np.zeros(self.n_params, np.float32)
+        _check(lib().esg_model_get_params(self._h, _p(p)))
+        return p
+
+    def set_params(self, p: np.ndarray) -> None:
+        p = np.ascontiguousarray(p, np.float32)
+        assert p.size == self.n_params
+        _check(lib().esg_model_set_params(self._h, _p(p)))
+
+    def param_hash(self) -> int:
+        return int(lib().esg_model_param_hash(self._h))
+
+    def prepare(self, g: Graph, species: np.ndarray, plan: Optional[CommPlan] = None) -> None:
+        sp = np.ascontiguousarray(species, np.int32)
+        _check(lib().esg_prepare(self._h, g._h, plan._h if plan is not None else None, _p(sp)))
+        info = np.zeros(3, np.int64)
+        _check(lib().esg_prepared_info(self._h, _p(info)))
+        self.n_rows, self.n_owned, self.n_edges = (int(x) for x in info)
+
+    def forward(self, copy_out: bool = True):
+        t = _Timing()
+        no = eo = None
+        if copy_out:
+            no = np.zeros((self.n_owned, self.out_len), np.float32)
+            eo = np.zeros((self.n_edges, self.out_len), np.float32)
+        _check(lib().esg_forward(self._h, _p(no), _p(eo), C.byref(t)))
+        return no, eo, Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches)
+
+    def forward_into(self, node_out: Optional[np.ndarray], edge_out: Optional[np.ndarray]) -> Timing:
+        """Forward with caller-owned (ideally pinned) host output buffers."""
+        t = _Timing()
+        _check(lib().esg_forward(self._h, _p(node_out), _p(edge_out), C.byref(t)))
+        return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches)
+
+    def device_outputs(self):
+        ptrs = [C.c_void_p() for _ in range(4)]
+        _check(lib().esg_forward_outputs(self._h, *[C.byref(p) for p in ptrs]))
+        return [p.value for p in ptrs]
+
+    def features(self):
+        H = (self.cfg.l_max + 1) ** 2
+        n = np.zeros((self.n_rows, H, self.cfg.e_width), np.float32)
+        e = np.zeros((self.n_edges, H, self.cfg.e_width), np.float32)
+        _check(lib().esg_features_export(self._h, _p(n), _p(e)))
+        return n, e
+
+    def blocks_uncoupled(self) -> np.ndarray:
+        n = C.c_int64()
+        _check(lib().esg_blocks_size(self._h, C.byref(n)))
+        out = np.zeros(n.value)
+        _check(lib().esg_blocks_uncoupled(self._h, _p(out)))
+        return out
+
+    def close(self) -> None:
+        if self._h:
+            lib().esg_model_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------- benchmark configs
+# SURVEY.md §8 "Config shorthand": l_max 4, E 16, 32 Gaussians, seed 1.
+SI, HF, O = 14, 72, 8
+BASIS_SI = {SI: [0, 0, 1, 1, 2]}
+BASIS_HFO2 = {HF: [0, 0, 1, 2], O: [0, 1]}
+
+
+def config_structure(name: str) -> tuple:
+    """Returns (structure, r_cut, layers, basis) for C1..C4."""
+    if name == "C1":
+        return make_jittered_lattice(512, 2.71, 0.30, [SI], 1), 8.0, 1, BASIS_SI
+    if name == "C2":
+        return make_jittered_lattice(3000, 2.20, 0.45, [HF, O, O], 2), 12.0, 3, BASIS_HFO2
+    if name == "C3":
+        return make_jittered_lattice(20000, 2.20, 0.45, [HF, O, O], 3), 12.0, 3, BASIS_HFO2
+    if name == "C4":
+        c2 = make_jittered_lattice(3000, 2.20, 0.45, [HF, O, O], 2)
+        return tile(c2, [4, 4, 4]), 10.0, 3, BASIS_HFO2
+    raise ValueError(name)

@@ -1,0 +1,278 @@
+"""ctypes wrapper of oracle/liboracle.so -- the CPU restatement of the
+reference (test infrastructure: only tests/, __graft_entry__.smoke() and
+bench.py's CPU-baseline legs may use it, and only as the checker)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Dict, List
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+_L = None
+
+
+def lib() -> C.CDLL:
+    global _L
+    if _L is None:
+        if not os.path.exists(ORACLE_SO):
+            subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True, capture_output=True)
+        L = C.CDLL(ORACLE_SO)
+        L.oracle_last_error.restype = C.c_char_p
+        L.oracle_build_graph.restype = C.c_int64
+        L.oracle_face_spacing.restype = C.c_double
+        L.oracle_model_create.restype = C.c_void_p
+        L.oracle_model_param_count.restype = C.c_int64
+        L.oracle_model_entry.restype = C.c_char_p
+        for f in ("oracle_model_destroy", "oracle_model_out_len", "oracle_model_n_entries",
+                  "oracle_model_params_f32", "oracle_model_params_f64", "oracle_model_set_params_f32",
+                  "oracle_forward_f32", "oracle_forward_f64", "oracle_uncoupled_block", "oracle_model_param_count",
+                  "oracle_model_entry"):
+            getattr(L, f).argtypes = None
+        _L = L
+    return _L
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _ok(rc):
+    if rc != 0:
+        raise RuntimeError(lib().oracle_last_error().decode())
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(C.c_int(n))
+
+
+def num_threads() -> int:
+    return lib().oracle_num_threads()
+
+
+def jittered_lattice(n, spacing, jitter, cycle, seed):
+    cyc = np.ascontiguousarray(cycle, np.int32)
+    pos = np.zeros((n, 3))
+    cell = np.zeros(9)
+    sp = np.zeros(n, np.int32)
+    _ok(lib().oracle_jittered_lattice(C.c_int(n), C.c_double(spacing), C.c_double(jitter), C.c_int(len(cyc)), _p(cyc),
+                                      C.c_uint64(seed), _p(pos), _p(cell), _p(sp)))
+    return pos, cell.reshape(3, 3), sp
+
+
+def tile(pos, cell, pbc, species, reps):
+    n = pos.shape[0] * int(np.prod(reps))
+    po = np.zeros((n, 3))
+    co = np.zeros(9)
+    so = np.zeros(n, np.int32)
+    _ok(lib().oracle_tile(C.c_int(pos.shape[0]), _p(np.ascontiguousarray(pos)), _p(np.ascontiguousarray(cell)),
+                          _p(np.ascontiguousarray(pbc, np.uint8)), _p(np.ascontiguousarray(species, np.int32)),
+                          _p(np.ascontiguousarray(reps, np.int32)), _p(po), _p(co), _p(so)))
+    return po, co.reshape(3, 3), so
+
+
+def wrap(pos, cell, pbc):
+    p = np.ascontiguousarray(pos, np.float64).copy()
+    _ok(lib().oracle_wrap(C.c_int(p.shape[0]), _p(p), _p(np.ascontiguousarray(cell)),
+                          _p(np.ascontiguousarray(pbc, np.uint8))))
+    return p
+
+
+def face_spacing(cell, d):
+    return lib().oracle_face_spacing(_p(np.ascontiguousarray(cell, np.float64)), C.c_int(d))
+
+
+def build_graph(pos, cell, pbc, r_cut) -> Dict[str, np.ndarray]:
+    E = lib().oracle_build_graph(C.c_int(pos.shape[0]), _p(np.ascontiguousarray(pos, np.float64)),
+                                 _p(np.ascontiguousarray(cell, np.float64)), _p(np.ascontiguousarray(pbc, np.uint8)),
+                                 C.c_double(r_cut))
+    if E < 0:
+        raise RuntimeError(lib().oracle_last_error().decode())
+    g = dict(src=np.zeros(E, np.int32), dst=np.zeros(E, np.int32), shift=np.zeros((E, 3), np.int32),
+             disp=np.zeros((E, 3)), dist=np.zeros(E))
+    lib().oracle_graph_export(_p(g["src"]), _p(g["dst"]), _p(g["shift"]), _p(g["disp"]), _p(g["dist"]))
+    return g
+
+
+def in_degrees(n, g):
+    return np.bincount(g["dst"], minlength=n).astype(np.int32)
+
+
+def lownn(pos, cell, pbc, deg, depth, r_cut):
+    out = np.zeros(pos.shape[0], np.int32)
+    _ok(lib().oracle_lownn(C.c_int(pos.shape[0]), _p(np.ascontiguousarray(pos, np.float64)),
+                           _p(np.ascontiguousarray(cell, np.float64)), _p(np.ascontiguousarray(pbc, np.uint8)),
+                           _p(np.ascontiguousarray(deg, np.int32)), C.c_int(depth), C.c_double(r_cut), _p(out)))
+    return out
+
+
+def comm_plan(n_nodes, src, dst, part, n_parts, rank):
+    E = len(src)
+    hdr = np.zeros(4, np.int32)
+    rg = np.zeros(n_nodes, np.int32)
+    ei = np.zeros(E, np.int32)
+    sr = np.zeros(E, np.int32)
+    dr = np.zeros(E, np.int32)
+    peer = np.zeros(n_parts, np.int32)
+    rr = np.zeros(n_parts, np.int32)
+    rc = np.zeros(n_parts, np.int32)
+    sc = np.zeros(n_parts, np.int32)
+    rows = np.zeros(E + n_nodes, np.int32)
+    _ok(lib().oracle_comm_plan(C.c_int(n_nodes), C.c_int64(E), _p(np.ascontiguousarray(src, np.int32)),
+                               _p(np.ascontiguousarray(dst, np.int32)), _p(np.ascontiguousarray(part, np.int32)),
+                               C.c_int(n_parts), C.c_int(rank), _p(hdr), _p(rg), _p(ei), _p(sr), _p(dr), _p(peer),
+                               _p(rr), _p(rc), _p(sc), _p(rows)))
+    n_rows, n_owned, ne, nn = (int(x) for x in hdr)
+    return dict(n_rows=n_rows, n_owned=n_owned, row_global=rg[:n_rows], edge_index=ei[:ne], src_row=sr[:ne],
+                dst_row=dr[:ne], nbr_peer=peer[:nn], nbr_recv_row=rr[:nn], nbr_recv_count=rc[:nn],
+                nbr_send_count=sc[:nn], send_rows=rows[:int(sc[:nn].sum())])
+
+
+def align_wigner(r, l_max):
+    R = np.zeros(9)
+    n = sum((2 * l + 1) ** 2 for l in range(l_max + 1))
+    D = np.zeros(n)
+    lib().oracle_align_wigner(_p(np.ascontiguousarray(r, np.float64)), C.c_int(l_max), _p(R), _p(D))
+    return R.reshape(3, 3), split_blocks(D, l_max)
+
+
+def wigner(R, l_max):
+    n = sum((2 * l + 1) ** 2 for l in range(l_max + 1))
+    D = np.zeros(n)
+    lib().oracle_wigner(_p(np.ascontiguousarray(R, np.float64)), C.c_int(l_max), _p(D))
+    return split_blocks(D, l_max)
+
+
+def split_blocks(D, l_max) -> List[np.ndarray]:
+    out, o = [], 0
+    for l in range(l_max + 1):
+        d = 2 * l + 1
+        out.append(D[o:o + d * d].reshape(d, d))
+        o += d * d
+    return out
+
+
+def real_sh(r, l_max):
+    y = np.zeros((l_max + 1) ** 2)
+    lib().oracle_real_sh(_p(np.ascontiguousarray(r, np.float64)), C.c_int(l_max), _p(y))
+    return y
+
+
+def coupling(la, lb, L):
+    out = np.zeros((2 * L + 1) * (2 * la + 1) * (2 * lb + 1))
+    _ok(lib().oracle_coupling(C.c_int(la), C.c_int(lb), C.c_int(L), _p(out)))
+    return out.reshape(2 * L + 1, (2 * la + 1) * (2 * lb + 1))
+
+
+def m_layout(l_max):
+    h = (l_max + 1) ** 2
+    to_m = np.zeros(h, np.int32)
+    to_l = np.zeros(h, np.int32)
+    mo = np.zeros(l_max + 1, np.int32)
+    lib().oracle_m_layout(C.c_int(l_max), _p(to_m), _p(to_l), _p(mo))
+    return to_m, to_l, mo
+
+
+class Model:
+    """Network<T> restatement: config + basis + seeded ParamStore."""
+
+    def __init__(self, l_max, e_width, layers, n_radial, r_cut, seed, basis: Dict[int, List[int]], gate=True):
+        zs = sorted(basis)
+        z = np.array(zs, np.int32)
+        ns = np.array([len(basis[k]) for k in zs], np.int32)
+        sh = np.array([l for k in zs for l in basis[k]], np.int32)
+        L = lib()
+        self.h = L.oracle_model_create(C.c_int(l_max), C.c_int(e_width), C.c_int(layers), C.c_int(n_radial),
+                                       C.c_double(r_cut), C.c_uint64(seed), C.c_int(int(gate)), C.c_int(len(z)), _p(z),
+                                       _p(ns), _p(sh))
+        if not self.h:
+            raise RuntimeError(L.oracle_last_error().decode())
+        self.l_max, self.e, self.layers = l_max, e_width, layers
+        self.H = (l_max + 1) ** 2
+        self.out_len = L.oracle_model_out_len(C.c_void_p(self.h))
+        self.n_params = L.oracle_model_param_count(C.c_void_p(self.h))
+
+    def __del__(self):
+        try:
+            lib().oracle_model_destroy(C.c_void_p(self.h))
+        except Exception:
+            pass
+
+    def entries(self):
+        out = []
+        for i in range(lib().oracle_model_n_entries(C.c_void_p(self.h))):
+            r, c, off = C.c_int(), C.c_int(), C.c_int64()
+            name = lib().oracle_model_entry(C.c_void_p(self.h), C.c_int(i), C.byref(r), C.byref(c), C.byref(off))
+            out.append((name.decode(), r.value, c.value, off.value))
+        return out
+
+    def params_f32(self):
+        p = np.zeros(self.n_params, np.float32)
+        lib().oracle_model_params_f32(C.c_void_p(self.h), _p(p))
+        return p
+
+    def params_f64(self):
+        p = np.zeros(self.n_params, np.float64)
+        lib().oracle_model_params_f64(C.c_void_p(self.h), _p(p))
+        return p
+
+    def set_params_f32(self, p):
+        lib().oracle_model_set_params_f32(C.c_void_p(self.h), _p(np.ascontiguousarray(p, np.float32)))
+
+    def _call(self, dtype, view, mode, nodes=None, edges=None, layer=0, node_block=0, node_out=None, edge_out=None):
+        f = lib().oracle_forward_f32 if dtype == np.float32 else lib().oracle_forward_f64
+        E = len(view["src_row"])
+        _ok(f(C.c_void_p(self.h), C.c_int(view["n_rows"]), C.c_int(view["n_owned"]),
+              _p(np.ascontiguousarray(view["row_species"], np.int32)), C.c_int64(E),
+              _p(np.ascontiguousarray(view["src_row"], np.int32)), _p(np.ascontiguousarray(view["dst_row"], np.int32)),
+              _p(np.ascontiguousarray(view["disp"], np.float64)), _p(np.ascontiguousarray(view["dist"], np.float64)),
+              C.c_int(mode), _p(nodes), _p(edges), C.c_int(layer), C.c_int(node_block), _p(node_out), _p(edge_out)))
+
+    def forward(self, view, dtype=np.float32, features=False):
+        """Serial forward (mode 0).  Returns node_out, edge_out[, nodes, edges]."""
+        E = len(view["src_row"])
+        no = np.zeros((view["n_owned"], self.out_len), dtype)
+        eo = np.zeros((E, self.out_len), dtype)
+        nodes = np.zeros((view["n_rows"], self.H, self.e), dtype) if features else None
+        edges = np.zeros((E, self.H, self.e), dtype) if features else None
+        self._call(dtype, view, 0, nodes, edges, node_out=no, edge_out=eo)
+        return (no, eo, nodes, edges) if features else (no, eo)
+
+    def init_tables(self, view, dtype=np.float32):
+        E = len(view["src_row"])
+        nodes = np.zeros((view["n_rows"], self.H, self.e), dtype)
+        edges = np.zeros((E, self.H, self.e), dtype)
+        self._call(dtype, view, 1, nodes, edges)
+        return nodes, edges
+
+    def block(self, view, nodes, edges, layer, node_block):
+        self._call(nodes.dtype.type, view, 2, nodes, edges, layer=layer, node_block=int(node_block))
+
+    def heads(self, view, nodes, edges):
+        E = len(view["src_row"])
+        no = np.zeros((view["n_owned"], self.out_len), nodes.dtype)
+        eo = np.zeros((E, self.out_len), nodes.dtype)
+        self._call(nodes.dtype.type, view, 3, nodes, edges, node_out=no, edge_out=eo)
+        return no, eo
+
+    def uncoupled_block(self, za, zb, row, n_orb_a, n_orb_b):
+        out = np.zeros(n_orb_a * n_orb_b)
+        _ok(lib().oracle_uncoupled_block(C.c_void_p(self.h), C.c_int(za), C.c_int(zb),
+                                         _p(np.ascontiguousarray(row, np.float32)), _p(out)))
+        return out.reshape(n_orb_a, n_orb_b)
+
+
+def serial_view(n, species, g):
+    """model::serial_view (graph_view.h:37-56) as plain arrays."""
+    return dict(n_rows=n, n_owned=n, row_species=np.asarray(species, np.int32), src_row=g["src"], dst_row=g["dst"],
+                disp=g["disp"], dist=g["dist"])
+
+
+def plan_view(plan, species, g):
+    ei = plan["edge_index"]
+    return dict(n_rows=plan["n_rows"], n_owned=plan["n_owned"],
+                row_species=np.asarray(species, np.int32)[plan["row_global"]], src_row=plan["src_row"],
+                dst_row=plan["dst_row"], disp=g["disp"][ei], dist=g["dist"][ei])

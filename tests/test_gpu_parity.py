@@ -1,0 +1,157 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle.
+
+Bars (SURVEY.md §8 / BASELINE.json north_star):
+  * graph (src, dst, shift) and fp64 displacement / distance: bit-exact
+  * partition assignments and comm plans from the GPU graph: bit-exact
+  * Hamiltonian heads, fp32 linears: max-abs error <= 2e-4 x max|ref| and
+    relative-L2 <= 2e-5 against the float oracle (stated fp32 tolerance)
+  * bf16 tcgen05 linears: relative-L2 <= 2e-2, max-abs <= 5e-2 x max|ref|
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2507_03840_b200 import esg
+
+pytestmark = pytest.mark.gpu
+
+SKEW = np.array([[6.0, 0.4, 0.0], [0.9, 5.5, 0.3], [0.2, 0.6, 6.5]])
+
+
+def same_graph(g, ref):
+    assert len(g["src"]) == len(ref["src"])
+    for k in ("src", "dst", "shift"):
+        assert np.array_equal(g[k], ref[k]), k
+    # bitwise fp64 equality (not allclose)
+    assert np.array_equal(g["disp"].view(np.uint64), ref["disp"].view(np.uint64))
+    assert np.array_equal(g["dist"].view(np.uint64), ref["dist"].view(np.uint64))
+
+
+@pytest.mark.parametrize("pbc", [(1, 1, 1), (0, 0, 0), (1, 0, 1)])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_graph_kat_random_skewed(gpu_ctx, pbc, seed):
+    rng = np.random.default_rng(seed)
+    pos = rng.random((8, 3)) @ SKEW
+    s = esg.AtomicStructure(pos, np.ones(8, np.int32), SKEW.copy(), np.array(pbc, bool))
+    g = esg.build_graph(gpu_ctx, s, 4.0).export()
+    same_graph(g, O.build_graph(pos, SKEW, np.array(pbc, np.uint8), 4.0))
+
+
+def test_graph_edge_cases(gpu_ctx):
+    two = esg.AtomicStructure(np.array([[0.0, 0, 0], [3.0, 0, 0]]), np.ones(2, np.int32), np.eye(3),
+                              np.zeros(3, bool))
+    assert esg.build_graph(gpu_ctx, two, 3.0).n_edges == 2  # inclusive cutoff
+    assert esg.build_graph(gpu_ctx, two, 2.9999999).n_edges == 0
+    one = esg.AtomicStructure(np.array([[1.0, 1, 1]]), np.array([6], np.int32), np.eye(3) * 2.0, np.ones(3, bool))
+    g = esg.build_graph(gpu_ctx, one, 2.5).export()
+    assert len(g["src"]) == 6 and np.allclose(g["dist"], 2.0)
+    lone = esg.AtomicStructure(np.array([[0.0, 0, 0], [50.0, 0, 0]]), np.ones(2, np.int32), np.eye(3),
+                               np.zeros(3, bool))
+    assert esg.build_graph(gpu_ctx, lone, 3.0).n_edges == 0  # empty graph
+    with pytest.raises(esg.UsageError):
+        esg.build_graph(gpu_ctx, two, -1.0)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_graph_configs_bit_exact(gpu_ctx, name):
+    s, r, _, _ = esg.config_structure(name)
+    g = esg.build_graph(gpu_ctx, s, r)
+    ref = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
+    same_graph(g.export(), ref)
+    # partitions from the GPU graph (depth 1..3) and every rank's plan
+    deg = g.in_degrees()
+    for depth in (1, 2, 3):
+        part = esg.lownn_partition(s, deg, depth, r)
+        assert np.array_equal(part, O.lownn(s.positions, s.cell, np.ones(3, np.uint8), deg, depth, r))
+        if name == "C1":
+            for rank in range(1 << depth):
+                got = esg.build_comm_plan(g, s.species, part, 1 << depth, rank).export()
+                want = O.comm_plan(s.n_atoms, ref["src"], ref["dst"], part, 1 << depth, rank)
+                for k in ("row_global", "edge_index", "src_row", "send_rows", "nbr_recv_row"):
+                    assert np.array_equal(got[k], want[k])
+
+
+def test_graph_tiling_x8(gpu_ctx):
+    s = esg.make_jittered_lattice(5, 2.0, 0.3, [1, 8], 13)
+    t = esg.tile(s, [2, 2, 2])
+    gs, gt = esg.build_graph(gpu_ctx, s, 4.0), esg.build_graph(gpu_ctx, t, 4.0)
+    assert gt.n_edges == 8 * gs.n_edges
+    assert np.array_equal(gt.in_degrees(), np.tile(gs.in_degrees(), 8))
+
+
+def run_both(ctx, s, r, layers, basis, l_max=4, e=16, prec=esg.LINEAR_FP32, dtype=np.float32):
+    cfg = esg.ModelConfig(l_max=l_max, e_width=e, layers=layers, n_radial=32, r_cut=r, seed=1,
+                          linear_precision=prec)
+    net = esg.Network(ctx, cfg, basis)
+    net.init_params()
+    g = esg.build_graph(ctx, s, r)
+    net.prepare(g, s.species)
+    no, eo, tm = net.forward()
+    ref = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
+    om = O.Model(l_max, e, layers, 32, r, 1, basis)
+    rno, reo = om.forward(O.serial_view(s.n_atoms, s.species, ref), dtype)
+    return net, (no, eo, tm), (rno, reo), om, ref
+
+
+def err(a, b):
+    scale = max(np.abs(b).max(), 1e-30)
+    return np.abs(a - b).max() / scale, np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+@pytest.mark.parametrize("l_max,e", [(4, 16), (2, 8)])
+def test_forward_fp32_small(gpu_ctx, l_max, e):
+    s = esg.make_jittered_lattice(40, 2.2, 0.45, [72, 8, 8], 4)
+    basis = esg.BASIS_HFO2 if l_max == 4 else {72: [0, 1], 8: [0, 1]}
+    net, (no, eo, tm), (rno, reo), _, _ = run_both(gpu_ctx, s, 4.5, 2, basis, l_max, e)
+    for got, want in ((no, rno), (eo, reo)):
+        mx, rl2 = err(got, want)
+        assert mx < 2e-4 and rl2 < 2e-5, (mx, rl2)
+    assert tm.gpu_launches > 0
+
+
+def test_forward_fp32_c1(gpu_ctx):
+    s, r, layers, basis = esg.config_structure("C1")
+    net, (no, eo, tm), (rno, reo), _, _ = run_both(gpu_ctx, s, r, layers, basis)
+    for got, want in ((no, rno), (eo, reo)):
+        mx, rl2 = err(got, want)
+        assert mx < 2e-4 and rl2 < 2e-5, (mx, rl2)
+    # deterministic: a second forward is bitwise identical
+    no2, eo2, _ = net.forward()
+    assert np.array_equal(no, no2) and np.array_equal(eo, eo2)
+
+
+def test_forward_bf16_tensor_cores(gpu_ctx):
+    s, r, layers, basis = esg.config_structure("C1")
+    net, (no, eo, tm), (rno, reo), _, _ = run_both(gpu_ctx, s, r, layers, basis, prec=esg.LINEAR_BF16)
+    for got, want in ((no, rno), (eo, reo)):
+        mx, rl2 = err(got, want)
+        assert mx < 5e-2 and rl2 < 2e-2, (mx, rl2)
+
+
+def test_uncoupled_blocks_match_oracle(gpu_ctx):
+    s = esg.make_jittered_lattice(40, 2.2, 0.45, [72, 8, 8], 4)
+    net, (no, eo, tm), _, om, ref = run_both(gpu_ctx, s, 4.5, 2, esg.BASIS_HFO2)
+    flat = net.blocks_uncoupled()
+    norb = {72: 10, 8: 4}
+    sp = s.species
+    at = 0
+    items = [(sp[i], sp[i], no[i]) for i in range(s.n_atoms)]
+    items += [(sp[a], sp[b], eo[k]) for k, (a, b) in enumerate(zip(ref["src"], ref["dst"]))]
+    for za, zb, row in items:
+        n = norb[za] * norb[zb]
+        want = om.uncoupled_block(za, zb, row, norb[za], norb[zb]).ravel()
+        assert np.abs(flat[at:at + n] - want).max() <= 1e-5 * max(1.0, np.abs(want).max())
+        at += n
+    assert at == flat.size
+
+
+def test_precision_switch_and_errors(gpu_ctx):
+    s = esg.make_jittered_lattice(20, 2.2, 0.45, [72, 8, 8], 4)
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=1, r_cut=4.5)
+    net = esg.Network(gpu_ctx, cfg, esg.BASIS_HFO2)
+    with pytest.raises(esg.UsageError):
+        net.forward()  # forward before prepare
+    net.init_params()
+    with pytest.raises(esg.DataError):  # species missing from the basis
+        g = esg.build_graph(gpu_ctx, s, 4.5)
+        net.prepare(g, np.full(20, 6, np.int32))
