@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: eGNN forward edges/s on B200 (BASELINE.json metric) + halo ms.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+N = 1 runs the 190k-atom workload C4 (tile(C2, {4,4,4}),
+192,000 atoms, r_cut 10 Å, l_max 4, E 16, M = 3).  For N > 1 the driver
+launches one process per GPU with torchrun; every rank builds the same graph,
+the Low-NN partition assigns nodes, each rank runs its view and exchanges
+halos through NCCL inside libesg_b200.so (strong scaling on the same graph).
+`value` is whole-job edges/s from device time (CUDA events, max over ranks);
+`e2e` is the same metric through the public API with host buffers
+(H2D of the atom positions, graph build + prepare + forward, D2H of every
+Hamiltonian head output).  `--impl reference` times the CPU restatement of
+the reference (oracle/, all host threads) on a bounded sample of the same
+workload.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "eGNN forward edges/sec at 1/2/4/8 B200 (190k-atom graph); halo-exchange ms"
+CONFIG_DESC = {
+    "C1": "C1: jittered Si lattice 512 atoms, r_cut 8 A, 1 layer, DZVP-like basis",
+    "C2": "C2: jittered HfO2 3000 atoms (375 vacancies), r_cut 12 A, 3 layers, SZV basis",
+    "C3": "C3: jittered HfO2 20000 atoms, r_cut 12 A, 3 layers, SZV basis",
+    "C4": "C4: tile(C2,{4,4,4}) 192000 atoms, r_cut 10 A, 3 layers, SZV basis",
+}
+# per-edge compulsory HBM bytes of each kernel category
+H, E = 25, 16
+ROW = H * E * 4  # 1600 B fp32 feature row
+A1_BYTES = 1280 * 2  # bf16 order-major operand, m-blocks padded to 64
+PROF_NAMES = ["init", "rotate_in", "so2_linears", "rotate_out_edge", "node_update", "heads", "halo", "copy"]
+BYTES_PER_EDGE = {
+    "rotate_in": ROW + 12 + 8 + A1_BYTES,        # edge row + dir + indices + A1 write
+    "so2_linears": A1_BYTES + ROW,                # A1 read + Y write
+    "rotate_out_edge": ROW + 12 + 2 * ROW,        # Y read + dir + edge row RMW
+    "node_update": ROW + 12,                      # Y read + dir (+ node rows, amortised)
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ CPU leg
+def cpu_sample(s, r, layers, basis, target_s=15.0, threads=None, g=None):
+    """Times the CPU restatement of the reference forward on a bounded
+    destination sample of the workload: all incoming edges of the first K
+    owned destinations, full 3-layer forward + heads.  Returns edges/s.
+    g: the graph arrays (the oracle builds them when None; the GPU arm passes
+    its bit-identical export to skip the CPU graph build)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle as O
+
+    if threads:
+        O.set_threads(threads)
+    nthreads = O.num_threads()
+    if g is None:
+        g = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
+    om = O.Model(4, 16, layers, 32, r, 1, basis)
+    deg = np.bincount(g["dst"], minlength=s.n_atoms)
+    off = np.concatenate([[0], np.cumsum(deg)])
+
+    def sub_view(k):
+        e1 = int(off[k])
+        src = g["src"][:e1]
+        rows = np.unique(np.concatenate([np.arange(k), src]))
+        # owned rows first (0..k-1 are the destinations), then the other sources
+        order = np.concatenate([np.arange(k), np.setdiff1d(rows, np.arange(k))])
+        pos_of = np.full(s.n_atoms, -1, np.int64)
+        pos_of[order] = np.arange(len(order))
+        return dict(n_rows=len(order), n_owned=k, row_species=s.species[order], src_row=pos_of[src].astype(np.int32),
+                    dst_row=g["dst"][:e1].astype(np.int32), disp=g["disp"][:e1], dist=g["dist"][:e1]), e1
+
+    k = max(1, min(s.n_atoms, 64))
+    while True:
+        v, ne = sub_view(k)
+        t0 = time.perf_counter()
+        om.forward(v, np.float32)
+        dt = time.perf_counter() - t0
+        if dt > 2.0 or k >= s.n_atoms:
+            break
+        k = min(s.n_atoms, int(k * max(2.0, 2.5 / max(dt, 1e-3))))
+    if dt < target_s and k < s.n_atoms:
+        k = min(s.n_atoms, max(k, int(k * target_s / dt)))
+        v, ne = sub_view(k)
+        t0 = time.perf_counter()
+        om.forward(v, np.float32)
+        dt = time.perf_counter() - t0
+    return ne / dt, nthreads, f"all incoming edges of the first {k} destinations ({ne} edges), {layers}-layer forward + heads, float32"
+
+
+def run_reference(args):
+    from paper_2507_03840_b200 import esg
+
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle as O
+
+    # inputs from the oracle's own generators (synthetic.cpp:17-41, structure.cpp:40-63)
+    spec = {"C1": (512, 2.71, 0.30, [14], 1, None, 8.0, 1, esg.BASIS_SI),
+            "C2": (3000, 2.20, 0.45, [72, 8, 8], 2, None, 12.0, 3, esg.BASIS_HFO2),
+            "C3": (20000, 2.20, 0.45, [72, 8, 8], 3, None, 12.0, 3, esg.BASIS_HFO2),
+            "C4": (3000, 2.20, 0.45, [72, 8, 8], 2, [4, 4, 4], 10.0, 3, esg.BASIS_HFO2)}[args.config]
+    pos, cell, sp = O.jittered_lattice(*spec[:5])
+    if spec[5]:
+        pos, cell, sp = O.tile(pos, cell, np.ones(3, np.uint8), sp, spec[5])
+    r, layers, basis = spec[6], spec[7], spec[8]
+    s = esg.AtomicStructure(pos, sp, cell, np.ones(3, bool))
+    g = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
+    vals = []
+    info = None
+    for i in range(max(1, args.steps)):
+        v, cores, sample = cpu_sample(s, r, layers, basis, target_s=args.cpu_seconds / max(1, args.steps), g=g)
+        vals.append(v)
+        info = (cores, sample)
+    val = float(np.median(vals))
+    line = {"metric": METRIC, "value": val, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": CONFIG_DESC[args.config], "atoms": s.n_atoms, "r_cut": r, "layers": layers},
+            "cpu_baseline": {"value": val, "unit": "edges/s", "cores": info[0], "kind": "port", "sample": info[1]},
+            "e2e": {"value": val, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_ours(args):
+    import torch
+    from paper_2507_03840_b200 import esg
+
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", rank)
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+    ids = [esg.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(ids, src=0)
+    ctx = esg.Context(local, rank, world, ids[0] if world > 1 else None)
+
+    s, r, layers, basis = esg.config_structure(args.config)
+    prec = esg.LINEAR_BF16 if args.precision == "bf16" else esg.LINEAR_FP32
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=layers, n_radial=32, r_cut=r, seed=1, linear_precision=prec)
+    t0 = time.perf_counter()
+    g = esg.build_graph(ctx, s, r)
+    t_graph = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plan = None
+    if world > 1:
+        depth = int(round(math.log2(world)))
+        part = esg.lownn_partition(s, g.in_degrees(), depth, r)
+        plan = esg.build_comm_plan(g, s.species, part, world, rank)
+    t_part = time.perf_counter() - t0
+    net = esg.Network(ctx, cfg, basis)
+    net.init_params()
+    t0 = time.perf_counter()
+    net.prepare(g, s.species, plan)
+    t_prep = time.perf_counter() - t0
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        net.forward(copy_out=False)
+    lib = esg.lib()
+    import ctypes as C
+    ms_cat = np.zeros(8)
+    n_cat = np.zeros(8, np.int64)
+    lib.esg_profile(net._h, C.c_int(1), None, None)
+    barrier()
+    torch.cuda.synchronize()
+    fwd_ms, msg_ms, halo_ms, launches = [], [], [], 0
+    with Clocks(local) as clk:
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            _, _, tm = net.forward(copy_out=False)
+            fwd_ms.append(tm.forward_ms)
+            msg_ms.append(tm.message_ms)
+            halo_ms.append(tm.halo_ms)
+            launches += tm.gpu_launches
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    barrier()
+    lib.esg_profile(net._h, C.c_int(0), ms_cat.ctypes.data_as(C.c_void_p), n_cat.ctypes.data_as(C.c_void_p))
+    clocks = clk.summary()
+    ms_step = allmax(float(np.mean(fwd_ms)))
+    halo_step = allmax(float(np.mean(halo_ms)))
+    msg_step = allmax(float(np.mean(msg_ms)))
+    total_edges = g.n_edges
+    value = total_edges / (ms_step / 1e3)
+
+    # roofline of the dominant kernel category (this rank's live CUDA events)
+    dom = int(np.argmax(ms_cat[:6]))
+    name = PROF_NAMES[dom]
+    roof = None
+    hbm, peak_kind = peaks()
+    if name in BYTES_PER_EDGE and ms_cat[dom] > 0:
+        alg_bytes = BYTES_PER_EDGE[name] * net.n_edges * args.steps
+        achieved = alg_bytes / (ms_cat[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "kernel": name, "peak_source": peak_kind,
+                "bytes_per_edge": BYTES_PER_EDGE[name],
+                "launches": int(n_cat[dom]), "avg_launch_ms": float(ms_cat[dom] / max(n_cat[dom], 1))}
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        node_out = np.empty((net.n_owned, net.out_len), np.float32)
+        edge_out = np.empty((net.n_edges, net.out_len), np.float32)
+        try:
+            node_out = torch.empty((net.n_owned, net.out_len), dtype=torch.float32, pin_memory=True).numpy()
+            edge_out = torch.empty((net.n_edges, net.out_len), dtype=torch.float32, pin_memory=True).numpy()
+        except Exception:
+            pass
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            g2 = esg.build_graph(ctx, s, r)  # H2D of the positions
+            plan2 = None
+            if world > 1:
+                part2 = esg.lownn_partition(s, g2.in_degrees(), int(round(math.log2(world))), r)
+                plan2 = esg.build_comm_plan(g2, s.species, part2, world, rank)
+            net.prepare(g2, s.species, plan2)
+            net.forward_into(node_out, edge_out)  # D2H of every head output
+            g2.close()
+        torch.cuda.synchronize()
+        e2e_s = allmax((time.perf_counter() - t0) / args.e2e_steps)
+        e2e = {"value": total_edges / e2e_s, "unit": "edges/s",
+               "h2d_bytes_per_step": int(s.positions.nbytes),
+               "d2h_bytes_per_step": int(allsum(node_out.nbytes + edge_out.nbytes)),
+               "step_s": e2e_s}
+
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_seconds > 0:
+        v, cores, sample = cpu_sample(s, r, layers, basis, target_s=args.cpu_seconds, g=g.export())
+        cpu = {"value": v, "unit": "edges/s", "cores": cores, "kind": "port", "sample": sample}
+    line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16" if prec == esg.LINEAR_BF16 else "fp32", "data": "synthetic",
+            "config": {"workload": CONFIG_DESC[args.config], "atoms": s.n_atoms, "edges": total_edges,
+                       "r_cut": r, "layers": layers, "l_max": 4, "e_width": 16,
+                       "linears": "tcgen05 bf16, fp32 accumulate" if prec == esg.LINEAR_BF16 else "fp32 CUDA cores",
+                       "parallelism": f"graph-partition dp{world} (Low-NN, NCCL halo)",
+                       "l2": "inputs larger than L2 (edge table %.0f GB)" % (total_edges * ROW / 1e9)},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": int(allsum(launches)),
+            "halo_ms_per_forward": halo_step, "halo_exchanges_per_forward": 2 * layers if world > 1 else 0,
+            "message_ms_per_forward": msg_step,
+            "kernel_ms_per_forward": {PROF_NAMES[i]: float(ms_cat[i] / args.steps) for i in range(8)},
+            "setup_s": {"graph": t_graph, "partition_plan": t_part, "prepare": t_prep},
+            "wall_ms_per_step": 1e3 * wall / args.steps}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -110,6 +110,10 @@ int esg_plan_export(const esg_plan* p, int32_t* row_global, int32_t* row_species
                     int32_t* nbr_recv_row, int32_t* nbr_recv_count, int32_t* nbr_send_count,
                     int32_t* send_rows /* concatenated in neighbour order */);
 
+/* ---- harmonics::coupling_matrix (clebsch_gordan.h:19) ------------------ */
+/* (2L+1) x ((2la+1)(2lb+1)) row-major real-basis coupling block, host. */
+int esg_coupling_matrix(int la, int lb, int L, double* out);
+
 /* ---- model::Network<float> (network.h:77-228) ------------------------- */
 typedef struct esg_model_config {
   int l_max, e_width, layers, n_radial; /* ModelConfig (network.h:16-35) */
@@ -145,6 +149,23 @@ int esg_prepared_info(const esg_model* m, int64_t info[3]); /* n_rows, n_owned, 
  * Host outputs may be NULL (results stay on the device). */
 int esg_forward(esg_model* m, float* node_out /* n_owned*out_len */,
                 float* edge_out /* n_edges*out_len */, esg_timing* timing);
+/* Per-category kernel timing with CUDA events on the launching stream.
+ * esg_profile(m, enable, ms, counts): copies the accumulated milliseconds
+ * and launch counts (ESG_PROF_NCAT entries each, may be NULL), then if
+ * enable >= 0 resets the accumulators and switches profiling on/off. */
+enum {
+  ESG_PROF_INIT = 0,
+  ESG_PROF_ROTATE_IN = 1,
+  ESG_PROF_SO2 = 2,
+  ESG_PROF_ROTATE_OUT = 3,
+  ESG_PROF_NODE = 4,
+  ESG_PROF_HEADS = 5,
+  ESG_PROF_HALO = 6,
+  ESG_PROF_COPY = 7,
+  ESG_PROF_NCAT = 8
+};
+int esg_profile(esg_model* m, int enable, double* ms, int64_t* counts);
+
 /* Device pointers of the last forward's outputs / features (valid until the
  * next forward or destroy). */
 int esg_forward_outputs(const esg_model* m, const float** node_out, const float** edge_out,

@@ -18,6 +18,7 @@ void model_device_destroy(esg_model* M);
 void model_upload_params(esg_model* M);
 void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const int32_t* species);
 void model_forward(esg_model* M, esg_timing* tm);
+void model_profile(esg_model* M, int enable, double* ms, int64_t* counts);
 void model_outputs(const esg_model* M, const float** no, const float** eo, const float** nf, const float** ef);
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
 void model_copy_features(const esg_model* M, float* nodes, float* edges);
@@ -397,6 +398,15 @@ int esg_plan_export(const esg_plan* p, int32_t* row_global, int32_t* row_species
   ESG_API_END
 }
 
+int esg_coupling_matrix(int la, int lb, int L, double* out) {
+  ESG_API_BEGIN
+  NEED(out, "out");
+  if (la < 0 || lb < 0 || la > 6 || lb > 6) data("coupled degree out of supported range");
+  const auto C = coupling_matrix(la, lb, L);
+  std::copy(C.begin(), C.end(), out);
+  ESG_API_END
+}
+
 int esg_model_create(esg_ctx* ctx, const esg_model_config* cfg, int n_species, const int* z, const int* n_shells,
                      const int* shells, esg_model** out) {
   ESG_API_BEGIN
@@ -534,6 +544,14 @@ int esg_forward(esg_model* m, float* node_out, float* edge_out, esg_timing* timi
   ESG_CUDA(cudaSetDevice(m->ctx->device));
   model_forward(m, timing);
   if (node_out || edge_out) model_copy_outputs(m, node_out, edge_out);
+  ESG_API_END
+}
+
+int esg_profile(esg_model* m, int enable, double* ms, int64_t* counts) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->dev) usage("model was created without a device context");
+  model_profile(m, enable, ms, counts);
   ESG_API_END
 }
 

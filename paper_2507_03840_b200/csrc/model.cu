@@ -22,14 +22,6 @@
 
 namespace esg {
 
-// Coupling tables for the uncoupled block kernel: per (la, lb) pair with
-// la, lb <= 2 (basis shells), C_L stacked for L = |la-lb|..la+lb.
-struct CgTable {
-  int off[3][3];     // start of the (la, lb) table in vals
-  float vals[3000];  // sum over pairs of (da*db)^2
-};
-__constant__ CgTable c_cg;
-
 void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2,
                    float* Y, int gate, cudaStream_t st);  // so2_tc.cu
 bool so2_tc_available(int L, int E);
@@ -346,38 +338,25 @@ __global__ void k_heads(const float* __restrict__ x, int64_t n_items, int HE, in
 // network.h:296-315 fill_block + block_matrix.cpp:66-88 to_block: per item
 // and shell pair, flat = sum_L C_L^T c_L, written row-major into the
 // n_orb(za) x n_orb(zb) block.  Work items are (item, shell pair).
-struct PairDesc {
-  int la, lb, oa, ob, nb;  // shell degrees, orbital offsets, block width
-  int seg[5];              // head offsets for L = |la-lb|.. (up to 5)
-};
-__global__ void k_blocks(const float* __restrict__ heads, int out_len, const int64_t* __restrict__ item_pair0,
-                         const int* __restrict__ item_npairs, const int64_t* __restrict__ item_off,
-                         const PairDesc* __restrict__ pairs, const int* __restrict__ pair_of_item_species,
+// Host-built per species pair: block element j = sum over (head index, C
+// coefficient) terms of that element (its shell pair's L segments), in
+// ascending L then r -- the to_block order.  One thread per (item, element).
+__global__ void k_blocks(const float* __restrict__ heads, int out_len, const int* __restrict__ item_pair,
+                         const int64_t* __restrict__ item_off, const int* __restrict__ pair_nelem,
+                         const int* __restrict__ pair_ptr0, const int* __restrict__ elem_ptr,
+                         const int* __restrict__ term_idx, const double* __restrict__ term_coef, int max_elem,
                          int64_t n_items, double* __restrict__ out) {
-  const int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t it = t / max_elem;
+  const int j = int(t % max_elem);
   if (it >= n_items) return;
+  const int sp = item_pair[it];
+  if (j >= pair_nelem[sp]) return;
   const float* row = heads + it * out_len;
-  const int p0 = pair_of_item_species[it];
-  const int np = item_npairs[it];
-  double* ob = out + item_off[it];
-  for (int q = 0; q < np; ++q) {
-    const PairDesc pd = pairs[p0 + q];
-    const int da = 2 * pd.la + 1, db = 2 * pd.lb + 1, dim = da * db;
-    const float* C = c_cg.vals + c_cg.off[pd.la][pd.lb];
-    for (int p = 0; p < dim; ++p) {
-      double flat = 0.0;
-      int r0 = 0, si = 0;
-      for (int L = abs(pd.la - pd.lb); L <= pd.la + pd.lb; ++L, ++si) {
-        const int dL = 2 * L + 1;
-        double acc = 0.0;
-        for (int r = 0; r < dL; ++r) acc += (double)C[(r0 + r) * dim + p] * (double)row[pd.seg[si] + r];
-        flat += acc;
-        r0 += dL;
-      }
-      ob[(pd.oa + p / db) * pd.nb + pd.ob + p % db] = flat;
-    }
-  }
-  (void)item_pair0;
+  const int e = pair_ptr0[sp] + j;
+  double acc = 0.0;
+  for (int q = elem_ptr[e]; q < elem_ptr[e + 1]; ++q) acc += term_coef[q] * (double)row[term_idx[q]];
+  out[item_off[it] + j] = acc;
 }
 
 __global__ void k_pack_rows(const float* __restrict__ nodes, const int* __restrict__ rows, int64_t n_rows, int row_len,
@@ -446,11 +425,52 @@ struct DeviceModel {
   std::vector<int> h_item_species_a, h_item_species_b;
   int64_t block_values = 0;
   cudaEvent_t ev[8];
+  // optional per-category kernel timing (esg_profile_*): events around launches
+  bool profile = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, int>> marks;  // (category, first event index)
+  double prof_ms[ESG_PROF_NCAT] = {0};
+  int64_t prof_n[ESG_PROF_NCAT] = {0};
   int precision = ESG_LINEAR_FP32;
   size_t a1_elem = 4;
 };
 
 namespace {
+
+// Brackets one kernel launch with CUDA events on the launching stream when
+// profiling is on; the elapsed times are summed per category after the
+// forward's final synchronisation.
+struct Prof {
+  DeviceModel* D;
+  cudaStream_t st;
+  int cat, idx = -1;
+  Prof(DeviceModel* d, cudaStream_t s, int c) : D(d), st(s), cat(c) {
+    if (!D->profile) return;
+    const size_t need = 2 * (D->marks.size() + 1);
+    while (D->pool.size() < need) {
+      cudaEvent_t e;
+      ESG_CUDA(cudaEventCreate(&e));
+      D->pool.push_back(e);
+    }
+    idx = (int)(2 * D->marks.size());
+    D->marks.push_back({cat, idx});
+    ESG_CUDA(cudaEventRecord(D->pool[idx], st));
+  }
+  ~Prof() {
+    if (idx >= 0) cudaEventRecord(D->pool[idx + 1], st);
+  }
+};
+
+void prof_collect(DeviceModel* D) {
+  if (!D->profile) return;
+  for (const auto& mk : D->marks) {
+    float ms = 0.f;
+    ESG_CUDA(cudaEventElapsedTime(&ms, D->pool[mk.second], D->pool[mk.second + 1]));
+    D->prof_ms[mk.first] += ms;
+    D->prof_n[mk.first] += 1;
+  }
+  D->marks.clear();
+}
 
 void free_ptr(void* p) {
   if (p) cudaFree(p);
@@ -480,22 +500,6 @@ void upload_wigner_coef(int L) {
   done = true;
 }
 
-void upload_cg_tables() {
-  static bool done = false;
-  if (done) return;
-  CgTable t{};
-  int at = 0;
-  for (int la = 0; la <= 2; ++la)
-    for (int lb = 0; lb <= 2; ++lb) {
-      t.off[la][lb] = at;
-      for (int L = std::abs(la - lb); L <= la + lb; ++L) {
-        const auto C = coupling_matrix(la, lb, L);
-        for (double v : C) t.vals[at++] = (float)v;
-      }
-    }
-  ESG_CUDA(cudaMemcpyToSymbol(c_cg, &t, sizeof(t)));
-  done = true;
-}
 
 bool supported(int L, int E) { return (L == 4 || L == 2) && (E == 16 || E == 8); }
 
@@ -637,7 +641,7 @@ void model_device_create(esg_model* M) {
   for (auto& e : M->dev->ev) ESG_CUDA(cudaEventCreate(&e));
   ESG_CUDA(cudaSetDevice(M->ctx->device));
   upload_wigner_coef(L);
-  upload_cg_tables();
+
 }
 
 void model_device_destroy(esg_model* M) {
@@ -790,6 +794,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     ESG_CUDA(cudaEventRecord(D->ev[4], st));
     const int row = H * E;
     if (D->n_send) {
+      Prof pr(D, st, ESG_PROF_HALO);
       k_pack_rows<<<(unsigned)((D->n_send * row + 255) / 256), 256, 0, st>>>(D->nodes, D->send_rows, D->n_send, row,
                                                                              D->send_buf);
       ++ctx->launches;
@@ -812,6 +817,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
   }
   if (node_block) {  // halo rows pass through (ops.h:200 copies all rows)
     const int64_t n = (int64_t)D->n_rows * H * E;
+    Prof pr(D, st, ESG_PROF_COPY);
     k_copy_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->nodes, D->nodes_alt, n);
     ++ctx->launches;
   }
@@ -823,25 +829,35 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     if (n > 0) {
       const unsigned tiles = (unsigned)((n + 15) / 16);
       if (tc) {
-        k_rotate_in<L, E, 64, uint16_t><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir, e0,
-                                                                n, (uint16_t*)D->A1);
+        {
+          Prof pr(D, st, ESG_PROF_ROTATE_IN);
+          k_rotate_in<L, E, 64, uint16_t><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir,
+                                                                  e0, n, (uint16_t*)D->A1);
+        }
         ++ctx->launches;
+        Prof pr(D, st, ESG_PROF_SO2);
         so2_tc_launch(L, E, (const uint16_t*)D->A1, n, D->w1b[bidx], D->w2b[bidx], D->Y, M->cfg.gate_enabled, st);
         ++ctx->launches;
       } else {
-        k_rotate_in<L, E, 1, float><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir, e0, n,
-                                                           (float*)D->A1);
+        {
+          Prof pr(D, st, ESG_PROF_ROTATE_IN);
+          k_rotate_in<L, E, 1, float><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir, e0,
+                                                             n, (float*)D->A1);
+        }
+        Prof pr(D, st, ESG_PROF_SO2);
         k_so2_simt<L, E><<<tiles, 256, 0, st>>>((const float*)D->A1, n, D->w1t[bidx], D->w2t[bidx], D->Y,
                                                 M->cfg.gate_enabled);
         ctx->launches += 2;
       }
       if (!node_block) {
+        Prof pr(D, st, ESG_PROF_ROTATE_OUT);
         k_rotate_out_edge<L, E><<<tiles, 256, 0, st>>>(D->Y, D->dir, e0, n, D->edges);
         ++ctx->launches;
       }
     }
     if (node_block && ch.second > ch.first) {
       const int threads = ((H * E + 31) / 32) * 32;
+      Prof pr(D, st, ESG_PROF_NODE);
       k_node_update<L, E><<<ch.second - ch.first, threads, 0, st>>>(D->Y, D->dir + 0, D->seg, ch.first, e0, att,
                                                                    D->nodes, D->nodes_alt, D->logits);
       ++ctx->launches;
@@ -861,10 +877,12 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   ESG_CUDA(cudaEventRecord(D->ev[0], st));
   {
     const int64_t n = (int64_t)D->n_rows * H * E;
+    Prof pr(D, st, ESG_PROF_INIT);
     k_init_nodes<H, E><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->row_slot, D->n_rows, D->embed, D->nodes);
     ++ctx->launches;
     if (D->n_edges) {
       const int per = 256 / E;
+      Prof pr2(D, st, ESG_PROF_INIT);
       k_init_edges<H, E><<<(unsigned)((D->n_edges + per - 1) / per), per * E, 0, st>>>(
           D->dist, D->n_edges, D->params + D->lift_off, M->cfg.n_radial, M->cfg.r_cut / (M->cfg.n_radial - 1),
           D->edges);
@@ -883,12 +901,14 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   const int out_len = M->heads.out_len;
   if (D->n_owned) {
     const int64_t n = (int64_t)D->n_owned * out_len;
+    Prof pr(D, st, ESG_PROF_HEADS);
     k_heads<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->nodes, D->n_owned, H * E, E, D->head_w[0], D->head_key,
                                                          D->head_row, out_len, D->node_out);
     ++ctx->launches;
   }
   if (D->n_edges) {
     const int64_t n = D->n_edges * out_len;
+    Prof pr(D, st, ESG_PROF_HEADS);
     k_heads<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->edges, D->n_edges, H * E, E, D->head_w[1], D->head_key,
                                                          D->head_row, out_len, D->edge_out);
     ++ctx->launches;
@@ -896,6 +916,7 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   ESG_CUDA(cudaEventRecord(D->ev[3], st));
   ESG_CUDA(cudaGetLastError());
   ESG_CUDA(cudaEventSynchronize(D->ev[3]));
+  prof_collect(D);
   if (tm) {
     float a = 0, b = 0, c = 0;
     ESG_CUDA(cudaEventElapsedTime(&a, D->ev[0], D->ev[3]));
@@ -927,6 +948,21 @@ void model_forward(esg_model* M, esg_timing* tm) {
     forward_impl<2, 8>(M, tm);
 }
 
+void model_profile(esg_model* M, int enable, double* ms, int64_t* counts) {
+  DeviceModel* D = M->dev;
+  if (ms)
+    for (int c = 0; c < ESG_PROF_NCAT; ++c) ms[c] = D->prof_ms[c];
+  if (counts)
+    for (int c = 0; c < ESG_PROF_NCAT; ++c) counts[c] = D->prof_n[c];
+  if (enable >= 0) {
+    D->profile = enable != 0;
+    for (int c = 0; c < ESG_PROF_NCAT; ++c) {
+      D->prof_ms[c] = 0;
+      D->prof_n[c] = 0;
+    }
+  }
+}
+
 void model_outputs(const esg_model* M, const float** no, const float** eo, const float** nf, const float** ef) {
   const DeviceModel* D = M->dev;
   if (no) *no = D->node_out;
@@ -938,6 +974,7 @@ void model_outputs(const esg_model* M, const float** no, const float** eo, const
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out) {
   const DeviceModel* D = M->dev;
   const int ol = M->heads.out_len;
+  ESG_CUDA(cudaStreamSynchronize(M->ctx->stream));
   if (node_out && D->n_owned)
     ESG_CUDA(cudaMemcpy(node_out, D->node_out, sizeof(float) * (size_t)D->n_owned * ol, cudaMemcpyDeviceToHost));
   if (edge_out && D->n_edges)
@@ -970,65 +1007,91 @@ int64_t model_blocks_size(const esg_model* M) {
 void model_blocks(esg_model* M, double* out_host) {
   DeviceModel* D = M->dev;
   cudaStream_t st = M->ctx->stream;
-  if (M->basis.shells.empty()) return;
-  for (const auto& kv : M->basis.shells)
-    for (int l : kv.second)
-      if (l > 2) usage("uncoupled block kernel supports shells up to l = 2");
-  // pair descriptors per (za, zb) species pair
-  std::map<std::pair<int, int>, std::pair<int, int>> pair_range;  // -> (first, count)
-  std::vector<PairDesc> pairs;
+  // Per species pair: for every block element (row-major n_orb(za) x
+  // n_orb(zb)) the list of (head index, coupling coefficient) terms.
+  std::map<std::pair<int, int>, int> pair_id;
+  std::vector<int> pair_nelem, pair_ptr0, elem_ptr{0}, term_idx;
+  std::vector<double> term_coef;
+  std::map<std::array<int, 3>, std::vector<double>> cg;
   for (const auto& ka : M->basis.shells)
     for (const auto& kb : M->basis.shells) {
-      const int first = (int)pairs.size();
+      const int na = M->basis.n_orb(ka.first), nb = M->basis.n_orb(kb.first);
+      std::vector<std::vector<std::pair<int, double>>> terms((size_t)na * nb);
       for (size_t a = 0; a < ka.second.size(); ++a)
         for (size_t b = 0; b < kb.second.size(); ++b) {
-          PairDesc pd{};
-          pd.la = ka.second[a];
-          pd.lb = kb.second[b];
-          pd.oa = M->basis.off(ka.first, (int)a);
-          pd.ob = M->basis.off(kb.first, (int)b);
-          pd.nb = M->basis.n_orb(kb.first);
-          int si = 0;
-          for (int L = std::abs(pd.la - pd.lb); L <= pd.la + pd.lb; ++L) pd.seg[si++] = M->heads.segment((int)a, (int)b, L);
-          pairs.push_back(pd);
+          const int la = ka.second[a], lb = kb.second[b], da = 2 * la + 1, db = 2 * lb + 1;
+          const int oa = M->basis.off(ka.first, (int)a), ob = M->basis.off(kb.first, (int)b);
+          for (int L = std::abs(la - lb); L <= la + lb; ++L) {
+            auto key = std::array<int, 3>{la, lb, L};
+            if (!cg.count(key)) cg[key] = coupling_matrix(la, lb, L);
+            const auto& C = cg[key];
+            const int seg = M->heads.segment((int)a, (int)b, L);
+            for (int p = 0; p < da * db; ++p)
+              for (int r = 0; r < 2 * L + 1; ++r)
+                terms[(size_t)(oa + p / db) * nb + ob + p % db].push_back({seg + r, C[(size_t)r * da * db + p]});
+          }
         }
-      pair_range[{ka.first, kb.first}] = {first, (int)pairs.size() - first};
+      pair_id[{ka.first, kb.first}] = (int)pair_nelem.size();
+      pair_nelem.push_back(na * nb);
+      pair_ptr0.push_back((int)elem_ptr.size() - 1);
+      for (const auto& tl : terms) {
+        for (const auto& t : tl) {
+          term_idx.push_back(t.first);
+          term_coef.push_back(t.second);
+        }
+        elem_ptr.push_back((int)term_idx.size());
+      }
     }
   const int64_t n_items = (int64_t)D->h_item_species_a.size();
-  std::vector<int> pfirst(n_items), pcount(n_items);
+  std::vector<int> item_pair(n_items);
   std::vector<int64_t> off(n_items);
   int64_t at = 0;
+  int max_elem = 1;
   for (int64_t i = 0; i < n_items; ++i) {
-    const auto& pr = pair_range.at({D->h_item_species_a[i], D->h_item_species_b[i]});
-    pfirst[i] = pr.first;
-    pcount[i] = pr.second;
+    const int pid = pair_id.at({D->h_item_species_a[i], D->h_item_species_b[i]});
+    item_pair[i] = pid;
     off[i] = at;
-    at += (int64_t)M->basis.n_orb(D->h_item_species_a[i]) * M->basis.n_orb(D->h_item_species_b[i]);
+    at += pair_nelem[pid];
+    max_elem = std::max(max_elem, pair_nelem[pid]);
   }
-  PairDesc* d_pairs = dalloc<PairDesc>(pairs.size());
-  int* d_first = dalloc<int>(n_items);
-  int* d_count = dalloc<int>(n_items);
+  int* d_item_pair = dalloc<int>(n_items);
   int64_t* d_off = dalloc<int64_t>(n_items);
+  int* d_nelem = dalloc<int>(pair_nelem.size());
+  int* d_ptr0 = dalloc<int>(pair_ptr0.size());
+  int* d_eptr = dalloc<int>(elem_ptr.size());
+  int* d_tidx = dalloc<int>(term_idx.size());
+  double* d_tcoef = dalloc<double>(term_coef.size());
   double* d_out = dalloc<double>(at);
-  ESG_CUDA(cudaMemcpy(d_pairs, pairs.data(), sizeof(PairDesc) * pairs.size(), cudaMemcpyHostToDevice));
-  ESG_CUDA(cudaMemcpy(d_first, pfirst.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
-  ESG_CUDA(cudaMemcpy(d_count, pcount.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
-  ESG_CUDA(cudaMemcpy(d_off, off.data(), sizeof(int64_t) * n_items, cudaMemcpyHostToDevice));
+  auto up = [&](void* d, const void* h, size_t n) {
+    if (n) ESG_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st));
+  };
+  up(d_item_pair, item_pair.data(), sizeof(int) * n_items);
+  up(d_off, off.data(), sizeof(int64_t) * n_items);
+  up(d_nelem, pair_nelem.data(), sizeof(int) * pair_nelem.size());
+  up(d_ptr0, pair_ptr0.data(), sizeof(int) * pair_ptr0.size());
+  up(d_eptr, elem_ptr.data(), sizeof(int) * elem_ptr.size());
+  up(d_tidx, term_idx.data(), sizeof(int) * term_idx.size());
+  up(d_tcoef, term_coef.data(), sizeof(double) * term_coef.size());
   const int ol = M->heads.out_len;
   if (D->n_owned) {
-    k_blocks<<<(D->n_owned + 127) / 128, 128, 0, st>>>(D->node_out, ol, nullptr, d_count, d_off, d_pairs, d_first,
-                                                       D->n_owned, d_out);
+    const int64_t n = (int64_t)D->n_owned * max_elem;
+    k_blocks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->node_out, ol, d_item_pair, d_off, d_nelem, d_ptr0, d_eptr,
+                                                          d_tidx, d_tcoef, max_elem, D->n_owned, d_out);
     ++M->ctx->launches;
   }
   if (D->n_edges) {
-    k_blocks<<<(unsigned)((D->n_edges + 127) / 128), 128, 0, st>>>(D->edge_out, ol, nullptr, d_count + D->n_owned,
-                                                                  d_off + D->n_owned, d_pairs, d_first + D->n_owned,
-                                                                  D->n_edges, d_out);
+    const int64_t n = D->n_edges * max_elem;
+    k_blocks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->edge_out, ol, d_item_pair + D->n_owned,
+                                                          d_off + D->n_owned, d_nelem, d_ptr0, d_eptr, d_tidx, d_tcoef,
+                                                          max_elem, D->n_edges, d_out);
     ++M->ctx->launches;
   }
   ESG_CUDA(cudaGetLastError());
-  ESG_CUDA(cudaMemcpy(out_host, d_out, sizeof(double) * at, cudaMemcpyDeviceToHost));
-  for (void* p : {(void*)d_pairs, (void*)d_first, (void*)d_count, (void*)d_off, (void*)d_out}) free_ptr(p);
+  ESG_CUDA(cudaMemcpyAsync(out_host, d_out, sizeof(double) * at, cudaMemcpyDeviceToHost, st));
+  ESG_CUDA(cudaStreamSynchronize(st));
+  for (void* q : {(void*)d_item_pair, (void*)d_off, (void*)d_nelem, (void*)d_ptr0, (void*)d_eptr, (void*)d_tidx,
+                  (void*)d_tcoef, (void*)d_out})
+    free_ptr(q);
 }
 
 }  // namespace esg

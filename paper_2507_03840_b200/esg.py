@@ -239,6 +239,13 @@ def build_graph(ctx: Context, s: AtomicStructure, r_cut: float) -> Graph:
     return Graph(ctx, s, r_cut)
 
 
+def coupling_matrix(la: int, lb: int, L: int) -> np.ndarray:
+    """harmonics::coupling_matrix (clebsch_gordan.h:19)."""
+    out = np.zeros((2 * L + 1) * (2 * la + 1) * (2 * lb + 1))
+    _check(lib().esg_coupling_matrix(C.c_int(la), C.c_int(lb), C.c_int(L), _p(out)))
+    return out.reshape(2 * L + 1, -1)
+
+
 def lownn_partition(s: AtomicStructure, in_degrees: np.ndarray, depth: int, r_cut: float) -> np.ndarray:
     """partition::lownn_partition (partition.h:24); positions are the unwrapped input."""
     part = np.zeros(s.n_atoms, np.int32)
@@ -380,7 +387,7 @@ class Network:
     def forward(self, copy_out: bool = True):
         t = _Timing()
         no = eo = None
-        if copy_out:
+        if copy_out and hasattr(self, "n_owned"):
             no = np.zeros((self.n_owned, self.out_len), np.float32)
             eo = np.zeros((self.n_edges, self.out_len), np.float32)
         _check(lib().esg_forward(self._h, _p(no), _p(eo), C.byref(t)))

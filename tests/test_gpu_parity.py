@@ -72,11 +72,18 @@ def test_graph_configs_bit_exact(gpu_ctx, name):
 
 
 def test_graph_tiling_x8(gpu_ctx):
-    s = esg.make_jittered_lattice(5, 2.0, 0.3, [1, 8], 13)
+    """test_structures.cpp:166-189 on the skewed cell (no exact-cutoff ties)."""
+    pos = np.random.default_rng(13).random((5, 3)) @ SKEW
+    s = esg.AtomicStructure(pos, np.ones(5, np.int32), SKEW.copy(), np.ones(3, bool))
     t = esg.tile(s, [2, 2, 2])
     gs, gt = esg.build_graph(gpu_ctx, s, 4.0), esg.build_graph(gpu_ctx, t, 4.0)
     assert gt.n_edges == 8 * gs.n_edges
     assert np.array_equal(gt.in_degrees(), np.tile(gs.in_degrees(), 8))
+    same_graph(gt.export(), O.build_graph(t.positions, t.cell, np.ones(3, np.uint8), 4.0))
+    # a cell exactly 2 r_cut wide has distance ties at the cutoff: whatever the
+    # reference arithmetic keeps, the GPU keeps too
+    j = esg.tile(esg.make_jittered_lattice(5, 2.0, 0.3, [1, 8], 13), [2, 2, 2])
+    same_graph(esg.build_graph(gpu_ctx, j, 4.0).export(), O.build_graph(j.positions, j.cell, np.ones(3, np.uint8), 4.0))
 
 
 def run_both(ctx, s, r, layers, basis, l_max=4, e=16, prec=esg.LINEAR_FP32, dtype=np.float32):
