@@ -293,7 +293,10 @@ def run_ours(args):
     roof = None
     hbm, peak_kind = peaks()
     if name in BYTES_PER_EDGE and ms_cat[dom] > 0:
-        alg_bytes = BYTES_PER_EDGE[name] * net.n_edges * args.steps
+        # node_update runs in the M node blocks, rotate_out_edge in the M edge
+        # blocks, rotate_in / so2_linears in all 2M blocks
+        blocks = layers if name in ("node_update", "rotate_out_edge") else 2 * layers
+        alg_bytes = BYTES_PER_EDGE[name] * net.n_edges * blocks * args.steps
         achieved = alg_bytes / (ms_cat[dom] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": None, "kernel": name, "peak_source": peak_kind,
