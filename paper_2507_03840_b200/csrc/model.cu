@@ -19,6 +19,7 @@
 
 #include "esg_internal.h"
 #include "model_kernels.cuh"
+#include "msg_kernels.cuh"
 
 namespace esg {
 
@@ -73,54 +74,6 @@ __global__ void k_init_edges(const double* __restrict__ dist, int64_t n_e, const
   float* row = edges + k * (H * E);
   row[c] = acc;
   for (int q = E + c; q < H * E; q += E) row[q] = 0.f;
-}
-
-// ----------------------------------------------------------- rotate in
-template <int L, int E, int KPAD, typename OutT>
-__global__ void __launch_bounds__(256) k_rotate_in(const float* __restrict__ nodes, const float* __restrict__ edges,
-                                                   const int* __restrict__ src_row, const int* __restrict__ dst_row,
-                                                   const float* __restrict__ dir, int64_t e0, int64_t n_e,
-                                                   OutT* __restrict__ A1) {
-  using G = Geo<L>;
-  using Y = Lay1<L, E, KPAD>;
-  constexpr int TE = 16, DSP = G::DS + 1, H = G::H, C3 = 3 * E;
-  __shared__ float sD[TE * DSP];
-  __shared__ float sdir[TE * 3];
-  const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
-  const int ne = (int)cmin64(TE, e0 + n_e - t0);
-  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
-  __syncthreads();
-  wigner_tile<L, DSP>(sdir, ne, sD);
-  for (int idx = threadIdx.x; idx < ne * C3; idx += blockDim.x) {
-    const int e = idx / C3, c = idx % C3, p = c / E, cc = c % E;
-    const int64_t k = t0 + e;
-    const float* base = p == 0 ? nodes + (int64_t)src_row[k] * H * E
-                               : (p == 1 ? nodes + (int64_t)dst_row[k] * H * E : edges + k * H * E);
-    float x[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) x[h] = base[h * E + cc];
-    const float* D = sD + e * DSP;
-    OutT* out = A1 + (k - e0) * Y::KTOT;
-#pragma unroll
-    for (int l = 0; l <= L; ++l) {
-      const int dd = 2 * l + 1;
-#pragma unroll
-      for (int a = -l; a <= l; ++a) {
-        float acc = 0.f;
-#pragma unroll
-        for (int b = -l; b <= l; ++b) acc = fmaf(D[G::doff(l) + (a + l) * dd + (b + l)], x[l * l + l + b], acc);
-        const int m = a < 0 ? -a : a;
-        const int r = G::mrow(l, a) - G::moff(m);
-        store_out(out + Y::kofs(m) + r * C3 + c, acc);
-      }
-    }
-  }
-  // zero the K padding of each order block
-  for (int idx = threadIdx.x; idx < ne * (L + 1) * KPAD; idx += blockDim.x) {
-    const int e = idx / ((L + 1) * KPAD), rem = idx % ((L + 1) * KPAD), m = rem / KPAD, q = rem % KPAD;
-    const int k = Y::K(m) + q;
-    if (k < Y::KP(m)) store_out(A1 + (t0 + e - e0) * Y::KTOT + Y::kofs(m) + k, 0.f);
-  }
 }
 
 // ------------------------------------------------- SO(2) linears, fp32
@@ -186,131 +139,6 @@ __global__ void __launch_bounds__(256) k_so2_simt(const float* __restrict__ A1, 
     w1 += (int64_t)K * N;
     w2 += (int64_t)N * N2;
   }
-}
-
-// --------------------------------------------------- rotate out (edge)
-// ops.h:115-117 rotate with D^T, then ops.h:265-283 residual add in place.
-template <int L, int E>
-__global__ void __launch_bounds__(256) k_rotate_out_edge(const float* __restrict__ Yin, const float* __restrict__ dir,
-                                                         int64_t e0, int64_t n_e, float* __restrict__ edges) {
-  using G = Geo<L>;
-  constexpr int TE = 16, DSP = G::DS + 1, H = G::H;
-  __shared__ float sD[TE * DSP];
-  __shared__ float sdir[TE * 3];
-  const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
-  const int ne = (int)cmin64(TE, e0 + n_e - t0);
-  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
-  __syncthreads();
-  wigner_tile<L, DSP>(sdir, ne, sD);
-  for (int idx = threadIdx.x; idx < ne * E; idx += blockDim.x) {
-    const int e = idx / E, c = idx % E;
-    const int64_t k = t0 + e;
-    const float* y = Yin + (k - e0) * H * E;
-    const float* D = sD + e * DSP;
-    float* row = edges + k * H * E;
-#pragma unroll
-    for (int l = 0; l <= L; ++l) {
-      const int dd = 2 * l + 1;
-      float yl[2 * L + 1];
-#pragma unroll
-      for (int b = -l; b <= l; ++b) yl[b + l] = y[G::mrow(l, b) * E + c];
-#pragma unroll
-      for (int a = -l; a <= l; ++a) {
-        float acc = 0.f;
-#pragma unroll
-        for (int b = -l; b <= l; ++b) acc = fmaf(D[G::doff(l) + (b + l) * dd + (a + l)], yl[b + l], acc);
-        row[(l * l + l + a) * E + c] += acc;
-      }
-    }
-  }
-}
-
-// --------------------------------------------------- node update
-// ops.h:192-263: logits from the l=0 channels, max-subtracted softmax per
-// destination segment, out_j = node_j + sum_k alpha_k msg_k in edge order.
-// One CTA per owned row; thread t <-> output (h, c); sequential over edges,
-// so the result depends only on the segment (partition-invariant).
-template <int L, int E>
-__global__ void __launch_bounds__(512) k_node_update(const float* __restrict__ Yin, const float* __restrict__ dir,
-                                                     const int64_t* __restrict__ seg, int j0, int64_t e0,
-                                                     const float* __restrict__ att, const float* __restrict__ nodes_in,
-                                                     float* __restrict__ nodes_out, float* __restrict__ logit_scratch) {
-  using G = Geo<L>;
-  constexpr int TE = 16, DSP = G::DS + 1, H = G::H;
-  __shared__ float sD[TE * DSP];
-  __shared__ float sdir[TE * 3];
-  __shared__ float sred[32];
-  __shared__ float sA[TE];
-  const int j = j0 + blockIdx.x;
-  const int64_t b = seg[j], e = seg[j + 1];
-  const int t = threadIdx.x;
-  const int h = t / E, c = t % E;
-  float out = 0.f;
-  if (t < H * E) out = nodes_in[(int64_t)j * H * E + t];
-  if (b == e) {
-    if (t < H * E) nodes_out[(int64_t)j * H * E + t] = out;
-    return;
-  }
-  float* lg = logit_scratch + (b - e0);
-  // pass 1: logits (msg row 0 == y row 0 because D_0 = 1) and the max
-  float mx = -INFINITY;
-  for (int64_t k = b + t; k < e; k += blockDim.x) {
-    const float* y = Yin + (k - e0) * H * E;
-    float s = 0.f;
-    for (int q = 0; q < E; ++q) s = fmaf(att[q], y[q], s);
-    lg[k - b] = s;
-    mx = fmaxf(mx, s);
-  }
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((t & 31) == 0) sred[t >> 5] = mx;
-  __syncthreads();
-  if (t < 32) {
-    float v = t < (int)(blockDim.x >> 5) ? sred[t] : -INFINITY;
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (t == 0) sred[0] = v;
-  }
-  __syncthreads();
-  mx = sred[0];
-  __syncthreads();
-  float z = 0.f;
-  for (int64_t k = b + t; k < e; k += blockDim.x) {
-    const float a = expf(lg[k - b] - mx);
-    lg[k - b] = a;
-    z += a;
-  }
-  for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-  if ((t & 31) == 0) sred[t >> 5] = z;
-  __syncthreads();
-  if (t < 32) {
-    float v = t < (int)(blockDim.x >> 5) ? sred[t] : 0.f;
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (t == 0) sred[0] = v;
-  }
-  __syncthreads();
-  z = sred[0];
-  // pass 2: weighted sum of rotated-back messages
-  int l = 0;
-  while ((l + 1) * (l + 1) <= h) ++l;
-  const int a = h - l * l - l;
-  for (int64_t k0 = b; k0 < e; k0 += TE) {
-    const int ne = (int)cmin64(TE, e - k0);
-    __syncthreads();
-    for (int i = t; i < ne * 3; i += blockDim.x) sdir[i] = dir[(k0 - e0) * 3 + i];
-    for (int i = t; i < ne; i += blockDim.x) sA[i] = lg[k0 - b + i] / z;
-    __syncthreads();
-    wigner_tile<L, DSP>(sdir, ne, sD);
-    if (t < H * E) {
-      const int dd = 2 * l + 1;
-      for (int i = 0; i < ne; ++i) {
-        const float* y = Yin + (k0 + i - e0) * H * E;
-        const float* D = sD + i * DSP + G::doff(l);
-        float msg = 0.f;
-        for (int bb = -l; bb <= l; ++bb) msg = fmaf(D[(bb + l) * dd + (a + l)], y[G::mrow(l, bb) * E + c], msg);
-        out = fmaf(sA[i], msg, out);
-      }
-    }
-  }
-  if (t < H * E) nodes_out[(int64_t)j * H * E + t] = out;
 }
 
 __global__ void k_copy_rows(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
@@ -425,6 +253,9 @@ struct DeviceModel {
   std::vector<int> h_item_species_a, h_item_species_b;
   int64_t block_values = 0;
   cudaEvent_t ev[8];
+  // expanded Wigner recursion (device copies)
+  WigRecipe rc{};
+  void* rc_mem[4] = {nullptr, nullptr, nullptr, nullptr};
   // optional per-category kernel timing (esg_profile_*): events around launches
   bool profile = false;
   std::vector<cudaEvent_t> pool;
@@ -641,7 +472,83 @@ void model_device_create(esg_model* M) {
   for (auto& e : M->dev->ev) ESG_CUDA(cudaEventCreate(&e));
   ESG_CUDA(cudaSetDevice(M->ctx->device));
   upload_wigner_coef(L);
-
+  // wigner.cpp:47-83 multiplied out: entry = sum coef * R[ri] * prev[pi]
+  std::vector<int> start{0};
+  std::vector<float> coef;
+  std::vector<uint8_t> ri;
+  std::vector<uint16_t> pi;
+  auto delta = [](int a, int b) { return a == b ? 1.0 : 0.0; };
+  for (int l = 0; l <= L; ++l) {
+    const int d = 2 * l + 1, dp = 2 * l - 1;
+    for (int m = -l; m <= l; ++m)
+      for (int n = -l; n <= l; ++n) {
+        if (l >= 2) {
+          struct T {
+            double c;
+            int r, p;
+          };
+          auto P = [&](double s, int i, int a, int b, std::vector<T>& out) {
+            auto idx = [&](int x, int y) { return (x + l - 1) * dp + (y + l - 1); };
+            if (b == l) {
+              out.push_back({s, (i + 1) * 3 + 2, idx(a, l - 1)});
+              out.push_back({-s, (i + 1) * 3 + 0, idx(a, -l + 1)});
+            } else if (b == -l) {
+              out.push_back({s, (i + 1) * 3 + 2, idx(a, -l + 1)});
+              out.push_back({s, (i + 1) * 3 + 0, idx(a, l - 1)});
+            } else {
+              out.push_back({s, (i + 1) * 3 + 1, idx(a, b)});
+            }
+          };
+          const double denom = (std::abs(n) == l) ? (2.0 * l) * (2.0 * l - 1.0) : double(l + n) * double(l - n);
+          const double u = std::sqrt(double(l + m) * double(l - m) / denom);
+          const double v = 0.5 * std::sqrt((1.0 + delta(m, 0)) * (l + std::abs(m) - 1.0) * (l + std::abs(m)) / denom) *
+                           (1.0 - 2.0 * delta(m, 0));
+          const double w = -0.5 * std::sqrt((l - std::abs(m) - 1.0) * (l - std::abs(m)) / denom) * (1.0 - delta(m, 0));
+          std::vector<T> terms;
+          if (u != 0.0) P(u, 0, m, n, terms);
+          if (v != 0.0) {
+            if (m == 0) {
+              P(v, 1, 1, n, terms);
+              P(v, -1, -1, n, terms);
+            } else if (m > 0) {
+              P(v * std::sqrt(1.0 + delta(m, 1)), 1, m - 1, n, terms);
+              if (m != 1) P(-v, -1, -m + 1, n, terms);
+            } else {
+              if (m != -1) P(v, 1, m + 1, n, terms);
+              P(v * std::sqrt(1.0 + delta(m, -1)), -1, -m - 1, n, terms);
+            }
+          }
+          if (w != 0.0) {
+            if (m > 0) {
+              P(w, 1, m + 1, n, terms);
+              P(w, -1, -m - 1, n, terms);
+            } else {
+              P(w, 1, m - 1, n, terms);
+              P(-w, -1, -m + 1, n, terms);
+            }
+          }
+          for (const auto& t : terms) {
+            coef.push_back((float)t.c);
+            ri.push_back((uint8_t)t.r);
+            pi.push_back((uint16_t)t.p);
+          }
+        }
+        start.push_back((int)coef.size());
+      }
+    (void)d;
+  }
+  DeviceModel* D = M->dev;
+  auto up = [&](int slot, const void* h, size_t bytes) {
+    void* p = nullptr;
+    ESG_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 4)));
+    if (bytes) ESG_CUDA(cudaMemcpy(p, h, bytes, cudaMemcpyHostToDevice));
+    D->rc_mem[slot] = p;
+    return p;
+  };
+  D->rc.start = (const int*)up(0, start.data(), sizeof(int) * start.size());
+  D->rc.coef = (const float*)up(1, coef.data(), sizeof(float) * coef.size());
+  D->rc.ri = (const uint8_t*)up(2, ri.data(), ri.size());
+  D->rc.pi = (const uint16_t*)up(3, pi.data(), sizeof(uint16_t) * pi.size());
 }
 
 void model_device_destroy(esg_model* M) {
@@ -828,11 +735,12 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     const int64_t n = e1 - e0;
     if (n > 0) {
       const unsigned tiles = (unsigned)((n + 15) / 16);
+      constexpr int RI_THREADS = 16 * 3 * E / 4;
       if (tc) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
-          k_rotate_in<L, E, 64, uint16_t><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir,
-                                                                  e0, n, (uint16_t*)D->A1);
+          k_rotate_in<L, E, 64, uint16_t><<<tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
+                                                                         D->dir, e0, n, (uint16_t*)D->A1, D->rc);
         }
         ++ctx->launches;
         Prof pr(D, st, ESG_PROF_SO2);
@@ -841,8 +749,8 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       } else {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
-          k_rotate_in<L, E, 1, float><<<tiles, 256, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row, D->dir, e0,
-                                                             n, (float*)D->A1);
+          k_rotate_in<L, E, 1, float><<<tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
+                                                                    D->dir, e0, n, (float*)D->A1, D->rc);
         }
         Prof pr(D, st, ESG_PROF_SO2);
         k_so2_simt<L, E><<<tiles, 256, 0, st>>>((const float*)D->A1, n, D->w1t[bidx], D->w2t[bidx], D->Y,
@@ -851,15 +759,15 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       }
       if (!node_block) {
         Prof pr(D, st, ESG_PROF_ROTATE_OUT);
-        k_rotate_out_edge<L, E><<<tiles, 256, 0, st>>>(D->Y, D->dir, e0, n, D->edges);
+        k_rotate_out_edge<L, E><<<(unsigned)((n + 31) / 32), 32 * E / 4, 0, st>>>(D->Y, D->dir, e0, n, D->edges,
+                                                                                   D->rc);
         ++ctx->launches;
       }
     }
     if (node_block && ch.second > ch.first) {
-      const int threads = ((H * E + 31) / 32) * 32;
       Prof pr(D, st, ESG_PROF_NODE);
-      k_node_update<L, E><<<ch.second - ch.first, threads, 0, st>>>(D->Y, D->dir + 0, D->seg, ch.first, e0, att,
-                                                                   D->nodes, D->nodes_alt, D->logits);
+      k_node_update<L, E><<<ch.second - ch.first, 256, 0, st>>>(D->Y, D->dir + 0, D->seg, ch.first, e0, att,
+                                                               D->nodes, D->nodes_alt, D->logits, D->rc);
       ++ctx->launches;
     }
   }

@@ -77,6 +77,48 @@ __device__ __forceinline__ void align_to_y(float x, float y, float z, float R[9]
   R[8] = cb * ca;
 }
 
+// Ivanic-Ruedenberg recursion expanded on the host into flat recipes: entry
+// q of degree l (stacked index doff(l) + (m+l)(2l+1) + (n+l)) is
+// sum_t coef[t] * R[ri[t]] * prev[pi[t]] with R the 3x3 band-1 block and prev
+// the degree l-1 block (wigner.cpp:58-81 with the u/v/w/P terms multiplied
+// out; zero-coefficient terms skipped exactly as the reference skips them).
+struct WigRecipe {
+  const int* start;   // per stacked entry (DS + 1)
+  const float* coef;  // per term
+  const uint8_t* ri;  // R index 0..8
+  const uint16_t* pi; // index inside the degree l-1 block
+};
+
+// Branch-free cooperative Wigner blocks for a tile of `ne` edges.
+template <int L, int DSP>
+__device__ void wigner_tile_recipe(const float* dirs, int ne, float* D, WigRecipe rc) {
+  using G = Geo<L>;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    float R[9];
+    align_to_y(dirs[3 * e], dirs[3 * e + 1], dirs[3 * e + 2], R);
+    float* d = D + e * DSP;
+    d[0] = 1.f;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) d[1 + i] = R[i];
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int l = 2; l <= L; ++l) {
+    const int dd = (2 * l + 1) * (2 * l + 1);
+    const int ob = G::doff(l), op = G::doff(l - 1);
+    for (int t = threadIdx.x; t < ne * dd; t += blockDim.x) {
+      const int e = t / dd, q = ob + t % dd;
+      const float* R = D + e * DSP + 1;
+      const float* pv = D + e * DSP + op;
+      float acc = 0.f;
+      const int t1 = __ldg(rc.start + q + 1);
+      for (int k = __ldg(rc.start + q); k < t1; ++k) acc = fmaf(__ldg(rc.coef + k) * R[__ldg(rc.ri + k)], pv[__ldg(rc.pi + k)], acc);
+      D[e * DSP + q] = acc;
+    }
+    __syncthreads();
+  }
+}
+
 // Cooperative Wigner blocks for a tile of `ne` edges: D[e*DSP + doff(l) + ...].
 // dirs: 3 floats per edge (displacement).  All threads of the block call it.
 template <int L, int DSP>

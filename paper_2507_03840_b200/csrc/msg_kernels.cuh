@@ -1,0 +1,233 @@
+// msg_kernels.cuh -- CUDA-core message kernels around the SO(2) linears:
+// gather + rotate in, rotate back + residual, segment softmax + aggregation.
+// Register-blocked on 4 channels per thread (float4 traffic, every Wigner
+// entry read from SMEM once per 4 FMAs); Wigner blocks are recomputed per
+// tile from the fp32 direction with the host-expanded recursion recipe.
+#pragma once
+#include "model_kernels.cuh"
+
+namespace esg {
+
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void st4(uint16_t* p, float4 v) {
+  auto bf = [](float x) {
+    uint32_t u = __float_as_uint(x);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return u >> 16;
+  };
+  uint2 w;
+  w.x = bf(v.x) | (bf(v.y) << 16);
+  w.y = bf(v.z) | (bf(v.w) << 16);
+  *reinterpret_cast<uint2*>(p) = w;
+}
+__device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
+  return make_float4(fmaf(d, x.x, a.x), fmaf(d, x.y, a.y), fmaf(d, x.z, a.z), fmaf(d, x.w, a.w));
+}
+
+// ops.h:68-122: message = [src | dst | edge] per harmonic row, rotated into
+// the edge frame with D_l (kernels.h:73-96), permuted to order-major rows
+// (kernels.h:98-115), written as the A1 operand of the SO(2) linears.
+// Thread = (edge, part in {src,dst,edge}, 4-channel quad); 16 edges per CTA.
+template <int L, int E, int KPAD, typename OutT>
+__global__ void __launch_bounds__(16 * 3 * E / 4) k_rotate_in(const float* __restrict__ nodes,
+                                                             const float* __restrict__ edges,
+                                                             const int* __restrict__ src_row,
+                                                             const int* __restrict__ dst_row,
+                                                             const float* __restrict__ dir, int64_t e0, int64_t n_e,
+                                                             OutT* __restrict__ A1, WigRecipe rc) {
+  using G = Geo<L>;
+  using Y = Lay1<L, E, KPAD>;
+  constexpr int TE = 16, DSP = G::DS + 1, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
+  __shared__ float sD[TE * DSP];
+  __shared__ float sdir[TE * 3];
+  const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
+  const int ne = (int)min64(TE, e0 + n_e - t0);
+  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
+  const int e = threadIdx.x / TPE, r = threadIdx.x % TPE, p = r / Q, q = r % Q;
+  float4 x[H];
+  if (e < ne) {  // issue the row loads before the Wigner work
+    const int64_t k = t0 + e;
+    const float* base = p == 0 ? nodes + (int64_t)__ldg(src_row + k) * H * E
+                               : (p == 1 ? nodes + (int64_t)__ldg(dst_row + k) * H * E : edges + k * H * E);
+#pragma unroll
+    for (int h = 0; h < H; ++h) x[h] = __ldg(reinterpret_cast<const float4*>(base + h * E) + q);
+  }
+  __syncthreads();
+  wigner_tile_recipe<L, DSP>(sdir, ne, sD, rc);
+  if (e < ne) {
+    const float* D = sD + e * DSP;
+    OutT* out = A1 + (t0 + e - e0) * Y::KTOT + p * E + q * 4;
+#pragma unroll
+    for (int l = 0; l <= L; ++l) {
+      const int dd = 2 * l + 1;
+#pragma unroll
+      for (int a = -l; a <= l; ++a) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (a + l) * dd + (b + l)], x[l * l + l + b], acc);
+        const int m = a < 0 ? -a : a;
+        st4(out + Y::kofs(m) + (G::mrow(l, a) - G::moff(m)) * C3, acc);
+      }
+    }
+  }
+  if (KPAD > 1) {  // zero the K padding of each order block (multiples of 4)
+    constexpr int PADW = KPAD / 4;
+    for (int idx = threadIdx.x; idx < ne * (L + 1) * PADW; idx += blockDim.x) {
+      const int ee = idx / ((L + 1) * PADW), rem = idx % ((L + 1) * PADW), m = rem / PADW, w = rem % PADW;
+      const int k = Y::K(m) + 4 * w;
+      if (k < Y::KP(m)) st4(A1 + (t0 + ee - e0) * Y::KTOT + Y::kofs(m) + k, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+  }
+}
+
+// ops.h:115-117 rotate back with D^T then ops.h:265-283 residual add in
+// place.  Thread = (edge, 4-channel quad); 32 edges per CTA.
+template <int L, int E>
+__global__ void __launch_bounds__(32 * E / 4) k_rotate_out_edge(const float* __restrict__ Yin,
+                                                               const float* __restrict__ dir, int64_t e0, int64_t n_e,
+                                                               float* __restrict__ edges, WigRecipe rc) {
+  using G = Geo<L>;
+  constexpr int TE = 32, DSP = G::DS + 1, H = G::H, Q = E / 4;
+  __shared__ float sD[TE * DSP];
+  __shared__ float sdir[TE * 3];
+  const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
+  const int ne = (int)min64(TE, e0 + n_e - t0);
+  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
+  const int e = threadIdx.x / Q, q = threadIdx.x % Q;
+  float4 y[H];
+  if (e < ne) {
+    const float4* yr = reinterpret_cast<const float4*>(Yin + (t0 + e - e0) * H * E) + q;
+#pragma unroll
+    for (int h = 0; h < H; ++h) y[h] = __ldg(yr + h * Q);  // order-major rows
+  }
+  __syncthreads();
+  wigner_tile_recipe<L, DSP>(sdir, ne, sD, rc);
+  if (e < ne) {
+    const float* D = sD + e * DSP;
+    float4* row = reinterpret_cast<float4*>(edges + (t0 + e) * H * E) + q;
+#pragma unroll
+    for (int l = 0; l <= L; ++l) {
+      const int dd = 2 * l + 1;
+#pragma unroll
+      for (int a = -l; a <= l; ++a) {
+        float4 acc = row[(l * l + l + a) * Q];
+#pragma unroll
+        for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (b + l) * dd + (a + l)], y[G::mrow(l, b)], acc);
+        row[(l * l + l + a) * Q] = acc;
+      }
+    }
+  }
+}
+
+// ops.h:192-263.  One CTA per owned destination j; logits from the l = 0
+// channels (msg row 0 == y row 0 since D_0 = 1), max-subtracted softmax, then
+// out_j = node_j + sum_k alpha_k msg_k.  Tiles of TE edges: thread (edge,
+// channel) rotates its message back into SMEM scaled by alpha, then thread
+// (h, c) adds the tile's rows in edge order -- fixed order, so the result
+// depends only on the segment (partition-invariant, deterministic).
+template <int L, int E>
+__global__ void __launch_bounds__(256) k_node_update(const float* __restrict__ Yin, const float* __restrict__ dir,
+                                                     const int64_t* __restrict__ seg, int j0, int64_t e0,
+                                                     const float* __restrict__ att,
+                                                     const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
+                                                     float* __restrict__ logit_scratch, WigRecipe rc) {
+  using G = Geo<L>;
+  constexpr int TE = 256 / E, DSP = G::DS + 1, H = G::H, HE = H * E, OUTS = (HE + 255) / 256;
+  __shared__ float sD[TE * DSP];
+  __shared__ float sdir[TE * 3];
+  __shared__ float sM[TE * HE];
+  __shared__ float sA[TE];
+  __shared__ float sred[8];
+  const int j = j0 + blockIdx.x;
+  const int64_t b = seg[j], en = seg[j + 1];
+  const int t = threadIdx.x;
+  float out[OUTS];
+#pragma unroll
+  for (int i = 0; i < OUTS; ++i) {
+    const int o = t + 256 * i;
+    out[i] = o < HE ? nodes_in[(int64_t)j * HE + o] : 0.f;
+  }
+  if (b < en) {
+    float* lg = logit_scratch + (b - e0);
+    float mx = -INFINITY;
+    for (int64_t k = b + t; k < en; k += 256) {
+      const float4* y = reinterpret_cast<const float4*>(Yin + (k - e0) * HE);
+      float s = 0.f;
+#pragma unroll
+      for (int q = 0; q < E / 4; ++q) {
+        const float4 v = __ldg(y + q);
+        s = fmaf(att[4 * q], v.x, s);
+        s = fmaf(att[4 * q + 1], v.y, s);
+        s = fmaf(att[4 * q + 2], v.z, s);
+        s = fmaf(att[4 * q + 3], v.w, s);
+      }
+      lg[k - b] = s;
+      mx = fmaxf(mx, s);
+    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((t & 31) == 0) sred[t >> 5] = mx;
+    __syncthreads();
+    mx = sred[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, sred[w]);
+    __syncthreads();
+    float z = 0.f;
+    for (int64_t k = b + t; k < en; k += 256) {
+      const float a = expf(lg[k - b] - mx);
+      lg[k - b] = a;
+      z += a;
+    }
+    for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if ((t & 31) == 0) sred[t >> 5] = z;
+    __syncthreads();
+    z = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) z += sred[w];
+    const int e = t / E, c = t % E;
+    for (int64_t k0 = b; k0 < en; k0 += TE) {
+      const int ne = (int)min64(TE, en - k0);
+      __syncthreads();
+      for (int i = t; i < ne * 3; i += 256) sdir[i] = dir[(k0 - e0) * 3 + i];
+      for (int i = t; i < ne; i += 256) sA[i] = lg[k0 - b + i] / z;
+      float y[H];
+      if (e < ne) {
+        const float* yr = Yin + (k0 + e - e0) * HE + c;
+#pragma unroll
+        for (int h = 0; h < H; ++h) y[h] = __ldg(yr + h * E);
+      }
+      __syncthreads();
+      wigner_tile_recipe<L, DSP>(sdir, ne, sD, rc);
+      if (e < ne) {
+        const float* D = sD + e * DSP;
+        const float al = sA[e];
+#pragma unroll
+        for (int l = 0; l <= L; ++l) {
+          const int dd = 2 * l + 1;
+#pragma unroll
+          for (int a = -l; a <= l; ++a) {
+            float m = 0.f;
+#pragma unroll
+            for (int bb = -l; bb <= l; ++bb) m = fmaf(D[G::doff(l) + (bb + l) * dd + (a + l)], y[G::mrow(l, bb)], m);
+            sM[e * HE + (l * l + l + a) * E + c] = al * m;
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < OUTS; ++i) {
+        const int o = t + 256 * i;
+        if (o < HE)
+          for (int ee = 0; ee < ne; ++ee) out[i] += sM[ee * HE + o];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < OUTS; ++i) {
+    const int o = t + 256 * i;
+    if (o < HE) nodes_out[(int64_t)j * HE + o] = out[i];
+  }
+}
+
+}  // namespace esg
