@@ -400,12 +400,23 @@ void model_upload_params(esg_model* M) {
           for (int o = 0; o < N1; ++o) t1.push_back(W1[(size_t)o * K1 + k]);
         for (int k = 0; k < N1; ++k)
           for (int o = 0; o < N2; ++o) t2.push_back(W2[(size_t)o * N1 + k]);
-        // tcgen05 operands: K-major (N rows, K contiguous), K padded to 64
-        const int K1p = pad64(K1), N1p = pad64(N1);
-        for (int o = 0; o < N1; ++o)
-          for (int k = 0; k < K1p; ++k) b1.push_back(k < K1 ? to_bf16(W1[(size_t)o * K1 + k]) : 0);
-        for (int o = 0; o < N2; ++o)
-          for (int k = 0; k < N1p; ++k) b2.push_back(k < N1 ? to_bf16(W2[(size_t)o * N1 + k]) : 0);
+        // tcgen05 B operands in the SMEM image so2_tc.cu bulk-copies: per
+        // 64-wide K chunk a block of N rows x 128 B, 16-byte units swizzled
+        // by row % 8 (SWIZZLE_128B, K-major); K padded to 64 with zeros.
+        auto pack = [&](const std::vector<float>& W, int N, int K, std::vector<uint16_t>& out) {
+          const int KP = pad64(K);
+          for (int kc = 0; kc < KP / 64; ++kc)
+            for (int n = 0; n < N; ++n)
+              for (int u = 0; u < 8; ++u) {
+                const int src_u = u ^ (n & 7);  // logical unit stored at physical slot u
+                for (int t = 0; t < 8; ++t) {
+                  const int k = kc * 64 + src_u * 8 + t;
+                  out.push_back(k < K ? to_bf16(W[(size_t)n * K + k]) : 0);
+                }
+              }
+        };
+        pack(W1, N1, K1, b1);
+        pack(W2, N2, N1, b2);
       }
       float* d1 = dalloc<float>(t1.size());
       float* d2 = dalloc<float>(t2.size());
@@ -658,7 +669,10 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     for (int m = 0; m <= D->L; ++m) t += ((m == 0 ? D->L + 1 : 2 * (D->L - m + 1)) * 3 * E + 63) / 64 * 64;
     return t;
   }();
-  D->A1 = (void*)dalloc<float>((size_t)D->chunk_cap * K1T);  // sized for fp32 (bf16 uses half)
+  // fp32 row-major (CUDA-core path) or bf16 tiles of 128 edges (tensor cores)
+  const size_t a1_fp32 = (size_t)D->chunk_cap * K1T * 4;
+  const size_t a1_bf16 = (size_t)((D->chunk_cap + 127) / 128) * 128 * K1T * 2;
+  D->A1 = (void*)dalloc<uint8_t>(std::max(a1_fp32, a1_bf16));
   D->Y = dalloc<float>((size_t)D->chunk_cap * row);
   D->logits = dalloc<float>((size_t)D->chunk_cap);
   D->node_out = dalloc<float>((size_t)std::max(n_owned, 1) * M->heads.out_len);

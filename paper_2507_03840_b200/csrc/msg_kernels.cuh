@@ -22,6 +22,19 @@ __device__ __forceinline__ void st4(uint16_t* p, float4 v) {
   w.y = bf(v.z) | (bf(v.w) << 16);
   *reinterpret_cast<uint2*>(p) = w;
 }
+// Element index of A1(edge el, K index k).  KPAD == 1: plain row-major
+// (fp32 CUDA-core path).  KPAD == 64: the tensor-core image -- tiles of 128
+// edges, one contiguous 16 KB block per 64-wide K chunk, 128-byte rows whose
+// 16-byte units are XOR-swizzled by row % 8 (UMMA SWIZZLE_128B, K-major), so
+// so2_tc.cu moves each chunk with a single bulk copy.
+template <int KTOT, int KPAD>
+__device__ __forceinline__ int64_t a1_index(int64_t el, int k) {
+  if (KPAD == 1) return el * KTOT + k;
+  const int64_t tile = el >> 7;
+  const int r = (int)(el & 127), kc = k >> 6, w = k & 63;
+  return (tile * (KTOT / 64) + kc) * 8192 + r * 64 + (((w >> 3) ^ (r & 7)) << 3) + (w & 7);
+}
+
 __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
   return make_float4(fmaf(d, x.x, a.x), fmaf(d, x.y, a.y), fmaf(d, x.z, a.z), fmaf(d, x.w, a.w));
 }
@@ -58,7 +71,7 @@ __global__ void __launch_bounds__(16 * 3 * E / 4) k_rotate_in(const float* __res
   wigner_tile_recipe<L, DSP>(sdir, ne, sD, rc);
   if (e < ne) {
     const float* D = sD + e * DSP;
-    OutT* out = A1 + (t0 + e - e0) * Y::KTOT + p * E + q * 4;
+    const int64_t el = t0 + e - e0;
 #pragma unroll
     for (int l = 0; l <= L; ++l) {
       const int dd = 2 * l + 1;
@@ -68,7 +81,8 @@ __global__ void __launch_bounds__(16 * 3 * E / 4) k_rotate_in(const float* __res
 #pragma unroll
         for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (a + l) * dd + (b + l)], x[l * l + l + b], acc);
         const int m = a < 0 ? -a : a;
-        st4(out + Y::kofs(m) + (G::mrow(l, a) - G::moff(m)) * C3, acc);
+        const int k = Y::kofs(m) + (G::mrow(l, a) - G::moff(m)) * C3 + p * E + q * 4;
+        st4(A1 + a1_index<Y::KTOT, KPAD>(el, k), acc);
       }
     }
   }
@@ -77,7 +91,7 @@ __global__ void __launch_bounds__(16 * 3 * E / 4) k_rotate_in(const float* __res
     for (int idx = threadIdx.x; idx < ne * (L + 1) * PADW; idx += blockDim.x) {
       const int ee = idx / ((L + 1) * PADW), rem = idx % ((L + 1) * PADW), m = rem / PADW, w = rem % PADW;
       const int k = Y::K(m) + 4 * w;
-      if (k < Y::KP(m)) st4(A1 + (t0 + ee - e0) * Y::KTOT + Y::kofs(m) + k, make_float4(0.f, 0.f, 0.f, 0.f));
+      if (k < Y::KP(m)) st4(A1 + a1_index<Y::KTOT, KPAD>(t0 + ee - e0, Y::kofs(m) + k), make_float4(0.f, 0.f, 0.f, 0.f));
     }
   }
 }
