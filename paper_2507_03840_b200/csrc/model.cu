@@ -749,7 +749,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     const int64_t n = e1 - e0;
     if (n > 0) {
       const unsigned tiles = (unsigned)((n + 15) / 16);
-      constexpr int RI_THREADS = 16 * 3 * E / 4;
+      constexpr int RI_THREADS = 16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4;  // >= 4 warps for the Wigner groups
       if (tc) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
@@ -773,7 +773,8 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       }
       if (!node_block) {
         Prof pr(D, st, ESG_PROF_ROTATE_OUT);
-        k_rotate_out_edge<L, E><<<(unsigned)((n + 31) / 32), 32 * E / 4, 0, st>>>(D->Y, D->dir, e0, n, D->edges,
+        k_rotate_out_edge<L, E><<<(unsigned)((n + 31) / 32), 32 * E / 4 < 128 ? 128 : 32 * E / 4, 0, st>>>(
+            D->Y, D->dir, e0, n, D->edges,
                                                                                    D->rc);
         ++ctx->launches;
       }

@@ -77,6 +77,37 @@ __device__ __forceinline__ void align_to_y(float x, float y, float z, float R[9]
   R[8] = cb * ca;
 }
 
+}  // namespace esg
+#include "wigner_gen.cuh"
+namespace esg {
+
+// Wigner blocks for a tile of ne <= 32 edges with the generated straight-line
+// recursion: lane = edge, warps 0..3 each own a quarter of every degree's
+// entries.  Needs blockDim.x >= 128; all threads must call it.  D rows use an
+// odd stride DSP so the per-lane bases hit distinct banks.
+template <int L, int DSP>
+__device__ void wigner_tile_gen(const float* dirs, int ne, float* D) {
+  using G = Geo<L>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool act = warp < kWigGroups && lane < ne;
+  float R[9];
+  if (act) {
+    align_to_y(dirs[3 * lane], dirs[3 * lane + 1], dirs[3 * lane + 2], R);
+    if (warp == 0) {
+      float* d = D + lane * DSP;
+      d[0] = 1.f;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) d[1 + i] = R[i];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int l = 2; l <= L; ++l) {
+    if (act) wigner_group(l, warp, R, D + lane * DSP + G::doff(l - 1), D + lane * DSP + G::doff(l));
+    __syncthreads();
+  }
+}
+
 // Ivanic-Ruedenberg recursion expanded on the host into flat recipes: entry
 // q of degree l (stacked index doff(l) + (m+l)(2l+1) + (n+l)) is
 // sum_t coef[t] * R[ri[t]] * prev[pi[t]] with R the 3x3 band-1 block and prev

@@ -44,7 +44,7 @@ __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
 // (kernels.h:98-115), written as the A1 operand of the SO(2) linears.
 // Thread = (edge, part in {src,dst,edge}, 4-channel quad); 16 edges per CTA.
 template <int L, int E, int KPAD, typename OutT>
-__global__ void __launch_bounds__(16 * 3 * E / 4) k_rotate_in(const float* __restrict__ nodes,
+__global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4) k_rotate_in(const float* __restrict__ nodes,
                                                              const float* __restrict__ edges,
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
@@ -52,34 +52,34 @@ __global__ void __launch_bounds__(16 * 3 * E / 4) k_rotate_in(const float* __res
                                                              OutT* __restrict__ A1, WigRecipe rc) {
   using G = Geo<L>;
   using Y = Lay1<L, E, KPAD>;
-  constexpr int TE = 16, DSP = G::DS + 1, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
+  constexpr int TE = 16, DSP = G::DS + 2, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
   __shared__ float sD[TE * DSP];
   __shared__ float sdir[TE * 3];
   const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
   const int ne = (int)min64(TE, e0 + n_e - t0);
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   const int e = threadIdx.x / TPE, r = threadIdx.x % TPE, p = r / Q, q = r % Q;
-  float4 x[H];
-  if (e < ne) {  // issue the row loads before the Wigner work
-    const int64_t k = t0 + e;
-    const float* base = p == 0 ? nodes + (int64_t)__ldg(src_row + k) * H * E
-                               : (p == 1 ? nodes + (int64_t)__ldg(dst_row + k) * H * E : edges + k * H * E);
-#pragma unroll
-    for (int h = 0; h < H; ++h) x[h] = __ldg(reinterpret_cast<const float4*>(base + h * E) + q);
-  }
   __syncthreads();
-  wigner_tile_recipe<L, DSP>(sdir, ne, sD, rc);
+  wigner_tile_gen<L, DSP>(sdir, ne, sD);
   if (e < ne) {
+    const int64_t k = t0 + e;
+    const float4* base = reinterpret_cast<const float4*>(
+                             p == 0 ? nodes + (int64_t)__ldg(src_row + k) * H * E
+                                    : (p == 1 ? nodes + (int64_t)__ldg(dst_row + k) * H * E : edges + k * H * E)) +
+                         q;
     const float* D = sD + e * DSP;
     const int64_t el = t0 + e - e0;
 #pragma unroll
     for (int l = 0; l <= L; ++l) {
       const int dd = 2 * l + 1;
+      float4 x[2 * L + 1];
+#pragma unroll
+      for (int b = -l; b <= l; ++b) x[b + l] = __ldg(base + (l * l + l + b) * (E / 4));
 #pragma unroll
       for (int a = -l; a <= l; ++a) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (a + l) * dd + (b + l)], x[l * l + l + b], acc);
+        for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (a + l) * dd + (b + l)], x[b + l], acc);
         const int m = a < 0 ? -a : a;
         const int k = Y::kofs(m) + (G::mrow(l, a) - G::moff(m)) * C3 + p * E + q * 4;
         st4(A1 + a1_index<Y::KTOT, KPAD>(el, k), acc);
@@ -99,36 +99,37 @@ __global__ void __launch_bounds__(16 * 3 * E / 4) k_rotate_in(const float* __res
 // ops.h:115-117 rotate back with D^T then ops.h:265-283 residual add in
 // place.  Thread = (edge, 4-channel quad); 32 edges per CTA.
 template <int L, int E>
-__global__ void __launch_bounds__(32 * E / 4) k_rotate_out_edge(const float* __restrict__ Yin,
+__global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4) k_rotate_out_edge(const float* __restrict__ Yin,
                                                                const float* __restrict__ dir, int64_t e0, int64_t n_e,
                                                                float* __restrict__ edges, WigRecipe rc) {
   using G = Geo<L>;
-  constexpr int TE = 32, DSP = G::DS + 1, H = G::H, Q = E / 4;
+  constexpr int TE = 32, DSP = G::DS + 2, H = G::H, Q = E / 4;
   __shared__ float sD[TE * DSP];
   __shared__ float sdir[TE * 3];
   const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
   const int ne = (int)min64(TE, e0 + n_e - t0);
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   const int e = threadIdx.x / Q, q = threadIdx.x % Q;
-  float4 y[H];
+  __syncthreads();
+  wigner_tile_gen<L, DSP>(sdir, ne, sD);
   if (e < ne) {
     const float4* yr = reinterpret_cast<const float4*>(Yin + (t0 + e - e0) * H * E) + q;
-#pragma unroll
-    for (int h = 0; h < H; ++h) y[h] = __ldg(yr + h * Q);  // order-major rows
-  }
-  __syncthreads();
-  wigner_tile_recipe<L, DSP>(sdir, ne, sD, rc);
-  if (e < ne) {
     const float* D = sD + e * DSP;
     float4* row = reinterpret_cast<float4*>(edges + (t0 + e) * H * E) + q;
 #pragma unroll
     for (int l = 0; l <= L; ++l) {
       const int dd = 2 * l + 1;
+      float4 y[2 * L + 1], old[2 * L + 1];
+#pragma unroll
+      for (int b = -l; b <= l; ++b) {
+        y[b + l] = __ldg(yr + G::mrow(l, b) * Q);  // order-major rows
+        old[b + l] = row[(l * l + l + b) * Q];
+      }
 #pragma unroll
       for (int a = -l; a <= l; ++a) {
-        float4 acc = row[(l * l + l + a) * Q];
+        float4 acc = old[a + l];
 #pragma unroll
-        for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (b + l) * dd + (a + l)], y[G::mrow(l, b)], acc);
+        for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (b + l) * dd + (a + l)], y[b + l], acc);
         row[(l * l + l + a) * Q] = acc;
       }
     }
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(256) k_node_update(const float* __restrict__ Y
                                                      const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
                                                      float* __restrict__ logit_scratch, WigRecipe rc) {
   using G = Geo<L>;
-  constexpr int TE = 256 / E, DSP = G::DS + 1, H = G::H, HE = H * E, OUTS = (HE + 255) / 256;
+  constexpr int TE = 256 / E, DSP = G::DS + 2, H = G::H, HE = H * E, OUTS = (HE + 255) / 256;
   __shared__ float sD[TE * DSP];
   __shared__ float sdir[TE * 3];
   __shared__ float sM[TE * HE];
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(256) k_node_update(const float* __restrict__ Y
         for (int h = 0; h < H; ++h) y[h] = __ldg(yr + h * E);
       }
       __syncthreads();
-      wigner_tile_recipe<L, DSP>(sdir, ne, sD, rc);
+      wigner_tile_gen<L, DSP>(sdir, ne, sD);
       if (e < ne) {
         const float* D = sD + e * DSP;
         const float al = sA[e];

@@ -1,0 +1,32 @@
+"""Multi-GPU parity (needs >= 2 GPUs; skipped otherwise): P-rank NCCL forward
+== 1-GPU forward bit for bit (tools/multi_gpu_check.py)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def n_gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_partitioned_forward_bit_exact(world, precision):
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
+           os.path.join(ROOT, "tools", "multi_gpu_check.py"), "--precision", precision]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "bit-exact True" in r.stdout

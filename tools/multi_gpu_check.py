@@ -1,0 +1,76 @@
+"""P-GPU forward (Low-NN partition, NCCL halo inside libesg_b200) versus the
+1-GPU serial forward of the same graph: every per-destination reduction is
+segment-local with a fixed order, so the outputs must agree bit for bit
+(the reference pins the same property: test_runtime.cpp:235-271).
+
+  torchrun --nproc-per-node P --master-addr 127.0.0.1 tools/multi_gpu_check.py [--config C2]
+"""
+import argparse
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2507_03840_b200 import esg  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="small")
+    ap.add_argument("--precision", default="fp32")
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    ids = [esg.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    ctx = esg.Context(local, rank, world, ids[0])
+    if args.config == "small":
+        s, r, layers, basis = esg.make_jittered_lattice(600, 2.2, 0.45, [72, 8, 8], 5), 6.0, 2, esg.BASIS_HFO2
+    else:
+        s, r, layers, basis = esg.config_structure(args.config)
+    prec = esg.LINEAR_BF16 if args.precision == "bf16" else esg.LINEAR_FP32
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=layers, n_radial=32, r_cut=r, seed=1, linear_precision=prec)
+    g = esg.build_graph(ctx, s, r)
+    part = esg.lownn_partition(s, g.in_degrees(), int(round(math.log2(world))), r)
+    plan = esg.build_comm_plan(g, s.species, part, world, rank)
+    net = esg.Network(ctx, cfg, basis)
+    net.init_params()
+    net.prepare(g, s.species, plan)
+    no, eo, tm = net.forward()
+    pe = plan.export()
+    owned = pe["row_global"][:plan.n_owned]
+    outs = [None] * world
+    dist.all_gather_object(outs, (owned, pe["edge_index"], no, eo, tm.exchanges, tm.halo_ms))
+    ok = True
+    if rank == 0:
+        ctx1 = esg.Context(local, 0, 1)
+        net1 = esg.Network(ctx1, cfg, basis)
+        net1.init_params()
+        g1 = esg.build_graph(ctx1, s, r)
+        net1.prepare(g1, s.species)
+        sno, seo, _ = net1.forward()
+        gno = np.zeros_like(sno)
+        geo = np.zeros_like(seo)
+        for o, ei, a, b, ex, hm in outs:
+            gno[o] = a
+            geo[ei] = b
+            ok &= ex == 2 * layers
+        same = np.array_equal(gno, sno) and np.array_equal(geo, seo)
+        print(f"world {world}: exchanges/forward {outs[0][4]}, halo ms {[round(x[5], 3) for x in outs]}, "
+              f"bit-exact {same}, max|diff| {max(np.abs(gno - sno).max(), np.abs(geo - seo).max())}")
+        ok &= same
+    flag = torch.tensor([int(ok)])
+    dist.broadcast(flag, 0)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() else 1)
+
+
+if __name__ == "__main__":
+    main()
