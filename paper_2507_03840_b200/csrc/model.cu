@@ -58,22 +58,32 @@ __global__ void k_init_nodes(const int* __restrict__ row_slot, int n_rows, const
   nodes[t] = q < E ? embed[row_slot[i] * E + q] : 0.f;
 }
 
+// One warp per edge: lane g evaluates Gaussian g once (fp64 exp, cast), lane
+// c < E sums lift[c][g] * rbf[g] over g in ascending order (the reference's
+// sequential float sum, no FMA); the warp then writes the 1,600-byte row.
 template <int H, int E>
 __global__ void k_init_edges(const double* __restrict__ dist, int64_t n_e, const float* __restrict__ lift, int ng,
                              double spacing, float* __restrict__ edges) {
-  const int64_t k = (int64_t)blockIdx.x * (blockDim.x / E) + threadIdx.x / E;
-  const int c = threadIdx.x % E;
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (k >= n_e) return;
   const double d0 = dist[k];
   float acc = 0.f;
-  for (int g = 0; g < ng; ++g) {
-    const double d = d0 - g * spacing;
-    const float rbf = (float)exp(-d * d / (2.0 * spacing * spacing));
-    acc = __fadd_rn(acc, __fmul_rn(lift[c * ng + g], rbf));
+  for (int g0 = 0; g0 < ng; g0 += 32) {
+    float rbf = 0.f;
+    if (g0 + lane < ng) {
+      const double d = d0 - (g0 + lane) * spacing;
+      rbf = (float)exp(-d * d / (2.0 * spacing * spacing));
+    }
+    const int gn = ng - g0 < 32 ? ng - g0 : 32;
+    for (int g = 0; g < gn; ++g) {
+      const float r = __shfl_sync(0xffffffffu, rbf, g);
+      if (lane < E) acc = __fadd_rn(acc, __fmul_rn(lift[lane * ng + g0 + g], r));
+    }
   }
-  float* row = edges + k * (H * E);
-  row[c] = acc;
-  for (int q = E + c; q < H * E; q += E) row[q] = 0.f;
+  float4* row = reinterpret_cast<float4*>(edges + k * (H * E));
+  for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (lane < E) edges[k * (H * E) + lane] = acc;
 }
 
 // ------------------------------------------------- SO(2) linears, fp32
@@ -148,18 +158,39 @@ __global__ void k_copy_rows(const float* __restrict__ src, float* __restrict__ d
 
 // ---------------------------------------------------------- heads
 // ops.h:287-335: out[i][off_k + r] = sum_c w_k[c] x[i][L^2 + r][c].
-__global__ void k_heads(const float* __restrict__ x, int64_t n_items, int HE, int E, const float* __restrict__ W,
-                        const int* __restrict__ key_of, const int* __restrict__ row_of, int out_len,
-                        float* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_items * out_len) return;
-  const int64_t i = t / out_len;
-  const int jj = int(t % out_len);
-  const float* plane = x + i * HE + row_of[jj] * E;
-  const float* w = W + key_of[jj] * E;
-  float acc = 0.f;
-  for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[c], plane[c]));
-  out[t] = acc;
+// One warp per item, lane h < H owns harmonic row h (its E channels in
+// registers) and produces every head output that projects row h:
+// hptr[h]..hptr[h+1] lists (output index, key).  Sequential fp32 sum over the
+// channels without FMA, as ops.h:293-306 does.
+template <int H, int E>
+__global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int64_t n_items,
+                                               const float* __restrict__ W, int n_keys,
+                                               const int* __restrict__ hptr, const int* __restrict__ hj,
+                                               const int* __restrict__ hk, int out_len, float* __restrict__ out) {
+  extern __shared__ float sW[];  // n_keys x E
+  for (int i = threadIdx.x; i < n_keys * E; i += blockDim.x) sW[i] = W[i];
+  __syncthreads();
+  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int h = threadIdx.x & 31;
+  if (item >= n_items || h >= H) return;
+  float v[E];
+  const float4* row = reinterpret_cast<const float4*>(x + item * (H * E) + h * E);
+#pragma unroll
+  for (int q = 0; q < E / 4; ++q) {
+    const float4 t = __ldg(row + q);
+    v[4 * q] = t.x;
+    v[4 * q + 1] = t.y;
+    v[4 * q + 2] = t.z;
+    v[4 * q + 3] = t.w;
+  }
+  float* o = out + item * out_len;
+  for (int t = __ldg(hptr + h); t < __ldg(hptr + h + 1); ++t) {
+    const float* w = sW + __ldg(hk + t) * E;
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[c], v[c]));
+    o[__ldg(hj + t)] = acc;
+  }
 }
 
 // ------------------------------------------------ uncoupled blocks
@@ -218,8 +249,9 @@ struct DeviceModel {
   std::vector<int64_t> att_off;      // per layer offset into params
   float* embed = nullptr;            // per species slot x E
   float* head_w[2] = {nullptr, nullptr};  // node / edge: n_keys x E
-  int* head_key = nullptr;
-  int* head_row = nullptr;
+  int* head_key = nullptr;   // per listed output: key index
+  int* head_row = nullptr;   // per listed output: output index
+  int* head_hptr = nullptr;  // per harmonic row: start of its outputs
   int64_t lift_off = 0;
   // prepared view
   bool prepared = false;
@@ -443,14 +475,26 @@ void model_upload_params(esg_model* M) {
   D->embed = dalloc<float>(emb.size());
   ESG_CUDA(cudaMemcpy(D->embed, emb.data(), sizeof(float) * emb.size(), cudaMemcpyHostToDevice));
   D->lift_off = M->params.at("radial/lift").offset;
-  std::vector<int> key_of, row_of;
-  for (size_t k = 0; k < M->heads.keys.size(); ++k) {
-    const int Lk = M->heads.keys[k].L;
-    for (int r = 0; r < 2 * Lk + 1; ++r) {
-      key_of.push_back((int)k);
-      row_of.push_back(Lk * Lk + r);
+  // head outputs grouped by the harmonic row they project (k_heads lanes)
+  std::vector<int> key_of, row_of, hptr(D->H + 1, 0);
+  {
+    std::vector<std::vector<std::pair<int, int>>> by_row(D->H);  // (output index, key)
+    int j = 0;
+    for (size_t k = 0; k < M->heads.keys.size(); ++k) {
+      const int Lk = M->heads.keys[k].L;
+      for (int r = 0; r < 2 * Lk + 1; ++r, ++j) by_row[Lk * Lk + r].push_back({j, (int)k});
+    }
+    for (int h = 0; h < D->H; ++h) {
+      for (const auto& jk : by_row[h]) {
+        row_of.push_back(jk.first);
+        key_of.push_back(jk.second);
+      }
+      hptr[h + 1] = (int)row_of.size();
     }
   }
+  free_ptr(D->head_hptr);
+  D->head_hptr = dalloc<int>(hptr.size());
+  ESG_CUDA(cudaMemcpy(D->head_hptr, hptr.data(), sizeof(int) * hptr.size(), cudaMemcpyHostToDevice));
   for (int s = 0; s < 2; ++s) {
     std::vector<float> hw;
     for (const auto& k : M->heads.keys) {
@@ -566,7 +610,7 @@ void model_device_destroy(esg_model* M) {
   DeviceModel* D = M->dev;
   if (!D) return;
   for (void* p : {(void*)D->params, (void*)D->embed, (void*)D->head_w[0], (void*)D->head_w[1], (void*)D->head_key,
-                  (void*)D->head_row, (void*)D->row_slot, (void*)D->src_row, (void*)D->dst_row, (void*)D->dir,
+                  (void*)D->head_row, (void*)D->head_hptr, (void*)D->row_slot, (void*)D->src_row, (void*)D->dst_row, (void*)D->dir,
                   (void*)D->dist, (void*)D->seg, (void*)D->send_rows, (void*)D->send_buf, (void*)D->nodes,
                   (void*)D->nodes_alt, (void*)D->edges, D->A1, (void*)D->Y, (void*)D->logits, (void*)D->node_out,
                   (void*)D->edge_out})
@@ -673,6 +717,8 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   const size_t a1_fp32 = (size_t)D->chunk_cap * K1T * 4;
   const size_t a1_bf16 = (size_t)((D->chunk_cap + 127) / 128) * 128 * K1T * 2;
   D->A1 = (void*)dalloc<uint8_t>(std::max(a1_fp32, a1_bf16));
+  // the K padding slots of the tensor-core image are never written again
+  ESG_CUDA(cudaMemset(D->A1, 0, std::max(a1_fp32, a1_bf16)));
   D->Y = dalloc<float>((size_t)D->chunk_cap * row);
   D->logits = dalloc<float>((size_t)D->chunk_cap);
   D->node_out = dalloc<float>((size_t)std::max(n_owned, 1) * M->heads.out_len);
@@ -804,9 +850,8 @@ void forward_impl(esg_model* M, esg_timing* tm) {
     k_init_nodes<H, E><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->row_slot, D->n_rows, D->embed, D->nodes);
     ++ctx->launches;
     if (D->n_edges) {
-      const int per = 256 / E;
       Prof pr2(D, st, ESG_PROF_INIT);
-      k_init_edges<H, E><<<(unsigned)((D->n_edges + per - 1) / per), per * E, 0, st>>>(
+      k_init_edges<H, E><<<(unsigned)((D->n_edges + 7) / 8), 256, 0, st>>>(
           D->dist, D->n_edges, D->params + D->lift_off, M->cfg.n_radial, M->cfg.r_cut / (M->cfg.n_radial - 1),
           D->edges);
       ++ctx->launches;
@@ -825,15 +870,17 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   if (D->n_owned) {
     const int64_t n = (int64_t)D->n_owned * out_len;
     Prof pr(D, st, ESG_PROF_HEADS);
-    k_heads<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->nodes, D->n_owned, H * E, E, D->head_w[0], D->head_key,
-                                                         D->head_row, out_len, D->node_out);
+    const int nk = (int)M->heads.keys.size();
+    k_heads<H, E><<<(unsigned)((D->n_owned + 7) / 8), 256, nk * E * sizeof(float), st>>>(
+        D->nodes, D->n_owned, D->head_w[0], nk, D->head_hptr, D->head_row, D->head_key, out_len, D->node_out);
     ++ctx->launches;
   }
   if (D->n_edges) {
     const int64_t n = D->n_edges * out_len;
     Prof pr(D, st, ESG_PROF_HEADS);
-    k_heads<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->edges, D->n_edges, H * E, E, D->head_w[1], D->head_key,
-                                                         D->head_row, out_len, D->edge_out);
+    const int nk = (int)M->heads.keys.size();
+    k_heads<H, E><<<(unsigned)((D->n_edges + 7) / 8), 256, nk * E * sizeof(float), st>>>(
+        D->edges, D->n_edges, D->head_w[1], nk, D->head_hptr, D->head_row, D->head_key, out_len, D->edge_out);
     ++ctx->launches;
   }
   ESG_CUDA(cudaEventRecord(D->ev[3], st));

@@ -44,7 +44,7 @@ __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
 // (kernels.h:98-115), written as the A1 operand of the SO(2) linears.
 // Thread = (edge, part in {src,dst,edge}, 4-channel quad); 16 edges per CTA.
 template <int L, int E, int KPAD, typename OutT>
-__global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4) k_rotate_in(const float* __restrict__ nodes,
+__global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4, 3) k_rotate_in(const float* __restrict__ nodes,
                                                              const float* __restrict__ edges,
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
@@ -86,20 +86,14 @@ __global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4) k
       }
     }
   }
-  if (KPAD > 1) {  // zero the K padding of each order block (multiples of 4)
-    constexpr int PADW = KPAD / 4;
-    for (int idx = threadIdx.x; idx < ne * (L + 1) * PADW; idx += blockDim.x) {
-      const int ee = idx / ((L + 1) * PADW), rem = idx % ((L + 1) * PADW), m = rem / PADW, w = rem % PADW;
-      const int k = Y::K(m) + 4 * w;
-      if (k < Y::KP(m)) st4(A1 + a1_index<Y::KTOT, KPAD>(t0 + ee - e0, Y::kofs(m) + k), make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-  }
+  // K padding of each order block is never written: the A1 scratch is zeroed
+  // once at prepare time and the padding positions are fixed.
 }
 
 // ops.h:115-117 rotate back with D^T then ops.h:265-283 residual add in
 // place.  Thread = (edge, 4-channel quad); 32 edges per CTA.
 template <int L, int E>
-__global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4) k_rotate_out_edge(const float* __restrict__ Yin,
+__global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rotate_out_edge(const float* __restrict__ Yin,
                                                                const float* __restrict__ dir, int64_t e0, int64_t n_e,
                                                                float* __restrict__ edges, WigRecipe rc) {
   using G = Geo<L>;
