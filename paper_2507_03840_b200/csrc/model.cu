@@ -61,29 +61,26 @@ __global__ void k_init_nodes(const int* __restrict__ row_slot, int n_rows, const
 // One warp per edge: lane g evaluates Gaussian g once (fp64 exp, cast), lane
 // c < E sums lift[c][g] * rbf[g] over g in ascending order (the reference's
 // sequential float sum, no FMA); the warp then writes the 1,600-byte row.
-template <int H, int E>
-__global__ void k_init_edges(const double* __restrict__ dist, int64_t n_e, const float* __restrict__ lift, int ng,
-                             double spacing, float* __restrict__ edges) {
-  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+template <int H, int E, int NG>
+__global__ void __launch_bounds__(256) k_init_edges(const double* __restrict__ dist, int64_t n_e,
+                                                    const float* __restrict__ lift, int ng, double spacing,
+                                                    float* __restrict__ edges) {
   const int lane = threadIdx.x & 31;
-  if (k >= n_e) return;
-  const double d0 = dist[k];
-  float acc = 0.f;
-  for (int g0 = 0; g0 < ng; g0 += 32) {
-    float rbf = 0.f;
-    if (g0 + lane < ng) {
-      const double d = d0 - (g0 + lane) * spacing;
-      rbf = (float)exp(-d * d / (2.0 * spacing * spacing));
-    }
-    const int gn = ng - g0 < 32 ? ng - g0 : 32;
-    for (int g = 0; g < gn; ++g) {
-      const float r = __shfl_sync(0xffffffffu, rbf, g);
-      if (lane < E) acc = __fadd_rn(acc, __fmul_rn(lift[lane * ng + g0 + g], r));
-    }
+  float w[NG];  // lane c < E keeps lift row c in registers (zero past ng)
+#pragma unroll
+  for (int g = 0; g < NG; ++g) w[g] = (lane < E && g < ng) ? lift[lane * ng + g] : 0.f;
+  const double inv_den = 2.0 * spacing * spacing;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_e; k += warps) {
+    const double d = dist[k] - lane * spacing;
+    const float rbf = lane < ng ? (float)exp(-d * d / inv_den) : 0.f;
+    float acc = 0.f;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) acc = __fadd_rn(acc, __fmul_rn(w[g], __shfl_sync(0xffffffffu, rbf, g)));
+    float4* row = reinterpret_cast<float4*>(edges + k * (H * E));
+    for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane < E) edges[k * (H * E) + lane] = acc;
   }
-  float4* row = reinterpret_cast<float4*>(edges + k * (H * E));
-  for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (lane < E) edges[k * (H * E) + lane] = acc;
 }
 
 // ------------------------------------------------- SO(2) linears, fp32
@@ -851,9 +848,11 @@ void forward_impl(esg_model* M, esg_timing* tm) {
     ++ctx->launches;
     if (D->n_edges) {
       Prof pr2(D, st, ESG_PROF_INIT);
-      k_init_edges<H, E><<<(unsigned)((D->n_edges + 7) / 8), 256, 0, st>>>(
-          D->dist, D->n_edges, D->params + D->lift_off, M->cfg.n_radial, M->cfg.r_cut / (M->cfg.n_radial - 1),
-          D->edges);
+      if (M->cfg.n_radial > 32) usage("the GPU radial lift supports up to 32 Gaussians");
+      const int64_t blocks = std::min<int64_t>((D->n_edges + 7) / 8, 148 * 64);
+      k_init_edges<H, E, 32><<<(unsigned)blocks, 256, 0, st>>>(D->dist, D->n_edges, D->params + D->lift_off,
+                                                                M->cfg.n_radial,
+                                                                M->cfg.r_cut / (M->cfg.n_radial - 1), D->edges);
       ++ctx->launches;
     }
   }

@@ -16,8 +16,9 @@
 // one contiguous block per 64-wide K chunk), so every chunk is a single
 // cp.async.bulk (TMA, 1-D) that completes on an mbarrier -- no tensor maps.
 //
-// Warp roles (192 threads, 1 CTA per SM, persistent over tiles):
-//   warp 0    producer: one lane streams A1 / W chunks through a 3-stage ring
+// Warp roles (224 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0    A producer: one lane streams A1 chunks through a 4-stage ring
+//   warp 6    B producer: one lane streams weight chunks through a 3-stage ring
 //   warp 1    MMA issuer: one lane issues tcgen05.mma, commits free stages
 //   warps 2-5 epilogue: gate and Y drain (warp w owns TMEM lanes 32*(w%4)+)
 #include <cuda_runtime.h>
@@ -31,12 +32,13 @@ namespace esg {
 namespace {
 
 constexpr int TILE_M = 128;
-constexpr int THREADS = 192;
-constexpr int NST = 3;
+constexpr int THREADS = 224;
+constexpr int NSA = 4;                  // A1 ring (streamed from HBM)
+constexpr int NSB = 3;                  // weight ring (L2-resident)
 constexpr int A_CHUNK = TILE_M * 128;   // 64 bf16 K x 128 rows = 16 KB
 constexpr int B_CHUNK = 256 * 128;      // up to 256 rows x 64 K = 32 KB
 constexpr int A2_BYTES = TILE_M * 256 * 2;
-constexpr int SMEM_BYTES = 1024 + NST * (A_CHUNK + B_CHUNK) + A2_BYTES + 256;
+constexpr int SMEM_BYTES = 1024 + NSA * A_CHUNK + NSB * B_CHUNK + A2_BYTES + 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -143,18 +145,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sA = smem_u32(base);
-  const uint32_t sB = sA + NST * A_CHUNK;
-  const uint32_t sA2 = sB + NST * B_CHUNK;
-  uint64_t* bars = (uint64_t*)(base + NST * (A_CHUNK + B_CHUNK) + A2_BYTES);
-  // full[NST], empty[NST], l1_full, a2_full, l2_full, l2_free
+  const uint32_t sB = sA + NSA * A_CHUNK;
+  const uint32_t sA2 = sB + NSB * B_CHUNK;
+  uint64_t* bars = (uint64_t*)(base + NSA * A_CHUNK + NSB * B_CHUNK + A2_BYTES);
   auto bar = [&](int i) { return smem_u32(&bars[i]); };
-  const int FULL = 0, EMPTY = NST, L1F = 2 * NST, A2F = 2 * NST + 1, L2F = 2 * NST + 2, L2E = 2 * NST + 3;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * NST + 4);
+  const int FA = 0, EA = NSA, FB = 2 * NSA, EB = 2 * NSA + NSB;
+  const int L1F = 2 * NSA + 2 * NSB, A2F = L1F + 1, L2F = L1F + 2, L2E = L1F + 3;
+  uint32_t* tmem_slot = (uint32_t*)(bars + L1F + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(bar(FULL + s), 1);
-      mbar_init(bar(EMPTY + s), 1);
+    for (int s = 0; s < NSA; ++s) {
+      mbar_init(bar(FA + s), 1);
+      mbar_init(bar(EA + s), 1);
+    }
+    for (int s = 0; s < NSB; ++s) {
+      mbar_init(bar(FB + s), 1);
+      mbar_init(bar(EB + s), 1);
     }
     mbar_init(bar(L1F), 1);
     mbar_init(bar(A2F), 128);
@@ -173,28 +179,41 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t n_tiles = (n_e + TILE_M - 1) / TILE_M;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ---------------------------------------------------------- A producer
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint8_t* a_tile = A1 + (size_t)tile * S::KCH * A_CHUNK;
+        for (int c = 0; c < S::KCH; ++c) {  // order-major chunks in m order
+          mbar_wait(bar(EA + st), ph ^ 1);
+          mbar_expect_tx(bar(FA + st), A_CHUNK);
+          bulk_g2s(sA + st * A_CHUNK, a_tile + (size_t)c * A_CHUNK, A_CHUNK, bar(FA + st));
+          if (++st == NSA) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------------------------------------------------- B producer
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int m = 0; m <= L; ++m) {
           const int N1 = Y1::N1(m), N2 = Y1::N2(m);
           const uint8_t* w1 = W1 + S::w1_off(m);
           for (int j = 0; j < Y1::KP(m) / 64; ++j) {
-            mbar_wait(bar(EMPTY + st), ph ^ 1);
-            mbar_expect_tx(bar(FULL + st), A_CHUNK + N1 * 128);
-            bulk_g2s(sA + st * A_CHUNK, a_tile + (size_t)(Y1::kofs(m) / 64 + j) * A_CHUNK, A_CHUNK, bar(FULL + st));
-            bulk_g2s(sB + st * B_CHUNK, w1 + (size_t)j * N1 * 128, N1 * 128, bar(FULL + st));
-            if (++st == NST) { st = 0; ph ^= 1; }
+            mbar_wait(bar(EB + st), ph ^ 1);
+            mbar_expect_tx(bar(FB + st), N1 * 128);
+            bulk_g2s(sB + st * B_CHUNK, w1 + (size_t)j * N1 * 128, N1 * 128, bar(FB + st));
+            if (++st == NSB) { st = 0; ph ^= 1; }
           }
           const uint8_t* w2 = W2 + S::w2_off(m);
           for (int j = 0; j < Y1::N1P(m) / 64; ++j) {
-            mbar_wait(bar(EMPTY + st), ph ^ 1);
-            mbar_expect_tx(bar(FULL + st), N2 * 128);
-            bulk_g2s(sB + st * B_CHUNK, w2 + (size_t)j * N2 * 128, N2 * 128, bar(FULL + st));
-            if (++st == NST) { st = 0; ph ^= 1; }
+            mbar_wait(bar(EB + st), ph ^ 1);
+            mbar_expect_tx(bar(FB + st), N2 * 128);
+            bulk_g2s(sB + st * B_CHUNK, w2 + (size_t)j * N2 * 128, N2 * 128, bar(FB + st));
+            if (++st == NSB) { st = 0; ph ^= 1; }
           }
         }
       }
@@ -202,20 +221,23 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      int st = 0;
-      uint32_t ph = 0, a2p = 0, l2e = 0;
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0, a2p = 0, l2e = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int m = 0; m <= L; ++m) {
           const int N1 = Y1::N1(m), N2 = Y1::N2(m);
           const uint32_t id1 = idesc_bf16(N1), id2 = idesc_bf16(N2);
           for (int j = 0; j < Y1::KP(m) / 64; ++j) {
-            mbar_wait(bar(FULL + st), ph);
+            mbar_wait(bar(FA + sa), pa);
+            mbar_wait(bar(FB + sb), pb);
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_bf16(t_h, sdesc(sA + st * A_CHUNK + k * 32), sdesc(sB + st * B_CHUNK + k * 32), id1, (j | k) ? 1u : 0u);
-            tc_commit(bar(EMPTY + st));
-            if (++st == NST) { st = 0; ph ^= 1; }
+              mma_bf16(t_h, sdesc(sA + sa * A_CHUNK + k * 32), sdesc(sB + sb * B_CHUNK + k * 32), id1, (j | k) ? 1u : 0u);
+            tc_commit(bar(EA + sa));
+            tc_commit(bar(EB + sb));
+            if (++sa == NSA) { sa = 0; pa ^= 1; }
+            if (++sb == NSB) { sb = 0; pb ^= 1; }
           }
           tc_commit(bar(L1F));
           mbar_wait(bar(A2F), a2p);  // gate of order m written to A2
@@ -224,19 +246,19 @@ __global__ void __launch_bounds__(THREADS, 1)
           l2e ^= 1;
           tc_fence_after();
           for (int j = 0; j < Y1::N1P(m) / 64; ++j) {
-            mbar_wait(bar(FULL + st), ph);
+            mbar_wait(bar(FB + sb), pb);
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_bf16(t_y, sdesc(sA2 + j * A_CHUNK + k * 32), sdesc(sB + st * B_CHUNK + k * 32), id2, (j | k) ? 1u : 0u);
-            tc_commit(bar(EMPTY + st));
-            if (++st == NST) { st = 0; ph ^= 1; }
+              mma_bf16(t_y, sdesc(sA2 + j * A_CHUNK + k * 32), sdesc(sB + sb * B_CHUNK + k * 32), id2, (j | k) ? 1u : 0u);
+            tc_commit(bar(EB + sb));
+            if (++sb == NSB) { sb = 0; pb ^= 1; }
           }
           tc_commit(bar(L2F));
         }
       }
     }
-  } else {
+  } else if (warp >= 2 && warp <= 5) {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
