@@ -824,8 +824,14 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     }
     if (node_block && ch.second > ch.first) {
       Prof pr(D, st, ESG_PROF_NODE);
-      k_node_update<L, E><<<ch.second - ch.first, 256, 0, st>>>(D->Y, D->dir + 0, D->seg, ch.first, e0, att,
-                                                               D->nodes, D->nodes_alt, D->logits, D->rc);
+      constexpr int dyn = (32 * H * E + 32 * (Geo<L>::DS + 2)) * (int)sizeof(float);
+      static bool attr = false;
+      if (!attr) {
+        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        attr = true;
+      }
+      k_node_update<L, E><<<ch.second - ch.first, 128, dyn, st>>>(D->Y, D->dir + 0, D->seg, ch.first, e0, att,
+                                                                 D->nodes, D->nodes_alt, D->logits, D->rc);
       ++ctx->launches;
     }
   }

@@ -132,40 +132,39 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
 
 // ops.h:192-263.  One CTA per owned destination j; logits from the l = 0
 // channels (msg row 0 == y row 0 since D_0 = 1), max-subtracted softmax, then
-// out_j = node_j + sum_k alpha_k msg_k.  Tiles of TE edges: thread (edge,
-// channel) rotates its message back into SMEM scaled by alpha, then thread
-// (h, c) adds the tile's rows in edge order -- fixed order, so the result
-// depends only on the segment (partition-invariant, deterministic).
+// out_j = node_j + sum_k alpha_k msg_k.  Tiles of 32 edges: thread (edge,
+// 4-channel quad) rotates its message back (float4, D from SMEM), scales it
+// by alpha and parks it in SMEM; thread (h, quad) then adds the tile's rows
+// in edge order -- a fixed order, so the result depends only on the segment
+// (partition-invariant and deterministic).  Dynamic SMEM: D + messages.
 template <int L, int E>
-__global__ void __launch_bounds__(256) k_node_update(const float* __restrict__ Yin, const float* __restrict__ dir,
+__global__ void __launch_bounds__(128) k_node_update(const float* __restrict__ Yin, const float* __restrict__ dir,
                                                      const int64_t* __restrict__ seg, int j0, int64_t e0,
                                                      const float* __restrict__ att,
                                                      const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
                                                      float* __restrict__ logit_scratch, WigRecipe rc) {
   using G = Geo<L>;
-  constexpr int TE = 256 / E, DSP = G::DS + 2, H = G::H, HE = H * E, OUTS = (HE + 255) / 256;
-  __shared__ float sD[TE * DSP];
+  constexpr int TE = 32, DSP = G::DS + 2, H = G::H, HE = H * E, Q = E / 4, HQ = H * Q;
+  extern __shared__ __align__(16) float dyn[];
+  float* sM = dyn;                 // TE x HE
+  float* sD = dyn + TE * HE;       // TE x DSP
   __shared__ float sdir[TE * 3];
-  __shared__ float sM[TE * HE];
   __shared__ float sA[TE];
-  __shared__ float sred[8];
+  __shared__ float sred[4];
   const int j = j0 + blockIdx.x;
   const int64_t b = seg[j], en = seg[j + 1];
   const int t = threadIdx.x;
-  float out[OUTS];
-#pragma unroll
-  for (int i = 0; i < OUTS; ++i) {
-    const int o = t + 256 * i;
-    out[i] = o < HE ? nodes_in[(int64_t)j * HE + o] : 0.f;
-  }
+  const bool owner = t < HQ;  // thread (h, quad) owns one float4 of the output row
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (owner) out = reinterpret_cast<const float4*>(nodes_in + (int64_t)j * HE)[t];
   if (b < en) {
     float* lg = logit_scratch + (b - e0);
     float mx = -INFINITY;
-    for (int64_t k = b + t; k < en; k += 256) {
+    for (int64_t k = b + t; k < en; k += 128) {
       const float4* y = reinterpret_cast<const float4*>(Yin + (k - e0) * HE);
       float s = 0.f;
 #pragma unroll
-      for (int q = 0; q < E / 4; ++q) {
+      for (int q = 0; q < Q; ++q) {
         const float4 v = __ldg(y + q);
         s = fmaf(att[4 * q], v.x, s);
         s = fmaf(att[4 * q + 1], v.y, s);
@@ -178,12 +177,10 @@ __global__ void __launch_bounds__(256) k_node_update(const float* __restrict__ Y
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((t & 31) == 0) sred[t >> 5] = mx;
     __syncthreads();
-    mx = sred[0];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, sred[w]);
+    mx = fmaxf(fmaxf(sred[0], sred[1]), fmaxf(sred[2], sred[3]));
     __syncthreads();
     float z = 0.f;
-    for (int64_t k = b + t; k < en; k += 256) {
+    for (int64_t k = b + t; k < en; k += 128) {
       const float a = expf(lg[k - b] - mx);
       lg[k - b] = a;
       z += a;
@@ -191,52 +188,47 @@ __global__ void __launch_bounds__(256) k_node_update(const float* __restrict__ Y
     for (int o = 16; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
     if ((t & 31) == 0) sred[t >> 5] = z;
     __syncthreads();
-    z = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) z += sred[w];
-    const int e = t / E, c = t % E;
+    z = (sred[0] + sred[1]) + (sred[2] + sred[3]);
+    const int e = t / Q, q = t % Q;
     for (int64_t k0 = b; k0 < en; k0 += TE) {
       const int ne = (int)min64(TE, en - k0);
       __syncthreads();
-      for (int i = t; i < ne * 3; i += 256) sdir[i] = dir[(k0 - e0) * 3 + i];
-      for (int i = t; i < ne; i += 256) sA[i] = lg[k0 - b + i] / z;
-      float y[H];
-      if (e < ne) {
-        const float* yr = Yin + (k0 + e - e0) * HE + c;
-#pragma unroll
-        for (int h = 0; h < H; ++h) y[h] = __ldg(yr + h * E);
-      }
+      for (int i = t; i < ne * 3; i += 128) sdir[i] = dir[(k0 - e0) * 3 + i];
+      for (int i = t; i < ne; i += 128) sA[i] = lg[k0 - b + i] / z;
       __syncthreads();
       wigner_tile_gen<L, DSP>(sdir, ne, sD);
       if (e < ne) {
+        const float4* yr = reinterpret_cast<const float4*>(Yin + (k0 + e - e0) * HE) + q;
         const float* D = sD + e * DSP;
         const float al = sA[e];
+        float4* mrow = reinterpret_cast<float4*>(sM + e * HE) + q;
 #pragma unroll
         for (int l = 0; l <= L; ++l) {
           const int dd = 2 * l + 1;
+          float4 y[2 * L + 1];
+#pragma unroll
+          for (int bb = -l; bb <= l; ++bb) y[bb + l] = __ldg(yr + G::mrow(l, bb) * Q);
 #pragma unroll
           for (int a = -l; a <= l; ++a) {
-            float m = 0.f;
+            float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int bb = -l; bb <= l; ++bb) m = fmaf(D[G::doff(l) + (bb + l) * dd + (a + l)], y[G::mrow(l, bb)], m);
-            sM[e * HE + (l * l + l + a) * E + c] = al * m;
+            for (int bb = -l; bb <= l; ++bb) m = fma4(D[G::doff(l) + (bb + l) * dd + (a + l)], y[bb + l], m);
+            mrow[(l * l + l + a) * Q] = make_float4(al * m.x, al * m.y, al * m.z, al * m.w);
           }
         }
       }
       __syncthreads();
-#pragma unroll
-      for (int i = 0; i < OUTS; ++i) {
-        const int o = t + 256 * i;
-        if (o < HE)
-          for (int ee = 0; ee < ne; ++ee) out[i] += sM[ee * HE + o];
-      }
+      if (owner)
+        for (int ee = 0; ee < ne; ++ee) {
+          const float4 v = reinterpret_cast<const float4*>(sM + ee * HE)[t];
+          out.x += v.x;
+          out.y += v.y;
+          out.z += v.z;
+          out.w += v.w;
+        }
     }
   }
-#pragma unroll
-  for (int i = 0; i < OUTS; ++i) {
-    const int o = t + 256 * i;
-    if (o < HE) nodes_out[(int64_t)j * HE + o] = out[i];
-  }
+  if (owner) reinterpret_cast<float4*>(nodes_out + (int64_t)j * HE)[t] = out;
 }
 
 }  // namespace esg

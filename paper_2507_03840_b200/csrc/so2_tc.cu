@@ -16,11 +16,14 @@
 // one contiguous block per 64-wide K chunk), so every chunk is a single
 // cp.async.bulk (TMA, 1-D) that completes on an mbarrier -- no tensor maps.
 //
-// Warp roles (224 threads, 1 CTA per SM, persistent over tiles):
-//   warp 0    A producer: one lane streams A1 chunks through a 4-stage ring
-//   warp 6    B producer: one lane streams weight chunks through a 3-stage ring
-//   warp 1    MMA issuer: one lane issues tcgen05.mma, commits free stages
-//   warps 2-5 epilogue: gate and Y drain (warp w owns TMEM lanes 32*(w%4)+)
+// Warp roles (352 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0     A producer: one lane streams A1 chunks through a 4-stage ring
+//   warp 10    B producer: one lane streams weight chunks through a 3-stage ring
+//   warp 1     MMA issuer: one lane issues tcgen05.mma, commits free stages
+//   warps 2-9  epilogue: gate and Y drain; warp w owns TMEM lanes 32*(w%4)+
+//              and the even (w < 6) or odd (w >= 6) 64-column chunks, and
+//              hands each gated A2 chunk to lin2 through its own mbarrier so
+//              lin2 runs while the rest of the gate is still being computed.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -32,7 +35,7 @@ namespace esg {
 namespace {
 
 constexpr int TILE_M = 128;
-constexpr int THREADS = 224;
+constexpr int THREADS = 352;
 constexpr int NSA = 4;                  // A1 ring (streamed from HBM)
 constexpr int NSB = 3;                  // weight ring (L2-resident)
 constexpr int A_CHUNK = TILE_M * 128;   // 64 bf16 K x 128 rows = 16 KB
@@ -150,8 +153,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* bars = (uint64_t*)(base + NSA * A_CHUNK + NSB * B_CHUNK + A2_BYTES);
   auto bar = [&](int i) { return smem_u32(&bars[i]); };
   const int FA = 0, EA = NSA, FB = 2 * NSA, EB = 2 * NSA + NSB;
-  const int L1F = 2 * NSA + 2 * NSB, A2F = L1F + 1, L2F = L1F + 2, L2E = L1F + 3;
-  uint32_t* tmem_slot = (uint32_t*)(bars + L1F + 4);
+  const int L1F = 2 * NSA + 2 * NSB, L2F = L1F + 1, L2E = L1F + 2, A2F = L1F + 3;  // A2F + chunk (4)
+  uint32_t* tmem_slot = (uint32_t*)(bars + A2F + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NSA; ++s) {
@@ -163,9 +166,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(bar(EB + s), 1);
     }
     mbar_init(bar(L1F), 1);
-    mbar_init(bar(A2F), 128);
+    for (int c = 0; c < 4; ++c) mbar_init(bar(A2F + c), 128);
     mbar_init(bar(L2F), 1);
-    mbar_init(bar(L2E), 128);
+    mbar_init(bar(L2E), 256);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp == 6) {
+  } else if (warp == 10) {
     // ---------------------------------------------------------- B producer
     if (lane == 0) {
       int st = 0;
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------------------------------------------------- MMA issuer
     if (lane == 0) {
       int sa = 0, sb = 0;
-      uint32_t pa = 0, pb = 0, a2p = 0, l2e = 0;
+      uint32_t pa = 0, pb = 0, l2e = 0, a2p[4] = {0, 0, 0, 0};
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int m = 0; m <= L; ++m) {
           const int N1 = Y1::N1(m), N2 = Y1::N2(m);
@@ -240,12 +243,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (++sb == NSB) { sb = 0; pb ^= 1; }
           }
           tc_commit(bar(L1F));
-          mbar_wait(bar(A2F), a2p);  // gate of order m written to A2
-          a2p ^= 1;
           mbar_wait(bar(L2E), l2e ^ 1);  // previous lin2 accumulator drained
           l2e ^= 1;
-          tc_fence_after();
           for (int j = 0; j < Y1::N1P(m) / 64; ++j) {
+            mbar_wait(bar(A2F + j), a2p[j]);  // gated chunk j of order m is in A2
+            a2p[j] ^= 1;
             mbar_wait(bar(FB + sb), pb);
             tc_fence_after();
 #pragma unroll
@@ -258,9 +260,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp >= 2 && warp <= 5) {
+  } else if (warp >= 2 && warp <= 9) {
     // ------------------------------------------------------------ epilogue
-    const int quad = warp & 3;
+    const int quad = warp & 3, half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     uint32_t l1p = 0, l2p = 0;
@@ -273,38 +275,44 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(bar(L1F), l1p);
         l1p ^= 1;
         tc_fence_after();
-        for (int q = 0; q < N1P / 32; ++q) {
+        if (m == 0) {  // gate scalars from the l = 0 channels of order 0
           float v[32];
-          if (q * 32 < N1) {
-            tmem_ld32(t_h + lane_off + q * 32, v);
-            if (m == 0 && q == 0) {
+          tmem_ld32(t_h + lane_off, v);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) s[i] = gate ? 1.f / (1.f + __expf(-v[i])) : 1.f;
+          for (int i = 0; i < 32; ++i) s[i] = gate ? 1.f / (1.f + __expf(-v[i])) : 1.f;
+        }
+        for (int c2 = half; c2 < N1P / 64; c2 += 2) {
+          const uint32_t cb = sA2 + (uint32_t)c2 * A_CHUNK;
+#pragma unroll
+          for (int hq = 0; hq < 2; ++hq) {
+            const int q = 2 * c2 + hq;
+            float v[32];
+            if (q * 32 < N1) {
+              tmem_ld32(t_h + lane_off + q * 32, v);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= s[i];
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
             }
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= s[i];
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            for (int j = 0; j < 4; ++j) {
+              const int c = hq * 4 + j;
+              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, c)),
+                           "r"(pack_bf16(v[8 * j], v[8 * j + 1])), "r"(pack_bf16(v[8 * j + 2], v[8 * j + 3])),
+                           "r"(pack_bf16(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16(v[8 * j + 6], v[8 * j + 7]))
+                           : "memory");
+            }
           }
-          const uint32_t cb = sA2 + (uint32_t)(q >> 1) * A_CHUNK;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int c = (q & 1) * 4 + j;
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, c)),
-                         "r"(pack_bf16(v[8 * j], v[8 * j + 1])), "r"(pack_bf16(v[8 * j + 2], v[8 * j + 3])),
-                         "r"(pack_bf16(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16(v[8 * j + 6], v[8 * j + 7]))
-                         : "memory");
-          }
+          fence_async_smem();
+          tc_fence_before();
+          mbar_arrive(bar(A2F + c2));
         }
-        fence_async_smem();
-        tc_fence_before();
-        mbar_arrive(bar(A2F));
         mbar_wait(bar(L2F), l2p);
         l2p ^= 1;
         tc_fence_after();
         float* yrow = Y + (e0 + row) * (G::H * E) + G::moff(m) * E;
-        for (int q = 0; q * 32 < N2; ++q) {
+        for (int q = half; q * 32 < N2; q += 2) {
           float v[32];
           tmem_ld32(t_y + lane_off + q * 32, v);
           if (valid) {
