@@ -44,7 +44,7 @@ __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
 // (kernels.h:98-115), written as the A1 operand of the SO(2) linears.
 // Thread = (edge, part in {src,dst,edge}, 4-channel quad); 16 edges per CTA.
 template <int L, int E, int KPAD, typename OutT>
-__global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4, 3) k_rotate_in(const float* __restrict__ nodes,
+__global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4, 4) k_rotate_in(const float* __restrict__ nodes,
                                                              const float* __restrict__ edges,
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
