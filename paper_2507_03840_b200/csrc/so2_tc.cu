@@ -36,8 +36,8 @@ namespace {
 
 constexpr int TILE_M = 128;
 constexpr int THREADS = 352;
-constexpr int NSA = 4;                  // A1 ring (streamed from HBM)
-constexpr int NSB = 3;                  // weight ring (L2-resident)
+constexpr int NSA = 6;                  // A1 ring (streamed from HBM)
+constexpr int NSB = 2;                  // weight ring (L2-resident)
 constexpr int A_CHUNK = TILE_M * 128;   // 64 bf16 K x 128 rows = 16 KB
 constexpr int B_CHUNK = 256 * 128;      // up to 256 rows x 64 K = 32 KB
 constexpr int A2_BYTES = TILE_M * 256 * 2;
@@ -68,10 +68,23 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+// L2 policies: A1 tiles are read once (evict first), weights by every tile (evict last)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -186,12 +199,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
+      const uint64_t pol = policy_evict_first();
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint8_t* a_tile = A1 + (size_t)tile * S::KCH * A_CHUNK;
         for (int c = 0; c < S::KCH; ++c) {  // order-major chunks in m order
           mbar_wait(bar(EA + st), ph ^ 1);
           mbar_expect_tx(bar(FA + st), A_CHUNK);
-          bulk_g2s(sA + st * A_CHUNK, a_tile + (size_t)c * A_CHUNK, A_CHUNK, bar(FA + st));
+          bulk_g2s(sA + st * A_CHUNK, a_tile + (size_t)c * A_CHUNK, A_CHUNK, bar(FA + st), pol);
           if (++st == NSA) { st = 0; ph ^= 1; }
         }
       }
@@ -201,6 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
+      const uint64_t pol = policy_evict_last();
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int m = 0; m <= L; ++m) {
           const int N1 = Y1::N1(m), N2 = Y1::N2(m);
@@ -208,14 +223,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int j = 0; j < Y1::KP(m) / 64; ++j) {
             mbar_wait(bar(EB + st), ph ^ 1);
             mbar_expect_tx(bar(FB + st), N1 * 128);
-            bulk_g2s(sB + st * B_CHUNK, w1 + (size_t)j * N1 * 128, N1 * 128, bar(FB + st));
+            bulk_g2s(sB + st * B_CHUNK, w1 + (size_t)j * N1 * 128, N1 * 128, bar(FB + st), pol);
             if (++st == NSB) { st = 0; ph ^= 1; }
           }
           const uint8_t* w2 = W2 + S::w2_off(m);
           for (int j = 0; j < Y1::N1P(m) / 64; ++j) {
             mbar_wait(bar(EB + st), ph ^ 1);
             mbar_expect_tx(bar(FB + st), N2 * 128);
-            bulk_g2s(sB + st * B_CHUNK, w2 + (size_t)j * N2 * 128, N2 * 128, bar(FB + st));
+            bulk_g2s(sB + st * B_CHUNK, w2 + (size_t)j * N2 * 128, N2 * 128, bar(FB + st), pol);
             if (++st == NSB) { st = 0; ph ^= 1; }
           }
         }
