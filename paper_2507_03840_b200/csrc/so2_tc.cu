@@ -36,8 +36,8 @@ namespace {
 
 constexpr int TILE_M = 128;
 constexpr int THREADS = 352;
-constexpr int NSA = 6;                  // A1 ring (streamed from HBM)
-constexpr int NSB = 2;                  // weight ring (L2-resident)
+constexpr int NSA = 4;                  // A1 ring (streamed from HBM)
+constexpr int NSB = 3;                  // weight ring (L2-resident)
 constexpr int A_CHUNK = TILE_M * 128;   // 64 bf16 K x 128 rows = 16 KB
 constexpr int B_CHUNK = 256 * 128;      // up to 256 rows x 64 K = 32 KB
 constexpr int A2_BYTES = TILE_M * 256 * 2;
