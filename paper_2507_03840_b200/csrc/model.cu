@@ -24,7 +24,7 @@
 namespace esg {
 
 void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2,
-                   float* Y, int gate, cudaStream_t st);  // so2_tc.cu
+                   uint16_t* Y, int gate, cudaStream_t st);  // so2_tc.cu (Y in bf16)
 bool so2_tc_available(int L, int E);
 
 namespace {
@@ -155,38 +155,45 @@ __global__ void k_copy_rows(const float* __restrict__ src, float* __restrict__ d
 
 // ---------------------------------------------------------- heads
 // ops.h:287-335: out[i][off_k + r] = sum_c w_k[c] x[i][L^2 + r][c].
-// One warp per item, lane h < H owns harmonic row h (its E channels in
-// registers) and produces every head output that projects row h:
-// hptr[h]..hptr[h+1] lists (output index, key).  Sequential fp32 sum over the
-// channels without FMA, as ops.h:293-306 does.
-template <int H, int E>
+// One warp per item (grid-stride): the item's H x E row is staged in shared
+// memory, lane t produces outputs j = t + 32 u (u < HT) with its keys' weight
+// rows held in registers; stores are coalesced along j.  Sequential fp32 sum
+// over the channels without FMA, as ops.h:293-306 does.
+template <int H, int E, int HT>
 __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int64_t n_items,
-                                               const float* __restrict__ W, int n_keys,
-                                               const int* __restrict__ hptr, const int* __restrict__ hj,
-                                               const int* __restrict__ hk, int out_len, float* __restrict__ out) {
-  extern __shared__ float sW[];  // n_keys x E
-  for (int i = threadIdx.x; i < n_keys * E; i += blockDim.x) sW[i] = W[i];
-  __syncthreads();
-  const int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int h = threadIdx.x & 31;
-  if (item >= n_items || h >= H) return;
-  float v[E];
-  const float4* row = reinterpret_cast<const float4*>(x + item * (H * E) + h * E);
+                                               const float* __restrict__ W, const int* __restrict__ key_of,
+                                               const int* __restrict__ row_of, int out_len, float* __restrict__ out) {
+  __shared__ __align__(16) float sx[8][H * E];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float w[HT][E];
+  int row[HT];
 #pragma unroll
-  for (int q = 0; q < E / 4; ++q) {
-    const float4 t = __ldg(row + q);
-    v[4 * q] = t.x;
-    v[4 * q + 1] = t.y;
-    v[4 * q + 2] = t.z;
-    v[4 * q + 3] = t.w;
+  for (int u = 0; u < HT; ++u) {
+    const int j = lane + 32 * u;
+    row[u] = j < out_len ? row_of[j] : 0;
+    const int k = j < out_len ? key_of[j] : 0;
+#pragma unroll
+    for (int c = 0; c < E; ++c) w[u][c] = W[k * E + c];
   }
-  float* o = out + item * out_len;
-  for (int t = __ldg(hptr + h); t < __ldg(hptr + h + 1); ++t) {
-    const float* w = sW + __ldg(hk + t) * E;
-    float acc = 0.f;
+  const int64_t warps = (int64_t)gridDim.x * 8;
+  for (int64_t it = (int64_t)blockIdx.x * 8 + warp; it < n_items; it += warps) {
+    const float4* src = reinterpret_cast<const float4*>(x + it * (H * E));
+    float4* dst = reinterpret_cast<float4*>(sx[warp]);
+    for (int q = lane; q < H * E / 4; q += 32) dst[q] = __ldg(src + q);
+    __syncwarp();
+    float* o = out + it * out_len;
 #pragma unroll
-    for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[c], v[c]));
-    o[__ldg(hj + t)] = acc;
+    for (int u = 0; u < HT; ++u) {
+      const int j = lane + 32 * u;
+      if (j < out_len) {
+        const float* plane = sx[warp] + row[u] * E;
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[u][c], plane[c]));
+        o[j] = acc;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -472,26 +479,15 @@ void model_upload_params(esg_model* M) {
   D->embed = dalloc<float>(emb.size());
   ESG_CUDA(cudaMemcpy(D->embed, emb.data(), sizeof(float) * emb.size(), cudaMemcpyHostToDevice));
   D->lift_off = M->params.at("radial/lift").offset;
-  // head outputs grouped by the harmonic row they project (k_heads lanes)
-  std::vector<int> key_of, row_of, hptr(D->H + 1, 0);
-  {
-    std::vector<std::vector<std::pair<int, int>>> by_row(D->H);  // (output index, key)
-    int j = 0;
-    for (size_t k = 0; k < M->heads.keys.size(); ++k) {
-      const int Lk = M->heads.keys[k].L;
-      for (int r = 0; r < 2 * Lk + 1; ++r, ++j) by_row[Lk * Lk + r].push_back({j, (int)k});
-    }
-    for (int h = 0; h < D->H; ++h) {
-      for (const auto& jk : by_row[h]) {
-        row_of.push_back(jk.first);
-        key_of.push_back(jk.second);
-      }
-      hptr[h + 1] = (int)row_of.size();
+  // per head output j: its key and the harmonic row it projects (k_heads)
+  std::vector<int> key_of, row_of;
+  for (size_t k = 0; k < M->heads.keys.size(); ++k) {
+    const int Lk = M->heads.keys[k].L;
+    for (int r = 0; r < 2 * Lk + 1; ++r) {
+      key_of.push_back((int)k);
+      row_of.push_back(Lk * Lk + r);
     }
   }
-  free_ptr(D->head_hptr);
-  D->head_hptr = dalloc<int>(hptr.size());
-  ESG_CUDA(cudaMemcpy(D->head_hptr, hptr.data(), sizeof(int) * hptr.size(), cudaMemcpyHostToDevice));
   for (int s = 0; s < 2; ++s) {
     std::vector<float> hw;
     for (const auto& k : M->heads.keys) {
@@ -801,7 +797,8 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         }
         ++ctx->launches;
         Prof pr(D, st, ESG_PROF_SO2);
-        so2_tc_launch(L, E, (const uint16_t*)D->A1, n, D->w1b[bidx], D->w2b[bidx], D->Y, M->cfg.gate_enabled, st);
+        so2_tc_launch(L, E, (const uint16_t*)D->A1, n, D->w1b[bidx], D->w2b[bidx], (uint16_t*)D->Y,
+                      M->cfg.gate_enabled, st);
         ++ctx->launches;
       } else {
         {
@@ -816,9 +813,13 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       }
       if (!node_block) {
         Prof pr(D, st, ESG_PROF_ROTATE_OUT);
-        k_rotate_out_edge<L, E><<<(unsigned)((n + 31) / 32), 32 * E / 4 < 128 ? 128 : 32 * E / 4, 0, st>>>(
-            D->Y, D->dir, e0, n, D->edges,
-                                                                                   D->rc);
+        const unsigned ro_grid = (unsigned)((n + 31) / 32);
+        constexpr int ro_threads = 32 * E / 4 < 128 ? 128 : 32 * E / 4;
+        if (tc)
+          k_rotate_out_edge<L, E, uint16_t><<<ro_grid, ro_threads, 0, st>>>((const uint16_t*)D->Y, D->dir, e0, n,
+                                                                            D->edges, D->rc);
+        else
+          k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->rc);
         ++ctx->launches;
       }
     }
@@ -827,16 +828,34 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       constexpr int dyn = (32 * H * E + 32 * (Geo<L>::DS + 2)) * (int)sizeof(float);
       static bool attr = false;
       if (!attr) {
-        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
         attr = true;
       }
-      k_node_update<L, E><<<ch.second - ch.first, 128, dyn, st>>>(D->Y, D->dir + 0, D->seg, ch.first, e0, att,
-                                                                 D->nodes, D->nodes_alt, D->logits, D->rc);
+      if (tc)
+        k_node_update<L, E, uint16_t><<<ch.second - ch.first, 128, dyn, st>>>(
+            (const uint16_t*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->rc);
+      else
+        k_node_update<L, E, float><<<ch.second - ch.first, 128, dyn, st>>>(D->Y, D->dir, D->seg, ch.first, e0, att,
+                                                                          D->nodes, D->nodes_alt, D->logits, D->rc);
       ++ctx->launches;
     }
   }
   ESG_CUDA(cudaGetLastError());
   if (node_block) std::swap(D->nodes, D->nodes_alt);
+}
+
+template <int H, int E>
+void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
+                  float* out, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 8);
+  const int ht = (out_len + 31) / 32;
+  if (ht <= 5)
+    k_heads<H, E, 5><<<blocks, 256, 0, st>>>(x, n, W, key_of, row_of, out_len, out);
+  else if (ht <= 8)
+    k_heads<H, E, 8><<<blocks, 256, 0, st>>>(x, n, W, key_of, row_of, out_len, out);
+  else
+    usage("head layout wider than 256 outputs");
 }
 
 template <int L, int E>
@@ -875,17 +894,13 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   if (D->n_owned) {
     const int64_t n = (int64_t)D->n_owned * out_len;
     Prof pr(D, st, ESG_PROF_HEADS);
-    const int nk = (int)M->heads.keys.size();
-    k_heads<H, E><<<(unsigned)((D->n_owned + 7) / 8), 256, nk * E * sizeof(float), st>>>(
-        D->nodes, D->n_owned, D->head_w[0], nk, D->head_hptr, D->head_row, D->head_key, out_len, D->node_out);
+    launch_heads<H, E>(D->nodes, D->n_owned, D->head_w[0], D->head_key, D->head_row, out_len, D->node_out, st);
     ++ctx->launches;
   }
   if (D->n_edges) {
     const int64_t n = D->n_edges * out_len;
     Prof pr(D, st, ESG_PROF_HEADS);
-    const int nk = (int)M->heads.keys.size();
-    k_heads<H, E><<<(unsigned)((D->n_edges + 7) / 8), 256, nk * E * sizeof(float), st>>>(
-        D->edges, D->n_edges, D->head_w[1], nk, D->head_hptr, D->head_row, D->head_key, out_len, D->edge_out);
+    launch_heads<H, E>(D->edges, D->n_edges, D->head_w[1], D->head_key, D->head_row, out_len, D->edge_out, st);
     ++ctx->launches;
   }
   ESG_CUDA(cudaEventRecord(D->ev[3], st));

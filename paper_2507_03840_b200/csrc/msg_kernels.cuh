@@ -35,6 +35,14 @@ __device__ __forceinline__ int64_t a1_index(int64_t el, int k) {
   return (tile * (KTOT / 64) + kc) * 8192 + r * 64 + (((w >> 3) ^ (r & 7)) << 3) + (w & 7);
 }
 
+// 4 consecutive Y values as float4 from fp32 or bf16 storage
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4(const uint16_t* p) {
+  const uint2 w = __ldg(reinterpret_cast<const uint2*>(p));
+  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
+                     __uint_as_float(w.y & 0xffff0000u));
+}
+
 __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
   return make_float4(fmaf(d, x.x, a.x), fmaf(d, x.y, a.y), fmaf(d, x.z, a.z), fmaf(d, x.w, a.w));
 }
@@ -92,8 +100,8 @@ __global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4, 4
 
 // ops.h:115-117 rotate back with D^T then ops.h:265-283 residual add in
 // place.  Thread = (edge, 4-channel quad); 32 edges per CTA.
-template <int L, int E>
-__global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rotate_out_edge(const float* __restrict__ Yin,
+template <int L, int E, typename YT>
+__global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rotate_out_edge(const YT* __restrict__ Yin,
                                                                const float* __restrict__ dir, int64_t e0, int64_t n_e,
                                                                float* __restrict__ edges, WigRecipe rc) {
   using G = Geo<L>;
@@ -107,7 +115,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
   __syncthreads();
   wigner_tile_gen<L, DSP>(sdir, ne, sD);
   if (e < ne) {
-    const float4* yr = reinterpret_cast<const float4*>(Yin + (t0 + e - e0) * H * E) + q;
+    const YT* yr = Yin + (t0 + e - e0) * H * E + 4 * q;
     const float* D = sD + e * DSP;
     float4* row = reinterpret_cast<float4*>(edges + (t0 + e) * H * E) + q;
 #pragma unroll
@@ -116,7 +124,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
       float4 y[2 * L + 1], old[2 * L + 1];
 #pragma unroll
       for (int b = -l; b <= l; ++b) {
-        y[b + l] = __ldg(yr + G::mrow(l, b) * Q);  // order-major rows
+        y[b + l] = ld4(yr + G::mrow(l, b) * E);  // order-major rows
         old[b + l] = row[(l * l + l + b) * Q];
       }
 #pragma unroll
@@ -137,8 +145,8 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
 // by alpha and parks it in SMEM; thread (h, quad) then adds the tile's rows
 // in edge order -- a fixed order, so the result depends only on the segment
 // (partition-invariant and deterministic).  Dynamic SMEM: D + messages.
-template <int L, int E>
-__global__ void __launch_bounds__(128) k_node_update(const float* __restrict__ Yin, const float* __restrict__ dir,
+template <int L, int E, typename YT>
+__global__ void __launch_bounds__(128) k_node_update(const YT* __restrict__ Yin, const float* __restrict__ dir,
                                                      const int64_t* __restrict__ seg, int j0, int64_t e0,
                                                      const float* __restrict__ att,
                                                      const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
@@ -161,11 +169,11 @@ __global__ void __launch_bounds__(128) k_node_update(const float* __restrict__ Y
     float* lg = logit_scratch + (b - e0);
     float mx = -INFINITY;
     for (int64_t k = b + t; k < en; k += 128) {
-      const float4* y = reinterpret_cast<const float4*>(Yin + (k - e0) * HE);
+      const YT* y = Yin + (k - e0) * HE;
       float s = 0.f;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const float4 v = __ldg(y + q);
+        const float4 v = ld4(y + 4 * q);
         s = fmaf(att[4 * q], v.x, s);
         s = fmaf(att[4 * q + 1], v.y, s);
         s = fmaf(att[4 * q + 2], v.z, s);
@@ -198,7 +206,7 @@ __global__ void __launch_bounds__(128) k_node_update(const float* __restrict__ Y
       __syncthreads();
       wigner_tile_gen<L, DSP>(sdir, ne, sD);
       if (e < ne) {
-        const float4* yr = reinterpret_cast<const float4*>(Yin + (k0 + e - e0) * HE) + q;
+        const YT* yr = Yin + (k0 + e - e0) * HE + 4 * q;
         const float* D = sD + e * DSP;
         const float al = sA[e];
         float4* mrow = reinterpret_cast<float4*>(sM + e * HE) + q;
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(128) k_node_update(const float* __restrict__ Y
           const int dd = 2 * l + 1;
           float4 y[2 * L + 1];
 #pragma unroll
-          for (int bb = -l; bb <= l; ++bb) y[bb + l] = __ldg(yr + G::mrow(l, bb) * Q);
+          for (int bb = -l; bb <= l; ++bb) y[bb + l] = ld4(yr + G::mrow(l, bb) * E);
 #pragma unroll
           for (int a = -l; a <= l; ++a) {
             float4 m = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -153,7 +153,7 @@ struct Shape {
 template <int L, int E>
 __global__ void __launch_bounds__(THREADS, 1)
     k_so2_tc(const uint8_t* __restrict__ A1, int64_t n_e, const uint8_t* __restrict__ W1,
-             const uint8_t* __restrict__ W2, float* __restrict__ Y, int gate) {
+             const uint8_t* __restrict__ W2, uint16_t* __restrict__ Y, int gate) {
   using G = Geo<L>;
   using S = Shape<L, E>;
   using Y1 = typename S::Y1;
@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(bar(EB + s), 1);
     }
     mbar_init(bar(L1F), 1);
-    for (int c = 0; c < 4; ++c) mbar_init(bar(A2F + c), 128);
+    mbar_init(bar(A2F), 256);  // chunk 0 is gated by both epilogue halves
+    for (int c = 1; c < 4; ++c) mbar_init(bar(A2F + c), 128);
     mbar_init(bar(L2F), 1);
     mbar_init(bar(L2E), 256);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -296,10 +297,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) s[i] = gate ? 1.f / (1.f + __expf(-v[i])) : 1.f;
         }
-        for (int c2 = half; c2 < N1P / 64; c2 += 2) {
+        // chunk 0 (columns 0..63) is split across the halves so lin2 can start
+        // as early as possible; chunks 1.. alternate between the halves
+        for (int c2 = 0; c2 < N1P / 64; ++c2) {
+          if (c2 > 0 && (c2 & 1) != (half ^ 1)) continue;
           const uint32_t cb = sA2 + (uint32_t)c2 * A_CHUNK;
 #pragma unroll
           for (int hq = 0; hq < 2; ++hq) {
+            if (c2 == 0 && hq != half) continue;
             const int q = 2 * c2 + hq;
             float v[32];
             if (q * 32 < N1) {
@@ -326,15 +331,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(bar(L2F), l2p);
         l2p ^= 1;
         tc_fence_after();
-        float* yrow = Y + (e0 + row) * (G::H * E) + G::moff(m) * E;
+        uint16_t* yrow = Y + (e0 + row) * (G::H * E) + G::moff(m) * E;  // bf16 order-major rows
         for (int q = half; q * 32 < N2; q += 2) {
           float v[32];
           tmem_ld32(t_y + lane_off + q * 32, v);
           if (valid) {
             const int nv = (N2 - q * 32) < 32 ? (N2 - q * 32) : 32;
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              if (i < nv) *(float4*)(yrow + q * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            for (int i = 0; i < 32; i += 8)
+              if (i < nv)
+                *(uint4*)(yrow + q * 32 + i) = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
+                                                          pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
           }
         }
         tc_fence_before();
@@ -353,8 +360,8 @@ bool so2_tc_available(int L, int E) { return L == 4 && E == 16; }
 
 // A1: tiled, pre-swizzled bf16 operand (so2_tc_a1_bytes per chunk); W1/W2
 // packed by so2_tc_pack_weights.
-void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2, float* Y,
-                   int gate, cudaStream_t st) {
+void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2,
+                   uint16_t* Y, int gate, cudaStream_t st) {
   if (!so2_tc_available(L, E)) usage("tcgen05 SO(2) chain is instantiated for l_max 4, e_width 16");
   static int n_sm = 0;
   if (!n_sm) {
