@@ -41,11 +41,12 @@ H, E = 25, 16
 ROW = H * E * 4  # 1600 B fp32 feature row
 A1_BYTES = 1280 * 2  # bf16 order-major operand, m-blocks padded to 64
 PROF_NAMES = ["init", "rotate_in", "so2_linears", "rotate_out_edge", "node_update", "heads", "halo", "copy"]
+Y_BF16 = H * E * 2  # lin2 output, bf16 in the tensor-core path
 BYTES_PER_EDGE = {
     "rotate_in": ROW + 12 + 8 + A1_BYTES,        # edge row + dir + indices + A1 write
-    "so2_linears": A1_BYTES + ROW,                # A1 read + Y write
-    "rotate_out_edge": ROW + 12 + 2 * ROW,        # Y read + dir + edge row RMW
-    "node_update": ROW + 12,                      # Y read + dir (+ node rows, amortised)
+    "so2_linears": A1_BYTES + Y_BF16,             # A1 read + Y write
+    "rotate_out_edge": Y_BF16 + 12 + 2 * ROW,     # Y read + dir + edge row RMW
+    "node_update": Y_BF16 + 12,                   # Y read + dir (+ node rows, amortised)
 }
 
 

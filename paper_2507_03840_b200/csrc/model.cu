@@ -155,45 +155,43 @@ __global__ void k_copy_rows(const float* __restrict__ src, float* __restrict__ d
 
 // ---------------------------------------------------------- heads
 // ops.h:287-335: out[i][off_k + r] = sum_c w_k[c] x[i][L^2 + r][c].
-// One warp per item (grid-stride): the item's H x E row is staged in shared
-// memory, lane t produces outputs j = t + 32 u (u < HT) with its keys' weight
-// rows held in registers; stores are coalesced along j.  Sequential fp32 sum
-// over the channels without FMA, as ops.h:293-306 does.
-template <int H, int E, int HT>
+// Tiles of 32 items: the CTA stages the 32 rows (H x E each) in shared memory
+// with coalesced float4 loads, then thread j (one per head output) computes
+// output j of every item in the tile with its key's weight row in registers;
+// stores are coalesced along j.  Sequential fp32 sum over the channels
+// without FMA, as ops.h:293-306 does.
+template <int H, int E>
 __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int64_t n_items,
                                                const float* __restrict__ W, const int* __restrict__ key_of,
                                                const int* __restrict__ row_of, int out_len, float* __restrict__ out) {
-  __shared__ __align__(16) float sx[8][H * E];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float w[HT][E];
-  int row[HT];
+  constexpr int TI = 32;
+  extern __shared__ __align__(16) float sx[];  // TI x H x E
+  const int j = threadIdx.x;
+  float w[E];
+  int row = 0;
+  if (j < out_len) {
+    row = row_of[j];
+    const int k = key_of[j];
 #pragma unroll
-  for (int u = 0; u < HT; ++u) {
-    const int j = lane + 32 * u;
-    row[u] = j < out_len ? row_of[j] : 0;
-    const int k = j < out_len ? key_of[j] : 0;
-#pragma unroll
-    for (int c = 0; c < E; ++c) w[u][c] = W[k * E + c];
+    for (int c = 0; c < E; ++c) w[c] = W[k * E + c];
   }
-  const int64_t warps = (int64_t)gridDim.x * 8;
-  for (int64_t it = (int64_t)blockIdx.x * 8 + warp; it < n_items; it += warps) {
-    const float4* src = reinterpret_cast<const float4*>(x + it * (H * E));
-    float4* dst = reinterpret_cast<float4*>(sx[warp]);
-    for (int q = lane; q < H * E / 4; q += 32) dst[q] = __ldg(src + q);
-    __syncwarp();
-    float* o = out + it * out_len;
-#pragma unroll
-    for (int u = 0; u < HT; ++u) {
-      const int j = lane + 32 * u;
-      if (j < out_len) {
-        const float* plane = sx[warp] + row[u] * E;
+  const int64_t n_tiles = (n_items + TI - 1) / TI;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t i0 = tile * TI;
+    const int ni = (int)(n_items - i0 < TI ? n_items - i0 : TI);
+    const float4* src = reinterpret_cast<const float4*>(x + i0 * (H * E));
+    float4* dst = reinterpret_cast<float4*>(sx);
+    for (int q = threadIdx.x; q < ni * H * E / 4; q += blockDim.x) dst[q] = __ldg(src + q);
+    __syncthreads();
+    if (j < out_len)
+      for (int it = 0; it < ni; ++it) {
+        const float* plane = sx + (it * H + row) * E;
         float acc = 0.f;
 #pragma unroll
-        for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[u][c], plane[c]));
-        o[j] = acc;
+        for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[c], plane[c]));
+        out[(i0 + it) * out_len + j] = acc;
       }
-    }
-    __syncwarp();
+    __syncthreads();
   }
 }
 
@@ -848,14 +846,16 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
 template <int H, int E>
 void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
                   float* out, cudaStream_t st) {
-  const unsigned blocks = (unsigned)std::min<int64_t>((n + 7) / 8, 148 * 8);
-  const int ht = (out_len + 31) / 32;
-  if (ht <= 5)
-    k_heads<H, E, 5><<<blocks, 256, 0, st>>>(x, n, W, key_of, row_of, out_len, out);
-  else if (ht <= 8)
-    k_heads<H, E, 8><<<blocks, 256, 0, st>>>(x, n, W, key_of, row_of, out_len, out);
-  else
-    usage("head layout wider than 256 outputs");
+  if (out_len > 256) usage("head layout wider than 256 outputs");
+  constexpr int smem = 32 * H * E * (int)sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    ESG_CUDA(cudaFuncSetAttribute(k_heads<H, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int threads = ((out_len + 31) / 32) * 32;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 31) / 32, 148 * 4);
+  k_heads<H, E><<<blocks, threads, smem, st>>>(x, n, W, key_of, row_of, out_len, out);
 }
 
 template <int L, int E>
