@@ -164,8 +164,8 @@ template <int H, int E>
 __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int64_t n_items,
                                                const float* __restrict__ W, const int* __restrict__ key_of,
                                                const int* __restrict__ row_of, int out_len, float* __restrict__ out) {
-  constexpr int TI = 32;
-  extern __shared__ __align__(16) float sx[];  // TI x H x E
+  constexpr int TI = 32, PS = E + 4;  // plane stride padded: distinct rows hit distinct banks
+  extern __shared__ __align__(16) float sx[];  // TI x H x PS
   const int j = threadIdx.x;
   float w[E];
   int row = 0;
@@ -180,12 +180,14 @@ __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int6
     const int64_t i0 = tile * TI;
     const int ni = (int)(n_items - i0 < TI ? n_items - i0 : TI);
     const float4* src = reinterpret_cast<const float4*>(x + i0 * (H * E));
-    float4* dst = reinterpret_cast<float4*>(sx);
-    for (int q = threadIdx.x; q < ni * H * E / 4; q += blockDim.x) dst[q] = __ldg(src + q);
+    for (int q = threadIdx.x; q < ni * H * E / 4; q += blockDim.x) {
+      const int pl = q / (E / 4), w4 = q % (E / 4);  // plane (item, row), float4 within it
+      *reinterpret_cast<float4*>(sx + pl * PS + 4 * w4) = __ldg(src + q);
+    }
     __syncthreads();
     if (j < out_len)
       for (int it = 0; it < ni; ++it) {
-        const float* plane = sx + (it * H + row) * E;
+        const float* plane = sx + (it * H + row) * PS;
         float acc = 0.f;
 #pragma unroll
         for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[c], plane[c]));
@@ -786,11 +788,12 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     const int64_t n = e1 - e0;
     if (n > 0) {
       const unsigned tiles = (unsigned)((n + 15) / 16);
-      constexpr int RI_THREADS = 16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4;  // >= 4 warps for the Wigner groups
+      const unsigned ri_tiles = (unsigned)((n + 31) / 32);
+      constexpr int RI_THREADS = 32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4;  // >= 4 warps for the Wigner groups
       if (tc) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
-          k_rotate_in<L, E, 64, uint16_t><<<tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
+          k_rotate_in<L, E, 64, uint16_t><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
                                                                          D->dir, e0, n, (uint16_t*)D->A1, D->rc);
         }
         ++ctx->launches;
@@ -801,7 +804,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       } else {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
-          k_rotate_in<L, E, 1, float><<<tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
+          k_rotate_in<L, E, 1, float><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
                                                                     D->dir, e0, n, (float*)D->A1, D->rc);
         }
         Prof pr(D, st, ESG_PROF_SO2);
@@ -847,7 +850,7 @@ template <int H, int E>
 void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
                   float* out, cudaStream_t st) {
   if (out_len > 256) usage("head layout wider than 256 outputs");
-  constexpr int smem = 32 * H * E * (int)sizeof(float);
+  constexpr int smem = 32 * H * (E + 4) * (int)sizeof(float);
   static bool attr = false;
   if (!attr) {
     ESG_CUDA(cudaFuncSetAttribute(k_heads<H, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

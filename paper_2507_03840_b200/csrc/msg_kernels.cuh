@@ -50,9 +50,10 @@ __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
 // ops.h:68-122: message = [src | dst | edge] per harmonic row, rotated into
 // the edge frame with D_l (kernels.h:73-96), permuted to order-major rows
 // (kernels.h:98-115), written as the A1 operand of the SO(2) linears.
-// Thread = (edge, part in {src,dst,edge}, 4-channel quad); 16 edges per CTA.
+// Thread = (edge, part in {src,dst,edge}, 4-channel quad); 32 edges per CTA
+// (the Wigner warps then run full 32-lane tiles).
 template <int L, int E, int KPAD, typename OutT>
-__global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4, 4) k_rotate_in(const float* __restrict__ nodes,
+__global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 2) k_rotate_in(const float* __restrict__ nodes,
                                                              const float* __restrict__ edges,
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(16 * 3 * E / 4 < 128 ? 128 : 16 * 3 * E / 4, 4
                                                              OutT* __restrict__ A1, WigRecipe rc) {
   using G = Geo<L>;
   using Y = Lay1<L, E, KPAD>;
-  constexpr int TE = 16, DSP = G::DS + 2, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
+  constexpr int TE = 32, DSP = G::DS + 2, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
   __shared__ float sD[TE * DSP];
   __shared__ float sdir[TE * 3];
   const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
