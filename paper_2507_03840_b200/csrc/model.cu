@@ -24,7 +24,8 @@
 namespace esg {
 
 void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2,
-                   uint16_t* Y, int gate, cudaStream_t st);  // so2_tc.cu (Y in bf16)
+                   uint16_t* Y, int gate, const float* att, float* logits,
+                   cudaStream_t st);  // so2_tc.cu (Y in bf16, node-block logits)
 bool so2_tc_available(int L, int E);
 
 namespace {
@@ -799,7 +800,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         ++ctx->launches;
         Prof pr(D, st, ESG_PROF_SO2);
         so2_tc_launch(L, E, (const uint16_t*)D->A1, n, D->w1b[bidx], D->w2b[bidx], (uint16_t*)D->Y,
-                      M->cfg.gate_enabled, st);
+                      M->cfg.gate_enabled, att, node_block ? D->logits : nullptr, st);
         ++ctx->launches;
       } else {
         {
@@ -829,15 +830,17 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       constexpr int dyn = (32 * H * E + 32 * (Geo<L>::DS + 2)) * (int)sizeof(float);
       static bool attr = false;
       if (!attr) {
-        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      dyn));
+        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, uint16_t, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
         attr = true;
       }
       if (tc)
-        k_node_update<L, E, uint16_t><<<ch.second - ch.first, 128, dyn, st>>>(
+        k_node_update<L, E, uint16_t, true><<<ch.second - ch.first, 128, dyn, st>>>(
             (const uint16_t*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->rc);
       else
-        k_node_update<L, E, float><<<ch.second - ch.first, 128, dyn, st>>>(D->Y, D->dir, D->seg, ch.first, e0, att,
+        k_node_update<L, E, float, false><<<ch.second - ch.first, 128, dyn, st>>>(D->Y, D->dir, D->seg, ch.first, e0, att,
                                                                           D->nodes, D->nodes_alt, D->logits, D->rc);
       ++ctx->launches;
     }

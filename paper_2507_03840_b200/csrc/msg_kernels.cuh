@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
 // by alpha and parks it in SMEM; thread (h, quad) then adds the tile's rows
 // in edge order -- a fixed order, so the result depends only on the segment
 // (partition-invariant and deterministic).  Dynamic SMEM: D + messages.
-template <int L, int E, typename YT>
+template <int L, int E, typename YT, bool LOGITS_GIVEN>
 __global__ void __launch_bounds__(128) k_node_update(const YT* __restrict__ Yin, const float* __restrict__ dir,
                                                      const int64_t* __restrict__ seg, int j0, int64_t e0,
                                                      const float* __restrict__ att,
@@ -170,17 +170,22 @@ __global__ void __launch_bounds__(128) k_node_update(const YT* __restrict__ Yin,
     float* lg = logit_scratch + (b - e0);
     float mx = -INFINITY;
     for (int64_t k = b + t; k < en; k += 128) {
-      const YT* y = Yin + (k - e0) * HE;
-      float s = 0.f;
+      float s;
+      if (LOGITS_GIVEN) {  // written by the tensor-core epilogue
+        s = lg[k - b];
+      } else {
+        const YT* y = Yin + (k - e0) * HE;
+        s = 0.f;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const float4 v = ld4(y + 4 * q);
-        s = fmaf(att[4 * q], v.x, s);
-        s = fmaf(att[4 * q + 1], v.y, s);
-        s = fmaf(att[4 * q + 2], v.z, s);
-        s = fmaf(att[4 * q + 3], v.w, s);
+        for (int q = 0; q < Q; ++q) {
+          const float4 v = ld4(y + 4 * q);
+          s = fmaf(att[4 * q], v.x, s);
+          s = fmaf(att[4 * q + 1], v.y, s);
+          s = fmaf(att[4 * q + 2], v.z, s);
+          s = fmaf(att[4 * q + 3], v.w, s);
+        }
+        lg[k - b] = s;
       }
-      lg[k - b] = s;
       mx = fmaxf(mx, s);
     }
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));

@@ -153,7 +153,8 @@ struct Shape {
 template <int L, int E>
 __global__ void __launch_bounds__(THREADS, 1)
     k_so2_tc(const uint8_t* __restrict__ A1, int64_t n_e, const uint8_t* __restrict__ W1,
-             const uint8_t* __restrict__ W2, uint16_t* __restrict__ Y, int gate) {
+             const uint8_t* __restrict__ W2, uint16_t* __restrict__ Y, int gate, const float* __restrict__ att,
+             float* __restrict__ logits) {
   using G = Geo<L>;
   using S = Shape<L, E>;
   using Y1 = typename S::Y1;
@@ -335,6 +336,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int q = half; q * 32 < N2; q += 2) {
           float v[32];
           tmem_ld32(t_y + lane_off + q * 32, v);
+          if (m == 0 && q == 0 && logits != nullptr && valid) {
+            // ops.h:203-209 attention logit from the l = 0 channels (msg row 0
+            // == y row 0 since D_0 = 1), taken from the fp32 accumulator
+            float lg = 0.f;
+#pragma unroll
+            for (int c = 0; c < E; ++c) lg = fmaf(__ldg(att + c), v[c], lg);
+            logits[e0 + row] = lg;
+          }
           if (valid) {
             const int nv = (N2 - q * 32) < 32 ? (N2 - q * 32) : 32;
 #pragma unroll
@@ -361,7 +370,7 @@ bool so2_tc_available(int L, int E) { return L == 4 && E == 16; }
 // A1: tiled, pre-swizzled bf16 operand (so2_tc_a1_bytes per chunk); W1/W2
 // packed by so2_tc_pack_weights.
 void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2,
-                   uint16_t* Y, int gate, cudaStream_t st) {
+                   uint16_t* Y, int gate, const float* att, float* logits, cudaStream_t st) {
   if (!so2_tc_available(L, E)) usage("tcgen05 SO(2) chain is instantiated for l_max 4, e_width 16");
   static int n_sm = 0;
   if (!n_sm) {
@@ -374,7 +383,7 @@ void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t
   const int grid = (int)(tiles < n_sm ? tiles : n_sm);
   if (grid > 0)
     k_so2_tc<4, 16><<<grid, THREADS, SMEM_BYTES, st>>>((const uint8_t*)A1, n_e, (const uint8_t*)W1,
-                                                       (const uint8_t*)W2, Y, gate);
+                                                       (const uint8_t*)W2, Y, gate, att, logits);
   ESG_CUDA(cudaGetLastError());
 }
 
