@@ -165,7 +165,7 @@ template <int H, int E>
 __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int64_t n_items,
                                                const float* __restrict__ W, const int* __restrict__ key_of,
                                                const int* __restrict__ row_of, int out_len, float* __restrict__ out) {
-  constexpr int TI = 32, PS = E + 4;  // plane stride padded: distinct rows hit distinct banks
+  constexpr int TI = 16, PS = E + 4;  // plane stride padded: distinct rows hit distinct banks
   extern __shared__ __align__(16) float sx[];  // TI x H x PS
   const int j = threadIdx.x;
   float w[E];
@@ -713,7 +713,9 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   D->A1 = (void*)dalloc<uint8_t>(std::max(a1_fp32, a1_bf16));
   // the K padding slots of the tensor-core image are never written again
   ESG_CUDA(cudaMemset(D->A1, 0, std::max(a1_fp32, a1_bf16)));
-  D->Y = dalloc<float>((size_t)D->chunk_cap * row);
+  // fp32 rows (CUDA-core path) or bf16 tiles of 128 edges (tcgen05 epilogue)
+  D->Y = (float*)dalloc<uint8_t>(std::max((size_t)D->chunk_cap * row * 4,
+                                          (size_t)((D->chunk_cap + 127) / 128) * 128 * row * 2));
   D->logits = dalloc<float>((size_t)D->chunk_cap);
   D->node_out = dalloc<float>((size_t)std::max(n_owned, 1) * M->heads.out_len);
   D->edge_out = dalloc<float>((size_t)std::max<int64_t>(ne, 1) * M->heads.out_len);
@@ -827,7 +829,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     }
     if (node_block && ch.second > ch.first) {
       Prof pr(D, st, ESG_PROF_NODE);
-      constexpr int dyn = (32 * H * E + 32 * (Geo<L>::DS + 2)) * (int)sizeof(float);
+      constexpr int dyn = (16 * H * E + 16 * (Geo<L>::DS + 2)) * (int)sizeof(float);
       static bool attr = false;
       if (!attr) {
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -853,14 +855,14 @@ template <int H, int E>
 void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
                   float* out, cudaStream_t st) {
   if (out_len > 256) usage("head layout wider than 256 outputs");
-  constexpr int smem = 32 * H * (E + 4) * (int)sizeof(float);
+  constexpr int smem = 16 * H * (E + 4) * (int)sizeof(float);
   static bool attr = false;
   if (!attr) {
     ESG_CUDA(cudaFuncSetAttribute(k_heads<H, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   const int threads = ((out_len + 31) / 32) * 32;
-  const unsigned blocks = (unsigned)std::min<int64_t>((n + 31) / 32, 148 * 4);
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 15) / 16, 148 * 8);
   k_heads<H, E><<<blocks, threads, smem, st>>>(x, n, W, key_of, row_of, out_len, out);
 }
 

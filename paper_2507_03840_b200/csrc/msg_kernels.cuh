@@ -35,6 +35,20 @@ __device__ __forceinline__ int64_t a1_index(int64_t el, int k) {
   return (tile * (KTOT / 64) + kc) * 8192 + r * 64 + (((w >> 3) ^ (r & 7)) << 3) + (w & 7);
 }
 
+// Element index of Y(edge el, column c), columns in order-major row order.
+// fp32 (CUDA-core path): plain row-major.  bf16 (tensor-core path): tiles of
+// 128 edges, [tile][c / 8][el % 128][c % 8] -- the tcgen05 epilogue stores one
+// 16-byte unit per edge contiguously across the warp, and the consumers'
+// 4-column loads of consecutive edges fall into the same 128-byte lines.
+template <int HE>
+__device__ __forceinline__ int64_t y_index(const float*, int64_t el, int c) {
+  return el * HE + c;
+}
+template <int HE>
+__device__ __forceinline__ int64_t y_index(const uint16_t*, int64_t el, int c) {
+  return (((el >> 7) * (HE / 8) + (c >> 3)) << 10) + ((el & 127) << 3) + (c & 7);
+}
+
 // 4 consecutive Y values as float4 from fp32 or bf16 storage
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ float4 ld4(const uint16_t* p) {
@@ -116,7 +130,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
   __syncthreads();
   wigner_tile_gen<L, DSP>(sdir, ne, sD);
   if (e < ne) {
-    const YT* yr = Yin + (t0 + e - e0) * H * E + 4 * q;
+    const int64_t el = t0 + e - e0;
     const float* D = sD + e * DSP;
     float4* row = reinterpret_cast<float4*>(edges + (t0 + e) * H * E) + q;
 #pragma unroll
@@ -125,7 +139,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
       float4 y[2 * L + 1], old[2 * L + 1];
 #pragma unroll
       for (int b = -l; b <= l; ++b) {
-        y[b + l] = ld4(yr + G::mrow(l, b) * E);  // order-major rows
+        y[b + l] = ld4(Yin + y_index<H * E>(Yin, el, G::mrow(l, b) * E + 4 * q));  // order-major rows
         old[b + l] = row[(l * l + l + b) * Q];
       }
 #pragma unroll
@@ -147,13 +161,13 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
 // in edge order -- a fixed order, so the result depends only on the segment
 // (partition-invariant and deterministic).  Dynamic SMEM: D + messages.
 template <int L, int E, typename YT, bool LOGITS_GIVEN>
-__global__ void __launch_bounds__(128) k_node_update(const YT* __restrict__ Yin, const float* __restrict__ dir,
+__global__ void __launch_bounds__(128, 6) k_node_update(const YT* __restrict__ Yin, const float* __restrict__ dir,
                                                      const int64_t* __restrict__ seg, int j0, int64_t e0,
                                                      const float* __restrict__ att,
                                                      const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
                                                      float* __restrict__ logit_scratch, WigRecipe rc) {
   using G = Geo<L>;
-  constexpr int TE = 32, DSP = G::DS + 2, H = G::H, HE = H * E, Q = E / 4, HQ = H * Q;
+  constexpr int TE = 16, DSP = G::DS + 2, H = G::H, HE = H * E, Q = E / 4, HQ = H * Q;
   extern __shared__ __align__(16) float dyn[];
   float* sM = dyn;                 // TE x HE
   float* sD = dyn + TE * HE;       // TE x DSP
@@ -174,11 +188,10 @@ __global__ void __launch_bounds__(128) k_node_update(const YT* __restrict__ Yin,
       if (LOGITS_GIVEN) {  // written by the tensor-core epilogue
         s = lg[k - b];
       } else {
-        const YT* y = Yin + (k - e0) * HE;
         s = 0.f;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const float4 v = ld4(y + 4 * q);
+          const float4 v = ld4(Yin + y_index<HE>(Yin, k - e0, 4 * q));
           s = fmaf(att[4 * q], v.x, s);
           s = fmaf(att[4 * q + 1], v.y, s);
           s = fmaf(att[4 * q + 2], v.z, s);
@@ -212,7 +225,7 @@ __global__ void __launch_bounds__(128) k_node_update(const YT* __restrict__ Yin,
       __syncthreads();
       wigner_tile_gen<L, DSP>(sdir, ne, sD);
       if (e < ne) {
-        const YT* yr = Yin + (k0 + e - e0) * HE + 4 * q;
+        const int64_t el = k0 + e - e0;
         const float* D = sD + e * DSP;
         const float al = sA[e];
         float4* mrow = reinterpret_cast<float4*>(sM + e * HE) + q;
@@ -221,7 +234,7 @@ __global__ void __launch_bounds__(128) k_node_update(const YT* __restrict__ Yin,
           const int dd = 2 * l + 1;
           float4 y[2 * L + 1];
 #pragma unroll
-          for (int bb = -l; bb <= l; ++bb) y[bb + l] = ld4(yr + G::mrow(l, bb) * E);
+          for (int bb = -l; bb <= l; ++bb) y[bb + l] = ld4(Yin + y_index<HE>(Yin, el, G::mrow(l, bb) * E + 4 * q));
 #pragma unroll
           for (int a = -l; a <= l; ++a) {
             float4 m = make_float4(0.f, 0.f, 0.f, 0.f);

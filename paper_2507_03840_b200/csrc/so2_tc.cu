@@ -18,12 +18,13 @@
 //
 // Warp roles (352 threads, 1 CTA per SM, persistent over tiles):
 //   warp 0     A producer: one lane streams A1 chunks through a 4-stage ring
-//   warp 10    B producer: one lane streams weight chunks through a 3-stage ring
-//   warp 1     MMA issuer: one lane issues tcgen05.mma, commits free stages
-//   warps 2-9  epilogue: gate and Y drain; warp w owns TMEM lanes 32*(w%4)+
-//              and the even (w < 6) or odd (w >= 6) 64-column chunks, and
-//              hands each gated A2 chunk to lin2 through its own mbarrier so
-//              lin2 runs while the rest of the gate is still being computed.
+//   warp 18    B producer: one lane streams weight chunks through a 3-stage ring
+//   warp 1     MMA issuer: one elected lane issues tcgen05.mma, commits stages
+//   warps 2-9  gate: warp w owns TMEM lanes 32*(w%4)+ and half of the 64-column
+//              chunks; each gated A2 chunk goes to lin2 through its own
+//              mbarrier, so lin2 runs while the rest of the gate is computed
+//   warps 10-17 drain: lin2 accumulator -> bf16 Y rows (+ attention logits),
+//              overlapping the next order's gate.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -35,13 +36,49 @@ namespace esg {
 namespace {
 
 constexpr int TILE_M = 128;
-constexpr int THREADS = 352;
+constexpr int THREADS = 608;
 constexpr int NSA = 4;                  // A1 ring (streamed from HBM)
 constexpr int NSB = 3;                  // weight ring (L2-resident)
 constexpr int A_CHUNK = TILE_M * 128;   // 64 bf16 K x 128 rows = 16 KB
-constexpr int B_CHUNK = 256 * 128;      // up to 256 rows x 64 K = 32 KB
-constexpr int A2_BYTES = TILE_M * 256 * 2;
-constexpr int SMEM_BYTES = 1024 + NSA * A_CHUNK + NSB * B_CHUNK + A2_BYTES + 256;
+constexpr int B_STAGE = 256 * 128;      // up to 256 weight rows x 64 K = 32 KB
+constexpr int A2_BYTES = TILE_M * 256 * 2;  // gated operand of one order, 64 KB
+constexpr int GATE_THREADS = 256, DRAIN_THREADS = 256;
+constexpr int SMEM_BYTES = 1024 + NSA * A_CHUNK + NSB * B_STAGE + A2_BYTES + 256;
+
+// SO2_PROBE (tools/so2_probe.cu only): per-role clock64 accounting of the
+// mbarrier waits; compiled out of the library.
+#ifdef SO2_PROBE
+__device__ long long g_so2_probe[1024 * 32];
+#define PW(slot, ...)                  \
+  do {                                 \
+    const long long _t = clock64();    \
+    __VA_ARGS__;                       \
+    prb[slot] += clock64() - _t;       \
+  } while (0)
+#define PROBE_DECL long long prb[32] = {}; const long long prb_t0 = clock64(); long long prb_m = 0
+#define PROBE_MARK(slot) prb_m = clock64()
+__device__ long long g_so2_trace[256];
+#define PT(tile, idx)                                                            \
+  do {                                                                           \
+    if (blockIdx.x == 0 && (tile) == 2 * (int64_t)gridDim.x) g_so2_trace[idx] = clock64(); \
+  } while (0)
+#define PROBE_ACC(slot) prb[slot] += clock64() - prb_m
+#define PROBE_END(total_slot, cond)                                                          \
+  do {                                                                                       \
+    if (cond) {                                                                              \
+      prb[total_slot] = clock64() - prb_t0;                                                  \
+      for (int _i = 0; _i < 32; ++_i)                                                        \
+        if (prb[_i]) g_so2_probe[blockIdx.x * 32 + _i] = prb[_i];                            \
+    }                                                                                        \
+  } while (0)
+#else
+#define PW(slot, ...) __VA_ARGS__
+#define PROBE_MARK(slot)
+#define PROBE_ACC(slot)
+#define PT(tile, idx)
+#define PROBE_DECL
+#define PROBE_END(total_slot, cond)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -60,6 +97,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(bar),
       "r"(parity)
+      : "memory");
+}
+// waiting roles that are not on the MMA critical path park in the barrier
+// (suspend-time hint) instead of spinning against the MMA issuer's SMSP
+__device__ __forceinline__ void mbar_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(0x100000)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -85,6 +135,19 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
   return p;
+}
+// one lane of a converged warp (always the lowest); keeps the MMA issuer's
+// operands warp-uniform so they live in uniform registers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(p));
+  return p != 0;
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -127,11 +190,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+// two fp32 -> packed bf16x2 (round to nearest even), a in the low half
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
-  ua += 0x7fffu + ((ua >> 16) & 1u);
-  ub += 0x7fffu + ((ub >> 16) & 1u);
-  return (ua >> 16) | (ub & 0xffff0000u);
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(b), "f"(a));
+  return r;
 }
 
 template <int L, int E>
@@ -150,6 +213,24 @@ struct Shape {
   }
 };
 
+// TMEM column plan (l_max 4, e_width 16; N1 = 160 256 192 128 64, N2 = N1/2).
+// lin1 of order m accumulates into R_m = [R0[m], R0[m] + N1); once the gate
+// has consumed it, lin2 accumulates Y_m into its tail [R0[m] + N1 - N2, ...).
+// Consecutive orders' regions are disjoint, so lin1 of order m + 1 runs while
+// order m is gated; a region is reused only after every Y overlapping it has
+// been drained: lin1 of unit u waits for units < u - LAG[m] to be drained.
+__device__ __forceinline__ int r0_col(int m) { return m == 1 || m == 3 ? 0 : (m == 4 ? 448 : 256); }
+__device__ __forceinline__ int lag(int m) { return m <= 1 ? 2 : (m == 2 ? 1 : 4); }
+
+__device__ __forceinline__ uint32_t ld_acquire(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t addr, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+
 template <int L, int E>
 __global__ void __launch_bounds__(THREADS, 1)
     k_so2_tc(const uint8_t* __restrict__ A1, int64_t n_e, const uint8_t* __restrict__ W1,
@@ -159,16 +240,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   using S = Shape<L, E>;
   using Y1 = typename S::Y1;
   static_assert(2 * E == 32, "gate scalars assume 2E = 32");
+  static_assert(L == 4 && E == 16, "TMEM column plan is laid out for l_max 4, e_width 16");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sA = smem_u32(base);
   const uint32_t sB = sA + NSA * A_CHUNK;
-  const uint32_t sA2 = sB + NSB * B_CHUNK;
-  uint64_t* bars = (uint64_t*)(base + NSA * A_CHUNK + NSB * B_CHUNK + A2_BYTES);
+  const uint32_t sA2 = sB + NSB * B_STAGE;
+  uint64_t* bars = (uint64_t*)(base + NSA * A_CHUNK + NSB * B_STAGE + A2_BYTES);
   auto bar = [&](int i) { return smem_u32(&bars[i]); };
   const int FA = 0, EA = NSA, FB = 2 * NSA, EB = 2 * NSA + NSB;
-  const int L1F = 2 * NSA + 2 * NSB, L2F = L1F + 1, L2E = L1F + 2, A2F = L1F + 3;  // A2F + chunk (4)
-  uint32_t* tmem_slot = (uint32_t*)(bars + A2F + 4);
+  const int L1F = 2 * NSA + 2 * NSB;  // + (unit & 1): lin1 of the unit complete
+  const int L2F = L1F + 2;            // + (unit & 1): lin2 of the unit complete
+  const int A2F = L2F + 2;            // gated operand of the unit written to A2
+  const int A2E = A2F + 1;            // lin2 of the unit finished reading A2
+  uint32_t* drained = (uint32_t*)(bars + A2E + 1);  // units drained so far
+  uint32_t* tmem_slot = drained + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NSA; ++s) {
@@ -179,11 +265,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(bar(FB + s), 1);
       mbar_init(bar(EB + s), 1);
     }
-    mbar_init(bar(L1F), 1);
-    mbar_init(bar(A2F), 256);  // chunk 0 is gated by both epilogue halves
-    for (int c = 1; c < 4; ++c) mbar_init(bar(A2F + c), 128);
-    mbar_init(bar(L2F), 1);
-    mbar_init(bar(L2E), 256);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(L1F + b), 1);
+      mbar_init(bar(L2F + b), 1);
+    }
+    mbar_init(bar(A2F), GATE_THREADS);
+    mbar_init(bar(A2E), 1);
+    *drained = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -193,149 +281,206 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot, t_h = tmem, t_y = tmem + 256;
+  const uint32_t tmem = *tmem_slot;
   const int64_t n_tiles = (n_e + TILE_M - 1) / TILE_M;
 
   if (warp == 0) {
     // ---------------------------------------------------------- A producer
     if (lane == 0) {
+      PROBE_DECL;
       int st = 0;
       uint32_t ph = 0;
       const uint64_t pol = policy_evict_first();
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint8_t* a_tile = A1 + (size_t)tile * S::KCH * A_CHUNK;
         for (int c = 0; c < S::KCH; ++c) {  // order-major chunks in m order
-          mbar_wait(bar(EA + st), ph ^ 1);
+          PW(6, mbar_wait(bar(EA + st), ph ^ 1));
           mbar_expect_tx(bar(FA + st), A_CHUNK);
           bulk_g2s(sA + st * A_CHUNK, a_tile + (size_t)c * A_CHUNK, A_CHUNK, bar(FA + st), pol);
           if (++st == NSA) { st = 0; ph ^= 1; }
         }
       }
+      PROBE_END(7, true);
     }
-  } else if (warp == 10) {
+  } else if (warp == 18) {
     // ---------------------------------------------------------- B producer
+    // weights in MMA issue order: lin1 of unit u, then lin2 of unit u - 1
     if (lane == 0) {
+      PROBE_DECL;
       int st = 0;
       uint32_t ph = 0;
       const uint64_t pol = policy_evict_last();
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      auto load = [&](const uint8_t* src, uint32_t bytes) {
+        PW(8, mbar_wait(bar(EB + st), ph ^ 1));
+        mbar_expect_tx(bar(FB + st), bytes);
+        bulk_g2s(sB + st * B_STAGE, src, bytes, bar(FB + st), pol);
+        if (++st == NSB) { st = 0; ph ^= 1; }
+      };
+      auto load_w2 = [&](int m) {
+        const uint8_t* w2 = W2 + S::w2_off(m);
+        for (int j = 0; j < Y1::N1P(m) / 64; ++j) load(w2 + (size_t)j * Y1::N2(m) * 128, Y1::N2(m) * 128);
+      };
+      int prev = -1;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
         for (int m = 0; m <= L; ++m) {
-          const int N1 = Y1::N1(m), N2 = Y1::N2(m);
           const uint8_t* w1 = W1 + S::w1_off(m);
-          for (int j = 0; j < Y1::KP(m) / 64; ++j) {
-            mbar_wait(bar(EB + st), ph ^ 1);
-            mbar_expect_tx(bar(FB + st), N1 * 128);
-            bulk_g2s(sB + st * B_CHUNK, w1 + (size_t)j * N1 * 128, N1 * 128, bar(FB + st), pol);
-            if (++st == NSB) { st = 0; ph ^= 1; }
-          }
-          const uint8_t* w2 = W2 + S::w2_off(m);
-          for (int j = 0; j < Y1::N1P(m) / 64; ++j) {
-            mbar_wait(bar(EB + st), ph ^ 1);
-            mbar_expect_tx(bar(FB + st), N2 * 128);
-            bulk_g2s(sB + st * B_CHUNK, w2 + (size_t)j * N2 * 128, N2 * 128, bar(FB + st), pol);
-            if (++st == NSB) { st = 0; ph ^= 1; }
-          }
+          for (int c = 0; c < Y1::KP(m) / 64; ++c) load(w1 + (size_t)c * Y1::N1(m) * 128, Y1::N1(m) * 128);
+          if (prev >= 0) load_w2(prev);
+          prev = m;
         }
-      }
+      if (prev >= 0) load_w2(prev);
+      PROBE_END(9, true);
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // unit u = (tile, m) in issue order: lin1(u), then lin2(u - 1). The whole
+    // warp runs the loop; one elected lane issues the MMAs and commits.
+    {
+      PROBE_DECL;
       int sa = 0, sb = 0;
-      uint32_t pa = 0, pb = 0, l2e = 0, a2p[4] = {0, 0, 0, 0};
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        for (int m = 0; m <= L; ++m) {
-          const int N1 = Y1::N1(m), N2 = Y1::N2(m);
-          const uint32_t id1 = idesc_bf16(N1), id2 = idesc_bf16(N2);
-          for (int j = 0; j < Y1::KP(m) / 64; ++j) {
-            mbar_wait(bar(FA + sa), pa);
-            mbar_wait(bar(FB + sb), pb);
-            tc_fence_after();
+      uint32_t pa = 0, pb = 0;
+      const uint32_t drained_addr = smem_u32(drained);
+      auto wait_drained = [&](int need) {
+        if (need > 0)
+          while ((int)ld_acquire(drained_addr) < need) {
+          }
+      };
+      auto lin2 = [&](int m, int u) {
+        PW(18, wait_drained(u - 1));  // Y of unit u - 2 drained: L2F[u & 1] cannot run ahead
+        PW(3, mbar_wait(bar(A2F), u & 1));  // gated operand of unit u is in A2
+        tc_fence_after();
+        const uint32_t id2 = idesc_bf16(Y1::N2(m));
+        const uint32_t t_y = tmem + r0_col(m) + Y1::N1(m) - Y1::N2(m);
+        for (int j = 0; j < Y1::N1P(m) / 64; ++j) {
+          PW(4, mbar_wait(bar(FB + sb), pb));
+          tc_fence_after();
+          PW(17, {
+            if (elect_one()) {
+              const uint64_t da = sdesc(sA2 + j * A_CHUNK), db = sdesc(sB + sb * B_STAGE);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16(t_h, sdesc(sA + sa * A_CHUNK + k * 32), sdesc(sB + sb * B_CHUNK + k * 32), id1, (j | k) ? 1u : 0u);
-            tc_commit(bar(EA + sa));
-            tc_commit(bar(EB + sb));
+              for (int k = 0; k < 4; ++k) mma_bf16(t_y, da + 2 * k, db + 2 * k, id2, (j | k) ? 1u : 0u);
+              tc_commit(bar(EB + sb));
+            }
+            __syncwarp();
+          });
+          if (++sb == NSB) { sb = 0; pb ^= 1; }
+        }
+        if (elect_one()) {
+          tc_commit(bar(A2E));
+          tc_commit(bar(L2F + (u & 1)));
+        }
+        __syncwarp();
+      };
+      int u = 0, prev_m = -1;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+        for (int m = 0; m <= L; ++m, ++u) {
+          PW(2, {
+            wait_drained(u - lag(m));
+            tc_fence_after();
+          });
+          const uint32_t id1 = idesc_bf16(Y1::N1(m)), t_r = tmem + r0_col(m);
+          if (lane == 0) PT(tile, m * 8 + 0);
+          for (int c = 0; c < Y1::KP(m) / 64; ++c) {
+            PW(0, mbar_wait(bar(FA + sa), pa));
+            PW(1, mbar_wait(bar(FB + sb), pb));
+            tc_fence_after();
+            PW(16, {
+              if (elect_one()) {
+                const uint64_t da = sdesc(sA + sa * A_CHUNK), db = sdesc(sB + sb * B_STAGE);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mma_bf16(t_r, da + 2 * k, db + 2 * k, id1, (c | k) ? 1u : 0u);
+                tc_commit(bar(EA + sa));
+                tc_commit(bar(EB + sb));
+              }
+              __syncwarp();
+            });
             if (++sa == NSA) { sa = 0; pa ^= 1; }
             if (++sb == NSB) { sb = 0; pb ^= 1; }
           }
-          tc_commit(bar(L1F));
-          mbar_wait(bar(L2E), l2e ^ 1);  // previous lin2 accumulator drained
-          l2e ^= 1;
-          for (int j = 0; j < Y1::N1P(m) / 64; ++j) {
-            mbar_wait(bar(A2F + j), a2p[j]);  // gated chunk j of order m is in A2
-            a2p[j] ^= 1;
-            mbar_wait(bar(FB + sb), pb);
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16(t_y, sdesc(sA2 + j * A_CHUNK + k * 32), sdesc(sB + sb * B_CHUNK + k * 32), id2, (j | k) ? 1u : 0u);
-            tc_commit(bar(EB + sb));
-            if (++sb == NSB) { sb = 0; pb ^= 1; }
-          }
-          tc_commit(bar(L2F));
+          if (elect_one()) tc_commit(bar(L1F + (u & 1)));
+          __syncwarp();
+          if (lane == 0) PT(tile, m * 8 + 1);
+          if (prev_m >= 0) lin2(prev_m, u - 1);
+          if (lane == 0) PT(tile, m * 8 + 2);
+          prev_m = m;
         }
-      }
+      if (prev_m >= 0) lin2(prev_m, u - 1);
+      PROBE_END(5, lane == 0);
     }
   } else if (warp >= 2 && warp <= 9) {
-    // ------------------------------------------------------------ epilogue
+    // ---------------------------------------------------------------- gate
+    // warp w owns TMEM lanes 32*(w%4)+; the two halves take alternate
+    // 32-column groups.
     const int quad = warp & 3, half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    uint32_t l1p = 0, l2p = 0;
-    float s[32];
+    float sg[32];
+    PROBE_DECL;
+    int u = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+      for (int m = 0; m <= L; ++m, ++u) {
+        const uint32_t t_r = tmem + lane_off + r0_col(m);
+        const int N1 = Y1::N1(m);
+        PW(10, mbar_sleep(bar(L1F + (u & 1)), (u >> 1) & 1));
+        if (warp == 2 && lane == 0) PT(tile, 64 + m * 8 + 0);
+        tc_fence_after();
+        if (m == 0) {  // gate scalars from the l = 0 channels of order 0
+          PW(20, {
+            float v[32];
+            tmem_ld32(t_r, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sg[i] = gate ? __fdividef(1.f, 1.f + __expf(-v[i])) : 1.f;
+          });
+        }
+        if (u > 0) PW(14, mbar_sleep(bar(A2E), (u - 1) & 1));  // lin2 of unit u - 1 done with A2
+        if (warp == 2 && lane == 0) PT(tile, 64 + m * 8 + 1);
+        for (int q = half; q < Y1::N1P(m) / 32; q += 2) {
+          float v[32];
+          if (q * 32 < N1) {
+            tmem_ld32(t_r + q * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= sg[i];  // column 32q + i uses scalar i
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          const uint32_t cb = sA2 + (uint32_t)(q >> 1) * A_CHUNK;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, (q & 1) * 4 + j)),
+                         "r"(pack_bf16(v[8 * j], v[8 * j + 1])), "r"(pack_bf16(v[8 * j + 2], v[8 * j + 3])),
+                         "r"(pack_bf16(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16(v[8 * j + 6], v[8 * j + 7]))
+                         : "memory");
+        }
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(bar(A2F));
+        if (warp == 2 && lane == 0) PT(tile, 64 + m * 8 + 2);
+      }
+    PROBE_END(11, warp == 2 && lane == 0);
+  } else if (warp >= 10 && warp <= 17) {
+    // --------------------------------------------------------------- drain
+    const int quad = warp & 3, half = (warp - 10) >> 2;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    PROBE_DECL;
+    int u = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int64_t e0 = tile * TILE_M;
       const bool valid = e0 + row < n_e;
-      for (int m = 0; m <= L; ++m) {
-        const int N1 = Y1::N1(m), N1P = Y1::N1P(m), N2 = Y1::N2(m);
-        mbar_wait(bar(L1F), l1p);
-        l1p ^= 1;
+      for (int m = 0; m <= L; ++m, ++u) {
+        const int N2 = Y1::N2(m);
+        const uint32_t t_y = tmem + lane_off + r0_col(m) + Y1::N1(m) - N2;
+        PW(12, mbar_sleep(bar(L2F + (u & 1)), (u >> 1) & 1));
+        if (warp == 10 && lane == 0) PT(tile, 128 + m * 4 + 0);
         tc_fence_after();
-        if (m == 0) {  // gate scalars from the l = 0 channels of order 0
-          float v[32];
-          tmem_ld32(t_h + lane_off, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[i] = gate ? 1.f / (1.f + __expf(-v[i])) : 1.f;
-        }
-        // chunk 0 (columns 0..63) is split across the halves so lin2 can start
-        // as early as possible; chunks 1.. alternate between the halves
-        for (int c2 = 0; c2 < N1P / 64; ++c2) {
-          if (c2 > 0 && (c2 & 1) != (half ^ 1)) continue;
-          const uint32_t cb = sA2 + (uint32_t)c2 * A_CHUNK;
-#pragma unroll
-          for (int hq = 0; hq < 2; ++hq) {
-            if (c2 == 0 && hq != half) continue;
-            const int q = 2 * c2 + hq;
-            float v[32];
-            if (q * 32 < N1) {
-              tmem_ld32(t_h + lane_off + q * 32, v);
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= s[i];
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0.f;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int c = hq * 4 + j;
-              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, c)),
-                           "r"(pack_bf16(v[8 * j], v[8 * j + 1])), "r"(pack_bf16(v[8 * j + 2], v[8 * j + 3])),
-                           "r"(pack_bf16(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16(v[8 * j + 6], v[8 * j + 7]))
-                           : "memory");
-            }
-          }
-          fence_async_smem();
-          tc_fence_before();
-          mbar_arrive(bar(A2F + c2));
-        }
-        mbar_wait(bar(L2F), l2p);
-        l2p ^= 1;
-        tc_fence_after();
-        uint16_t* yrow = Y + (e0 + row) * (G::H * E) + G::moff(m) * E;  // bf16 order-major rows
+        // bf16 Y tile [c / 8][row][c % 8] (msg_kernels.cuh y_index): each
+        // 16-byte store of the warp lands next to its neighbour lane's
+        uint16_t* ytile = Y + tile * (int64_t)TILE_M * (G::H * E) + (int64_t)row * 8;
+        const int c0 = G::moff(m) * E;
         for (int q = half; q * 32 < N2; q += 2) {
           float v[32];
-          tmem_ld32(t_y + lane_off + q * 32, v);
+          tmem_ld32(t_y + q * 32, v);
           if (m == 0 && q == 0 && logits != nullptr && valid) {
             // ops.h:203-209 attention logit from the l = 0 channels (msg row 0
             // == y row 0 since D_0 = 1), taken from the fp32 accumulator
@@ -344,19 +489,29 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int c = 0; c < E; ++c) lg = fmaf(__ldg(att + c), v[c], lg);
             logits[e0 + row] = lg;
           }
+#ifdef SO2_PROBE_NOSTORE
+          if (valid && v[0] == 12345.f) {
+#else
           if (valid) {
+#endif
             const int nv = (N2 - q * 32) < 32 ? (N2 - q * 32) : 32;
 #pragma unroll
             for (int i = 0; i < 32; i += 8)
               if (i < nv)
-                *(uint4*)(yrow + q * 32 + i) = make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]),
-                                                          pack_bf16(v[i + 4], v[i + 5]), pack_bf16(v[i + 6], v[i + 7]));
+                *(uint4*)(ytile + (int64_t)((c0 + q * 32 + i) >> 3) * (TILE_M * 8)) =
+                    make_uint4(pack_bf16(v[i], v[i + 1]), pack_bf16(v[i + 2], v[i + 3]), pack_bf16(v[i + 4], v[i + 5]),
+                               pack_bf16(v[i + 6], v[i + 7]));
           }
         }
         tc_fence_before();
-        mbar_arrive(bar(L2E));
+        asm volatile("bar.sync 1, %0;\n" ::"n"(DRAIN_THREADS) : "memory");  // all drain lanes read their Y
+        if (warp == 10 && lane == 0) {
+          st_release(smem_u32(drained), (uint32_t)(u + 1));
+          PT(tile, 128 + m * 4 + 1);
+        }
       }
     }
+    PROBE_END(13, warp == 10 && lane == 0);
   }
   tc_fence_before();
   __syncthreads();
