@@ -11,16 +11,14 @@ namespace esg {
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+// bf16x2 round-to-nearest-even pack, first argument in the low half
+__device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 __device__ __forceinline__ void st4(uint16_t* p, float4 v) {
-  auto bf = [](float x) {
-    uint32_t u = __float_as_uint(x);
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return u >> 16;
-  };
-  uint2 w;
-  w.x = bf(v.x) | (bf(v.y) << 16);
-  w.y = bf(v.z) | (bf(v.w) << 16);
-  *reinterpret_cast<uint2*>(p) = w;
+  *reinterpret_cast<uint2*>(p) = make_uint2(bf16x2(v.x, v.y), bf16x2(v.z, v.w));
 }
 // Element index of A1(edge el, K index k).  KPAD == 1: plain row-major
 // (fp32 CUDA-core path).  KPAD == 64: the tensor-core image -- tiles of 128
@@ -47,6 +45,14 @@ __device__ __forceinline__ int64_t y_index(const float*, int64_t el, int c) {
 template <int HE>
 __device__ __forceinline__ int64_t y_index(const uint16_t*, int64_t el, int c) {
   return (((el >> 7) * (HE / 8) + (c >> 3)) << 10) + ((el & 127) << 3) + (c & 7);
+}
+
+// a1_index(el, k) - a1_index(el, 0): the within-tile-row offset of K index k
+template <int KPAD>
+__device__ __forceinline__ int a1_offset(int64_t el, int k) {
+  if (KPAD == 1) return k;
+  const int r7 = (int)(el & 7), w = k & 63;
+  return (k >> 6) * 8192 + (((w >> 3) ^ r7) - r7) * 8 + (w & 7);
 }
 
 // 4 consecutive Y values as float4 from fp32 or bf16 storage
@@ -92,6 +98,10 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 2
                          q;
     const float* D = sD + e * DSP;
     const int64_t el = t0 + e - e0;
+    // A1 element (el, k) with k = K0 + pq, K0 a compile-time multiple of 16
+    // and pq = p * E + 4 q < 48 fixed per thread (a1_index, split once)
+    const int pq = p * E + q * 4;
+    OutT* a1_row = A1 + a1_index<Y::KTOT, KPAD>(el, 0);
 #pragma unroll
     for (int l = 0; l <= L; ++l) {
       const int dd = 2 * l + 1;
@@ -104,8 +114,8 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 2
 #pragma unroll
         for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (a + l) * dd + (b + l)], x[b + l], acc);
         const int m = a < 0 ? -a : a;
-        const int k = Y::kofs(m) + (G::mrow(l, a) - G::moff(m)) * C3 + p * E + q * 4;
-        st4(A1 + a1_index<Y::KTOT, KPAD>(el, k), acc);
+        const int k = Y::kofs(m) + (G::mrow(l, a) - G::moff(m)) * C3 + pq;
+        st4(a1_row + a1_offset<KPAD>(el, k), acc);
       }
     }
   }
