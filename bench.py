@@ -50,6 +50,17 @@ BYTES_PER_EDGE = {
 }
 
 
+def measured_traffic(name):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per edge of a kernel
+    category, from the committed capture summary (profiles/traffic.json), or
+    None when that kernel has not been captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(name)
+    except (OSError, ValueError):
+        return None
+
+
 def env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -299,10 +310,15 @@ def run_ours(args):
         blocks = layers if name in ("node_update", "rotate_out_edge") else 2 * layers
         alg_bytes = BYTES_PER_EDGE[name] * net.n_edges * blocks * args.steps
         achieved = alg_bytes / (ms_cat[dom] / 1e3) / 1e9
+        launches_dom = max(int(n_cat[dom]), 1)
+        edges_per_launch = net.n_edges * blocks * args.steps / launches_dom
+        tr = measured_traffic(name)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "kernel": name, "peak_source": peak_kind,
-                "bytes_per_edge": BYTES_PER_EDGE[name],
-                "launches": int(n_cat[dom]), "avg_launch_ms": float(ms_cat[dom] / max(n_cat[dom], 1))}
+                "traffic": (tr["dram_bytes_per_edge"] * edges_per_launch) if tr else None,
+                "kernel": name, "peak_source": peak_kind,
+                "bytes_per_edge": BYTES_PER_EDGE[name], "edges_per_launch": edges_per_launch,
+                "traffic_source": tr.get("source") if tr else None,
+                "launches": int(n_cat[dom]), "avg_launch_ms": float(ms_cat[dom] / launches_dom)}
 
     # e2e through the public API with host buffers
     e2e = None
