@@ -829,17 +829,18 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     }
     if (node_block && ch.second > ch.first) {
       Prof pr(D, st, ESG_PROF_NODE);
-      constexpr int dyn = (16 * H * E + 16 * (Geo<L>::DS + 2)) * (int)sizeof(float);
+      constexpr int dyn = node_update_smem_floats<L, E, float>() * (int)sizeof(float);
+      constexpr int dyn_bf16 = node_update_smem_floats<L, E, uint16_t>() * (int)sizeof(float);
       static bool attr = false;
       if (!attr) {
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       dyn));
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, uint16_t, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bf16));
         attr = true;
       }
       if (tc)
-        k_node_update<L, E, uint16_t, true><<<ch.second - ch.first, 128, dyn, st>>>(
+        k_node_update<L, E, uint16_t, true><<<ch.second - ch.first, 128, dyn_bf16, st>>>(
             (const uint16_t*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->rc);
       else
         k_node_update<L, E, float, false><<<ch.second - ch.first, 128, dyn, st>>>(D->Y, D->dir, D->seg, ch.first, e0, att,

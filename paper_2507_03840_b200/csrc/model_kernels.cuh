@@ -81,6 +81,17 @@ __device__ __forceinline__ void align_to_y(float x, float y, float z, float R[9]
 #include "wigner_gen.cuh"
 namespace esg {
 
+// degrees l0..L of the recursion, one barrier per degree (compile-time l, so
+// only the degrees this l_max needs are instantiated)
+template <int L, int l, int DSP>
+__device__ __forceinline__ void wigner_levels(bool act, int warp, const float* R, float* d) {
+  if constexpr (l <= L) {
+    if (act) wigner_deg<l>(warp, R, d + Geo<L>::doff(l - 1), d + Geo<L>::doff(l));
+    __syncthreads();
+    wigner_levels<L, l + 1, DSP>(act, warp, R, d);
+  }
+}
+
 // Wigner blocks for a tile of ne <= 32 edges with the generated straight-line
 // recursion: lane = edge, warps 0..3 each own a quarter of every degree's
 // entries.  Needs blockDim.x >= 128; all threads must call it.  D rows use an
@@ -101,11 +112,7 @@ __device__ void wigner_tile_gen(const float* dirs, int ne, float* D) {
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int l = 2; l <= L; ++l) {
-    if (act) wigner_group(l, warp, R, D + lane * DSP + G::doff(l - 1), D + lane * DSP + G::doff(l));
-    __syncthreads();
-  }
+  wigner_levels<L, 2, DSP>(act, warp, R, D + lane * DSP);
 }
 
 // Ivanic-Ruedenberg recursion expanded on the host into flat recipes: entry

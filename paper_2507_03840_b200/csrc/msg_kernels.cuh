@@ -163,33 +163,128 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
   }
 }
 
-// ops.h:192-263.  One CTA per owned destination j; logits from the l = 0
-// channels (msg row 0 == y row 0 since D_0 = 1), max-subtracted softmax, then
-// out_j = node_j + sum_k alpha_k msg_k.  Tiles of 32 edges: thread (edge,
-// 4-channel quad) rotates its message back (float4, D from SMEM), scales it
-// by alpha and parks it in SMEM; thread (h, quad) then adds the tile's rows
-// in edge order -- a fixed order, so the result depends only on the segment
-// (partition-invariant and deterministic).  Dynamic SMEM: D + messages.
+// Row split of the back-rotation D^T y for the node update: four parts of
+// about equal FMA work (l_max 4: l = 4 with a <= 0, l = 4 with a > 0, l = 3,
+// l <= 2), one part per warp so every warp runs one straight-line path.
+// Lower l_max: part p takes degree p.
+template <int L>
+struct NodeSplit {
+  static_assert(L <= 4, "node update row split is laid out for l_max <= 4");
+  __host__ __device__ static constexpr bool owns(int p, int l, int a) {
+    return L == 4 ? (l == 4 ? (p == (a <= 0 ? 0 : 1)) : (l == 3 ? p == 2 : p == 3)) : l == p;
+  }
+  __host__ __device__ static constexpr int rows(int p) {
+    int n = 0;
+    for (int l = 0; l <= L; ++l)
+      for (int a = -l; a <= l; ++a) n += owns(p, l, a) ? 1 : 0;
+    return n;
+  }
+  static constexpr int RMAX = L == 4 ? 9 : 2 * L + 1;
+};
+
+// Y of one edge: from global memory (fp32 rows) or from the SMEM copy of the
+// edge tile (bf16, [col / 8][edge in tile][col % 8], like the global tiles)
+template <int HE>
+struct YGlobal {
+  const float* Y;
+  int64_t el;
+  __device__ __forceinline__ float4 operator()(int c) const { return ld4(Y + y_index<HE>(Y, el, c)); }
+};
+struct YTileSmem {
+  const uint16_t* sY;
+  int i;
+  __device__ __forceinline__ float4 operator()(int c) const {
+    const uint2 w = *reinterpret_cast<const uint2*>(sY + (((c >> 3) * 32 + i) << 3) + (c & 7));
+    return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
+                       __uint_as_float(w.y & 0xffff0000u));
+  }
+};
+
+// acc[slot of (l, a) in part P] += al * sum_b D[b][a] y_b for one edge
+template <int L, int E, int P, typename YSrc>
+__device__ __forceinline__ void node_part(const YSrc& ysrc, int q, const float* D, float al, float4* acc) {
+  using G = Geo<L>;
+  using S = NodeSplit<L>;
+  int r = 0;
+#pragma unroll
+  for (int l = 0; l <= L; ++l) {
+    bool any = false;
+#pragma unroll
+    for (int a = -l; a <= l; ++a) any |= S::owns(P, l, a);
+    if (!any) continue;
+    const int dd = 2 * l + 1;
+    float4 y[2 * L + 1];
+#pragma unroll
+    for (int b = -l; b <= l; ++b) y[b + l] = ysrc(G::mrow(l, b) * E + 4 * q);
+#pragma unroll
+    for (int a = -l; a <= l; ++a) {
+      if (!S::owns(P, l, a)) continue;
+      float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int b = -l; b <= l; ++b) m = fma4(D[G::doff(l) + (b + l) * dd + (a + l)], y[b + l], m);
+      acc[r] = make_float4(fmaf(al, m.x, acc[r].x), fmaf(al, m.y, acc[r].y), fmaf(al, m.z, acc[r].z),
+                           fmaf(al, m.w, acc[r].w));
+      ++r;
+    }
+  }
+}
+template <int L, int P>
+__device__ __forceinline__ void node_part_park(float* red, int slot, int q, int Q, const float4* acc) {
+  using G = Geo<L>;
+  int r = 0;
+#pragma unroll
+  for (int l = 0; l <= L; ++l)
+#pragma unroll
+    for (int a = -l; a <= l; ++a)
+      if (NodeSplit<L>::owns(P, l, a))
+        reinterpret_cast<float4*>(red)[(slot * G::H + l * l + l + a) * Q + q] = acc[r++];
+}
+
+// dynamic SMEM of k_node_update: D of the edge tile (+ its bf16 Y rows when
+// Y is bf16), reused for the slot partial sums
+template <int L, int E, typename YT>
+constexpr int node_update_smem_floats() {
+  constexpr int TE = 32, DSP = Geo<L>::DS + 2, NSLOT = 32 / (E / 4);
+  constexpr int tile = TE * DSP + (sizeof(YT) == 2 ? TE * Geo<L>::H * E / 2 : 0);
+  return tile > NSLOT * Geo<L>::H * E ? tile : NSLOT * Geo<L>::H * E;
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ops.h:192-263.  One CTA (4 warps) per owned destination j; logits from the
+// l = 0 channels (msg row 0 == y row 0 since D_0 = 1), max-subtracted
+// softmax, then out_j = node_j + sum_k alpha_k D_k^T y_k.  Tiles of 32
+// edges: the Wigner blocks go to SMEM, then warp p (row part p of NodeSplit)
+// lane (slot, quad) accumulates alpha_k D_k^T y_k of the tile's edges
+// slot, slot + NSLOT, ... in registers.  The NSLOT partial sums are added in
+// slot order at the end: a fixed order that depends only on the segment
+// (partition-invariant and deterministic).  Dynamic SMEM: node_update_smem_floats.
 template <int L, int E, typename YT, bool LOGITS_GIVEN>
-__global__ void __launch_bounds__(128, 6) k_node_update(const YT* __restrict__ Yin, const float* __restrict__ dir,
+__global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Yin, const float* __restrict__ dir,
                                                      const int64_t* __restrict__ seg, int j0, int64_t e0,
                                                      const float* __restrict__ att,
                                                      const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
                                                      float* __restrict__ logit_scratch, WigRecipe rc) {
   using G = Geo<L>;
-  constexpr int TE = 16, DSP = G::DS + 2, H = G::H, HE = H * E, Q = E / 4, HQ = H * Q;
+  constexpr int TE = 32, DSP = G::DS + 2, H = G::H, HE = H * E, Q = E / 4, HQ = H * Q, NSLOT = 32 / Q;
+  constexpr bool YSMEM = sizeof(YT) == 2;  // bf16 Y: stage the tile's rows in SMEM
   extern __shared__ __align__(16) float dyn[];
-  float* sM = dyn;                 // TE x HE
-  float* sD = dyn + TE * HE;       // TE x DSP
+  float* sD = dyn;  // TE x DSP; reused for the NSLOT x H x E partial sums
+  uint16_t* sY = reinterpret_cast<uint16_t*>(dyn + TE * DSP);  // [HE / 8][TE][8] bf16 (YSMEM)
   __shared__ float sdir[TE * 3];
   __shared__ float sA[TE];
   __shared__ float sred[4];
   const int j = j0 + blockIdx.x;
   const int64_t b = seg[j], en = seg[j + 1];
-  const int t = threadIdx.x;
-  const bool owner = t < HQ;  // thread (h, quad) owns one float4 of the output row
-  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (owner) out = reinterpret_cast<const float4*>(nodes_in + (int64_t)j * HE)[t];
+  const int t = threadIdx.x, part = t >> 5, slot = (t & 31) / Q, q = t % Q;
+  float4 acc[NodeSplit<L>::RMAX];
+#pragma unroll
+  for (int r = 0; r < NodeSplit<L>::RMAX; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (b < en) {
     float* lg = logit_scratch + (b - e0);
     float mx = -INFINITY;
@@ -200,12 +295,12 @@ __global__ void __launch_bounds__(128, 6) k_node_update(const YT* __restrict__ Y
       } else {
         s = 0.f;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const float4 v = ld4(Yin + y_index<HE>(Yin, k - e0, 4 * q));
-          s = fmaf(att[4 * q], v.x, s);
-          s = fmaf(att[4 * q + 1], v.y, s);
-          s = fmaf(att[4 * q + 2], v.z, s);
-          s = fmaf(att[4 * q + 3], v.w, s);
+        for (int qq = 0; qq < Q; ++qq) {
+          const float4 v = ld4(Yin + y_index<HE>(Yin, k - e0, 4 * qq));
+          s = fmaf(att[4 * qq], v.x, s);
+          s = fmaf(att[4 * qq + 1], v.y, s);
+          s = fmaf(att[4 * qq + 2], v.z, s);
+          s = fmaf(att[4 * qq + 3], v.w, s);
         }
         lg[k - b] = s;
       }
@@ -226,46 +321,73 @@ __global__ void __launch_bounds__(128, 6) k_node_update(const YT* __restrict__ Y
     if ((t & 31) == 0) sred[t >> 5] = z;
     __syncthreads();
     z = (sred[0] + sred[1]) + (sred[2] + sred[3]);
-    const int e = t / Q, q = t % Q;
     for (int64_t k0 = b; k0 < en; k0 += TE) {
       const int ne = (int)min64(TE, en - k0);
-      __syncthreads();
+      __syncthreads();  // the previous tile's D is no longer read
       for (int i = t; i < ne * 3; i += 128) sdir[i] = dir[(k0 - e0) * 3 + i];
       for (int i = t; i < ne; i += 128) sA[i] = lg[k0 - b + i] / z;
-      __syncthreads();
-      wigner_tile_gen<L, DSP>(sdir, ne, sD);
-      if (e < ne) {
-        const int64_t el = k0 + e - e0;
-        const float* D = sD + e * DSP;
-        const float al = sA[e];
-        float4* mrow = reinterpret_cast<float4*>(sM + e * HE) + q;
-#pragma unroll
-        for (int l = 0; l <= L; ++l) {
-          const int dd = 2 * l + 1;
-          float4 y[2 * L + 1];
-#pragma unroll
-          for (int bb = -l; bb <= l; ++bb) y[bb + l] = ld4(Yin + y_index<HE>(Yin, el, G::mrow(l, bb) * E + 4 * q));
-#pragma unroll
-          for (int a = -l; a <= l; ++a) {
-            float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int bb = -l; bb <= l; ++bb) m = fma4(D[G::doff(l) + (bb + l) * dd + (a + l)], y[bb + l], m);
-            mrow[(l * l + l + a) * Q] = make_float4(al * m.x, al * m.y, al * m.z, al * m.w);
-          }
+      if constexpr (YSMEM) {  // the tile's Y rows arrive while the Wigner blocks are computed
+        for (int u = t; u < (HE / 8) * ne; u += 128) {
+          const int blk = u / ne, i = u - blk * ne;
+          cp_async16(sY + ((blk * TE + i) << 3), Yin + y_index<HE>(Yin, k0 + i - e0, blk * 8));
         }
       }
       __syncthreads();
-      if (owner)
-        for (int ee = 0; ee < ne; ++ee) {
-          const float4 v = reinterpret_cast<const float4*>(sM + ee * HE)[t];
-          out.x += v.x;
-          out.y += v.y;
-          out.z += v.z;
-          out.w += v.w;
+      wigner_tile_gen<L, DSP>(sdir, ne, sD);
+      if constexpr (YSMEM) {
+        cp_async_wait_all();
+        __syncthreads();
+      }
+      for (int i = slot; i < ne; i += NSLOT) {
+        const float* D = sD + i * DSP;
+        const float al = sA[i];
+        if constexpr (YSMEM) {
+          const YTileSmem ys{sY, i};
+          switch (part) {
+            case 0: node_part<L, E, 0>(ys, q, D, al, acc); break;
+            case 1: node_part<L, E, 1>(ys, q, D, al, acc); break;
+            case 2: node_part<L, E, 2>(ys, q, D, al, acc); break;
+            default: node_part<L, E, 3>(ys, q, D, al, acc); break;
+          }
+        } else {
+          const YGlobal<HE> ys{reinterpret_cast<const float*>(Yin), k0 + i - e0};
+          switch (part) {
+            case 0: node_part<L, E, 0>(ys, q, D, al, acc); break;
+            case 1: node_part<L, E, 1>(ys, q, D, al, acc); break;
+            case 2: node_part<L, E, 2>(ys, q, D, al, acc); break;
+            default: node_part<L, E, 3>(ys, q, D, al, acc); break;
+          }
         }
+      }
     }
   }
-  if (owner) reinterpret_cast<float4*>(nodes_out + (int64_t)j * HE)[t] = out;
+  // park the slot partial sums, then add them in slot order
+  __syncthreads();
+  switch (part) {
+    case 0: node_part_park<L, 0>(dyn, slot, q, Q, acc); break;
+    case 1: node_part_park<L, 1>(dyn, slot, q, Q, acc); break;
+    case 2: node_part_park<L, 2>(dyn, slot, q, Q, acc); break;
+    default: node_part_park<L, 3>(dyn, slot, q, Q, acc); break;
+  }
+  __syncthreads();
+  for (int o = t; o < HQ; o += 128) {
+    float4 out = reinterpret_cast<const float4*>(nodes_in + (int64_t)j * HE)[o];
+    if (b < en) {
+      float4 s = reinterpret_cast<const float4*>(dyn)[o];
+      for (int sl = 1; sl < NSLOT; ++sl) {
+        const float4 v = reinterpret_cast<const float4*>(dyn)[sl * HQ + o];
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      out.x += s.x;
+      out.y += s.y;
+      out.z += s.z;
+      out.w += s.w;
+    }
+    reinterpret_cast<float4*>(nodes_out + (int64_t)j * HE)[o] = out;
+  }
 }
 
 }  // namespace esg
