@@ -59,28 +59,47 @@ __global__ void k_init_nodes(const int* __restrict__ row_slot, int n_rows, const
   nodes[t] = q < E ? embed[row_slot[i] * E + q] : 0.f;
 }
 
-// One warp per edge: lane g evaluates Gaussian g once (fp64 exp, cast), lane
-// c < E sums lift[c][g] * rbf[g] over g in ascending order (the reference's
-// sequential float sum, no FMA); the warp then writes the 1,600-byte row.
+// A warp owns blocks of 32 consecutive edges: lane i loads the distance of
+// edge i of the block (one coalesced load), then the warp walks the block 4
+// edges at a time: lane g evaluates Gaussian g (fp64 exp, cast), lane c < E
+// sums lift[c][g] * rbf[g] over g in ascending order (the reference's
+// sequential float sum, no FMA; four edges' chains interleave), and the warp
+// writes each 1,600-byte row.
 template <int H, int E, int NG>
 __global__ void __launch_bounds__(256) k_init_edges(const double* __restrict__ dist, int64_t n_e,
                                                     const float* __restrict__ lift, int ng, double spacing,
                                                     float* __restrict__ edges) {
+  constexpr int U = 4;
   const int lane = threadIdx.x & 31;
   float w[NG];  // lane c < E keeps lift row c in registers (zero past ng)
 #pragma unroll
   for (int g = 0; g < NG; ++g) w[g] = (lane < E && g < ng) ? lift[lane * ng + g] : 0.f;
   const double inv_den = 2.0 * spacing * spacing;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_e; k += warps) {
-    const double d = dist[k] - lane * spacing;
-    const float rbf = lane < ng ? (float)exp(-d * d / inv_den) : 0.f;
-    float acc = 0.f;
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < n_e; base += warps * 32) {
+    const int cnt = (int)(n_e - base < 32 ? n_e - base : 32);
+    const double myd = lane < cnt ? dist[base + lane] : 0.0;
+    for (int e0 = 0; e0 < cnt; e0 += U) {
+      float rbf[U], acc[U];
 #pragma unroll
-    for (int g = 0; g < NG; ++g) acc = __fadd_rn(acc, __fmul_rn(w[g], __shfl_sync(0xffffffffu, rbf, g)));
-    float4* row = reinterpret_cast<float4*>(edges + k * (H * E));
-    for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lane < E) edges[k * (H * E) + lane] = acc;
+      for (int u = 0; u < U; ++u) {
+        const double d = __shfl_sync(0xffffffffu, myd, e0 + u) - lane * spacing;
+        rbf[u] = lane < ng ? (float)exp(-d * d / inv_den) : 0.f;
+        acc[u] = 0.f;
+      }
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = __fadd_rn(acc[u], __fmul_rn(w[g], __shfl_sync(0xffffffffu, rbf[u], g)));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (e0 + u >= cnt) break;
+        const int64_t k = base + e0 + u;
+        float4* row = reinterpret_cast<float4*>(edges + k * (H * E));
+        for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane < E) edges[k * (H * E) + lane] = acc[u];
+      }
+    }
   }
 }
 
@@ -156,17 +175,24 @@ __global__ void k_copy_rows(const float* __restrict__ src, float* __restrict__ d
 
 // ---------------------------------------------------------- heads
 // ops.h:287-335: out[i][off_k + r] = sum_c w_k[c] x[i][L^2 + r][c].
-// Tiles of 32 items: the CTA stages the 32 rows (H x E each) in shared memory
-// with coalesced float4 loads, then thread j (one per head output) computes
-// output j of every item in the tile with its key's weight row in registers;
-// stores are coalesced along j.  Sequential fp32 sum over the channels
-// without FMA, as ops.h:293-306 does.
+// Persistent CTAs stream tiles of HT items (H x E rows each) into a 2-stage
+// shared-memory ring with cp.async (the next tile loads while this one is
+// computed); thread j (one per head output) computes output j of every item
+// of the tile with its key's weight row in registers, stores coalesced along
+// j.  Sequential fp32 sum over the channels without FMA, as ops.h:293-306.
+constexpr int HT = 16;  // items per tile
+template <int H, int E>
+constexpr int heads_smem_bytes() {
+  return 2 * HT * H * (E + 4) * (int)sizeof(float);
+}
 template <int H, int E>
 __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int64_t n_items,
                                                const float* __restrict__ W, const int* __restrict__ key_of,
                                                const int* __restrict__ row_of, int out_len, float* __restrict__ out) {
-  constexpr int TI = 16, PS = E + 4;  // plane stride padded: distinct rows hit distinct banks
-  extern __shared__ __align__(16) float sx[];  // TI x H x PS
+  constexpr int PS = E + 4;        // plane stride padded: distinct rows hit distinct banks
+  constexpr int STAGE = HT * H * PS;
+  constexpr int U = H * E / 4;     // 16-byte units per item
+  extern __shared__ __align__(16) float sx[];  // 2 x HT x H x PS
   const int j = threadIdx.x;
   float w[E];
   int row = 0;
@@ -176,26 +202,48 @@ __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int6
 #pragma unroll
     for (int c = 0; c < E; ++c) w[c] = W[k * E + c];
   }
-  const int64_t n_tiles = (n_items + TI - 1) / TI;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t i0 = tile * TI;
-    const int ni = (int)(n_items - i0 < TI ? n_items - i0 : TI);
-    const float4* src = reinterpret_cast<const float4*>(x + i0 * (H * E));
-    for (int q = threadIdx.x; q < ni * H * E / 4; q += blockDim.x) {
-      const int pl = q / (E / 4), w4 = q % (E / 4);  // plane (item, row), float4 within it
-      *reinterpret_cast<float4*>(sx + pl * PS + 4 * w4) = __ldg(src + q);
+  const int64_t n_tiles = (n_items + HT - 1) / HT;
+  auto issue = [&](int64_t tile, int stage) {
+    if (tile < n_tiles) {
+      const int64_t i0 = tile * HT;
+      const int ni = (int)(n_items - i0 < HT ? n_items - i0 : HT);
+      const float* src = x + i0 * (H * E);
+      float* dst = sx + stage * STAGE;
+      for (int u = threadIdx.x; u < ni * U; u += blockDim.x) {
+        const int pl = u / (E / 4), w4 = u % (E / 4);  // plane (item, row), 16 bytes within it
+        cp_async16(dst + pl * PS + 4 * w4, src + 4 * u);
+      }
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int stage = 0;
+  issue(blockIdx.x, 0);
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, stage ^= 1) {
+    issue(tile + gridDim.x, stage ^ 1);  // next tile streams in meanwhile
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncthreads();
-    if (j < out_len)
+    const int64_t i0 = tile * HT;
+    const int ni = (int)(n_items - i0 < HT ? n_items - i0 : HT);
+    if (j < out_len) {
+      const float* base = sx + stage * STAGE + row * PS;
+#pragma unroll 4
       for (int it = 0; it < ni; ++it) {
-        const float* plane = sx + (it * H + row) * PS;
+        const float4* plane = reinterpret_cast<const float4*>(base + it * H * PS);
         float acc = 0.f;
 #pragma unroll
-        for (int c = 0; c < E; ++c) acc = __fadd_rn(acc, __fmul_rn(w[c], plane[c]));
+        for (int c4 = 0; c4 < E / 4; ++c4) {
+          const float4 v = plane[c4];
+          acc = __fadd_rn(acc, __fmul_rn(w[4 * c4], v.x));
+          acc = __fadd_rn(acc, __fmul_rn(w[4 * c4 + 1], v.y));
+          acc = __fadd_rn(acc, __fmul_rn(w[4 * c4 + 2], v.z));
+          acc = __fadd_rn(acc, __fmul_rn(w[4 * c4 + 3], v.w));
+        }
         out[(i0 + it) * out_len + j] = acc;
       }
-    __syncthreads();
+    }
+    __syncthreads();  // this stage is refilled two tiles later
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // ------------------------------------------------ uncoupled blocks
@@ -856,14 +904,14 @@ template <int H, int E>
 void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
                   float* out, cudaStream_t st) {
   if (out_len > 256) usage("head layout wider than 256 outputs");
-  constexpr int smem = 16 * H * (E + 4) * (int)sizeof(float);
+  constexpr int smem = heads_smem_bytes<H, E>();
   static bool attr = false;
   if (!attr) {
     ESG_CUDA(cudaFuncSetAttribute(k_heads<H, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   const int threads = ((out_len + 31) / 32) * 32;
-  const unsigned blocks = (unsigned)std::min<int64_t>((n + 15) / 16, 148 * 8);
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + HT - 1) / HT, 148 * 3);  // 3 x 64 KB per SM
   k_heads<H, E><<<blocks, threads, smem, st>>>(x, n, W, key_of, row_of, out_len, out);
 }
 
@@ -883,7 +931,7 @@ void forward_impl(esg_model* M, esg_timing* tm) {
     if (D->n_edges) {
       Prof pr2(D, st, ESG_PROF_INIT);
       if (M->cfg.n_radial > 32) usage("the GPU radial lift supports up to 32 Gaussians");
-      const int64_t blocks = std::min<int64_t>((D->n_edges + 7) / 8, 148 * 64);
+      const int64_t blocks = std::min<int64_t>((D->n_edges + 255) / 256, 148 * 8);  // 8 warps x 32-edge blocks
       k_init_edges<H, E, 32><<<(unsigned)blocks, 256, 0, st>>>(D->dist, D->n_edges, D->params + D->lift_off,
                                                                 M->cfg.n_radial,
                                                                 M->cfg.r_cut / (M->cfg.n_radial - 1), D->edges);
