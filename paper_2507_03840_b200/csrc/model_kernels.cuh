@@ -83,24 +83,24 @@ namespace esg {
 
 // degrees l0..L of the recursion, one barrier per degree (compile-time l, so
 // only the degrees this l_max needs are instantiated)
-template <int L, int l, int DSP>
+template <int L, int l, int NG>
 __device__ __forceinline__ void wigner_levels(bool act, int warp, const float* R, float* d) {
   if constexpr (l <= L) {
-    if (act) wigner_deg<l>(warp, R, d + Geo<L>::doff(l - 1), d + Geo<L>::doff(l));
+    if (act) wigner_deg<l, NG>(warp, R, d + Geo<L>::doff(l - 1), d + Geo<L>::doff(l));
     __syncthreads();
-    wigner_levels<L, l + 1, DSP>(act, warp, R, d);
+    wigner_levels<L, l + 1, NG>(act, warp, R, d);
   }
 }
 
 // Wigner blocks for a tile of ne <= 32 edges with the generated straight-line
-// recursion: lane = edge, warps 0..3 each own a quarter of every degree's
-// entries.  Needs blockDim.x >= 128; all threads must call it.  D rows use an
+// recursion: lane = edge, warps 0..NG-1 each own 1/NG of every degree's
+// entries.  Needs blockDim.x >= 32 NG; all threads must call it.  D rows use an
 // odd stride DSP so the per-lane bases hit distinct banks.
-template <int L, int DSP>
+template <int L, int DSP, int NG = 4>
 __device__ void wigner_tile_gen(const float* dirs, int ne, float* D) {
   using G = Geo<L>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool act = warp < kWigGroups && lane < ne;
+  const bool act = warp < NG && lane < ne;
   float R[9];
   if (act) {
     align_to_y(dirs[3 * lane], dirs[3 * lane + 1], dirs[3 * lane + 2], R);
@@ -112,7 +112,7 @@ __device__ void wigner_tile_gen(const float* dirs, int ne, float* D) {
     }
   }
   __syncthreads();
-  wigner_levels<L, 2, DSP>(act, warp, R, D + lane * DSP);
+  wigner_levels<L, 2, NG>(act, warp, R, D + lane * DSP);
 }
 
 // Ivanic-Ruedenberg recursion expanded on the host into flat recipes: entry

@@ -73,7 +73,7 @@ __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
 // Thread = (edge, part in {src,dst,edge}, 4-channel quad); 32 edges per CTA
 // (the Wigner warps then run full 32-lane tiles).
 template <int L, int E, int KPAD, typename OutT>
-__global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 2) k_rotate_in(const float* __restrict__ nodes,
+__global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3) k_rotate_in(const float* __restrict__ nodes,
                                                              const float* __restrict__ edges,
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 2
   using G = Geo<L>;
   using Y = Lay1<L, E, KPAD>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
+  constexpr int NG = TE * TPE >= 384 ? 12 : 4;  // every warp takes a share of the Wigner recursion
   __shared__ float sD[TE * DSP];
   __shared__ float sdir[TE * 3];
   const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 2
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   const int e = threadIdx.x / TPE, r = threadIdx.x % TPE, p = r / Q, q = r % Q;
   __syncthreads();
-  wigner_tile_gen<L, DSP>(sdir, ne, sD);
+  wigner_tile_gen<L, DSP, NG>(sdir, ne, sD);
   if (e < ne) {
     const int64_t k = t0 + e;
     const float4* base = reinterpret_cast<const float4*>(
