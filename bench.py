@@ -332,22 +332,31 @@ def run_ours(args):
             pass
         barrier()
         torch.cuda.synchronize()
+        phases = np.zeros(3)  # graph (+ plan), prepare, forward + D2H of the outputs
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
+            ta = time.perf_counter()
             g2 = esg.build_graph(ctx, s, r)  # H2D of the positions
             plan2 = None
             if world > 1:
                 part2 = esg.lownn_partition(s, g2.in_degrees(), int(round(math.log2(world))), r)
                 plan2 = esg.build_comm_plan(g2, s.species, part2, world, rank)
+            tb = time.perf_counter()
             net.prepare(g2, s.species, plan2)
+            tc = time.perf_counter()
             net.forward_into(node_out, edge_out)  # D2H of every head output
+            td = time.perf_counter()
+            phases += [tb - ta, tc - tb, td - tc]
             g2.close()
         torch.cuda.synchronize()
         e2e_s = allmax((time.perf_counter() - t0) / args.e2e_steps)
+        d2h = int(allsum(node_out.nbytes + edge_out.nbytes))
         e2e = {"value": total_edges / e2e_s, "unit": "edges/s",
                "h2d_bytes_per_step": int(s.positions.nbytes),
-               "d2h_bytes_per_step": int(allsum(node_out.nbytes + edge_out.nbytes)),
-               "step_s": e2e_s}
+               "d2h_bytes_per_step": d2h, "step_s": e2e_s,
+               "phases_s": {"graph": phases[0] / args.e2e_steps, "prepare": phases[1] / args.e2e_steps,
+                            "forward_and_d2h": phases[2] / args.e2e_steps},
+               "pinned_host_outputs": bool(getattr(torch.from_numpy(edge_out), "is_pinned", lambda: False)())}
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:

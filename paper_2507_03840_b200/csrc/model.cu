@@ -39,6 +39,17 @@ T* dalloc(size_t n) {
   return p;
 }
 
+// Device buffer of at least n elements: the previous one when it is big
+// enough (repeated prepares of same-sized views reuse their memory), else a
+// fresh allocation.  cap tracks the allocated elements of p.
+template <typename T>
+T* grow(T* p, size_t& cap, size_t n) {
+  if (p && cap >= n) return p;
+  if (p) cudaFree(p);
+  cap = n;
+  return dalloc<T>(n);
+}
+
 __device__ __forceinline__ void store_out(float* p, float v) { *p = v; }
 __device__ __forceinline__ void store_out(uint16_t* p, float v) {
   // round-to-nearest-even fp32 -> bf16
@@ -334,8 +345,14 @@ struct DeviceModel {
   int64_t chunk_cap = 0;
   float* node_out = nullptr;
   float* edge_out = nullptr;
-  // uncoupled block bookkeeping
-  std::vector<int> h_item_species_a, h_item_species_b;
+  // uncoupled block bookkeeping (filled on first use, model_blocks)
+  mutable std::vector<int> h_item_species_a, h_item_species_b;
+  mutable bool item_species_ready = false;
+  // allocated elements of the view buffers (grow)
+  size_t cap_row_slot = 0, cap_src = 0, cap_dst = 0, cap_dir = 0, cap_dist = 0, cap_seg = 0, cap_nodes = 0,
+         cap_nodes_alt = 0, cap_edges = 0, cap_a1 = 0, cap_y = 0, cap_logits = 0, cap_node_out = 0,
+         cap_edge_out = 0, cap_send_rows = 0, cap_send_buf = 0;
+  bool a1_tc_clean = false;  // A1 holds zeros in every tensor-core K padding slot
   int64_t block_values = 0;
   cudaEvent_t ev[8];
   // expanded Wigner recursion (device copies)
@@ -668,30 +685,39 @@ void model_device_destroy(esg_model* M) {
 
 // Network::prepare on a rank view (comm_plan.cpp layout; plan == nullptr is
 // the serial view of the whole graph).
+// k_fill_dst: dst_row[k] = j for the edges of destination segment j
+__global__ void k_fill_dst(const int64_t* __restrict__ off, int n, int* __restrict__ dst_row) {
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= n) return;
+  for (int64_t k = off[j] + (threadIdx.x & 31); k < off[j + 1]; k += 32) dst_row[k] = j;
+}
+
 void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const int32_t* species) {
   DeviceModel* D = M->dev;
   cudaStream_t st = M->ctx->stream;
-  g->host_sync();
   const int E = D->E, H = D->H;
-  std::vector<int32_t> row_global, src_row, dst_row, eidx;
   int n_rows, n_owned;
+  int64_t ne;
+  std::vector<int32_t> row_global;
+  std::vector<int64_t> seg;
   if (plan) {
     n_rows = plan->n_rows;
     n_owned = plan->n_owned;
     row_global = plan->row_global;
-    src_row = plan->src_row;
-    dst_row = plan->dst_row;
-    eidx = plan->edge_index;
+    ne = (int64_t)plan->src_row.size();
+    seg.assign(n_owned + 1, 0);
+    for (int64_t k = 0; k < ne; ++k) seg[plan->dst_row[k] + 1]++;
+    for (int j = 0; j < n_owned; ++j) seg[j + 1] += seg[j];
   } else {
+    // the whole graph as the view: indices stay on the device (CSR src, the
+    // segment offsets are the CSR offsets); only the offsets come to the host
     n_rows = n_owned = g->n;
+    ne = g->E;
     row_global.resize(g->n);
     for (int i = 0; i < g->n; ++i) row_global[i] = i;
-    src_row = g->h_src;
-    dst_row.resize(g->E);
-    for (int j = 0; j < g->n; ++j)
-      for (int64_t k = g->h_off[j]; k < g->h_off[j + 1]; ++k) dst_row[k] = j;
+    seg.resize(g->n + 1);
+    ESG_CUDA(cudaMemcpy(seg.data(), g->d_off, sizeof(int64_t) * (g->n + 1), cudaMemcpyDeviceToHost));
   }
-  const int64_t ne = (int64_t)src_row.size();
   std::vector<int> slot(n_rows);
   D->row_species.resize(n_rows);
   for (int i = 0; i < n_rows; ++i) {
@@ -701,38 +727,37 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     if (it == M->species_list.end()) data("species " + element_symbol(z) + " missing from the model's basis");
     slot[i] = int(it - M->species_list.begin());
   }
-  std::vector<int64_t> seg(n_owned + 1, 0);
-  for (int64_t k = 0; k < ne; ++k) seg[dst_row[k] + 1]++;
-  for (int j = 0; j < n_owned; ++j) seg[j + 1] += seg[j];
-  for (void* p : {(void*)D->row_slot, (void*)D->src_row, (void*)D->dst_row, (void*)D->dir, (void*)D->dist,
-                  (void*)D->seg, (void*)D->nodes, (void*)D->nodes_alt, (void*)D->edges, D->A1, (void*)D->Y,
-                  (void*)D->logits, (void*)D->node_out, (void*)D->edge_out, (void*)D->send_rows, (void*)D->send_buf})
-    free_ptr(p);
   D->n_rows = n_rows;
   D->n_owned = n_owned;
   D->n_edges = ne;
   D->h_seg = seg;
-  D->row_slot = dalloc<int>(n_rows);
-  D->src_row = dalloc<int>(ne);
-  D->dst_row = dalloc<int>(ne);
-  D->dir = dalloc<float>(3 * ne);
-  D->dist = dalloc<double>(ne);
-  D->seg = dalloc<int64_t>(n_owned + 1);
-  ESG_CUDA(cudaMemcpy(D->row_slot, slot.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice));
-  ESG_CUDA(cudaMemcpy(D->src_row, src_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice));
-  ESG_CUDA(cudaMemcpy(D->dst_row, dst_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice));
-  ESG_CUDA(cudaMemcpy(D->seg, seg.data(), sizeof(int64_t) * (n_owned + 1), cudaMemcpyHostToDevice));
+  D->item_species_ready = false;
+  D->row_slot = grow(D->row_slot, D->cap_row_slot, n_rows);
+  D->src_row = grow(D->src_row, D->cap_src, ne);
+  D->dst_row = grow(D->dst_row, D->cap_dst, ne);
+  D->dir = grow(D->dir, D->cap_dir, 3 * ne);
+  D->dist = grow(D->dist, D->cap_dist, ne);
+  D->seg = grow(D->seg, D->cap_seg, n_owned + 1);
+  ESG_CUDA(cudaMemcpyAsync(D->row_slot, slot.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice, st));
   int* d_eidx = nullptr;
   if (plan) {
+    ESG_CUDA(cudaMemcpyAsync(D->src_row, plan->src_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+    ESG_CUDA(cudaMemcpyAsync(D->dst_row, plan->dst_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+    ESG_CUDA(cudaMemcpyAsync(D->seg, seg.data(), sizeof(int64_t) * (n_owned + 1), cudaMemcpyHostToDevice, st));
     d_eidx = dalloc<int>(ne);
-    ESG_CUDA(cudaMemcpy(d_eidx, eidx.data(), sizeof(int) * ne, cudaMemcpyHostToDevice));
+    ESG_CUDA(cudaMemcpyAsync(d_eidx, plan->edge_index.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+  } else {
+    if (ne) ESG_CUDA(cudaMemcpyAsync(D->src_row, g->d_src, sizeof(int) * ne, cudaMemcpyDeviceToDevice, st));
+    ESG_CUDA(cudaMemcpyAsync(D->seg, g->d_off, sizeof(int64_t) * (n_owned + 1), cudaMemcpyDeviceToDevice, st));
+    if (n_owned) {
+      k_fill_dst<<<(unsigned)((n_owned + 7) / 8), 256, 0, st>>>(D->seg, n_owned, D->dst_row);
+      ++M->ctx->launches;
+    }
   }
   if (ne) {
     k_gather_dirs<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(g->d_disp, d_eidx, ne, D->dir, g->d_dist, D->dist);
     ++M->ctx->launches;
   }
-  ESG_CUDA(cudaStreamSynchronize(st));
-  free_ptr(d_eidx);
   // destination-aligned chunks of about chunk_cap edges
   const int64_t cap = std::max<int64_t>(std::min<int64_t>(ne, 2 << 20), 1);
   int64_t maxseg = 0;
@@ -747,9 +772,9 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   }
   // tables and scratch
   const int64_t row = (int64_t)H * E;
-  D->nodes = dalloc<float>((size_t)n_rows * row);
-  D->nodes_alt = dalloc<float>((size_t)n_rows * row);
-  D->edges = dalloc<float>((size_t)std::max<int64_t>(ne, 1) * row);
+  D->nodes = grow(D->nodes, D->cap_nodes, (size_t)n_rows * row);
+  D->nodes_alt = grow(D->nodes_alt, D->cap_nodes_alt, (size_t)n_rows * row);
+  D->edges = grow(D->edges, D->cap_edges, (size_t)std::max<int64_t>(ne, 1) * row);
   const int K1T = [&] {
     int t = 0;
     for (int m = 0; m <= D->L; ++m) t += ((m == 0 ? D->L + 1 : 2 * (D->L - m + 1)) * 3 * E + 63) / 64 * 64;
@@ -758,15 +783,15 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   // fp32 row-major (CUDA-core path) or bf16 tiles of 128 edges (tensor cores)
   const size_t a1_fp32 = (size_t)D->chunk_cap * K1T * 4;
   const size_t a1_bf16 = (size_t)((D->chunk_cap + 127) / 128) * 128 * K1T * 2;
-  D->A1 = (void*)dalloc<uint8_t>(std::max(a1_fp32, a1_bf16));
-  // the K padding slots of the tensor-core image are never written again
-  ESG_CUDA(cudaMemset(D->A1, 0, std::max(a1_fp32, a1_bf16)));
+  void* a1_prev = D->A1;
+  D->A1 = (void*)grow((uint8_t*)D->A1, D->cap_a1, std::max(a1_fp32, a1_bf16));
+  if (D->A1 != a1_prev) D->a1_tc_clean = false;  // zeroed before the first tensor-core use (run_block)
   // fp32 rows (CUDA-core path) or bf16 tiles of 128 edges (tcgen05 epilogue)
-  D->Y = (float*)dalloc<uint8_t>(std::max((size_t)D->chunk_cap * row * 4,
-                                          (size_t)((D->chunk_cap + 127) / 128) * 128 * row * 2));
-  D->logits = dalloc<float>((size_t)D->chunk_cap);
-  D->node_out = dalloc<float>((size_t)std::max(n_owned, 1) * M->heads.out_len);
-  D->edge_out = dalloc<float>((size_t)std::max<int64_t>(ne, 1) * M->heads.out_len);
+  D->Y = (float*)grow((uint8_t*)D->Y, D->cap_y,
+                      std::max((size_t)D->chunk_cap * row * 4, (size_t)((D->chunk_cap + 127) / 128) * 128 * row * 2));
+  D->logits = grow(D->logits, D->cap_logits, (size_t)D->chunk_cap);
+  D->node_out = grow(D->node_out, D->cap_node_out, (size_t)std::max(n_owned, 1) * M->heads.out_len);
+  D->edge_out = grow(D->edge_out, D->cap_edge_out, (size_t)std::max<int64_t>(ne, 1) * M->heads.out_len);
   // halo
   D->nbrs.clear();
   D->n_send = 0;
@@ -775,19 +800,36 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     std::vector<int> all;
     for (const auto& nb : plan->nbrs) all.insert(all.end(), nb.send_rows.begin(), nb.send_rows.end());
     D->n_send = (int64_t)all.size();
-    D->send_rows = dalloc<int>(all.size());
-    D->send_buf = dalloc<float>(all.size() * row);
-    if (!all.empty()) ESG_CUDA(cudaMemcpy(D->send_rows, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice));
+    D->send_rows = grow(D->send_rows, D->cap_send_rows, all.size());
+    D->send_buf = grow(D->send_buf, D->cap_send_buf, all.size() * row);
+    if (!all.empty())
+      ESG_CUDA(cudaMemcpyAsync(D->send_rows, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
   }
-  // per-item species for block assembly (nodes: owned rows, edges: view edges)
+  ESG_CUDA(cudaStreamSynchronize(st));  // host vectors above are freed on return
+  free_ptr(d_eidx);
+  D->prepared = true;
+}
+
+// per-item species for block assembly (nodes: owned rows, edges: view edges),
+// built from the device index arrays the first time blocks are requested
+void ensure_item_species(const esg_model* M) {
+  const DeviceModel* D = M->dev;
+  if (D->item_species_ready) return;
+  const int n_owned = D->n_owned;
+  const int64_t ne = D->n_edges;
+  std::vector<int> src(ne), dst(ne);
+  if (ne) {
+    ESG_CUDA(cudaMemcpy(src.data(), D->src_row, sizeof(int) * ne, cudaMemcpyDeviceToHost));
+    ESG_CUDA(cudaMemcpy(dst.data(), D->dst_row, sizeof(int) * ne, cudaMemcpyDeviceToHost));
+  }
   D->h_item_species_a.assign(n_owned + ne, 0);
   D->h_item_species_b.assign(n_owned + ne, 0);
   for (int i = 0; i < n_owned; ++i) D->h_item_species_a[i] = D->h_item_species_b[i] = D->row_species[i];
   for (int64_t k = 0; k < ne; ++k) {
-    D->h_item_species_a[n_owned + k] = D->row_species[src_row[k]];
-    D->h_item_species_b[n_owned + k] = D->row_species[dst_row[k]];
+    D->h_item_species_a[n_owned + k] = D->row_species[src[k]];
+    D->h_item_species_b[n_owned + k] = D->row_species[dst[k]];
   }
-  D->prepared = true;
+  D->item_species_ready = true;
 }
 
 namespace {
@@ -833,6 +875,12 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     ++ctx->launches;
   }
   const bool tc = D->precision == ESG_LINEAR_BF16 && so2_tc_available(L, E);
+  if (tc && !D->a1_tc_clean) {  // the K padding slots of the tensor-core image are never written by rotate_in
+    ESG_CUDA(cudaMemsetAsync(D->A1, 0, D->cap_a1, st));
+    D->a1_tc_clean = true;
+  } else if (!tc) {
+    D->a1_tc_clean = false;  // the CUDA-core path writes fp32 rows over the whole buffer
+  }
   const float* att = D->params + D->att_off[layer];
   for (const auto& ch : D->chunks) {
     const int64_t e0 = D->h_seg[ch.first], e1 = D->h_seg[ch.second];
@@ -1044,6 +1092,7 @@ void model_prepared_info(const esg_model* M, int64_t info[3]) {
 
 // Uncoupled blocks of the last forward, items = owned nodes then view edges.
 int64_t model_blocks_size(const esg_model* M) {
+  ensure_item_species(M);
   const DeviceModel* D = M->dev;
   int64_t n = 0;
   for (size_t i = 0; i < D->h_item_species_a.size(); ++i)
@@ -1052,6 +1101,7 @@ int64_t model_blocks_size(const esg_model* M) {
 }
 
 void model_blocks(esg_model* M, double* out_host) {
+  ensure_item_species(M);
   DeviceModel* D = M->dev;
   cudaStream_t st = M->ctx->stream;
   // Per species pair: for every block element (row-major n_orb(za) x
