@@ -179,6 +179,39 @@ int esg_features_export(const esg_model* m, float* nodes, float* edges);
 int esg_blocks_size(const esg_model* m, int64_t* n_values);
 int esg_blocks_uncoupled(esg_model* m, double* out);
 
+/* ---- training (config 5) -------------------------- */
+/* Loss targets in head space for the prepared view (network.h:187-214
+ * build_targets): node rows n_owned x out_len, edge rows n_edges x out_len in
+ * view order, 1-byte masks (1 = the element is a target). */
+int esg_set_targets(esg_model* m, const float* node_target, const uint8_t* node_mask, const float* edge_target,
+                    const uint8_t* edge_mask);
+/* Masked L1+L2 loss and parameter gradients at the current parameters
+ * (distributed.h:208-226 without the optimizer step): forward on the fp32
+ * path keeping every block's inputs, loss = (sum_abs + sum_sq) / n_total
+ * over all ranks (ops.h:347-371, network.h:218-227), the reverse pass
+ * (ops.h backward closures, kernels.h:163-250, halo backward
+ * distributed.h:98-129), gradients summed over ranks in rank order in fp64
+ * (allreduce_gradients, distributed.h:147-163).  partials: this rank's
+ * {sum_abs, sum_sq, count}; grads: param_count floats, flat parameter
+ * layout (may be NULL). */
+int esg_loss_grad(esg_model* m, int64_t n_total, double partials[3], double* loss, float* grads);
+/* Adam with reduce-on-plateau (optimizer.h:15-80), moments in fp64, host. */
+typedef struct esg_adam_config {
+  double lr, beta1, beta2, eps;
+  int patience;
+  double factor, threshold, min_lr;
+} esg_adam_config;
+void esg_adam_default_config(esg_adam_config* cfg); /* OptimizerConfig defaults */
+typedef struct esg_adam esg_adam;
+int esg_adam_create(const esg_model* m, const esg_adam_config* cfg, esg_adam** out);
+void esg_adam_destroy(esg_adam* a);
+double esg_adam_lr(const esg_adam* a);
+/* DistributedRunner::train_step (distributed.h:208-235): parameter-sync
+ * check (hash allgather; divergence -> status 4), loss + gradients, Adam
+ * step, check again.  timing may be NULL; forward_ms = the forward,
+ * message_ms = the backward (CUDA events). */
+int esg_train_step(esg_model* m, esg_adam* opt, int64_t n_total, double* loss, esg_timing* timing);
+
 #ifdef __cplusplus
 }
 #endif

@@ -886,6 +886,49 @@ Rot<T> edge_rotations(const View& view, int l_max, int k0, int k1) {
   return r;
 }
 
+// so2_linear (kernels.h:133-161), vectorised across n items: out[i][o] =
+// sum_k W[o][k] in[i][k] with the k-sum in ascending order for every (i, o).
+template <typename T>
+void message_lin(const Model<T>& M, int n, const T* in, T* out, const std::string& wb, int cin, int cout) {
+  const int L = M.cfg.l_max, H = M.lay.h;
+  std::vector<T> xt, acc;
+  auto gemv = [&](const T* W, int rows, int cols, int in_off, int sgn, int out_off, bool accumulate) {
+    // W (rows x cols); in rows at element offset in_off (cols contiguous)
+    xt.resize((size_t)cols * n);
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < cols; ++k) xt[(size_t)k * n + i] = in[(size_t)i * H * cin + in_off + k];
+    acc.assign((size_t)n, T(0));
+    for (int o = 0; o < rows; ++o) {
+      std::fill(acc.begin(), acc.end(), T(0));
+      const T* wr = W + (size_t)o * cols;
+      for (int k = 0; k < cols; ++k) {
+        const T wk = wr[k];
+        const T* xk = &xt[(size_t)k * n];
+        for (int i = 0; i < n; ++i) acc[i] += wk * xk[i];
+      }
+      for (int i = 0; i < n; ++i) {
+        T& dst = out[(size_t)i * H * cout + out_off + o];
+        if (!accumulate)
+          dst = acc[i];
+        else
+          dst = sgn > 0 ? T(dst + acc[i]) : T(dst - acc[i]);
+      }
+    }
+  };
+  const int nd0 = M.lay.nd(0);
+  gemv(M.P(wb + "/m0"), nd0 * cout, nd0 * cin, 0, 1, 0, false);
+  for (int m = 1; m <= L; ++m) {
+    const int nd = M.lay.nd(m), mo = M.lay.m_offset[m];
+    const T* wr = M.P(wb + "/m" + std::to_string(m) + "r");
+    const T* wi = M.P(wb + "/m" + std::to_string(m) + "i");
+    const int xm = mo * cin, xp = (mo + nd) * cin, ym = mo * cout, yp = (mo + nd) * cout;
+    gemv(wr, nd * cout, nd * cin, xm, 1, ym, false);  // ym = wr xm
+    gemv(wi, nd * cout, nd * cin, xp, 1, ym, true);   //    + wi xp
+    gemv(wr, nd * cout, nd * cin, xp, 1, yp, false);  // yp = wr xp
+    gemv(wi, nd * cout, nd * cin, xm, -1, yp, true);  //    - wi xm
+  }
+}
+
 // One message block for edges [k0,k1) (kernels.h:73-226 composition,
 // network.h:140-149).  Writes msg (n,H,E) in degree-major order.
 template <typename T>
@@ -932,45 +975,8 @@ void message_block(const Model<T>& M, const View& view, const T* nodes, const T*
   };
   rotate(x, y, C3, false);
   permute(y, x, C3, M.lay.to_m);  // x := m-major aligned message
-  // so2_linear, vectorised across edges: out[i][o] = sum_k W[o][k] in[i][k]
-  // with the k-sum in ascending order for every (i, o).
   auto so2 = [&](const std::vector<T>& in, std::vector<T>& out, const std::string& wb, int cin, int cout) {
-    std::vector<T> xt, acc;
-    auto gemv = [&](const T* W, int rows, int cols, int in_off, int sgn, int out_off, bool accumulate) {
-      // W (rows x cols); in rows at element offset in_off (cols contiguous)
-      xt.resize((size_t)cols * n);
-      for (int i = 0; i < n; ++i)
-        for (int k = 0; k < cols; ++k) xt[(size_t)k * n + i] = in[(size_t)i * H * cin + in_off + k];
-      acc.assign((size_t)n, T(0));
-      for (int o = 0; o < rows; ++o) {
-        std::fill(acc.begin(), acc.end(), T(0));
-        const T* wr = W + (size_t)o * cols;
-        for (int k = 0; k < cols; ++k) {
-          const T wk = wr[k];
-          const T* xk = &xt[(size_t)k * n];
-          for (int i = 0; i < n; ++i) acc[i] += wk * xk[i];
-        }
-        for (int i = 0; i < n; ++i) {
-          T& dst = out[(size_t)i * H * cout + out_off + o];
-          if (!accumulate)
-            dst = acc[i];
-          else
-            dst = sgn > 0 ? T(dst + acc[i]) : T(dst - acc[i]);
-        }
-      }
-    };
-    const int nd0 = M.lay.nd(0);
-    gemv(M.P(wb + "/m0"), nd0 * cout, nd0 * cin, 0, 1, 0, false);
-    for (int m = 1; m <= L; ++m) {
-      const int nd = M.lay.nd(m), mo = M.lay.m_offset[m];
-      const T* wr = M.P(wb + "/m" + std::to_string(m) + "r");
-      const T* wi = M.P(wb + "/m" + std::to_string(m) + "i");
-      const int xm = mo * cin, xp = (mo + nd) * cin, ym = mo * cout, yp = (mo + nd) * cout;
-      gemv(wr, nd * cout, nd * cin, xm, 1, ym, false);  // ym = wr xm
-      gemv(wi, nd * cout, nd * cin, xp, 1, ym, true);   //    + wi xp
-      gemv(wr, nd * cout, nd * cin, xp, 1, yp, false);  // yp = wr xp
-      gemv(wi, nd * cout, nd * cin, xm, -1, yp, true);  //    - wi xm
-    }
+    message_lin(M, n, in.data(), out.data(), wb, cin, cout);
   };
   std::vector<T> hid((size_t)n * H * C2);
   so2(x, hid, base + "/lin1", C3, C2);
@@ -1115,6 +1121,351 @@ void heads_eval(const Model<T>& M, const T* x, int n_items, const char* set, T* 
         for (int c = 0; c < E; ++c) acc += w[k][c] * plane[c];
         o[M.heads.offsets[k] + r] = acc;
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- backward
+// Reverse mode of the forward above, restating the tape closures of
+// ops.h (embed 27-33, lift 52-60, concat 88-105, rotate 115-117, permute
+// 128-130, so2_linear 157-171 -> kernels.h:163-199, gate 179-181 ->
+// kernels.h:228-250, attention 227-262, add 273-281, heads 309-333).  Each
+// block recomputes its forward intermediates from the block's input tables
+// (the reference keeps them on the tape).  Parameter gradients accumulate
+// into a flat vector laid out like the parameters.
+
+// so2_linear_backward (kernels.h:163-199) over n items: x (n, H, cin)
+// m-major, g (n, H, cout); dx += W^T g, dW += g x^T.  dW partials are per
+// item range (caller merges); dx is per item.
+template <typename T>
+void so2_backward(const Model<T>& M, const std::string& wb, int n, const T* x, const T* g, int cin, int cout,
+                  T* dx, T* gw) {
+  const int L = M.cfg.l_max, H = M.lay.h;
+  auto W = [&](const std::string& nm) { return M.P(wb + nm); };
+  auto G = [&](const std::string& nm) { return gw + M.params.at(wb + nm).offset; };
+  for (int i = 0; i < n; ++i) {
+    const T* xr = x + (size_t)i * H * cin;
+    const T* gr = g + (size_t)i * H * cout;
+    T* dxr = dx + (size_t)i * H * cin;
+    {
+      const int nd = M.lay.nd(0), R = nd * cout, C = nd * cin;
+      const T* w0 = W("/m0");
+      T* d0 = G("/m0");
+      for (int k = 0; k < C; ++k) {
+        T acc = 0;
+        for (int o = 0; o < R; ++o) acc += w0[(size_t)o * C + k] * gr[o];
+        dxr[k] += acc;
+      }
+      for (int o = 0; o < R; ++o)
+        for (int k = 0; k < C; ++k) d0[(size_t)o * C + k] += gr[o] * xr[k];
+    }
+    for (int m = 1; m <= L; ++m) {
+      const int nd = M.lay.nd(m), mo = M.lay.m_offset[m], R = nd * cout, C = nd * cin;
+      const T* wr = W("/m" + std::to_string(m) + "r");
+      const T* wi = W("/m" + std::to_string(m) + "i");
+      T* dwr = G("/m" + std::to_string(m) + "r");
+      T* dwi = G("/m" + std::to_string(m) + "i");
+      const T* xm = xr + (size_t)mo * cin;
+      const T* xp = xr + (size_t)(mo + nd) * cin;
+      const T* gm = gr + (size_t)mo * cout;
+      const T* gp = gr + (size_t)(mo + nd) * cout;
+      T* dxm = dxr + (size_t)mo * cin;
+      T* dxp = dxr + (size_t)(mo + nd) * cin;
+      for (int k = 0; k < C; ++k) {
+        T a = 0, b = 0, c = 0, d = 0;
+        for (int o = 0; o < R; ++o) {
+          a += wr[(size_t)o * C + k] * gm[o];
+          b += wi[(size_t)o * C + k] * gp[o];
+          c += wr[(size_t)o * C + k] * gp[o];
+          d += wi[(size_t)o * C + k] * gm[o];
+        }
+        dxm[k] += a - b;  // Wr^T gm - Wi^T gp
+        dxp[k] += c + d;  // Wr^T gp + Wi^T gm
+      }
+      for (int o = 0; o < R; ++o)
+        for (int k = 0; k < C; ++k) {
+          dwr[(size_t)o * C + k] += gm[o] * xm[k] + gp[o] * xp[k];
+          dwi[(size_t)o * C + k] += gm[o] * xp[k] - gp[o] * xm[k];
+        }
+    }
+  }
+}
+
+// Backward of message_block for edges [k0,k1): g_msg (n,H,E) degree-major ->
+// g_x (n, H, 3E) degree-major concat gradient; lin1/lin2 gradients into gw.
+template <typename T>
+void message_block_backward(const Model<T>& M, const View& view, const T* nodes, const T* edges_tab,
+                            const std::string& base, int k0, int k1, const T* g_msg, std::vector<T>& g_x, T* gw) {
+  const int L = M.cfg.l_max, H = M.lay.h, E = M.cfg.e, C3 = 3 * E, C2 = 2 * E;
+  const int n = k1 - k0;
+  const Rot<T> rot = edge_rotations<T>(view, L, k0, k1);
+  auto rotate = [&](const T* in, T* out, int C, bool tr) {
+    for (int i = 0; i < n; ++i)
+      for (int l = 0; l <= L; ++l) {
+        const int dd = 2 * l + 1;
+        const T* D = &rot.v[(size_t)i * rot.stride + rot.off[l]];
+        const T* xi = &in[((size_t)i * H + l * l) * C];
+        T* yo = &out[((size_t)i * H + l * l) * C];
+        for (int a = 0; a < dd; ++a)
+          for (int c = 0; c < C; ++c) {
+            T acc = 0;
+            for (int b = 0; b < dd; ++b) acc += (tr ? D[b * dd + a] : D[a * dd + b]) * xi[b * C + c];
+            yo[a * C + c] = acc;
+          }
+      }
+  };
+  // permute: out[perm[r]] = in[r]; its adjoint: g_in[r] = g_out[perm[r]]
+  auto permute_adj = [&](const T* g_out, T* g_in, int C, const std::vector<int>& perm) {
+    for (int i = 0; i < n; ++i)
+      for (int r = 0; r < H; ++r)
+        std::memcpy(&g_in[((size_t)i * H + r) * C], &g_out[((size_t)i * H + perm[r]) * C], sizeof(T) * C);
+  };
+  // forward recompute: xm (m-major aligned message), hid (lin1), gated
+  std::vector<T> x((size_t)n * H * C3), y((size_t)n * H * C3), xm((size_t)n * H * C3);
+  for (int i = 0; i < n; ++i) {
+    const int k = k0 + i;
+    const T* s = nodes + (size_t)view.src_row[k] * H * E;
+    const T* d = nodes + (size_t)view.dst_row[k] * H * E;
+    const T* g = edges_tab + (size_t)k * H * E;
+    T* o = &x[(size_t)i * H * C3];
+    for (int r = 0; r < H; ++r)
+      for (int c = 0; c < E; ++c) {
+        o[(r * 3 + 0) * E + c] = s[r * E + c];
+        o[(r * 3 + 1) * E + c] = d[r * E + c];
+        o[(r * 3 + 2) * E + c] = g[r * E + c];
+      }
+  }
+  rotate(x.data(), y.data(), C3, false);
+  for (int i = 0; i < n; ++i)
+    for (int r = 0; r < H; ++r)
+      std::memcpy(&xm[((size_t)i * H + M.lay.to_m[r]) * C3], &y[((size_t)i * H + r) * C3], sizeof(T) * C3);
+  std::vector<T> hid((size_t)n * H * C2, T(0)), gated;
+  message_lin(M, n, xm.data(), hid.data(), base + "/lin1", C3, C2);  // as message_block
+  gated = hid;
+  if (M.cfg.gate)
+    for (int i = 0; i < n; ++i) {
+      T* r = &gated[(size_t)i * H * C2];
+      const T* h0 = &hid[(size_t)i * H * C2];
+      for (int c = 0; c < C2; ++c) {
+        const T sg = T(1) / (T(1) + std::exp(-h0[c]));
+        r[c] = h0[c] * sg;
+        for (int q = 1; q < H; ++q) r[q * C2 + c] = h0[q * C2 + c] * sg;
+      }
+    }
+  // backward
+  std::vector<T> g_lmaj((size_t)n * H * E), g_nar((size_t)n * H * E);
+  rotate(g_msg, g_lmaj.data(), E, false);  // msg = D^T lmaj  ->  g_lmaj = D g_msg
+  permute_adj(g_lmaj.data(), g_nar.data(), E, M.lay.to_l);
+  std::vector<T> g_gated((size_t)n * H * C2, T(0));
+  so2_backward(M, base + "/lin2", n, gated.data(), g_nar.data(), C2, E, g_gated.data(), gw);
+  std::vector<T> g_hid((size_t)n * H * C2, T(0));
+  if (!M.cfg.gate) {  // kernels.h:230-232
+    for (size_t t = 0; t < g_hid.size(); ++t) g_hid[t] += g_gated[t];
+  } else {  // kernels.h:233-249
+    for (int i = 0; i < n; ++i) {
+      const T* xr = &hid[(size_t)i * H * C2];
+      const T* gr = &g_gated[(size_t)i * H * C2];
+      T* dxr = &g_hid[(size_t)i * H * C2];
+      for (int cc = 0; cc < C2; ++cc) {
+        const T sg = T(1) / (T(1) + std::exp(-xr[cc]));
+        const T ds = sg * (T(1) - sg);
+        T acc = gr[cc] * (sg + xr[cc] * ds);
+        for (int r = 1; r < H; ++r) {
+          const size_t k = (size_t)r * C2 + cc;
+          dxr[k] += gr[k] * sg;
+          acc += gr[k] * xr[k] * ds;
+        }
+        dxr[cc] += acc;
+      }
+    }
+  }
+  std::vector<T> g_xm((size_t)n * H * C3, T(0));
+  so2_backward(M, base + "/lin1", n, xm.data(), g_hid.data(), C3, C2, g_xm.data(), gw);
+  permute_adj(g_xm.data(), y.data(), C3, M.lay.to_m);  // y := g of the aligned message
+  g_x.assign((size_t)n * H * C3, T(0));
+  rotate(y.data(), g_x.data(), C3, true);  // aligned = D x  ->  g_x = D^T g_aligned
+}
+
+// One block backward over the whole view.  In: the block's input tables and
+// the gradients of its output tables (g_nodes, g_edges, replaced by the
+// gradients of the inputs).  Parameter gradients accumulate into gw.
+template <typename T>
+void run_block_backward(const Model<T>& M, const View& view, const T* nodes, const T* edges, int layer,
+                        bool node_block, std::vector<T>& g_nodes, std::vector<T>& g_edges, T* gw) {
+  const int H = M.lay.h, E = M.cfg.e, C3 = 3 * E;
+  const std::string base = "layer" + std::to_string(layer) + (node_block ? "/node" : "/edge");
+  const int ne = view.n_edges();
+  // chunks of whole destination segments (as run_block)
+  std::vector<std::pair<int, int>> chunks;
+  {
+    int j = 0;
+    while (j < view.n_owned) {
+      int j1 = j, cnt = 0;
+      while (j1 < view.n_owned && (cnt == 0 || cnt < 256)) {
+        cnt += view.ranges[j1].second - view.ranges[j1].first;
+        ++j1;
+      }
+      chunks.push_back({j, j1});
+      j = j1;
+    }
+  }
+  std::vector<T> g_msg((size_t)ne * H * E, T(0));
+  std::vector<T> g_att;
+  if (!node_block) {
+    std::copy(g_edges.begin(), g_edges.end(), g_msg.begin());  // add (ops.h:273-281)
+  } else {
+    // attention backward (ops.h:227-262) from the recomputed messages
+    const T* att = M.P("layer" + std::to_string(layer) + "/att");
+    T* g_att_p = gw + M.params.at("layer" + std::to_string(layer) + "/att").offset;
+    std::vector<std::vector<T>> att_part(chunks.size(), std::vector<T>(E, T(0)));
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int ci = 0; ci < (int)chunks.size(); ++ci) {
+      const int j0 = chunks[ci].first, j1 = chunks[ci].second;
+      int k0 = -1, k1 = -1;
+      for (int j = j0; j < j1; ++j)
+        if (view.ranges[j].second > view.ranges[j].first) {
+          if (k0 < 0) k0 = view.ranges[j].first;
+          k1 = view.ranges[j].second;
+        }
+      if (k0 < 0) continue;
+      std::vector<T> msg;
+      message_block(M, view, nodes, edges, base, k0, k1, msg);
+      for (int j = j0; j < j1; ++j) {
+        const int b = view.ranges[j].first, e = view.ranges[j].second;
+        if (b == e) continue;
+        std::vector<T> al(e - b);
+        T mx = -std::numeric_limits<T>::infinity();
+        for (int k = b; k < e; ++k) {
+          T logit = 0;
+          for (int c = 0; c < E; ++c) logit += att[c] * msg[(size_t)(k - k0) * H * E + c];
+          al[k - b] = logit;
+          mx = std::max(mx, logit);
+        }
+        T z = 0;
+        for (int k = b; k < e; ++k) {
+          al[k - b] = std::exp(al[k - b] - mx);
+          z += al[k - b];
+        }
+        for (int k = b; k < e; ++k) al[k - b] /= z;
+        const T* gj = &g_nodes[(size_t)j * H * E];
+        T mean = 0;
+        std::vector<T> dots(e - b);
+        for (int k = b; k < e; ++k) {
+          const T* m = &msg[(size_t)(k - k0) * H * E];
+          T d = 0;
+          for (int t = 0; t < H * E; ++t) d += gj[t] * m[t];
+          dots[k - b] = d;
+          mean += al[k - b] * d;
+        }
+        for (int k = b; k < e; ++k) {
+          const T a = al[k - b];
+          T* gm = &g_msg[(size_t)k * H * E];
+          for (int t = 0; t < H * E; ++t) gm[t] += a * gj[t];
+          const T dl = a * (dots[k - b] - mean);
+          for (int c = 0; c < E; ++c) {
+            gm[c] += dl * att[c];
+            att_part[ci][c] += dl * msg[(size_t)(k - k0) * H * E + c];
+          }
+        }
+      }
+    }
+    for (const auto& pa : att_part)
+      for (int c = 0; c < E; ++c) g_att_p[c] += pa[c];
+  }
+  // message backward per chunk: lin gradients per chunk (merged in chunk
+  // order), concat gradients scattered in edge order (ops.h:92-104)
+  const size_t np = M.params.total;
+  std::vector<std::vector<T>> gx(chunks.size());
+  std::vector<std::vector<T>> gw_part(chunks.size());
+  std::vector<int> ck0(chunks.size(), -1);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int ci = 0; ci < (int)chunks.size(); ++ci) {
+    const int j0 = chunks[ci].first, j1 = chunks[ci].second;
+    int k0 = -1, k1 = -1;
+    for (int j = j0; j < j1; ++j)
+      if (view.ranges[j].second > view.ranges[j].first) {
+        if (k0 < 0) k0 = view.ranges[j].first;
+        k1 = view.ranges[j].second;
+      }
+    if (k0 < 0) continue;
+    ck0[ci] = k0;
+    gw_part[ci].assign(np, T(0));
+    message_block_backward(M, view, nodes, edges, base, k0, k1, &g_msg[(size_t)k0 * H * E], gx[ci],
+                           gw_part[ci].data());
+  }
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    if (ck0[ci] < 0) continue;
+    for (size_t t = 0; t < np; ++t) gw[t] += gw_part[ci][t];
+    const int n = (int)(gx[ci].size() / ((size_t)H * C3));
+    for (int i = 0; i < n; ++i) {
+      const int k = ck0[ci] + i;
+      T* src = &g_nodes[(size_t)view.src_row[k] * H * E];
+      T* dst = &g_nodes[(size_t)view.dst_row[k] * H * E];
+      T* edg = &g_edges[(size_t)k * H * E];
+      const T* o = &gx[ci][(size_t)i * H * C3];
+      for (int r = 0; r < H; ++r)
+        for (int c = 0; c < E; ++c) {
+          src[r * E + c] += o[(r * 3 + 0) * E + c];
+          dst[r * E + c] += o[(r * 3 + 1) * E + c];
+          edg[r * E + c] += o[(r * 3 + 2) * E + c];
+        }
+    }
+  }
+}
+
+// heads backward (ops.h:309-333): g_x += up * w, g_w += up * x
+template <typename T>
+void heads_backward(const Model<T>& M, const T* x, int n_items, const char* set, const T* g_out, T* g_x, T* gw) {
+  const int H = M.lay.h, E = M.cfg.e;
+  std::vector<const T*> w(M.heads.keys.size());
+  std::vector<T*> wg(M.heads.keys.size());
+  for (size_t k = 0; k < M.heads.keys.size(); ++k) {
+    const auto& hk = M.heads.keys[k];
+    const std::string nm = std::string("head/") + set + "/s" + std::to_string(hk.sa) + "s" + std::to_string(hk.sb) +
+                           "L" + std::to_string(hk.L);
+    w[k] = M.P(nm);
+    wg[k] = gw + M.params.at(nm).offset;
+  }
+  for (int i = 0; i < n_items; ++i) {
+    const T* gr = g_out + (size_t)i * M.heads.out_len;
+    T* dxr = g_x + (size_t)i * H * E;
+    const T* xr = x + (size_t)i * H * E;
+    for (size_t k = 0; k < M.heads.keys.size(); ++k) {
+      const int L = M.heads.keys[k].L;
+      for (int r = 0; r < 2 * L + 1; ++r) {
+        const T up = gr[M.heads.offsets[k] + r];
+        if (up == T(0)) continue;
+        T* dplane = dxr + (size_t)(L * L + r) * E;
+        const T* plane = xr + (size_t)(L * L + r) * E;
+        for (int c = 0; c < E; ++c) {
+          dplane[c] += up * w[k][c];
+          wg[k][c] += up * plane[c];
+        }
+      }
+    }
+  }
+}
+
+// embed (ops.h:27-33) and lift (ops.h:52-60) backward
+template <typename T>
+void init_backward(const Model<T>& M, const View& view, const T* g_nodes, const T* g_edges, T* gw) {
+  const int H = M.lay.h, E = M.cfg.e, NG = M.cfg.n_radial;
+  for (int i = 0; i < view.n_rows; ++i) {
+    T* eg = gw + M.params.at("embed/" + symbol(view.row_species[i])).offset;
+    for (int c = 0; c < E; ++c) eg[c] += g_nodes[(size_t)i * H * E + c];
+  }
+  T* wg = gw + M.params.at("radial/lift").offset;  // (E, NG)
+  const double spacing = M.cfg.r_cut / (NG - 1);
+  for (int k = 0; k < view.n_edges(); ++k) {
+    T rbf[64];
+    for (int g = 0; g < NG; ++g) {
+      const double d = view.dist[k] - g * spacing;
+      rbf[g] = static_cast<T>(std::exp(-d * d / (2.0 * spacing * spacing)));
+    }
+    for (int c = 0; c < E; ++c) {
+      const T up = g_edges[(size_t)k * H * E + c];
+      if (up == T(0)) continue;
+      for (int g = 0; g < NG; ++g) wg[c * NG + g] += up * rbf[g];
     }
   }
 }
@@ -1446,6 +1797,10 @@ void oracle_model_set_params_f32(void* h, const float* in) {
   auto* om = (OracleModel*)h;
   std::copy(in, in + om->pf.size(), om->pf.begin());
 }
+void oracle_model_set_params_f64(void* h, const double* in) {
+  auto* om = (OracleModel*)h;
+  std::copy(in, in + om->pd.size(), om->pd.begin());
+}
 
 }  // extern "C"
 
@@ -1502,6 +1857,24 @@ int forward_impl(const Model<T>& M, const View& v, int mode, T* nodes_io, T* edg
   }
   return 0;
 }
+template <typename T>
+int backward_impl(const Model<T>& M, const View& v, int mode, const T* nodes, const T* edges, int layer,
+                  int node_block, const T* g_node_out, const T* g_edge_out, T* g_nodes, T* g_edges, T* grads) {
+  const size_t row = (size_t)M.lay.h * M.cfg.e;
+  if (mode == 0) {
+    std::vector<T> gn(g_nodes, g_nodes + (size_t)v.n_rows * row);
+    std::vector<T> ge(g_edges, g_edges + (size_t)v.n_edges() * row);
+    run_block_backward(M, v, nodes, edges, layer, node_block != 0, gn, ge, grads);
+    std::copy(gn.begin(), gn.end(), g_nodes);
+    std::copy(ge.begin(), ge.end(), g_edges);
+  } else if (mode == 1) {
+    if (g_node_out) heads_backward(M, nodes, v.n_owned, "node", g_node_out, g_nodes, grads);
+    if (g_edge_out) heads_backward(M, edges, v.n_edges(), "edge", g_edge_out, g_edges, grads);
+  } else if (mode == 2) {
+    init_backward(M, v, g_nodes, g_edges, grads);
+  }
+  return 0;
+}
 }  // namespace
 
 extern "C" {
@@ -1526,6 +1899,163 @@ int oracle_forward_f64(void* h, int n_rows, int n_owned, const int* row_species,
     auto* om = (OracleModel*)h;
     View v = make_view(n_rows, n_owned, row_species, n_edges, src_row, dst_row, disp, dist);
     forward_impl(om->md, v, mode, nodes_io, edges_io, layer, node_block, node_out, edge_out);
+  })
+}
+
+// Loss targets for the serial view in graph-edge order (test
+// infrastructure): synthetic.cpp:66-121 toy_hamiltonian (uncoupled blocks)
+// encoded into head space with encode_target (network.h:318-343,
+// clebsch_gordan.cpp:142-155 to_coupled).  node rows n x out_len, edge rows
+// E x out_len; masks 1 where a target element exists.
+int oracle_toy_targets(void* h, int n, const int* species, int64_t n_edges, const int* src, const int* dst,
+                       const int* shift, const double* disp, const double* dist, float* node_t, uint8_t* node_m,
+                       double* node_t64, float* edge_t, uint8_t* edge_m, double* edge_t64) {
+  GUARD({
+    const auto& M = ((OracleModel*)h)->md;
+    const Basis& basis = M.basis;
+    const double decay = 2.0, pair_scale = 1.0, onsite_scale = 0.5;
+    using Mat = std::vector<double>;  // row-major
+    auto add_pair_term = [&](Mat& block, int ncol, int row0, int col0, int la, int lb, const V3& u, double r,
+                             double scale, int salt) {
+      const auto ysh = real_sh(la + lb, u);
+      const int rows = 2 * la + 1, cols = 2 * lb + 1;
+      std::vector<double> vec((size_t)rows * cols, 0.0);
+      for (int L = std::abs(la - lb); L <= la + lb; ++L) {
+        const double sigma = decay / (1.0 + 0.3 * L);
+        const double a = scale * (0.6 + 0.1 * ((salt + 3 * (la + 1) * (lb + 1) + L) % 5)) / (1.0 + L);
+        const auto& c = coupling(la, lb, L);  // (2L+1) x (rows*cols)
+        const double f = a * std::exp(-r / sigma);
+        for (int q = 0; q < rows * cols; ++q) {
+          double acc = 0.0;
+          for (int t = 0; t < 2 * L + 1; ++t) acc += c[(size_t)t * rows * cols + q] * ysh[L * L + t];
+          vec[q] += f * acc;
+        }
+      }
+      for (int i = 0; i < rows; ++i)
+        for (int j = 0; j < cols; ++j) block[(size_t)(row0 + i) * ncol + col0 + j] += vec[(size_t)i * cols + j];
+    };
+    // encode_target: coupled coefficients of each shell-pair rectangle
+    auto encode = [&](int za, int zb, const Mat& block, int ncol, float* row, uint8_t* mask, double* row64) {
+      const auto& sha = basis.shells.at(za);
+      const auto& shb = basis.shells.at(zb);
+      for (size_t a = 0; a < sha.size(); ++a)
+        for (size_t b = 0; b < shb.size(); ++b) {
+          const int la = sha[a], lb = shb[b], da = 2 * la + 1, db = 2 * lb + 1;
+          const int oa = basis.off(za, (int)a), ob = basis.off(zb, (int)b);
+          std::vector<double> flat((size_t)da * db);
+          for (int i = 0; i < da; ++i)
+            for (int j = 0; j < db; ++j) flat[(size_t)i * db + j] = block[(size_t)(oa + i) * ncol + ob + j];
+          for (int L = std::abs(la - lb); L <= la + lb; ++L) {
+            const auto& c = coupling(la, lb, L);
+            const int off = M.heads.segment((int)a, (int)b, L);
+            for (int r = 0; r < 2 * L + 1; ++r) {
+              double acc = 0.0;
+              for (int q = 0; q < da * db; ++q) acc += c[(size_t)r * da * db + q] * flat[q];
+              row[off + r] = static_cast<float>(acc);
+              if (row64) row64[off + r] = acc;
+              mask[off + r] = 1;
+            }
+          }
+        }
+    };
+    const int ol = M.heads.out_len;
+    // on-site blocks: neighbour sums, symmetrised, plus per-shell levels
+    std::vector<Mat> onsite(n);
+    for (int i = 0; i < n; ++i) {
+      const int no = basis.n_orb(species[i]);
+      onsite[i].assign((size_t)no * no, 0.0);
+    }
+    for (int64_t e = 0; e < n_edges; ++e) {
+      const int i = dst[e], z = species[i];
+      const V3 u{{-disp[3 * e] / dist[e], -disp[3 * e + 1] / dist[e], -disp[3 * e + 2] / dist[e]}};
+      const auto& sh = basis.shells.at(z);
+      const int no = basis.n_orb(z);
+      for (int a = 0; a < (int)sh.size(); ++a)
+        for (int b = 0; b < (int)sh.size(); ++b)
+          add_pair_term(onsite[i], no, basis.off(z, a), basis.off(z, b), sh[a], sh[b], u, dist[e], onsite_scale,
+                        z + species[src[e]]);
+    }
+    for (int i = 0; i < n; ++i) {
+      const int z = species[i], no = basis.n_orb(z);
+      Mat& B = onsite[i];
+      Mat S = B;
+      for (int r = 0; r < no; ++r)
+        for (int c = 0; c < no; ++c) S[(size_t)r * no + c] = (B[(size_t)r * no + c] + B[(size_t)c * no + r]) * 0.5;
+      const auto& sh = basis.shells.at(z);
+      for (int a = 0; a < (int)sh.size(); ++a) {
+        const double level = -1.0 - 0.25 * a - 0.01 * z;
+        const int off = basis.off(z, a);
+        for (int m = 0; m < 2 * sh[a] + 1; ++m) S[(size_t)(off + m) * no + off + m] += level;
+      }
+      std::fill(node_t + (size_t)i * ol, node_t + (size_t)(i + 1) * ol, 0.f);
+      std::fill(node_m + (size_t)i * ol, node_m + (size_t)(i + 1) * ol, 0);
+      if (node_t64) std::fill(node_t64 + (size_t)i * ol, node_t64 + (size_t)(i + 1) * ol, 0.0);
+      encode(z, z, S, no, node_t + (size_t)i * ol, node_m + (size_t)i * ol, node_t64 ? node_t64 + (size_t)i * ol : nullptr);
+    }
+    // pair blocks: the canonical direction of each (key, mirror) pair, the
+    // mirror is its transpose (synthetic.cpp:79-95)
+    std::map<std::array<int, 5>, int64_t> index;
+    for (int64_t e = 0; e < n_edges; ++e)
+      index[{src[e], dst[e], shift[3 * e], shift[3 * e + 1], shift[3 * e + 2]}] = e;
+    for (int64_t e = 0; e < n_edges; ++e) {
+      const std::array<int, 5> key{src[e], dst[e], shift[3 * e], shift[3 * e + 1], shift[3 * e + 2]};
+      const std::array<int, 5> mir{dst[e], src[e], -shift[3 * e], -shift[3 * e + 1], -shift[3 * e + 2]};
+      const int za = species[src[e]], zb = species[dst[e]];
+      const int na = basis.n_orb(za), nb = basis.n_orb(zb);
+      Mat B((size_t)na * nb, 0.0);
+      if (mir < key) {  // this edge is the mirror: transpose of the canonical block
+        const int64_t ec = index.at(mir);
+        Mat C((size_t)nb * na, 0.0);
+        const V3 u{{disp[3 * ec] / dist[ec], disp[3 * ec + 1] / dist[ec], disp[3 * ec + 2] / dist[ec]}};
+        const auto& sa = basis.shells.at(zb);
+        const auto& sb = basis.shells.at(za);
+        for (int a = 0; a < (int)sa.size(); ++a)
+          for (int b = 0; b < (int)sb.size(); ++b)
+            add_pair_term(C, na, basis.off(zb, a), basis.off(za, b), sa[a], sb[b], u, dist[ec], pair_scale,
+                          zb + 2 * za);
+        for (int r = 0; r < na; ++r)
+          for (int c = 0; c < nb; ++c) B[(size_t)r * nb + c] = C[(size_t)c * na + r];
+      } else {
+        const V3 u{{disp[3 * e] / dist[e], disp[3 * e + 1] / dist[e], disp[3 * e + 2] / dist[e]}};
+        const auto& sa = basis.shells.at(za);
+        const auto& sb = basis.shells.at(zb);
+        for (int a = 0; a < (int)sa.size(); ++a)
+          for (int b = 0; b < (int)sb.size(); ++b)
+            add_pair_term(B, nb, basis.off(za, a), basis.off(zb, b), sa[a], sb[b], u, dist[e], pair_scale,
+                          za + 2 * zb);
+      }
+      std::fill(edge_t + (size_t)e * ol, edge_t + (size_t)(e + 1) * ol, 0.f);
+      std::fill(edge_m + (size_t)e * ol, edge_m + (size_t)(e + 1) * ol, 0);
+      if (edge_t64) std::fill(edge_t64 + (size_t)e * ol, edge_t64 + (size_t)(e + 1) * ol, 0.0);
+      encode(za, zb, B, nb, edge_t + (size_t)e * ol, edge_m + (size_t)e * ol, edge_t64 ? edge_t64 + (size_t)e * ol : nullptr);
+    }
+  })
+}
+
+// Backward (test infrastructure).  mode 0: block (layer, node_block) backward
+// from the block's input tables; g_nodes / g_edges hold the gradients of its
+// outputs and are replaced by those of its inputs.  mode 1: heads backward
+// from the final tables (g_node_out / g_edge_out seeds, added into g_nodes /
+// g_edges).  mode 2: embed + lift backward.  grads: flat, like the params.
+int oracle_backward_f32(void* h, int n_rows, int n_owned, const int* row_species, int64_t n_edges,
+                        const int* src_row, const int* dst_row, const double* disp, const double* dist, int mode,
+                        const float* nodes, const float* edges, int layer, int node_block, const float* g_node_out,
+                        const float* g_edge_out, float* g_nodes, float* g_edges, float* grads) {
+  GUARD({
+    auto* om = (OracleModel*)h;
+    View v = make_view(n_rows, n_owned, row_species, n_edges, src_row, dst_row, disp, dist);
+    backward_impl(om->mf, v, mode, nodes, edges, layer, node_block, g_node_out, g_edge_out, g_nodes, g_edges, grads);
+  })
+}
+int oracle_backward_f64(void* h, int n_rows, int n_owned, const int* row_species, int64_t n_edges,
+                        const int* src_row, const int* dst_row, const double* disp, const double* dist, int mode,
+                        const double* nodes, const double* edges, int layer, int node_block,
+                        const double* g_node_out, const double* g_edge_out, double* g_nodes, double* g_edges,
+                        double* grads) {
+  GUARD({
+    auto* om = (OracleModel*)h;
+    View v = make_view(n_rows, n_owned, row_species, n_edges, src_row, dst_row, disp, dist);
+    backward_impl(om->md, v, mode, nodes, edges, layer, node_block, g_node_out, g_edge_out, g_nodes, g_edges, grads);
   })
 }
 

@@ -5,7 +5,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <random>
 
@@ -40,6 +42,45 @@ const char* last_error() { return g_last.c_str(); }
 }  // namespace esg
 
 using namespace esg;
+
+struct esg_adam {
+  esg_adam_config cfg{};
+  std::vector<double> m, v;
+  double lr = -1.0, best = std::numeric_limits<double>::infinity();
+  long t = 0;
+  int stale = 0;
+};
+
+namespace esg {
+void model_set_targets(esg_model* M, const float* node_target, const uint8_t* node_mask, const float* edge_target,
+                       const uint8_t* edge_mask);
+void model_loss_grad(esg_model* M, int64_t n_total, double partials[3], double* loss, float* grads_out);
+void model_train_timing(const esg_model* M, double* fwd_ms, double* bwd_ms);
+}  // namespace esg
+
+namespace {
+// check_param_sync (distributed.h:133-145): every rank's parameter hash,
+// allgathered; any mismatch is a divergence error on every rank
+void check_param_sync(esg_model* m, const char* where) {
+  esg_ctx* ctx = m->ctx;
+  if (!ctx || ctx->world <= 1) return;
+  const uint64_t h = esg::param_hash(m->params, m->host_params);
+  const double mine[2] = {double(h >> 32), double(h & 0xffffffffULL)};
+  double *d_mine = nullptr, *d_all = nullptr;
+  ESG_CUDA(cudaMalloc(&d_mine, sizeof(mine)));
+  ESG_CUDA(cudaMalloc(&d_all, sizeof(mine) * ctx->world));
+  ESG_CUDA(cudaMemcpyAsync(d_mine, mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
+  ESG_NCCL(ncclAllGather(d_mine, d_all, 2, ncclDouble, ctx->comm, ctx->stream));
+  std::vector<double> all(2 * ctx->world);
+  ESG_CUDA(cudaMemcpyAsync(all.data(), d_all, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  ESG_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_mine);
+  cudaFree(d_all);
+  for (int p = 0; p < ctx->world; ++p)
+    if (all[2 * p] != mine[0] || all[2 * p + 1] != mine[1])
+      throw esg::Error(ESG_ERR_DIVERGENCE, std::string("parameter state diverged between ranks (") + where + ")");
+}
+}  // namespace
 
 #define ESG_API_BEGIN try {
 #define ESG_API_END                       \
@@ -585,6 +626,94 @@ int esg_blocks_uncoupled(esg_model* m, double* out) {
   NEED(out, "out");
   ESG_CUDA(cudaSetDevice(m->ctx->device));
   model_blocks(m, out);
+  ESG_API_END
+}
+
+int esg_set_targets(esg_model* m, const float* node_target, const uint8_t* node_mask, const float* edge_target,
+                    const uint8_t* edge_mask) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_set_targets(m, node_target, node_mask, edge_target, edge_mask);
+  ESG_API_END
+}
+
+int esg_loss_grad(esg_model* m, int64_t n_total, double partials[3], double* loss, float* grads) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  NEED(loss, "loss");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  double p[3];
+  model_loss_grad(m, n_total, partials ? partials : p, loss, grads);
+  ESG_API_END
+}
+
+void esg_adam_default_config(esg_adam_config* c) {
+  if (!c) return;
+  *c = esg_adam_config{5e-3, 0.9, 0.999, 1e-8, 100, 0.5, 1e-4, 1e-6};
+}
+
+int esg_adam_create(const esg_model* m, const esg_adam_config* cfg, esg_adam** out) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  NEED(out, "out");
+  auto* a = new esg_adam();
+  if (cfg)
+    a->cfg = *cfg;
+  else
+    esg_adam_default_config(&a->cfg);
+  a->m.assign(m->host_params.size(), 0.0);
+  a->v.assign(m->host_params.size(), 0.0);
+  *out = a;
+  ESG_API_END
+}
+void esg_adam_destroy(esg_adam* a) { delete a; }
+double esg_adam_lr(const esg_adam* a) { return a ? (a->lr < 0 ? a->cfg.lr : a->lr) : 0.0; }
+
+int esg_train_step(esg_model* m, esg_adam* opt, int64_t n_total, double* loss, esg_timing* timing) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  NEED(opt, "optimizer");
+  NEED(loss, "loss");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  if (opt->m.size() != m->host_params.size()) usage("optimizer built for another model");
+  check_param_sync(m, "before step");
+  std::vector<float> g(m->host_params.size());
+  double partials[3];
+  model_loss_grad(m, n_total, partials, loss, g.data());
+  // Optimizer::step (optimizer.h:42-59), moments in fp64
+  if (opt->lr < 0) opt->lr = opt->cfg.lr;
+  ++opt->t;
+  const double bc1 = 1.0 - std::pow(opt->cfg.beta1, double(opt->t));
+  const double bc2 = 1.0 - std::pow(opt->cfg.beta2, double(opt->t));
+  for (size_t k = 0; k < g.size(); ++k) {
+    const double gk = double(g[k]);
+    opt->m[k] = opt->cfg.beta1 * opt->m[k] + (1.0 - opt->cfg.beta1) * gk;
+    opt->v[k] = opt->cfg.beta2 * opt->v[k] + (1.0 - opt->cfg.beta2) * gk * gk;
+    const double mh = opt->m[k] / bc1;
+    const double vh = opt->v[k] / bc2;
+    m->host_params[k] = static_cast<float>(double(m->host_params[k]) - opt->lr * mh / (std::sqrt(vh) + opt->cfg.eps));
+  }
+  // reduce-on-plateau (optimizer.h:62-72)
+  if (*loss < opt->best * (1.0 - opt->cfg.threshold)) {
+    opt->best = *loss;
+    opt->stale = 0;
+  } else if (++opt->stale >= opt->cfg.patience) {
+    opt->lr = std::max(opt->cfg.min_lr, opt->lr * opt->cfg.factor);
+    opt->stale = 0;
+  }
+  model_upload_params(m);
+  check_param_sync(m, "after update");
+  if (timing) {
+    double f = 0, b = 0;
+    model_train_timing(m, &f, &b);
+    *timing = esg_timing{};
+    timing->forward_ms = f;
+    timing->message_ms = b;
+  }
   ESG_API_END
 }
 

@@ -1,0 +1,91 @@
+// device_model.h -- the device state of one model (weights, the prepared
+// view, feature tables, chunk scratch, halo buffers and training buffers).
+// Shared by model.cu (forward) and train.cu (backward).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+#include "esg_internal.h"
+#include "model_kernels.cuh"
+
+namespace esg {
+
+struct TrainState;  // train.cu
+
+struct DeviceModel {
+  int L = 0, E = 0, H = 0;
+  // weights (device)
+  float* params = nullptr;  // raw flat parameters
+  std::vector<float*> w1t, w2t;      // per block (2*layers): SIMT packed
+  std::vector<uint16_t*> w1b, w2b;   // per block: tcgen05 bf16 packed
+  std::vector<int64_t> att_off;      // per layer offset into params
+  float* embed = nullptr;            // per species slot x E
+  float* head_w[2] = {nullptr, nullptr};  // node / edge: n_keys x E
+  int* head_key = nullptr;   // per listed output: key index
+  int* head_row = nullptr;   // per listed output: output index
+  int* head_hptr = nullptr;  // per harmonic row: start of its outputs
+  int64_t lift_off = 0;
+  // prepared view
+  bool prepared = false;
+  int n_rows = 0, n_owned = 0;
+  int64_t n_edges = 0;
+  int* row_slot = nullptr;
+  std::vector<int> row_species;
+  int* src_row = nullptr;
+  int* dst_row = nullptr;
+  float* dir = nullptr;
+  double* dist = nullptr;
+  int64_t* seg = nullptr;  // n_owned + 1
+  std::vector<int64_t> h_seg;
+  std::vector<std::pair<int, int>> chunks;  // owned-row ranges, dst aligned
+  // halo
+  std::vector<esg::Neighbor> nbrs;
+  int* send_rows = nullptr;
+  int64_t n_send = 0;
+  float* send_buf = nullptr;
+  // tables / scratch
+  float* nodes = nullptr;
+  float* nodes_alt = nullptr;
+  float* edges = nullptr;
+  void* A1 = nullptr;
+  float* Y = nullptr;
+  float* logits = nullptr;
+  int64_t chunk_cap = 0;
+  float* node_out = nullptr;
+  float* edge_out = nullptr;
+  // uncoupled block bookkeeping (filled on first use, model_blocks)
+  mutable std::vector<int> h_item_species_a, h_item_species_b;
+  mutable bool item_species_ready = false;
+  // allocated elements of the view buffers (grow)
+  size_t cap_row_slot = 0, cap_src = 0, cap_dst = 0, cap_dir = 0, cap_dist = 0, cap_seg = 0, cap_nodes = 0,
+         cap_nodes_alt = 0, cap_edges = 0, cap_a1 = 0, cap_y = 0, cap_logits = 0, cap_node_out = 0,
+         cap_edge_out = 0, cap_send_rows = 0, cap_send_buf = 0;
+  bool a1_tc_clean = false;  // A1 holds zeros in every tensor-core K padding slot
+  // training (train.cu): the forward saves every block's input tables when
+  // save_inputs is set -- the node table after the block's halo exchange
+  // (per block) and the edge table entering each layer (per layer)
+  bool save_inputs = false;
+  std::vector<float*> saved_nodes, saved_edges;
+  TrainState* train = nullptr;
+  bool train_stale = true;  // set by every prepare
+  int64_t block_values = 0;
+  cudaEvent_t ev[8];
+  // expanded Wigner recursion (device copies)
+  WigRecipe rc{};
+  void* rc_mem[4] = {nullptr, nullptr, nullptr, nullptr};
+  // optional per-category kernel timing (esg_profile_*): events around launches
+  bool profile = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, int>> marks;  // (category, first event index)
+  double prof_ms[ESG_PROF_NCAT] = {0};
+  int64_t prof_n[ESG_PROF_NCAT] = {0};
+  int precision = ESG_LINEAR_FP32;
+  size_t a1_elem = 4;
+};
+
+void free_ptr(void* p);
+
+}  // namespace esg

@@ -20,6 +20,7 @@
 #include "esg_internal.h"
 #include "model_kernels.cuh"
 #include "msg_kernels.cuh"
+#include "device_model.h"
 
 namespace esg {
 
@@ -304,69 +305,10 @@ __global__ void k_gather_dirs(const double* __restrict__ disp, const int* __rest
 }  // namespace
 
 // =================================================================== host
-struct DeviceModel {
-  int L = 0, E = 0, H = 0;
-  // weights (device)
-  float* params = nullptr;  // raw flat parameters
-  std::vector<float*> w1t, w2t;      // per block (2*layers): SIMT packed
-  std::vector<uint16_t*> w1b, w2b;   // per block: tcgen05 bf16 packed
-  std::vector<int64_t> att_off;      // per layer offset into params
-  float* embed = nullptr;            // per species slot x E
-  float* head_w[2] = {nullptr, nullptr};  // node / edge: n_keys x E
-  int* head_key = nullptr;   // per listed output: key index
-  int* head_row = nullptr;   // per listed output: output index
-  int* head_hptr = nullptr;  // per harmonic row: start of its outputs
-  int64_t lift_off = 0;
-  // prepared view
-  bool prepared = false;
-  int n_rows = 0, n_owned = 0;
-  int64_t n_edges = 0;
-  int* row_slot = nullptr;
-  std::vector<int> row_species;
-  int* src_row = nullptr;
-  int* dst_row = nullptr;
-  float* dir = nullptr;
-  double* dist = nullptr;
-  int64_t* seg = nullptr;  // n_owned + 1
-  std::vector<int64_t> h_seg;
-  std::vector<std::pair<int, int>> chunks;  // owned-row ranges, dst aligned
-  // halo
-  std::vector<esg::Neighbor> nbrs;
-  int* send_rows = nullptr;
-  int64_t n_send = 0;
-  float* send_buf = nullptr;
-  // tables / scratch
-  float* nodes = nullptr;
-  float* nodes_alt = nullptr;
-  float* edges = nullptr;
-  void* A1 = nullptr;
-  float* Y = nullptr;
-  float* logits = nullptr;
-  int64_t chunk_cap = 0;
-  float* node_out = nullptr;
-  float* edge_out = nullptr;
-  // uncoupled block bookkeeping (filled on first use, model_blocks)
-  mutable std::vector<int> h_item_species_a, h_item_species_b;
-  mutable bool item_species_ready = false;
-  // allocated elements of the view buffers (grow)
-  size_t cap_row_slot = 0, cap_src = 0, cap_dst = 0, cap_dir = 0, cap_dist = 0, cap_seg = 0, cap_nodes = 0,
-         cap_nodes_alt = 0, cap_edges = 0, cap_a1 = 0, cap_y = 0, cap_logits = 0, cap_node_out = 0,
-         cap_edge_out = 0, cap_send_rows = 0, cap_send_buf = 0;
-  bool a1_tc_clean = false;  // A1 holds zeros in every tensor-core K padding slot
-  int64_t block_values = 0;
-  cudaEvent_t ev[8];
-  // expanded Wigner recursion (device copies)
-  WigRecipe rc{};
-  void* rc_mem[4] = {nullptr, nullptr, nullptr, nullptr};
-  // optional per-category kernel timing (esg_profile_*): events around launches
-  bool profile = false;
-  std::vector<cudaEvent_t> pool;
-  std::vector<std::pair<int, int>> marks;  // (category, first event index)
-  double prof_ms[ESG_PROF_NCAT] = {0};
-  int64_t prof_n[ESG_PROF_NCAT] = {0};
-  int precision = ESG_LINEAR_FP32;
-  size_t a1_elem = 4;
-};
+void free_ptr(void* p) {
+  if (p) cudaFree(p);
+}
+
 
 namespace {
 
@@ -405,9 +347,6 @@ void prof_collect(DeviceModel* D) {
   D->marks.clear();
 }
 
-void free_ptr(void* p) {
-  if (p) cudaFree(p);
-}
 
 void upload_wigner_coef(int L) {
   static bool done = false;
@@ -436,6 +375,16 @@ void upload_wigner_coef(int L) {
 
 bool supported(int L, int E) { return (L == 4 || L == 2) && (E == 16 || E == 8); }
 
+
+uint16_t to_bf16(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+}  // namespace
+
 // Expanded SO(2) weight of order m in (N x K) row-major form:
 // m = 0: W0 ; m >= 1: [[Wr, Wi], [-Wi, Wr]].
 std::vector<float> expanded(const esg_model* M, const std::string& base, int m, int cin, int cout) {
@@ -460,15 +409,6 @@ std::vector<float> expanded(const esg_model* M, const std::string& base, int m, 
     }
   return W;
 }
-
-uint16_t to_bf16(float v) {
-  uint32_t u;
-  std::memcpy(&u, &v, 4);
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return uint16_t(u >> 16);
-}
-
-}  // namespace
 
 void model_upload_params(esg_model* M) {
   DeviceModel* D = M->dev;
@@ -665,9 +605,12 @@ void model_device_create(esg_model* M) {
   D->rc.pi = (const uint16_t*)up(3, pi.data(), sizeof(uint16_t) * pi.size());
 }
 
+void train_free(DeviceModel* D);  // train.cu
+
 void model_device_destroy(esg_model* M) {
   DeviceModel* D = M->dev;
   if (!D) return;
+  train_free(D);
   for (void* p : {(void*)D->params, (void*)D->embed, (void*)D->head_w[0], (void*)D->head_w[1], (void*)D->head_key,
                   (void*)D->head_row, (void*)D->head_hptr, (void*)D->row_slot, (void*)D->src_row, (void*)D->dst_row, (void*)D->dir,
                   (void*)D->dist, (void*)D->seg, (void*)D->send_rows, (void*)D->send_buf, (void*)D->nodes,
@@ -808,6 +751,7 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   ESG_CUDA(cudaStreamSynchronize(st));  // host vectors above are freed on return
   free_ptr(d_eidx);
   D->prepared = true;
+  D->train_stale = true;
 }
 
 // per-item species for block assembly (nodes: owned rows, edges: view edges),
@@ -867,6 +811,13 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     float ms = 0.f;
     ESG_CUDA(cudaEventElapsedTime(&ms, D->ev[4], D->ev[5]));
     *halo_ms += ms;
+  }
+  if (D->save_inputs) {  // training: this block's input tables (after the exchange)
+    const size_t row_bytes = sizeof(float) * H * E;
+    ESG_CUDA(cudaMemcpyAsync(D->saved_nodes[bidx], D->nodes, row_bytes * D->n_rows, cudaMemcpyDeviceToDevice, st));
+    if (node_block && D->n_edges)
+      ESG_CUDA(cudaMemcpyAsync(D->saved_edges[layer], D->edges, row_bytes * D->n_edges, cudaMemcpyDeviceToDevice,
+                               st));
   }
   if (node_block) {  // halo rows pass through (ops.h:200 copies all rows)
     const int64_t n = (int64_t)D->n_rows * H * E;

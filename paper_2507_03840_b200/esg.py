@@ -91,6 +91,7 @@ def lib() -> C.CDLL:
         L.esg_last_error.restype = C.c_char_p
         L.esg_model_param_count.restype = C.c_int64
         L.esg_model_param_hash.restype = C.c_uint64
+        L.esg_adam_lr.restype = C.c_double
         _lib_handle = L
     return _lib_handle
 
@@ -384,6 +385,31 @@ class Network:
         _check(lib().esg_prepared_info(self._h, _p(info)))
         self.n_rows, self.n_owned, self.n_edges = (int(x) for x in info)
 
+    # ---- training (config 5) ---------------------------------------------
+    def set_targets(self, node_target, node_mask, edge_target, edge_mask) -> None:
+        """Head-space loss targets of the prepared view (Network::build_targets)."""
+        nt = np.ascontiguousarray(node_target, np.float32)
+        nm = np.ascontiguousarray(node_mask, np.uint8)
+        et = np.ascontiguousarray(edge_target, np.float32)
+        em = np.ascontiguousarray(edge_mask, np.uint8)
+        assert nt.size == self.n_owned * self.out_len and et.size == self.n_edges * self.out_len
+        _check(lib().esg_set_targets(self._h, _p(nt), _p(nm), _p(et), _p(em)))
+
+    def loss_grad(self, n_total: int):
+        """Loss (all ranks), this rank's partials and the rank-summed gradients."""
+        partials = np.zeros(3)
+        loss = C.c_double()
+        g = np.zeros(self.n_params, np.float32)
+        _check(lib().esg_loss_grad(self._h, C.c_int64(n_total), _p(partials), C.byref(loss), _p(g)))
+        return loss.value, partials, g
+
+    def train_step(self, opt: "Adam", n_total: int):
+        """DistributedRunner::train_step; returns (loss, forward_ms, backward_ms)."""
+        loss = C.c_double()
+        t = _Timing()
+        _check(lib().esg_train_step(self._h, opt._h, C.c_int64(n_total), C.byref(loss), C.byref(t)))
+        return loss.value, t.forward_ms, t.message_ms
+
     def forward(self, copy_out: bool = True):
         t = _Timing()
         no = eo = None
@@ -421,6 +447,38 @@ class Network:
     def close(self) -> None:
         if self._h:
             lib().esg_model_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _AdamConfig(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("patience", C.c_int), ("factor", C.c_double), ("threshold", C.c_double), ("min_lr", C.c_double)]
+
+
+class Adam:
+    """model::Optimizer (optimizer.h): Adam, fp64 moments, reduce-on-plateau."""
+
+    def __init__(self, net: Network, **overrides):
+        cfg = _AdamConfig()
+        lib().esg_adam_default_config(C.byref(cfg))
+        for k, v in overrides.items():
+            setattr(cfg, k, v)
+        self._h = C.c_void_p()
+        _check(lib().esg_adam_create(net._h, C.byref(cfg), C.byref(self._h)))
+
+    @property
+    def lr(self) -> float:
+        return float(lib().esg_adam_lr(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            lib().esg_adam_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

@@ -30,7 +30,8 @@ def lib() -> C.CDLL:
         for f in ("oracle_model_destroy", "oracle_model_out_len", "oracle_model_n_entries",
                   "oracle_model_params_f32", "oracle_model_params_f64", "oracle_model_set_params_f32",
                   "oracle_forward_f32", "oracle_forward_f64", "oracle_uncoupled_block", "oracle_model_param_count",
-                  "oracle_model_entry"):
+                  "oracle_model_entry", "oracle_backward_f32", "oracle_backward_f64", "oracle_toy_targets",
+                  "oracle_model_set_params_f64"):
             getattr(L, f).argtypes = None
         _L = L
     return _L
@@ -258,6 +259,51 @@ class Model:
         self._call(nodes.dtype.type, view, 3, nodes, edges, node_out=no, edge_out=eo)
         return no, eo
 
+    def set_params_f64(self, p):
+        lib().oracle_model_set_params_f64(C.c_void_p(self.h), _p(np.ascontiguousarray(p, np.float64)))
+
+    def _bwd(self, view, mode, nodes, edges, layer=0, node_block=0, g_node_out=None, g_edge_out=None, g_nodes=None,
+             g_edges=None, grads=None):
+        dt = grads.dtype.type
+        f = lib().oracle_backward_f32 if dt == np.float32 else lib().oracle_backward_f64
+        E = len(view["src_row"])
+        _ok(f(C.c_void_p(self.h), C.c_int(view["n_rows"]), C.c_int(view["n_owned"]),
+              _p(np.ascontiguousarray(view["row_species"], np.int32)), C.c_int64(E),
+              _p(np.ascontiguousarray(view["src_row"], np.int32)), _p(np.ascontiguousarray(view["dst_row"], np.int32)),
+              _p(np.ascontiguousarray(view["disp"], np.float64)), _p(np.ascontiguousarray(view["dist"], np.float64)),
+              C.c_int(mode), _p(nodes), _p(edges), C.c_int(layer), C.c_int(int(node_block)), _p(g_node_out),
+              _p(g_edge_out), _p(g_nodes), _p(g_edges), _p(grads)))
+
+    def block_backward(self, view, nodes, edges, layer, node_block, g_nodes, g_edges, grads):
+        """ops.h backward closures of one block; g_nodes/g_edges: output grads in, input grads out."""
+        self._bwd(view, 0, nodes, edges, layer, node_block, g_nodes=g_nodes, g_edges=g_edges, grads=grads)
+
+    def heads_backward(self, view, nodes, edges, g_node_out, g_edge_out, g_nodes, g_edges, grads):
+        self._bwd(view, 1, nodes, edges, g_node_out=g_node_out, g_edge_out=g_edge_out, g_nodes=g_nodes,
+                  g_edges=g_edges, grads=grads)
+
+    def init_backward(self, view, g_nodes, g_edges, grads):
+        self._bwd(view, 2, None, None, g_nodes=g_nodes, g_edges=g_edges, grads=grads)
+
+    def toy_targets(self, n, species, g):
+        """synthetic.cpp toy_hamiltonian encoded into head space (serial view,
+        graph-edge order): (node_t, node_m, edge_t, edge_m, node_t64, edge_t64)."""
+        E = len(g["src"])
+        nt = np.zeros((n, self.out_len), np.float32)
+        nm = np.zeros((n, self.out_len), np.uint8)
+        et = np.zeros((E, self.out_len), np.float32)
+        em = np.zeros((E, self.out_len), np.uint8)
+        nt64 = np.zeros((n, self.out_len))
+        et64 = np.zeros((E, self.out_len))
+        _ok(lib().oracle_toy_targets(C.c_void_p(self.h), C.c_int(n), _p(np.ascontiguousarray(species, np.int32)),
+                                      C.c_int64(E), _p(np.ascontiguousarray(g["src"], np.int32)),
+                                      _p(np.ascontiguousarray(g["dst"], np.int32)),
+                                      _p(np.ascontiguousarray(g["shift"], np.int32)),
+                                      _p(np.ascontiguousarray(g["disp"], np.float64)),
+                                      _p(np.ascontiguousarray(g["dist"], np.float64)), _p(nt), _p(nm), _p(nt64), _p(et),
+                                      _p(em), _p(et64)))
+        return nt, nm, et, em, nt64, et64
+
     def uncoupled_block(self, za, zb, row, n_orb_a, n_orb_b):
         out = np.zeros(n_orb_a * n_orb_b)
         _ok(lib().oracle_uncoupled_block(C.c_void_p(self.h), C.c_int(za), C.c_int(zb),
@@ -276,3 +322,73 @@ def plan_view(plan, species, g):
     return dict(n_rows=plan["n_rows"], n_owned=plan["n_owned"],
                 row_species=np.asarray(species, np.int32)[plan["row_global"]], src_row=plan["src_row"],
                 dst_row=plan["dst_row"], disp=g["disp"][ei], dist=g["dist"][ei])
+
+
+# ------------------------------------------------------------------ training
+def masked_loss(pred, target, mask, n_total):
+    """ops.h:347-371: partials (sum_abs, sum_sq, count) in fp64 and the seed
+    gradient (sign(d) + 2 d) / n_total cast to the prediction's type."""
+    d = pred.astype(np.float64) - np.asarray(target, np.float64)
+    m = np.asarray(mask, bool)
+    sa = float(np.abs(d[m]).sum())
+    sq = float((d[m] ** 2).sum())
+    g = np.where(m, (np.sign(d) + 2.0 * d) / float(n_total), 0.0).astype(pred.dtype)
+    return (sa, sq, int(m.sum())), g
+
+
+def loss_grad(model, view, targets, n_total, dtype=np.float64, exchange=None, exchange_bwd=None):
+    """Network::record_loss + Tape::backward (serial or one rank): returns
+    (partials, grads) with grads laid out like the parameters.  exchange /
+    exchange_bwd(g_nodes) run around every block for multi-rank drivers."""
+    node_t, node_m, edge_t, edge_m = targets
+    nodes, edges = model.init_tables(view, dtype)
+    saved = []
+    for layer in range(model.layers):
+        for nb in (True, False):
+            if exchange is not None:
+                exchange(nodes)
+            saved.append((layer, nb, nodes.copy(), edges.copy()))
+            model.block(view, nodes, edges, layer, nb)
+    no, eo = model.heads(view, nodes, edges)
+    pn, gno = masked_loss(no, node_t, node_m, n_total)
+    pe, geo = masked_loss(eo, edge_t, edge_m, n_total)
+    grads = np.zeros(model.n_params, dtype)
+    g_nodes = np.zeros_like(nodes)
+    g_edges = np.zeros_like(edges)
+    model.heads_backward(view, nodes, edges, np.ascontiguousarray(gno), np.ascontiguousarray(geo), g_nodes, g_edges,
+                         grads)
+    for layer, nb, n_in, e_in in reversed(saved):
+        model.block_backward(view, n_in, e_in, layer, nb, g_nodes, g_edges, grads)
+        if exchange_bwd is not None:
+            exchange_bwd(g_nodes)
+    model.init_backward(view, g_nodes, g_edges, grads)
+    return (pn[0] + pe[0], pn[1] + pe[1], pn[2] + pe[2]), grads
+
+
+class Adam:
+    """optimizer.h:15-80 (moments in fp64, reduce-on-plateau)."""
+
+    def __init__(self, n, lr=5e-3, beta1=0.9, beta2=0.999, eps=1e-8, patience=100, factor=0.5, threshold=1e-4,
+                 min_lr=1e-6):
+        self.m = np.zeros(n)
+        self.v = np.zeros(n)
+        self.lr, self.b1, self.b2, self.eps = lr, beta1, beta2, eps
+        self.patience, self.factor, self.threshold, self.min_lr = patience, factor, threshold, min_lr
+        self.t, self.best, self.stale = 0, float("inf"), 0
+
+    def step(self, params, grads, loss):
+        self.t += 1
+        g = np.asarray(grads, np.float64)
+        self.m = self.b1 * self.m + (1.0 - self.b1) * g
+        self.v = self.b2 * self.v + (1.0 - self.b2) * g * g
+        mh = self.m / (1.0 - self.b1 ** self.t)
+        vh = self.v / (1.0 - self.b2 ** self.t)
+        out = (params.astype(np.float64) - self.lr * mh / (np.sqrt(vh) + self.eps)).astype(params.dtype)
+        if loss < self.best * (1.0 - self.threshold):
+            self.best, self.stale = loss, 0
+        else:
+            self.stale += 1
+            if self.stale >= self.patience:
+                self.lr = max(self.min_lr, self.lr * self.factor)
+                self.stale = 0
+        return out
