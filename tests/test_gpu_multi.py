@@ -30,3 +30,16 @@ def test_partitioned_forward_bit_exact(world, precision):
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0
     assert "bit-exact True" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_partitioned_training_step_matches_serial(world):
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + world),
+           os.path.join(ROOT, "tools", "multi_gpu_train_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "train lockstep True" in r.stdout
