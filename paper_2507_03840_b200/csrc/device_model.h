@@ -21,6 +21,8 @@ struct DeviceModel {
   float* params = nullptr;  // raw flat parameters
   std::vector<float*> w1t, w2t;      // per block (2*layers): SIMT packed
   std::vector<uint16_t*> w1b, w2b;   // per block: tcgen05 bf16 packed
+  std::vector<float*> w1n, w2n;      // per block: expanded, not transposed (training dx = W^T g)
+  bool weights_allocated = false;
   std::vector<int64_t> att_off;      // per layer offset into params
   float* embed = nullptr;            // per species slot x E
   float* head_w[2] = {nullptr, nullptr};  // node / edge: n_keys x E

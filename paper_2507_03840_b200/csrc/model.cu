@@ -304,6 +304,41 @@ __global__ void k_gather_dirs(const double* __restrict__ disp, const int* __rest
 
 }  // namespace
 
+// ------------------------------------------------------- weight packing
+// One order block of one SO(2) linear from the flat parameters
+// (network.h:266-276 names): the expanded matrix W (N x K; m = 0: W0,
+// m >= 1: [[Wr, Wi], [-Wi, Wr]]) written as
+//   t  -- transposed (K x N), the CUDA-core forward operand,
+//   w  -- row-major (N x K), the training dx operand (W^T g),
+//   b  -- bf16 tcgen05 B image: per 64-wide K chunk N rows x 128 B, 16-byte
+//         units swizzled by row % 8 (SWIZZLE_128B, K-major), K padded to 64.
+__global__ void k_pack_lin(const float* __restrict__ params, int64_t off_a, int64_t off_b, int m, int R, int C,
+                           float* __restrict__ t, float* __restrict__ w, uint16_t* __restrict__ b) {
+  const int N = m == 0 ? R : 2 * R, K = m == 0 ? C : 2 * C, KP = (K + 63) / 64 * 64;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto W = [&](int n, int k) -> float {
+    if (m == 0) return params[off_a + (int64_t)n * C + k];
+    const bool lo_n = n < R, lo_k = k < C;
+    const int nn = lo_n ? n : n - R, kk = lo_k ? k : k - C;
+    const float wr = params[off_a + (int64_t)nn * C + kk], wi = params[off_b + (int64_t)nn * C + kk];
+    return lo_n ? (lo_k ? wr : wi) : (lo_k ? -wi : wr);
+  };
+  if (i < (int64_t)N * K) {
+    const int n = (int)(i / K), k = (int)(i % K);
+    const float v = W(n, k);
+    w[i] = v;
+    t[(int64_t)k * N + n] = v;
+  }
+  if (i < (int64_t)KP * N) {  // bf16 image: (chunk, row, unit, lane) in storage order
+    const int kc = (int)(i / (64 * N)), rem = (int)(i % (64 * N)), n = rem / 64, u = (rem % 64) / 8, tl = rem % 8;
+    const int k = kc * 64 + ((u ^ (n & 7)) * 8) + tl;
+    float v = k < K ? W(n, k) : 0.f;
+    uint32_t bits = __float_as_uint(v);
+    bits += 0x7fffu + ((bits >> 16) & 1u);
+    b[i] = k < K ? uint16_t(bits >> 16) : 0;
+  }
+}
+
 // =================================================================== host
 void free_ptr(void* p) {
   if (p) cudaFree(p);
@@ -414,76 +449,76 @@ void model_upload_params(esg_model* M) {
   DeviceModel* D = M->dev;
   cudaStream_t st = M->ctx->stream;
   const int L = M->cfg.l_max, E = M->cfg.e_width;
-  free_ptr(D->params);
-  D->params = dalloc<float>(M->host_params.size());
+  const int nb = 2 * M->cfg.layers;
+  auto pad64 = [](int x) { return (x + 63) / 64 * 64; };
+  // sizes of every block's packs (fixed per model): allocated once, reused
+  auto lin_sizes = [&](int cin, int cout, size_t& dense, size_t& bf) {
+    dense = bf = 0;
+    for (int m = 0; m <= L; ++m) {
+      const int rows = m == 0 ? M->lay.nd(0) : 2 * M->lay.nd(m), K = rows * cin, N = rows * cout;
+      dense += (size_t)K * N;
+      bf += (size_t)pad64(K) * N;
+    }
+  };
+  size_t d1, bf1, d2, bf2;
+  lin_sizes(3 * E, 2 * E, d1, bf1);
+  lin_sizes(2 * E, E, d2, bf2);
+  if (!D->weights_allocated) {
+    D->params = dalloc<float>(M->host_params.size());
+    for (auto* v : {&D->w1t, &D->w2t, &D->w1n, &D->w2n}) v->assign(nb, nullptr);
+    D->w1b.assign(nb, nullptr);
+    D->w2b.assign(nb, nullptr);
+    for (int b = 0; b < nb; ++b) {
+      D->w1t[b] = dalloc<float>(d1);
+      D->w1n[b] = dalloc<float>(d1);
+      D->w2t[b] = dalloc<float>(d2);
+      D->w2n[b] = dalloc<float>(d2);
+      D->w1b[b] = dalloc<uint16_t>(bf1);
+      D->w2b[b] = dalloc<uint16_t>(bf2);
+    }
+    D->embed = dalloc<float>(M->species_list.size() * E);
+    D->head_w[0] = dalloc<float>(M->heads.keys.size() * E);
+    D->head_w[1] = dalloc<float>(M->heads.keys.size() * E);
+    D->head_key = dalloc<int>(M->heads.out_len);
+    D->head_row = dalloc<int>(M->heads.out_len);
+    D->weights_allocated = true;
+  }
   ESG_CUDA(cudaMemcpyAsync(D->params, M->host_params.data(), sizeof(float) * M->host_params.size(),
                            cudaMemcpyHostToDevice, st));
-  for (auto p : D->w1t) free_ptr(p);
-  for (auto p : D->w2t) free_ptr(p);
-  for (auto p : D->w1b) free_ptr(p);
-  for (auto p : D->w2b) free_ptr(p);
-  D->w1t.clear();
-  D->w2t.clear();
-  D->w1b.clear();
-  D->w2b.clear();
+  // every linear's three images from the device parameters
   D->att_off.clear();
-  auto pad64 = [](int x) { return (x + 63) / 64 * 64; };
   for (int layer = 0; layer < M->cfg.layers; ++layer) {
-    for (const char* blk : {"node", "edge"}) {
-      const std::string base = "layer" + std::to_string(layer) + "/" + blk;
-      std::vector<float> t1, t2;
-      std::vector<uint16_t> b1, b2;
-      for (int m = 0; m <= L; ++m) {
-        const int rows = m == 0 ? M->lay.nd(0) : 2 * M->lay.nd(m);
-        const int K1 = rows * 3 * E, N1 = rows * 2 * E, N2 = rows * E;
-        const auto W1 = expanded(M, base + "/lin1", m, 3 * E, 2 * E);  // N1 x K1
-        const auto W2 = expanded(M, base + "/lin2", m, 2 * E, E);      // N2 x N1
-        for (int k = 0; k < K1; ++k)
-          for (int o = 0; o < N1; ++o) t1.push_back(W1[(size_t)o * K1 + k]);
-        for (int k = 0; k < N1; ++k)
-          for (int o = 0; o < N2; ++o) t2.push_back(W2[(size_t)o * N1 + k]);
-        // tcgen05 B operands in the SMEM image so2_tc.cu bulk-copies: per
-        // 64-wide K chunk a block of N rows x 128 B, 16-byte units swizzled
-        // by row % 8 (SWIZZLE_128B, K-major); K padded to 64 with zeros.
-        auto pack = [&](const std::vector<float>& W, int N, int K, std::vector<uint16_t>& out) {
-          const int KP = pad64(K);
-          for (int kc = 0; kc < KP / 64; ++kc)
-            for (int n = 0; n < N; ++n)
-              for (int u = 0; u < 8; ++u) {
-                const int src_u = u ^ (n & 7);  // logical unit stored at physical slot u
-                for (int t = 0; t < 8; ++t) {
-                  const int k = kc * 64 + src_u * 8 + t;
-                  out.push_back(k < K ? to_bf16(W[(size_t)n * K + k]) : 0);
-                }
-              }
-        };
-        pack(W1, N1, K1, b1);
-        pack(W2, N2, N1, b2);
+    for (int bi = 0; bi < 2; ++bi) {
+      const int b = 2 * layer + bi;
+      const std::string base = "layer" + std::to_string(layer) + (bi == 0 ? "/node" : "/edge");
+      for (int li = 0; li < 2; ++li) {
+        const int cin = li == 0 ? 3 * E : 2 * E, cout = li == 0 ? 2 * E : E;
+        const std::string wb = base + (li == 0 ? "/lin1" : "/lin2");
+        size_t dense = 0, bf = 0;
+        for (int m = 0; m <= L; ++m) {
+          const int nd = M->lay.nd(m), R = nd * cout, C = nd * cin;
+          const int N = m == 0 ? R : 2 * R, K = m == 0 ? C : 2 * C;
+          const int64_t oa = M->params.at(m == 0 ? wb + "/m0" : wb + "/m" + std::to_string(m) + "r").offset;
+          const int64_t ob = m == 0 ? oa : M->params.at(wb + "/m" + std::to_string(m) + "i").offset;
+          const int64_t work = std::max<int64_t>((int64_t)N * K, (int64_t)pad64(K) * N);
+          k_pack_lin<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(
+              D->params, oa, ob, m, R, C, (li == 0 ? D->w1t[b] : D->w2t[b]) + dense,
+              (li == 0 ? D->w1n[b] : D->w2n[b]) + dense, (li == 0 ? D->w1b[b] : D->w2b[b]) + bf);
+          dense += (size_t)N * K;
+          bf += (size_t)pad64(K) * N;
+        }
       }
-      float* d1 = dalloc<float>(t1.size());
-      float* d2 = dalloc<float>(t2.size());
-      uint16_t* e1 = dalloc<uint16_t>(b1.size());
-      uint16_t* e2 = dalloc<uint16_t>(b2.size());
-      ESG_CUDA(cudaMemcpy(d1, t1.data(), sizeof(float) * t1.size(), cudaMemcpyHostToDevice));
-      ESG_CUDA(cudaMemcpy(d2, t2.data(), sizeof(float) * t2.size(), cudaMemcpyHostToDevice));
-      ESG_CUDA(cudaMemcpy(e1, b1.data(), sizeof(uint16_t) * b1.size(), cudaMemcpyHostToDevice));
-      ESG_CUDA(cudaMemcpy(e2, b2.data(), sizeof(uint16_t) * b2.size(), cudaMemcpyHostToDevice));
-      D->w1t.push_back(d1);
-      D->w2t.push_back(d2);
-      D->w1b.push_back(e1);
-      D->w2b.push_back(e2);
     }
     D->att_off.push_back(M->params.at("layer" + std::to_string(layer) + "/att").offset);
   }
+  ESG_CUDA(cudaGetLastError());
   // embeddings per species slot (ascending Z), lift, heads
   std::vector<float> emb;
   for (int z : M->species_list) {
     const auto& e = M->params.at("embed/" + element_symbol(z));
     emb.insert(emb.end(), M->host_params.begin() + e.offset, M->host_params.begin() + e.offset + E);
   }
-  free_ptr(D->embed);
-  D->embed = dalloc<float>(emb.size());
-  ESG_CUDA(cudaMemcpy(D->embed, emb.data(), sizeof(float) * emb.size(), cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpyAsync(D->embed, emb.data(), sizeof(float) * emb.size(), cudaMemcpyHostToDevice, st));
   D->lift_off = M->params.at("radial/lift").offset;
   // per head output j: its key and the harmonic row it projects (k_heads)
   std::vector<int> key_of, row_of;
@@ -494,23 +529,18 @@ void model_upload_params(esg_model* M) {
       row_of.push_back(Lk * Lk + r);
     }
   }
+  std::vector<float> hw[2];
   for (int s = 0; s < 2; ++s) {
-    std::vector<float> hw;
     for (const auto& k : M->heads.keys) {
       const auto& e = M->params.at(std::string("head/") + (s == 0 ? "node" : "edge") + "/s" + std::to_string(k.sa) +
                                    "s" + std::to_string(k.sb) + "L" + std::to_string(k.L));
-      hw.insert(hw.end(), M->host_params.begin() + e.offset, M->host_params.begin() + e.offset + E);
+      hw[s].insert(hw[s].end(), M->host_params.begin() + e.offset, M->host_params.begin() + e.offset + E);
     }
-    free_ptr(D->head_w[s]);
-    D->head_w[s] = dalloc<float>(hw.size());
-    ESG_CUDA(cudaMemcpy(D->head_w[s], hw.data(), sizeof(float) * hw.size(), cudaMemcpyHostToDevice));
+    ESG_CUDA(cudaMemcpyAsync(D->head_w[s], hw[s].data(), sizeof(float) * hw[s].size(), cudaMemcpyHostToDevice, st));
   }
-  free_ptr(D->head_key);
-  free_ptr(D->head_row);
-  D->head_key = dalloc<int>(key_of.size());
-  D->head_row = dalloc<int>(row_of.size());
-  ESG_CUDA(cudaMemcpy(D->head_key, key_of.data(), sizeof(int) * key_of.size(), cudaMemcpyHostToDevice));
-  ESG_CUDA(cudaMemcpy(D->head_row, row_of.data(), sizeof(int) * row_of.size(), cudaMemcpyHostToDevice));
+  ESG_CUDA(cudaMemcpyAsync(D->head_key, key_of.data(), sizeof(int) * key_of.size(), cudaMemcpyHostToDevice, st));
+  ESG_CUDA(cudaMemcpyAsync(D->head_row, row_of.data(), sizeof(int) * row_of.size(), cudaMemcpyHostToDevice, st));
+  ESG_CUDA(cudaStreamSynchronize(st));  // the host staging vectors go out of scope
 }
 
 void model_device_create(esg_model* M) {
@@ -619,6 +649,8 @@ void model_device_destroy(esg_model* M) {
     free_ptr(p);
   for (auto p : D->w1t) free_ptr(p);
   for (auto p : D->w2t) free_ptr(p);
+  for (auto p : D->w1n) free_ptr(p);
+  for (auto p : D->w2n) free_ptr(p);
   for (auto p : D->w1b) free_ptr(p);
   for (auto p : D->w2b) free_ptr(p);
   for (auto& e : D->ev) cudaEventDestroy(e);

@@ -33,6 +33,17 @@ namespace esg {
 
 std::vector<float> expanded(const esg_model* M, const std::string& base, int m, int cin, int cout);  // model.cu
 
+// one 64-output tile of an order block of a per-order linear (k_gemm_m)
+struct LinTile {
+  int m, o0, K, N;
+  int64_t p_off;  // offset of P_m
+};
+// one 64 x 64 output tile of a weight-gradient product (k_outer_tiled)
+struct OuterTile {
+  int m, n0, k0, N, K;  // order, tile origin, block dims
+  int64_t acc_off;      // offset of the order block in the accumulator
+};
+
 struct TrainState {
   // loss targets in head space, view order (network.h:187-214)
   float* node_target = nullptr;
@@ -46,8 +57,6 @@ struct TrainState {
   float* g_nodes_out = nullptr;  // node blocks: snapshot of the output gradient (attention backward input)
   float* g_node_out = nullptr;
   float* g_edge_out = nullptr;
-  // expanded weights, not transposed (dx = W^T g): per block, concatenated over m
-  std::vector<float*> w1n, w2n;
   // chunk scratch
   int64_t cap = 0;
   float *A1 = nullptr, *Hh = nullptr, *Gg = nullptr, *Yy = nullptr, *msg = nullptr, *gY = nullptr, *gG = nullptr,
@@ -65,6 +74,14 @@ struct TrainState {
   // reduction partials
   double* part = nullptr;
   int64_t part_n = 0;
+  // tiled dW: tile lists of lin1 (g 2E x A1 3E) and lin2 (g E x G 2E), split partials
+  LinTile* lt[4] = {nullptr, nullptr, nullptr, nullptr};  // lin1 fwd, lin2 fwd, lin2 dx, lin1 dx
+  int n_lt[4] = {0, 0, 0, 0};
+  OuterTile* tiles1 = nullptr;
+  OuterTile* tiles2 = nullptr;
+  int n_tiles1 = 0, n_tiles2 = 0;
+  double* opart = nullptr;
+  int64_t opart_n = 0;
   // per head output j: its harmonic plane, and per plane the outputs (in key order)
   int* plane_ptr = nullptr;
   int* plane_out = nullptr;
@@ -204,6 +221,64 @@ __global__ void __launch_bounds__(256) k_lin(const float* __restrict__ in, int c
   }
 }
 
+// The per-order linear as a register-blocked SGEMM: CTA tile of 64 edges x
+// 64 outputs of one order block (tile list: (m, o0)), 16-deep K stages in
+// SMEM, thread (ty, tx) owns 4 edges x 4 outputs.  Each output sums its K
+// terms in ascending order with fmaf, exactly as k_so2_simt / k_lin.
+template <int L>
+__global__ void __launch_bounds__(256) k_gemm_m(const float* __restrict__ in, int cin, int64_t n_e,
+                                                const float* __restrict__ P, const LinTile* __restrict__ tiles, int cout,
+                                                float* __restrict__ out) {
+  using G = Geo<L>;
+  constexpr int TM = 64, TK = 16;
+  __shared__ float As[TK][TM + 4];
+  __shared__ __align__(16) float Bs[TK][64];
+  const LinTile t = tiles[blockIdx.y];
+  const int64_t e0 = (int64_t)blockIdx.x * TM;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const int io = G::moff(t.m) * cin, oo = G::moff(t.m) * cout;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int k0 = 0; k0 < t.K; k0 += TK) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < TM * TK; u += 256) {  // A: 64 edges x 16 k (edge rows contiguous in k)
+      const int e = u / TK, k = u % TK;
+      const int64_t ee = e0 + e;
+      As[k][e] = (ee < n_e && k0 + k < t.K) ? in[ee * G::H * cin + io + k0 + k] : 0.f;
+    }
+    for (int u = threadIdx.x; u < TK * 64; u += 256) {  // B: 16 k x 64 outputs
+      const int k = u / 64, o = u % 64;
+      Bs[k][o] = (k0 + k < t.K && t.o0 + o < t.N) ? P[t.p_off + (int64_t)(k0 + k) * t.N + t.o0 + o] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < TK; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t ee = e0 + ty * 4 + i;
+    if (ee >= n_e) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int o = t.o0 + tx * 4 + j;
+      if (o < t.N) out[ee * G::H * cout + oo + o] = acc[i][j];
+    }
+  }
+}
+
 // dWexp_m[o][k] += sum_e g_m[e][o] x_m[e][k] over the chunk's edges in
 // order, fp64; one thread per output element, no two CTAs share an output.
 template <int L>
@@ -227,6 +302,70 @@ __global__ void k_outer(const float* __restrict__ g, int cg, const float* __rest
   double a = 0.0;
   for (int64_t e = 0; e < n_e; ++e) a += double(gp[e * G::H * cg]) * double(xp[e * G::H * cx]);
   acc[u] += a;
+}
+
+// The same sums as a tiled NT GEMM: CTA (tile, split) accumulates a 64 x 64
+// output tile of order block m over its edge split [s0, s1) -- thread
+// (ty, tx) a 4 x 4 block, 16 edges per SMEM stage, fp64 accumulators (the
+// fp32 products are exact in fp64) -- and writes the tile to its split's
+// partial slot; k_outer_reduce then adds the splits in order (fp64).  Within
+// a split (<= 2048 edges) the sums are fp32 fmaf in edge order.
+template <int L>
+__global__ void __launch_bounds__(256) k_outer_tiled(const float* __restrict__ g, int cg, const float* __restrict__ x,
+                                                     int cx, int64_t n_e, const OuterTile* __restrict__ tiles,
+                                                     int n_tiles, int64_t per_split, double* __restrict__ part) {
+  using G = Geo<L>;
+  constexpr int TE = 16;
+  __shared__ float sg[TE][64];
+  __shared__ float sx[TE][64];
+  const OuterTile t = tiles[blockIdx.x];
+  const int split = blockIdx.y;
+  const int64_t s0 = split * per_split, s1 = s0 + per_split < n_e ? s0 + per_split : n_e;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const int go = G::moff(t.m) * cg + t.n0, xo = G::moff(t.m) * cx + t.k0;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int64_t e0 = s0; e0 < s1; e0 += TE) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < TE * 64; u += 256) {
+      const int e = u / 64, c = u % 64;
+      const int64_t ee = e0 + e;
+      sg[e][c] = (ee < s1 && t.n0 + c < t.N) ? g[ee * G::H * cg + go + c] : 0.f;
+      sx[e][c] = (ee < s1 && t.k0 + c < t.K) ? x[ee * G::H * cx + xo + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int e = 0; e < TE; ++e) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sg[e][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sx[e][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+  }
+  double* out = part + ((int64_t)split * n_tiles + blockIdx.x) * 4096;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out[(ty * 4 + i) * 64 + tx * 4 + j] = acc[i][j];
+}
+__global__ void k_outer_reduce(const double* __restrict__ part, int n_tiles, int n_split,
+                               const OuterTile* __restrict__ tiles, double* __restrict__ acc) {
+  const OuterTile t = tiles[blockIdx.x];
+  for (int u = threadIdx.x; u < 4096; u += blockDim.x) {
+    const int n = t.n0 + u / 64, k = t.k0 + u % 64;
+    if (n >= t.N || k >= t.K) continue;
+    double s = 0.0;
+    for (int sp = 0; sp < n_split; ++sp) s += part[((int64_t)sp * n_tiles + blockIdx.x) * 4096 + u];
+    acc[t.acc_off + (int64_t)n * t.K + k] += s;
+  }
 }
 
 // gate (kernels.h:210-226) and its backward (kernels.h:228-250); rows are
@@ -519,10 +658,9 @@ void train_free(DeviceModel* D) {
                   (void*)T->Hh, (void*)T->Gg, (void*)T->Yy, (void*)T->msg, (void*)T->gY, (void*)T->gG, (void*)T->gH,
                   (void*)T->gA1, (void*)T->gx, (void*)T->gacc, (void*)T->part, (void*)T->plane_ptr,
                   (void*)T->plane_out, (void*)T->out_plane, (void*)T->out_key, (void*)T->rbf_scratch,
-                  (void*)T->halo_send, (void*)T->halo_recv})
+                  (void*)T->halo_send, (void*)T->halo_recv, (void*)T->tiles1, (void*)T->tiles2, (void*)T->opart,
+                  (void*)T->lt[0], (void*)T->lt[1], (void*)T->lt[2], (void*)T->lt[3]})
     free_ptr(p);
-  for (auto* v : {&T->w1n, &T->w2n})
-    for (float* p : *v) free_ptr(p);
   for (auto* v : {&T->src_perm, &T->src_off, &T->src_row_u})
     for (int* p : *v) free_ptr(p);
   for (float* p : D->saved_nodes) free_ptr(p);
@@ -599,6 +737,9 @@ void gacc_layout(esg_model* M, TrainState* T) {
   o += (int64_t)M->species_list.size() * E;
   T->gacc_n = o;
 }
+
+void outer_tiles(esg_model* M, TrainState* T);
+void lin_tiles(esg_model* M, TrainState* T);
 
 // (Re)builds everything that depends on the prepared view and the weights.
 void train_setup(esg_model* M) {
@@ -719,6 +860,8 @@ void train_setup(esg_model* M) {
   ESG_CUDA(cudaMemcpy(T->out_key, out_key.data(), sizeof(int) * ol, cudaMemcpyHostToDevice));
   // accumulators and partials
   gacc_layout(M, T);
+  outer_tiles(M, T);
+  lin_tiles(M, T);
   free_ptr(T->gacc);
   T->gacc = talloc<double>(T->gacc_n);
   free_ptr(T->part);
@@ -739,54 +882,73 @@ void train_setup(esg_model* M) {
   T->halo_recv = talloc<float>((size_t)std::max<int64_t>(send_rows, 1) * row);
 }
 
-// expanded weights, not transposed, per block (dx = W^T g)
-void train_weights(esg_model* M) {
-  DeviceModel* D = M->dev;
-  TrainState* T = D->train;
-  const int L = M->cfg.l_max, E = M->cfg.e_width;
-  for (auto* v : {&T->w1n, &T->w2n})
-    for (float* p : *v) free_ptr(p);
-  T->w1n.clear();
-  T->w2n.clear();
-  for (int layer = 0; layer < M->cfg.layers; ++layer)
-    for (const char* blk : {"node", "edge"}) {
-      const std::string base = "layer" + std::to_string(layer) + "/" + blk;
-      std::vector<float> a, b;
-      for (int m = 0; m <= L; ++m) {
-        const auto W1 = expanded(M, base + "/lin1", m, 3 * E, 2 * E);  // N1 x K1
-        const auto W2 = expanded(M, base + "/lin2", m, 2 * E, E);      // N2 x N1
-        a.insert(a.end(), W1.begin(), W1.end());
-        b.insert(b.end(), W2.begin(), W2.end());
-      }
-      float* d1 = talloc<float>(a.size());
-      float* d2 = talloc<float>(b.size());
-      ESG_CUDA(cudaMemcpy(d1, a.data(), sizeof(float) * a.size(), cudaMemcpyHostToDevice));
-      ESG_CUDA(cudaMemcpy(d2, b.data(), sizeof(float) * b.size(), cudaMemcpyHostToDevice));
-      T->w1n.push_back(d1);
-      T->w2n.push_back(d2);
-    }
+
+// kind 0: lin1 forward (3E -> 2E, P = W1^T), 1: lin2 forward (2E -> E, W2^T),
+// 2: lin2 dx (E -> 2E, P = W2), 3: lin1 dx (2E -> 3E, P = W1)
+template <int L, int E>
+void lin(int kind, const float* in, int64_t n, const float* P, float* out, TrainState* T, cudaStream_t st) {
+  static const int cin_of[4] = {3 * E, 2 * E, E, 2 * E}, cout_of[4] = {2 * E, E, 2 * E, 3 * E};
+  if (n > 0)
+    k_gemm_m<L><<<dim3((unsigned)((n + 63) / 64), (unsigned)T->n_lt[kind]), 256, 0, st>>>(
+        in, cin_of[kind], n, P, T->lt[kind], cout_of[kind], out);
 }
 
-template <int L, int E>
-void lin(const float* in, int cin, int64_t n, const float* P, int cout, float* out, cudaStream_t st) {
-  using G = Geo<L>;
-  int kmax = 0;
-  for (int m = 0; m <= L; ++m) kmax = std::max(kmax, G::rows(m) * cin);
-  const int smem = 16 * kmax * (int)sizeof(float);
-  static int attr_set = 0;
-  if (smem > attr_set) {
-    ESG_CUDA(cudaFuncSetAttribute(k_lin<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr_set = 96 * 1024;
+void lin_tiles(esg_model* M, TrainState* T) {
+  const int L = M->cfg.l_max, E = M->cfg.e_width;
+  const int cin_of[4] = {3 * E, 2 * E, E, 2 * E}, cout_of[4] = {2 * E, E, 2 * E, 3 * E};
+  for (int kind = 0; kind < 4; ++kind) {
+    std::vector<LinTile> v;
+    int64_t off = 0;
+    for (int m = 0; m <= L; ++m) {
+      const int rows = m == 0 ? L + 1 : 2 * (L - m + 1), K = rows * cin_of[kind], N = rows * cout_of[kind];
+      for (int o0 = 0; o0 < N; o0 += 64) v.push_back({m, o0, K, N, off});
+      off += (int64_t)K * N;
+    }
+    free_ptr(T->lt[kind]);
+    T->lt[kind] = talloc<LinTile>(v.size());
+    ESG_CUDA(cudaMemcpy(T->lt[kind], v.data(), sizeof(LinTile) * v.size(), cudaMemcpyHostToDevice));
+    T->n_lt[kind] = (int)v.size();
   }
-  if (n > 0) k_lin<L><<<(unsigned)((n + 15) / 16), 256, smem, st>>>(in, cin, n, P, cout, out);
 }
+
+constexpr int OUTER_SPLIT = 2048;       // edges per split of a weight-gradient tile
+constexpr int OUTER_SPLIT_MAX = 128;    // splits per tile (chunk cap 256k edges)
 
 template <int L>
-void outer(const float* g, int cg, const float* x, int cx, int64_t n, double* acc, cudaStream_t st) {
-  using G = Geo<L>;
-  int64_t total = 0;
-  for (int m = 0; m <= L; ++m) total += (int64_t)G::rows(m) * cg * G::rows(m) * cx;
-  if (n > 0) k_outer<L><<<(unsigned)((total + 127) / 128), 128, 0, st>>>(g, cg, x, cx, n, acc);
+void outer(const float* g, int cg, const float* x, int cx, int64_t n, double* acc, bool lin1, TrainState* T,
+           cudaStream_t st) {
+  if (n <= 0) return;
+  const int n_tiles = lin1 ? T->n_tiles1 : T->n_tiles2;
+  const OuterTile* tiles = lin1 ? T->tiles1 : T->tiles2;
+  const int split = (int)std::min<int64_t>(OUTER_SPLIT_MAX, (n + OUTER_SPLIT - 1) / OUTER_SPLIT);
+  const int64_t per = (n + split - 1) / split;
+  k_outer_tiled<L><<<dim3((unsigned)n_tiles, (unsigned)split), 256, 0, st>>>(g, cg, x, cx, n, tiles, n_tiles, per,
+                                                                             T->opart);
+  k_outer_reduce<<<(unsigned)n_tiles, 256, 0, st>>>(T->opart, n_tiles, split, tiles, acc);
+}
+
+// tile lists of the two dW products (per order block: N x K outputs)
+void outer_tiles(esg_model* M, TrainState* T) {
+  const int L = M->cfg.l_max, E = M->cfg.e_width;
+  for (int which = 0; which < 2; ++which) {
+    const int cg = which == 0 ? 2 * E : E, cx = which == 0 ? 3 * E : 2 * E;
+    std::vector<OuterTile> v;
+    int64_t off = 0;
+    for (int m = 0; m <= L; ++m) {
+      const int rows = m == 0 ? L + 1 : 2 * (L - m + 1), N = rows * cg, K = rows * cx;
+      for (int n0 = 0; n0 < N; n0 += 64)
+        for (int k0 = 0; k0 < K; k0 += 64) v.push_back({m, n0, k0, N, K, off});
+      off += (int64_t)N * K;
+    }
+    OuterTile*& dst = which == 0 ? T->tiles1 : T->tiles2;
+    free_ptr(dst);
+    dst = talloc<OuterTile>(v.size());
+    ESG_CUDA(cudaMemcpy(dst, v.data(), sizeof(OuterTile) * v.size(), cudaMemcpyHostToDevice));
+    (which == 0 ? T->n_tiles1 : T->n_tiles2) = (int)v.size();
+  }
+  free_ptr(T->opart);
+  T->opart_n = (int64_t)OUTER_SPLIT_MAX * std::max(T->n_tiles1, T->n_tiles2) * 4096;
+  T->opart = talloc<double>(T->opart_n);
 }
 
 // reverse of the forward's exchange: halo-row gradients go back to their
@@ -852,11 +1014,11 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     // forward recompute: A1, H, G (+ Y and msg for the attention backward)
     k_rotate_in<L, E, 1, float><<<t32, RI_THREADS, 0, st>>>(nodes, edges, D->src_row, D->dst_row, D->dir, e0, n, T->A1,
                                                             D->rc);
-    lin<L, E>(T->A1, 3 * E, n, D->w1t[b], 2 * E, T->Hh, st);
+    lin<L, E>(0, T->A1, n, D->w1t[b], T->Hh, T, st);
     k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, 2 * E, n, M->cfg.gate_enabled, T->Gg);
     const float* g_msg;
     if (node_block) {
-      lin<L, E>(T->Gg, 2 * E, n, D->w2t[b], E, T->Yy, st);
+      lin<L, E>(1, T->Gg, n, D->w2t[b], T->Yy, T, st);
       k_rot1<L, E, 0><<<t32, 128, 0, st>>>(T->Yy, D->dir, e0, n, T->msg);
       // attention backward into gY's buffer (used as g_msg scratch)
       k_attn_bwd<H, E><<<(unsigned)(ch.second - ch.first), 128, 0, st>>>(
@@ -869,13 +1031,13 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     }
     k_rot1<L, E, 1><<<t32, 128, 0, st>>>(g_msg, D->dir, e0, n, T->gY);
     // lin2 adjoint
-    outer<L>(T->gY, E, T->Gg, 2 * E, n, T->gacc + T->off_lin2[b], st);
-    lin<L, E>(T->gY, E, n, T->w2n[b], 2 * E, T->gG, st);
+    outer<L>(T->gY, E, T->Gg, 2 * E, n, T->gacc + T->off_lin2[b], false, T, st);
+    lin<L, E>(2, T->gY, n, D->w2n[b], T->gG, T, st);
     k_gate_bwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, T->gG, 2 * E, n, M->cfg.gate_enabled,
                                                                        T->gH);
     // lin1 adjoint
-    outer<L>(T->gH, 2 * E, T->A1, 3 * E, n, T->gacc + T->off_lin1[b], st);
-    lin<L, E>(T->gH, 2 * E, n, T->w1n[b], 3 * E, T->gA1, st);
+    outer<L>(T->gH, 2 * E, T->A1, 3 * E, n, T->gacc + T->off_lin1[b], true, T, st);
+    lin<L, E>(3, T->gH, n, D->w1n[b], T->gA1, T, st);
     // rotate-in / concat adjoint, ordered row reductions
     k_rot_in_bwd<L, E><<<t32, RI_THREADS, 0, st>>>(T->gA1, D->dir, e0, n, T->g_edges, T->gx);
     k_dst_reduce<<<(unsigned)(ch.second - ch.first), 128, 0, st>>>(T->gx, HE, D->seg, ch.first, e0, T->g_nodes);
@@ -1086,7 +1248,6 @@ void model_loss_grad(esg_model* M, int64_t n_total, double partials[3], double* 
     train_setup(M);
     D->train_stale = false;
   }
-  train_weights(M);
   if (L == 4 && E == 16)
     loss_grad_impl<4, 16>(M, n_total, partials, loss, grads_out);
   else if (L == 4 && E == 8)
