@@ -23,6 +23,10 @@ struct DeviceModel {
   std::vector<uint16_t*> w1b, w2b;   // per block: tcgen05 bf16 packed
   std::vector<float*> w1n, w2n;      // per block: expanded, not transposed (training dx = W^T g)
   bool weights_allocated = false;
+  struct LinTile* lt[4] = {nullptr, nullptr, nullptr, nullptr};  // k_gemm_m tile lists (lin_kernels.cuh)
+  int n_lt[4] = {0, 0, 0, 0};
+  float* Hbuf = nullptr;  // fp32 path: lin1 output / gated operand of a chunk
+  size_t cap_hbuf = 0;
   std::vector<int64_t> att_off;      // per layer offset into params
   float* embed = nullptr;            // per species slot x E
   float* head_w[2] = {nullptr, nullptr};  // node / edge: n_keys x E

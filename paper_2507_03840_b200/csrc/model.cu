@@ -5,7 +5,7 @@
 //                 direction (recomputed, never stored), rotate into the edge
 //                 frame, scatter to the order-major A1 operand     (a8-a10)
 //   SO(2) linears lin1 -> gate -> lin2 per order m                  (a11-a12)
-//                 fp32 CUDA cores (k_so2_simt) or tcgen05 bf16 (so2_tc.cu)
+//                 fp32 CUDA-core SGEMMs (lin_kernels.cuh) or tcgen05 bf16 (so2_tc.cu)
 //   k_rotate_out_edge   rotate back (D^T) and residual-add in place (a13 edge)
 //   k_node_update       segment softmax over the dst CSR segment, weighted
 //                       sum of rotated-back messages, one store per node
@@ -21,6 +21,7 @@
 #include "model_kernels.cuh"
 #include "msg_kernels.cuh"
 #include "device_model.h"
+#include "lin_kernels.cuh"
 
 namespace esg {
 
@@ -116,69 +117,10 @@ __global__ void __launch_bounds__(256) k_init_edges(const double* __restrict__ d
 }
 
 // ------------------------------------------------- SO(2) linears, fp32
-// kernels.h:133-161 (lin1 3E->2E), :210-226 (gate), lin2 2E->E, per order m
-// with the expanded weight [[Wr, Wi], [-Wi, Wr]] so ym = Wr xm + Wi xp and
-// yp = Wr xp - Wi xm come out of one product.  W1T/W2T are the expanded
-// matrices transposed (K x N, N contiguous) and concatenated over m.
-template <int L, int E>
-__global__ void __launch_bounds__(256) k_so2_simt(const float* __restrict__ A1, int64_t n_e,
-                                                  const float* __restrict__ W1T, const float* __restrict__ W2T,
-                                                  float* __restrict__ Yout, int gate) {
-  using G = Geo<L>;
-  using Y = Lay1<L, E, 1>;
-  constexpr int TE = 16, C2 = 2 * E;
-  constexpr int KMAX = Y::K(L > 0 ? 1 : 0) > Y::K(0) ? Y::K(1) : Y::K(0);
-  constexpr int NMAX = Y::N1(L > 0 ? 1 : 0) > Y::N1(0) ? Y::N1(1) : Y::N1(0);
-  __shared__ float sA[TE * KMAX];
-  __shared__ float sH[TE * NMAX];
-  __shared__ float sS[TE * C2];
-  const int64_t t0 = (int64_t)blockIdx.x * TE;
-  const int ne = (int)cmin64(TE, n_e - t0);
-  int64_t w1 = 0, w2 = 0;
-#pragma unroll 1
-  for (int m = 0; m <= L; ++m) {
-    const int K = Y::K(m), N = Y::N1(m), N2 = Y::N2(m);
-    for (int i = threadIdx.x; i < TE * K; i += blockDim.x) {
-      const int e = i / K, k = i % K;
-      sA[i] = e < ne ? A1[(t0 + e) * Y::KTOT + Y::kofs(m) + k] : 0.f;
-    }
-    __syncthreads();
-    float acc[TE];
-    const int o = threadIdx.x;
-    if (o < N) {
-#pragma unroll
-      for (int e = 0; e < TE; ++e) acc[e] = 0.f;
-      for (int k = 0; k < K; ++k) {
-        const float w = W1T[w1 + (int64_t)k * N + o];
-#pragma unroll
-        for (int e = 0; e < TE; ++e) acc[e] = fmaf(sA[e * K + k], w, acc[e]);
-      }
-      if (m == 0 && o < C2) {
-#pragma unroll
-        for (int e = 0; e < TE; ++e) sS[e * C2 + o] = gate ? 1.f / (1.f + expf(-acc[e])) : 1.f;
-      }
-    }
-    __syncthreads();
-    if (o < N) {
-#pragma unroll
-      for (int e = 0; e < TE; ++e) sH[e * N + o] = acc[e] * sS[e * C2 + (o % C2)];
-    }
-    __syncthreads();
-    if (o < N2) {
-#pragma unroll
-      for (int e = 0; e < TE; ++e) acc[e] = 0.f;
-      for (int k = 0; k < N; ++k) {
-        const float w = W2T[w2 + (int64_t)k * N2 + o];
-#pragma unroll
-        for (int e = 0; e < TE; ++e) acc[e] = fmaf(sH[e * N + k], w, acc[e]);
-      }
-      for (int e = 0; e < ne; ++e) Yout[(t0 + e) * (G::H * E) + G::moff(m) * E + o] = acc[e];
-    }
-    __syncthreads();
-    w1 += (int64_t)K * N;
-    w2 += (int64_t)N * N2;
-  }
-}
+// The CUDA-core path runs kernels.h:133-161 (lin1 3E->2E), :210-226 (gate)
+// and lin2 2E->E as per-order SGEMMs with the expanded weight
+// [[Wr, Wi], [-Wi, Wr]] (lin_kernels.cuh k_gemm_m, k_gate_fwd), so
+// ym = Wr xm + Wi xp and yp = Wr xp - Wi xm come out of one product.
 
 __global__ void k_copy_rows(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -481,6 +423,21 @@ void model_upload_params(esg_model* M) {
     D->head_w[1] = dalloc<float>(M->heads.keys.size() * E);
     D->head_key = dalloc<int>(M->heads.out_len);
     D->head_row = dalloc<int>(M->heads.out_len);
+    // tile lists of the CUDA-core SGEMM per linear kind (lin_kernels.cuh)
+    const int cin_of[4] = {3 * E, 2 * E, E, 2 * E}, cout_of[4] = {2 * E, E, 2 * E, 3 * E};
+    for (int kind = 0; kind < 4; ++kind) {
+      std::vector<LinTile> v;
+      int64_t off = 0;
+      for (int m = 0; m <= L; ++m) {
+        const int rows = m == 0 ? M->lay.nd(0) : 2 * M->lay.nd(m), K = rows * cin_of[kind],
+                  N = rows * cout_of[kind];
+        for (int o0 = 0; o0 < N; o0 += 64) v.push_back({m, o0, K, N, off});
+        off += (int64_t)K * N;
+      }
+      D->lt[kind] = dalloc<LinTile>(v.size());
+      ESG_CUDA(cudaMemcpy(D->lt[kind], v.data(), sizeof(LinTile) * v.size(), cudaMemcpyHostToDevice));
+      D->n_lt[kind] = (int)v.size();
+    }
     D->weights_allocated = true;
   }
   ESG_CUDA(cudaMemcpyAsync(D->params, M->host_params.data(), sizeof(float) * M->host_params.size(),
@@ -650,6 +607,8 @@ void model_device_destroy(esg_model* M) {
   for (auto p : D->w1t) free_ptr(p);
   for (auto p : D->w2t) free_ptr(p);
   for (auto p : D->w1n) free_ptr(p);
+  for (int k = 0; k < 4; ++k) free_ptr(D->lt[k]);
+  free_ptr(D->Hbuf);
   for (auto p : D->w2n) free_ptr(p);
   for (auto p : D->w1b) free_ptr(p);
   for (auto p : D->w2b) free_ptr(p);
@@ -869,7 +828,6 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     const int64_t e0 = D->h_seg[ch.first], e1 = D->h_seg[ch.second];
     const int64_t n = e1 - e0;
     if (n > 0) {
-      const unsigned tiles = (unsigned)((n + 15) / 16);
       const unsigned ri_tiles = (unsigned)((n + 31) / 32);
       constexpr int RI_THREADS = 32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4;  // >= 4 warps for the Wigner groups
       if (tc) {
@@ -890,9 +848,13 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
                                                                     D->dir, e0, n, (float*)D->A1, D->rc);
         }
         Prof pr(D, st, ESG_PROF_SO2);
-        k_so2_simt<L, E><<<tiles, 256, 0, st>>>((const float*)D->A1, n, D->w1t[bidx], D->w2t[bidx], D->Y,
-                                                M->cfg.gate_enabled);
-        ctx->launches += 2;
+        // CUDA-core SGEMM per order block, gate in place, SGEMM
+        D->Hbuf = grow(D->Hbuf, D->cap_hbuf, (size_t)D->chunk_cap * H * 2 * E);
+        lin_launch<L, E>(0, (const float*)D->A1, n, D->w1t[bidx], D->Hbuf, D->lt[0], D->n_lt[0], st);
+        k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(D->Hbuf, 2 * E, n, M->cfg.gate_enabled,
+                                                                            D->Hbuf);
+        lin_launch<L, E>(1, D->Hbuf, n, D->w2t[bidx], D->Y, D->lt[1], D->n_lt[1], st);
+        ctx->launches += 4;
       }
       if (!node_block) {
         Prof pr(D, st, ESG_PROF_ROTATE_OUT);

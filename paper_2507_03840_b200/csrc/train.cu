@@ -28,16 +28,12 @@
 #include "esg_internal.h"
 #include "model_kernels.cuh"
 #include "msg_kernels.cuh"
+#include "lin_kernels.cuh"
 
 namespace esg {
 
 std::vector<float> expanded(const esg_model* M, const std::string& base, int m, int cin, int cout);  // model.cu
 
-// one 64-output tile of an order block of a per-order linear (k_gemm_m)
-struct LinTile {
-  int m, o0, K, N;
-  int64_t p_off;  // offset of P_m
-};
 // one 64 x 64 output tile of a weight-gradient product (k_outer_tiled)
 struct OuterTile {
   int m, n0, k0, N, K;  // order, tile origin, block dims
@@ -75,8 +71,6 @@ struct TrainState {
   double* part = nullptr;
   int64_t part_n = 0;
   // tiled dW: tile lists of lin1 (g 2E x A1 3E) and lin2 (g E x G 2E), split partials
-  LinTile* lt[4] = {nullptr, nullptr, nullptr, nullptr};  // lin1 fwd, lin2 fwd, lin2 dx, lin1 dx
-  int n_lt[4] = {0, 0, 0, 0};
   OuterTile* tiles1 = nullptr;
   OuterTile* tiles2 = nullptr;
   int n_tiles1 = 0, n_tiles2 = 0;
@@ -187,7 +181,7 @@ __global__ void k_reduce_parts(const double* __restrict__ part, int n_parts, int
 // Per order m and edge: out_m[o] = sum_i P_m[i][o] in_m[i], the order blocks
 // of 25 order-major rows x C channels at offset moff(m) C.  P_m is the
 // expanded weight transposed (forward) or not transposed (dx = W^T g);
-// the k-sum runs in ascending i with fmaf, as k_so2_simt.
+// the k-sum runs in ascending i with fmaf.
 template <int L>
 __global__ void __launch_bounds__(256) k_lin(const float* __restrict__ in, int cin, int64_t n_e,
                                              const float* __restrict__ P, int cout, float* __restrict__ out) {
@@ -221,63 +215,6 @@ __global__ void __launch_bounds__(256) k_lin(const float* __restrict__ in, int c
   }
 }
 
-// The per-order linear as a register-blocked SGEMM: CTA tile of 64 edges x
-// 64 outputs of one order block (tile list: (m, o0)), 16-deep K stages in
-// SMEM, thread (ty, tx) owns 4 edges x 4 outputs.  Each output sums its K
-// terms in ascending order with fmaf, exactly as k_so2_simt / k_lin.
-template <int L>
-__global__ void __launch_bounds__(256) k_gemm_m(const float* __restrict__ in, int cin, int64_t n_e,
-                                                const float* __restrict__ P, const LinTile* __restrict__ tiles, int cout,
-                                                float* __restrict__ out) {
-  using G = Geo<L>;
-  constexpr int TM = 64, TK = 16;
-  __shared__ float As[TK][TM + 4];
-  __shared__ __align__(16) float Bs[TK][64];
-  const LinTile t = tiles[blockIdx.y];
-  const int64_t e0 = (int64_t)blockIdx.x * TM;
-  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-  const int io = G::moff(t.m) * cin, oo = G::moff(t.m) * cout;
-  float acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  for (int k0 = 0; k0 < t.K; k0 += TK) {
-    __syncthreads();
-    for (int u = threadIdx.x; u < TM * TK; u += 256) {  // A: 64 edges x 16 k (edge rows contiguous in k)
-      const int e = u / TK, k = u % TK;
-      const int64_t ee = e0 + e;
-      As[k][e] = (ee < n_e && k0 + k < t.K) ? in[ee * G::H * cin + io + k0 + k] : 0.f;
-    }
-    for (int u = threadIdx.x; u < TK * 64; u += 256) {  // B: 16 k x 64 outputs
-      const int k = u / 64, o = u % 64;
-      Bs[k][o] = (k0 + k < t.K && t.o0 + o < t.N) ? P[t.p_off + (int64_t)(k0 + k) * t.N + t.o0 + o] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < TK; ++k) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t ee = e0 + ty * 4 + i;
-    if (ee >= n_e) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int o = t.o0 + tx * 4 + j;
-      if (o < t.N) out[ee * G::H * cout + oo + o] = acc[i][j];
-    }
-  }
-}
 
 // dWexp_m[o][k] += sum_e g_m[e][o] x_m[e][k] over the chunk's edges in
 // order, fp64; one thread per output element, no two CTAs share an output.
@@ -370,17 +307,6 @@ __global__ void k_outer_reduce(const double* __restrict__ part, int n_tiles, int
 
 // gate (kernels.h:210-226) and its backward (kernels.h:228-250); rows are
 // the 25 order-major rows of 2E channels, row 0 the l = 0 scalar
-template <int H>
-__global__ void k_gate_fwd(const float* __restrict__ h, int c2, int64_t n_e, int enabled, float* __restrict__ g) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_e * c2) return;
-  const int64_t e = t / c2;
-  const int c = (int)(t % c2);
-  const float* hr = h + e * H * c2;
-  float* gr = g + e * H * c2;
-  const float s = enabled ? 1.f / (1.f + expf(-hr[c])) : 1.f;
-  for (int r = 0; r < H; ++r) gr[r * c2 + c] = hr[r * c2 + c] * s;
-}
 template <int H>
 __global__ void k_gate_bwd(const float* __restrict__ h, const float* __restrict__ gg, int c2, int64_t n_e,
                            int enabled, float* __restrict__ gh) {
@@ -658,8 +584,7 @@ void train_free(DeviceModel* D) {
                   (void*)T->Hh, (void*)T->Gg, (void*)T->Yy, (void*)T->msg, (void*)T->gY, (void*)T->gG, (void*)T->gH,
                   (void*)T->gA1, (void*)T->gx, (void*)T->gacc, (void*)T->part, (void*)T->plane_ptr,
                   (void*)T->plane_out, (void*)T->out_plane, (void*)T->out_key, (void*)T->rbf_scratch,
-                  (void*)T->halo_send, (void*)T->halo_recv, (void*)T->tiles1, (void*)T->tiles2, (void*)T->opart,
-                  (void*)T->lt[0], (void*)T->lt[1], (void*)T->lt[2], (void*)T->lt[3]})
+                  (void*)T->halo_send, (void*)T->halo_recv, (void*)T->tiles1, (void*)T->tiles2, (void*)T->opart})
     free_ptr(p);
   for (auto* v : {&T->src_perm, &T->src_off, &T->src_row_u})
     for (int* p : *v) free_ptr(p);
@@ -739,7 +664,6 @@ void gacc_layout(esg_model* M, TrainState* T) {
 }
 
 void outer_tiles(esg_model* M, TrainState* T);
-void lin_tiles(esg_model* M, TrainState* T);
 
 // (Re)builds everything that depends on the prepared view and the weights.
 void train_setup(esg_model* M) {
@@ -861,7 +785,6 @@ void train_setup(esg_model* M) {
   // accumulators and partials
   gacc_layout(M, T);
   outer_tiles(M, T);
-  lin_tiles(M, T);
   free_ptr(T->gacc);
   T->gacc = talloc<double>(T->gacc_n);
   free_ptr(T->part);
@@ -883,32 +806,13 @@ void train_setup(esg_model* M) {
 }
 
 
+
+
 // kind 0: lin1 forward (3E -> 2E, P = W1^T), 1: lin2 forward (2E -> E, W2^T),
 // 2: lin2 dx (E -> 2E, P = W2), 3: lin1 dx (2E -> 3E, P = W1)
 template <int L, int E>
-void lin(int kind, const float* in, int64_t n, const float* P, float* out, TrainState* T, cudaStream_t st) {
-  static const int cin_of[4] = {3 * E, 2 * E, E, 2 * E}, cout_of[4] = {2 * E, E, 2 * E, 3 * E};
-  if (n > 0)
-    k_gemm_m<L><<<dim3((unsigned)((n + 63) / 64), (unsigned)T->n_lt[kind]), 256, 0, st>>>(
-        in, cin_of[kind], n, P, T->lt[kind], cout_of[kind], out);
-}
-
-void lin_tiles(esg_model* M, TrainState* T) {
-  const int L = M->cfg.l_max, E = M->cfg.e_width;
-  const int cin_of[4] = {3 * E, 2 * E, E, 2 * E}, cout_of[4] = {2 * E, E, 2 * E, 3 * E};
-  for (int kind = 0; kind < 4; ++kind) {
-    std::vector<LinTile> v;
-    int64_t off = 0;
-    for (int m = 0; m <= L; ++m) {
-      const int rows = m == 0 ? L + 1 : 2 * (L - m + 1), K = rows * cin_of[kind], N = rows * cout_of[kind];
-      for (int o0 = 0; o0 < N; o0 += 64) v.push_back({m, o0, K, N, off});
-      off += (int64_t)K * N;
-    }
-    free_ptr(T->lt[kind]);
-    T->lt[kind] = talloc<LinTile>(v.size());
-    ESG_CUDA(cudaMemcpy(T->lt[kind], v.data(), sizeof(LinTile) * v.size(), cudaMemcpyHostToDevice));
-    T->n_lt[kind] = (int)v.size();
-  }
+void lin(int kind, const float* in, int64_t n, const float* P, float* out, DeviceModel* D, cudaStream_t st) {
+  lin_launch<L, E>(kind, in, n, P, out, D->lt[kind], D->n_lt[kind], st);
 }
 
 constexpr int OUTER_SPLIT = 2048;       // edges per split of a weight-gradient tile
@@ -1014,11 +918,11 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     // forward recompute: A1, H, G (+ Y and msg for the attention backward)
     k_rotate_in<L, E, 1, float><<<t32, RI_THREADS, 0, st>>>(nodes, edges, D->src_row, D->dst_row, D->dir, e0, n, T->A1,
                                                             D->rc);
-    lin<L, E>(0, T->A1, n, D->w1t[b], T->Hh, T, st);
+    lin<L, E>(0, T->A1, n, D->w1t[b], T->Hh, D, st);
     k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, 2 * E, n, M->cfg.gate_enabled, T->Gg);
     const float* g_msg;
     if (node_block) {
-      lin<L, E>(1, T->Gg, n, D->w2t[b], T->Yy, T, st);
+      lin<L, E>(1, T->Gg, n, D->w2t[b], T->Yy, D, st);
       k_rot1<L, E, 0><<<t32, 128, 0, st>>>(T->Yy, D->dir, e0, n, T->msg);
       // attention backward into gY's buffer (used as g_msg scratch)
       k_attn_bwd<H, E><<<(unsigned)(ch.second - ch.first), 128, 0, st>>>(
@@ -1032,12 +936,12 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     k_rot1<L, E, 1><<<t32, 128, 0, st>>>(g_msg, D->dir, e0, n, T->gY);
     // lin2 adjoint
     outer<L>(T->gY, E, T->Gg, 2 * E, n, T->gacc + T->off_lin2[b], false, T, st);
-    lin<L, E>(2, T->gY, n, D->w2n[b], T->gG, T, st);
+    lin<L, E>(2, T->gY, n, D->w2n[b], T->gG, D, st);
     k_gate_bwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, T->gG, 2 * E, n, M->cfg.gate_enabled,
                                                                        T->gH);
     // lin1 adjoint
     outer<L>(T->gH, 2 * E, T->A1, 3 * E, n, T->gacc + T->off_lin1[b], true, T, st);
-    lin<L, E>(3, T->gH, n, D->w1n[b], T->gA1, T, st);
+    lin<L, E>(3, T->gH, n, D->w1n[b], T->gA1, D, st);
     // rotate-in / concat adjoint, ordered row reductions
     k_rot_in_bwd<L, E><<<t32, RI_THREADS, 0, st>>>(T->gA1, D->dir, e0, n, T->g_edges, T->gx);
     k_dst_reduce<<<(unsigned)(ch.second - ch.first), 128, 0, st>>>(T->gx, HE, D->seg, ch.first, e0, T->g_nodes);
