@@ -19,7 +19,7 @@ struct LinTile {
 // The per-order linear as a register-blocked SGEMM: CTA tile of 128 edges x
 // 64 outputs of one order block (tile list: (m, o0)), 16-deep K stages in
 // SMEM, thread (ty, tx) owns 8 edges x 4 outputs (16-byte SMEM loads).  Each output sums its K
-// terms in ascending order with fmaf, exactly as k_so2_simt / k_lin.
+// terms in ascending order with fmaf.
 template <int L>
 __global__ void __launch_bounds__(256) k_gemm_m(const float* __restrict__ in, int cin, int64_t n_e,
                                                 const float* __restrict__ P, const LinTile* __restrict__ tiles, int cout,

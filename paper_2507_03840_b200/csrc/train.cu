@@ -178,75 +178,15 @@ __global__ void k_reduce_parts(const double* __restrict__ part, int n_parts, int
 }
 
 // --------------------------------------------------------- SO(2) linears
-// Per order m and edge: out_m[o] = sum_i P_m[i][o] in_m[i], the order blocks
-// of 25 order-major rows x C channels at offset moff(m) C.  P_m is the
-// expanded weight transposed (forward) or not transposed (dx = W^T g);
-// the k-sum runs in ascending i with fmaf.
-template <int L>
-__global__ void __launch_bounds__(256) k_lin(const float* __restrict__ in, int cin, int64_t n_e,
-                                             const float* __restrict__ P, int cout, float* __restrict__ out) {
-  using G = Geo<L>;
-  constexpr int TE = 16;
-  extern __shared__ float s_in[];  // TE x (max rows) x cin
-  const int64_t t0 = (int64_t)blockIdx.x * TE;
-  const int ne = (int)(n_e - t0 < TE ? n_e - t0 : TE);
-  int64_t po = 0;
-  for (int m = 0; m <= L; ++m) {
-    const int K = G::rows(m) * cin, N = G::rows(m) * cout;
-    const int io = G::moff(m) * cin, oo = G::moff(m) * cout;
-    __syncthreads();
-    for (int i = threadIdx.x; i < TE * K; i += blockDim.x) {
-      const int e = i / K, k = i % K;
-      s_in[i] = e < ne ? in[(t0 + e) * (G::H * cin) + io + k] : 0.f;
-    }
-    __syncthreads();
-    for (int o = threadIdx.x; o < N; o += blockDim.x) {
-      float acc[TE];
-#pragma unroll
-      for (int e = 0; e < TE; ++e) acc[e] = 0.f;
-      for (int k = 0; k < K; ++k) {
-        const float w = P[po + (int64_t)k * N + o];
-#pragma unroll
-        for (int e = 0; e < TE; ++e) acc[e] = fmaf(s_in[e * K + k], w, acc[e]);
-      }
-      for (int e = 0; e < ne; ++e) out[(t0 + e) * (G::H * cout) + oo + o] = acc[e];
-    }
-    po += (int64_t)K * N;
-  }
-}
+// (forward and dx products: lin_kernels.cuh k_gemm_m)
 
 
-// dWexp_m[o][k] += sum_e g_m[e][o] x_m[e][k] over the chunk's edges in
-// order, fp64; one thread per output element, no two CTAs share an output.
-template <int L>
-__global__ void k_outer(const float* __restrict__ g, int cg, const float* __restrict__ x, int cx, int64_t n_e,
-                        double* __restrict__ acc) {
-  using G = Geo<L>;
-  int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int m = 0;
-  int64_t base = 0;
-  for (; m <= L; ++m) {
-    const int64_t sz = (int64_t)G::rows(m) * cg * G::rows(m) * cx;
-    if (u < base + sz) break;
-    base += sz;
-  }
-  if (m > L) return;
-  const int64_t v = u - base;
-  const int Kx = G::rows(m) * cx;
-  const int o = (int)(v / Kx), k = (int)(v % Kx);
-  const float* gp = g + G::moff(m) * cg + o;
-  const float* xp = x + G::moff(m) * cx + k;
-  double a = 0.0;
-  for (int64_t e = 0; e < n_e; ++e) a += double(gp[e * G::H * cg]) * double(xp[e * G::H * cx]);
-  acc[u] += a;
-}
-
-// The same sums as a tiled NT GEMM: CTA (tile, split) accumulates a 64 x 64
-// output tile of order block m over its edge split [s0, s1) -- thread
-// (ty, tx) a 4 x 4 block, 16 edges per SMEM stage, fp64 accumulators (the
-// fp32 products are exact in fp64) -- and writes the tile to its split's
-// partial slot; k_outer_reduce then adds the splits in order (fp64).  Within
-// a split (<= 2048 edges) the sums are fp32 fmaf in edge order.
+// dWexp_m[o][k] += sum_e g_m[e][o] x_m[e][k] over the chunk's edges as a
+// tiled NT GEMM: CTA (tile, split) accumulates a 64 x 64 output tile of
+// order block m over its edge split [s0, s1) -- thread (ty, tx) a 4 x 4
+// block, 16 edges per SMEM stage, fp32 fmaf in edge order within the split
+// (<= 2048 edges) -- and writes the tile to its split's partial slot;
+// k_outer_reduce then adds the splits in order in fp64.
 template <int L>
 __global__ void __launch_bounds__(256) k_outer_tiled(const float* __restrict__ g, int cg, const float* __restrict__ x,
                                                      int cx, int64_t n_e, const OuterTile* __restrict__ tiles,
