@@ -377,12 +377,57 @@ def run_ours(args):
             "kernel_ms_per_forward": {PROF_NAMES[i]: float(ms_cat[i] / args.steps) for i in range(8)},
             "setup_s": {"graph": t_graph, "partition_plan": t_part, "prepare": t_prep},
             "wall_ms_per_step": 1e3 * wall / args.steps}
+    if world == 1 and args.train_steps > 0:
+        # config 5's training step, measured on C2 after the
+        # C4 tables are released: forward (fp32 path, inputs kept), masked
+        # loss, reverse pass, gradient sums and the Adam step
+        net.close()
+        g.close()
+        node_out = edge_out = None  # noqa: F841  (the e2e pinned host buffers)
+        import gc
+        gc.collect()
+        line["train"] = train_measure(ctx, args.train_steps)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def train_measure(ctx, steps, config="C2"):
+    import torch
+    from paper_2507_03840_b200 import esg
+    s, r, layers, basis = esg.config_structure(config)
+    g = esg.build_graph(ctx, s, r)
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=layers, n_radial=32, r_cut=r, seed=1,
+                          linear_precision=esg.LINEAR_FP32)
+    net = esg.Network(ctx, cfg, basis)
+    net.init_params()
+    net.prepare(g, s.species)
+    rng = np.random.default_rng(7)
+    ol = net.out_len
+    nt = (rng.standard_normal((net.n_owned, ol)) * 0.1).astype(np.float32)
+    et = (rng.standard_normal((net.n_edges, ol)) * 0.1).astype(np.float32)
+    nm = (rng.random((net.n_owned, ol)) < 0.5).astype(np.uint8)
+    em = (rng.random((net.n_edges, ol)) < 0.5).astype(np.uint8)
+    net.set_targets(nt, nm, et, em)
+    n_total = int(nm.sum() + em.sum())
+    opt = esg.Adam(net)
+    net.train_step(opt, n_total)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = [net.train_step(opt, n_total) for _ in range(steps)]
+    torch.cuda.synchronize()
+    step_s = (time.perf_counter() - t0) / steps
+    out = {"workload": CONFIG_DESC[config] + ", training step (fp32 linears)", "edges": net.n_edges,
+           "steps": steps, "step_ms": 1e3 * step_s, "forward_ms": float(np.mean([x[1] for x in res])),
+           "backward_ms": float(np.mean([x[2] for x in res])), "edges_per_s": net.n_edges / step_s,
+           "loss_first_last": [res[0][0], res[-1][0]], "targets": "seeded head-space values, half masked"}
+    opt.close()
+    net.close()
+    g.close()
+    return out
 
 
 def main():
@@ -395,6 +440,7 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--train-steps", type=int, default=2, help="C2 training steps after the forward (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
