@@ -231,6 +231,24 @@ class Network {
     check(esg_forward(h_, node_out ? node_out->data() : nullptr, edge_out ? edge_out->data() : nullptr, &t));
     return t;
   }
+  // ---- training (Network::build_targets/record_loss, DistributedRunner::train_step)
+  void set_targets(const std::vector<float>& node_target, const std::vector<uint8_t>& node_mask,
+                   const std::vector<float>& edge_target, const std::vector<uint8_t>& edge_mask) {
+    check(esg_set_targets(h_, node_target.data(), node_mask.data(), edge_target.data(), edge_mask.data()));
+  }
+  double loss_grad(int64_t n_total, std::vector<float>* grads = nullptr) {
+    double loss = 0, partials[3];
+    if (grads) grads->resize(esg_model_param_count(h_));
+    check(esg_loss_grad(h_, n_total, partials, &loss, grads ? grads->data() : nullptr));
+    return loss;
+  }
+  double train_step(esg_adam* opt, int64_t n_total, esg_timing* t = nullptr) {
+    double loss = 0;
+    check(esg_train_step(h_, opt, n_total, &loss, t));
+    return loss;
+  }
+  esg_model* get() const { return h_; }
+
   std::vector<double> blocks_uncoupled() {
     int64_t n = 0;
     check(esg_blocks_size(h_, &n));
@@ -242,6 +260,20 @@ class Network {
  private:
   esg_model* h_ = nullptr;
   int64_t n_owned_ = 0, n_edges_ = 0;
+};
+
+// model::Optimizer (optimizer.h): Adam, fp64 moments, reduce-on-plateau
+class Adam {
+ public:
+  explicit Adam(const Network& net, const esg_adam_config* cfg = nullptr) { check(esg_adam_create(net.get(), cfg, &h_)); }
+  ~Adam() { esg_adam_destroy(h_); }
+  Adam(const Adam&) = delete;
+  Adam& operator=(const Adam&) = delete;
+  esg_adam* get() const { return h_; }
+  double lr() const { return esg_adam_lr(h_); }
+
+ private:
+  esg_adam* h_ = nullptr;
 };
 
 inline std::vector<double> coupling_matrix(int la, int lb, int L) {
