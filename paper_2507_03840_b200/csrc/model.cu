@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 
@@ -806,7 +807,8 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
   if (D->save_inputs) {  // training: this block's input tables (after the exchange)
     const size_t row_bytes = sizeof(float) * H * E;
     ESG_CUDA(cudaMemcpyAsync(D->saved_nodes[bidx], D->nodes, row_bytes * D->n_rows, cudaMemcpyDeviceToDevice, st));
-    if (node_block && D->n_edges)
+    // edge tables of layers >= 1 (layer 0's is recomputed by the backward, model_init_edges)
+    if (node_block && D->n_edges && (layer >= 1 || M->cfg.layers == 1))
       ESG_CUDA(cudaMemcpyAsync(D->saved_edges[layer], D->edges, row_bytes * D->n_edges, cudaMemcpyDeviceToDevice,
                                st));
   }
@@ -972,6 +974,34 @@ void forward_impl(esg_model* M, esg_timing* tm) {
 }
 
 }  // namespace
+
+// The initial edge table (k_init_edges) into out: the training backward
+// recomputes layer 0's input instead of keeping it.
+void model_init_edges(esg_model* M, float* out, cudaStream_t st) {
+  DeviceModel* D = M->dev;
+  const int L = D->L, E = D->E;
+  if (!D->n_edges) return;
+  const int64_t blocks = std::min<int64_t>((D->n_edges + 255) / 256, 148 * 8);
+  const double spacing = M->cfg.r_cut / (M->cfg.n_radial - 1);
+  auto go = [&](auto h, auto e) {
+    constexpr int H = decltype(h)::value, EE = decltype(e)::value;
+    k_init_edges<H, EE, 32><<<(unsigned)blocks, 256, 0, st>>>(D->dist, D->n_edges, D->params + D->lift_off,
+                                                               M->cfg.n_radial, spacing, out);
+  };
+  using I25 = std::integral_constant<int, 25>;
+  using I9 = std::integral_constant<int, 9>;
+  using I16 = std::integral_constant<int, 16>;
+  using I8 = std::integral_constant<int, 8>;
+  if (L == 4 && E == 16)
+    go(I25{}, I16{});
+  else if (L == 4 && E == 8)
+    go(I25{}, I8{});
+  else if (L == 2 && E == 16)
+    go(I9{}, I16{});
+  else
+    go(I9{}, I8{});
+  ESG_CUDA(cudaGetLastError());
+}
 
 void model_forward(esg_model* M, esg_timing* tm) {
   DeviceModel* D = M->dev;

@@ -102,8 +102,9 @@ T* talloc(size_t n) {
 // ------------------------------------------------------------------ loss
 // ops.h:347-371 masked_loss: partial sums of |d| and d^2 (fp64) and the
 // count; the recorded backward seeds (sign(d) + 2 d) / n_total directly.
-__global__ void k_loss(const float* __restrict__ pred, const float* __restrict__ tgt, const uint8_t* __restrict__ mask,
-                       int64_t n, double inv_total, float* __restrict__ g_out, double* __restrict__ part) {
+// g_out may alias pred (the seed overwrites the prediction it came from)
+__global__ void k_loss(const float* pred, const float* __restrict__ tgt, const uint8_t* __restrict__ mask, int64_t n,
+                       double inv_total, float* g_out, double* __restrict__ part) {
   double sa = 0.0, sq = 0.0, cnt = 0.0;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     float g = 0.f;
@@ -520,7 +521,7 @@ void train_free(DeviceModel* D) {
   TrainState* T = D->train;
   if (!T) return;
   for (void* p : {(void*)T->node_target, (void*)T->node_mask, (void*)T->edge_target, (void*)T->edge_mask,
-                  (void*)T->g_nodes, (void*)T->g_edges, (void*)T->g_nodes_out, (void*)T->g_node_out, (void*)T->g_edge_out, (void*)T->A1,
+                  (void*)T->g_nodes, (void*)T->g_edges, (void*)T->g_nodes_out, (void*)T->A1,
                   (void*)T->Hh, (void*)T->Gg, (void*)T->Yy, (void*)T->msg, (void*)T->gY, (void*)T->gG, (void*)T->gH,
                   (void*)T->gA1, (void*)T->gx, (void*)T->gacc, (void*)T->part, (void*)T->plane_ptr,
                   (void*)T->plane_out, (void*)T->out_plane, (void*)T->out_key, (void*)T->rbf_scratch,
@@ -529,7 +530,8 @@ void train_free(DeviceModel* D) {
   for (auto* v : {&T->src_perm, &T->src_off, &T->src_row_u})
     for (int* p : *v) free_ptr(p);
   for (float* p : D->saved_nodes) free_ptr(p);
-  for (float* p : D->saved_edges) free_ptr(p);
+  for (size_t l = 0; l < D->saved_edges.size(); ++l)
+    if (!(l == 0 && D->saved_edges.size() > 1)) free_ptr(D->saved_edges[l]);  // [0] aliases [1]
   D->saved_nodes.clear();
   D->saved_edges.clear();
   for (auto& e : T->ev) cudaEventDestroy(e);
@@ -614,7 +616,8 @@ void train_setup(esg_model* M) {
   // saved tables
   if ((int)D->saved_nodes.size() != 2 * layers) {
     for (float* p : D->saved_nodes) free_ptr(p);
-    for (float* p : D->saved_edges) free_ptr(p);
+    for (size_t l = 0; l < D->saved_edges.size(); ++l)
+      if (!(l == 0 && D->saved_edges.size() > 1)) free_ptr(D->saved_edges[l]);
     D->saved_nodes.assign(2 * layers, nullptr);
     D->saved_edges.assign(layers, nullptr);
   }
@@ -622,19 +625,21 @@ void train_setup(esg_model* M) {
     free_ptr(p);
     p = talloc<float>((size_t)std::max(D->n_rows, 1) * row);
   }
-  for (auto& p : D->saved_edges) {
-    free_ptr(p);
-    p = talloc<float>((size_t)std::max<int64_t>(D->n_edges, 1) * row);
+  // edge tables entering layers >= 1; layer 0's input is recomputed into
+  // layer 1's buffer once layer 1's backward is done (one table fewer)
+  for (int l = 0; l < layers; ++l) {
+    if (l == 0 && layers > 1) continue;
+    free_ptr(D->saved_edges[l]);
+    D->saved_edges[l] = talloc<float>((size_t)std::max<int64_t>(D->n_edges, 1) * row);
   }
+  if (layers > 1) D->saved_edges[0] = D->saved_edges[1];
   // gradient tables
-  for (void* p : {(void*)T->g_nodes, (void*)T->g_edges, (void*)T->g_nodes_out, (void*)T->g_node_out,
-                  (void*)T->g_edge_out})
-    free_ptr(p);
+  for (void* p : {(void*)T->g_nodes, (void*)T->g_edges, (void*)T->g_nodes_out}) free_ptr(p);
   T->g_nodes = talloc<float>((size_t)std::max(D->n_rows, 1) * row);
   T->g_nodes_out = talloc<float>((size_t)std::max(D->n_rows, 1) * row);
   T->g_edges = talloc<float>((size_t)std::max<int64_t>(D->n_edges, 1) * row);
-  T->g_node_out = talloc<float>((size_t)std::max(D->n_owned, 1) * M->heads.out_len);
-  T->g_edge_out = talloc<float>((size_t)std::max<int64_t>(D->n_edges, 1) * M->heads.out_len);
+  T->g_node_out = D->node_out;  // the loss seed overwrites the prediction (k_loss in place)
+  T->g_edge_out = D->edge_out;
   // training chunks: destination-aligned, <= 256k edges (scratch ~ 6 KB/edge fp32)
   const int64_t cap0 = 256 * 1024;
   int64_t maxseg = 0;
@@ -894,7 +899,8 @@ void block_backward(esg_model* M, int layer, bool node_block) {
 
 }  // namespace
 
-void model_forward(esg_model* M, esg_timing* tm);  // model.cu
+void model_forward(esg_model* M, esg_timing* tm);               // model.cu
+void model_init_edges(esg_model* M, float* out, cudaStream_t st);  // model.cu
 
 // ops.h:347-371 + the reverse pass + distributed.h:147-163: loss partials of
 // this rank, the global loss and the parameter gradients summed over ranks
@@ -956,6 +962,7 @@ void loss_grad_impl(esg_model* M, int64_t n_total, double partials[3], double* l
   // blocks in reverse; each block's exchange is undone after its backward
   for (int layer = M->cfg.layers - 1; layer >= 0; --layer)
     for (bool nb : {false, true}) {
+      if (layer == 0 && !nb && M->cfg.layers > 1) model_init_edges(M, D->saved_edges[0], st);  // E_0 into E_1's buffer
       if (nb)
         block_backward<L, E>(M, layer, true);
       else
