@@ -52,6 +52,7 @@ struct esg_adam {
 };
 
 namespace esg {
+esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32_t* part, int n_parts, int rank);
 void model_set_targets(esg_model* M, const float* node_target, const uint8_t* node_mask, const float* edge_target,
                        const uint8_t* edge_mask);
 void model_loss_grad(esg_model* M, int64_t n_total, double partials[3], double* loss, float* grads_out);
@@ -276,7 +277,7 @@ int esg_graph_in_degrees(const esg_graph* g, int32_t* deg) {
   ESG_API_BEGIN
   NEED(g, "graph");
   NEED(deg, "deg");
-  g->host_sync();
+  g->host_sync_offsets();
   for (int j = 0; j < g->n; ++j) deg[j] = (int32_t)(g->h_off[j + 1] - g->h_off[j]);
   ESG_API_END
 }
@@ -285,7 +286,7 @@ int esg_graph_offsets(const esg_graph* g, int64_t* off) {
   ESG_API_BEGIN
   NEED(g, "graph");
   NEED(off, "off");
-  g->host_sync();
+  g->host_sync_offsets();
   std::copy(g->h_off.begin(), g->h_off.end(), off);
   ESG_API_END
 }
@@ -383,8 +384,8 @@ int esg_plan_build(const esg_graph* g, const int32_t* species, const int32_t* pa
   NEED(g, "graph");
   NEED(part, "node_to_part");
   NEED(out, "out");
-  g->host_sync();
-  *out = plan_from_csr(g->n, g->h_off.data(), g->h_src.data(), species, part, n_parts, rank);
+  ESG_CUDA(cudaSetDevice(g->ctx->device));
+  *out = plan_build_gpu(g, species, part, n_parts, rank);  // the device CSR, same plan as plan_from_csr
   ESG_API_END
 }
 

@@ -125,7 +125,8 @@ struct esg_graph {
   // host mirrors filled lazily
   mutable std::vector<int64_t> h_off;
   mutable std::vector<int32_t> h_src;
-  void host_sync() const;
+  void host_sync() const;          // offsets and sources
+  void host_sync_offsets() const;  // offsets only (in-degrees, segment ranges)
 };
 
 struct esg_plan {

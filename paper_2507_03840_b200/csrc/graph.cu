@@ -282,10 +282,14 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
 
 }  // namespace esg
 
-void esg_graph::host_sync() const {
-  if ((int64_t)h_off.size() == n + 1 && (int64_t)h_src.size() == E) return;
+void esg_graph::host_sync_offsets() const {
+  if ((int64_t)h_off.size() == n + 1) return;
   h_off.resize(n + 1);
-  h_src.resize(E);
   ESG_CUDA(cudaMemcpy(h_off.data(), d_off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+}
+void esg_graph::host_sync() const {
+  host_sync_offsets();
+  if ((int64_t)h_src.size() == E) return;
+  h_src.resize(E);
   if (E) ESG_CUDA(cudaMemcpy(h_src.data(), d_src, sizeof(int32_t) * E, cudaMemcpyDeviceToHost));
 }

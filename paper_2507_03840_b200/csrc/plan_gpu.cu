@@ -1,0 +1,246 @@
+// plan_gpu.cu -- runtime::build_comm_plan (comm_plan.cpp:11-106) on the
+// device from the device CSR.  Produces the same esg_plan as the host
+// restatement plan_from_csr (capi.cpp), bit for bit:
+//   owned rows    nodes of this rank in ascending global id        (:24-30)
+//   halo rows     distinct remote sources of owned edges, sorted by
+//                 (owner, id)                                        (:32-50)
+//   owned edges   edges whose destination this rank owns, in global
+//                 (dst-major) order, with local src / dst rows       (:53-71)
+//   send rows     per peer, the owned sources of that peer's edges,
+//                 ascending id                                       (:73-92)
+//   recv ranges   contiguous halo rows per owner                     (:94-103)
+// Every rank scans all E edges on the GPU (a few ms at C4) instead of on
+// the host; only the rank-local results travel to the host.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <map>
+#include <vector>
+
+#include "esg_internal.h"
+
+namespace esg {
+namespace {
+
+template <typename T>
+T* galloc(size_t n) {
+  T* p = nullptr;
+  if (n) ESG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+__global__ void k_flag_owned(const int* __restrict__ part, int n, int rank, int* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = part[i] == rank;
+}
+__global__ void k_owned_rows(const int* __restrict__ part, int n, int rank, const int* __restrict__ scan,
+                             int* __restrict__ owned_row, int* __restrict__ row_global) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool own = part[i] == rank;
+  owned_row[i] = own ? scan[i] : -1;
+  if (own) row_global[scan[i]] = i;
+}
+// warp per destination j of this rank: remote sources need a halo row;
+// owned-edge counts for the edge compaction
+__global__ void k_halo_need(const int64_t* __restrict__ off, const int* __restrict__ src,
+                            const int* __restrict__ part, int n, int rank, uint8_t* __restrict__ need,
+                            int64_t* __restrict__ cnt) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const bool own = part[j] == rank;
+  if (lane == 0) cnt[j] = own ? off[j + 1] - off[j] : 0;
+  if (!own) return;
+  for (int64_t k = off[j] + lane; k < off[j + 1]; k += 32) {
+    const int s = src[k];
+    if (part[s] != rank) need[s] = 1;
+  }
+}
+__global__ void k_halo_keys(const int* __restrict__ ids, int m, const int* __restrict__ part,
+                            uint64_t* __restrict__ keys) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < m) keys[q] = ((uint64_t)(uint32_t)part[ids[q]] << 32) | (uint32_t)ids[q];
+}
+__global__ void k_halo_rows(const uint64_t* __restrict__ keys, int m, int n_owned, int* __restrict__ halo_row,
+                            int* __restrict__ row_global) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  const int s = (int)(keys[q] & 0xffffffffu);
+  halo_row[s] = n_owned + q;
+  row_global[n_owned + q] = s;
+}
+// warp per owned destination: its edges at base[j], in CSR order
+__global__ void k_fill_edges(const int64_t* __restrict__ off, const int* __restrict__ src,
+                             const int* __restrict__ part, int n, int rank, const int64_t* __restrict__ base,
+                             const int* __restrict__ owned_row, const int* __restrict__ halo_row,
+                             int* __restrict__ edge_index, int* __restrict__ src_row, int* __restrict__ dst_row) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (j >= n || part[j] != rank) return;
+  const int64_t b = base[j];
+  const int dr = owned_row[j];
+  for (int64_t k = off[j] + lane; k < off[j + 1]; k += 32) {
+    const int s = src[k];
+    const int64_t t = b + (k - off[j]);
+    edge_index[t] = (int)k;
+    src_row[t] = owned_row[s] >= 0 ? owned_row[s] : halo_row[s];
+    dst_row[t] = dr;
+  }
+}
+// warp per destination of another rank p: owned sources are sent to p
+__global__ void k_send_flags(const int64_t* __restrict__ off, const int* __restrict__ src,
+                             const int* __restrict__ part, int n, int rank, int n_parts, uint8_t* __restrict__ flags) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (j >= n) return;
+  const int p = part[j];
+  if (p == rank) return;
+  for (int64_t k = off[j] + lane; k < off[j + 1]; k += 32) {
+    const int s = src[k];
+    if (part[s] == rank) flags[(int64_t)p * n + s] = 1;
+  }
+}
+
+}  // namespace
+
+esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32_t* part_h, int n_parts,
+                         int rank) {
+  if (rank < 0 || rank >= n_parts) usage("rank outside the assignment");
+  const int n = g->n;
+  for (int i = 0; i < n; ++i)
+    if (part_h[i] < 0 || part_h[i] >= n_parts) data("assignment part out of range");
+  cudaStream_t st = g->ctx->stream;
+  auto* P = new esg_plan();
+  P->rank = rank;
+  P->world = n_parts;
+  int* part = galloc<int>(n);
+  int* flag = galloc<int>(n + 1);
+  int* scan = galloc<int>(n + 1);
+  int* owned_row = galloc<int>(n);
+  int* halo_row = galloc<int>(n);
+  int* row_global = galloc<int>(n);
+  uint8_t* need = galloc<uint8_t>(n);
+  int64_t* cnt = galloc<int64_t>(n + 1);
+  int64_t* base = galloc<int64_t>(n + 1);
+  int* ids = galloc<int>(n);
+  int* n_sel = galloc<int>(1);
+  uint64_t* keys = galloc<uint64_t>(n);
+  uint64_t* keys_sorted = galloc<uint64_t>(n);
+  uint8_t* sflags = galloc<uint8_t>((size_t)n * n_parts);
+  ESG_CUDA(cudaMemcpyAsync(part, part_h, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  ESG_CUDA(cudaMemsetAsync(need, 0, n, st));
+  ESG_CUDA(cudaMemsetAsync(halo_row, 0xff, sizeof(int) * n, st));
+  ESG_CUDA(cudaMemsetAsync(sflags, 0, (size_t)n * n_parts, st));
+  ESG_CUDA(cudaMemsetAsync(flag + n, 0, sizeof(int), st));
+  ESG_CUDA(cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), st));
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  auto ensure_tmp = [&](size_t b) {
+    if (b > tmp_bytes) {
+      if (tmp) cudaFree(tmp);
+      tmp = galloc<uint8_t>(b);
+      tmp_bytes = b;
+    }
+  };
+  const unsigned b1 = (unsigned)((n + 255) / 256), bw = (unsigned)(((int64_t)n * 32 + 255) / 256);
+  // owned rows
+  k_flag_owned<<<b1, 256, 0, st>>>(part, n, rank, flag);
+  size_t need_b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need_b, flag, scan, n + 1, st);
+  ensure_tmp(need_b);
+  cub::DeviceScan::ExclusiveSum(tmp, need_b, flag, scan, n + 1, st);
+  k_owned_rows<<<b1, 256, 0, st>>>(part, n, rank, scan, owned_row, row_global);
+  int n_owned = 0;
+  ESG_CUDA(cudaMemcpyAsync(&n_owned, scan + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  // halo rows, sorted by (owner, id)
+  if (n) k_halo_need<<<bw, 256, 0, st>>>(g->d_off, g->d_src, part, n, rank, need, cnt);
+  thrust::counting_iterator<int> it(0);
+  need_b = 0;
+  cub::DeviceSelect::Flagged(nullptr, need_b, it, need, ids, n_sel, n, st);
+  ensure_tmp(need_b);
+  cub::DeviceSelect::Flagged(tmp, need_b, it, need, ids, n_sel, n, st);
+  int n_halo = 0;
+  ESG_CUDA(cudaMemcpyAsync(&n_halo, n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+  ESG_CUDA(cudaStreamSynchronize(st));
+  if (n_halo) {
+    k_halo_keys<<<(unsigned)((n_halo + 255) / 256), 256, 0, st>>>(ids, n_halo, part, keys);
+    need_b = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need_b, keys, keys_sorted, n_halo, 0, 64, st);
+    ensure_tmp(need_b);
+    cub::DeviceRadixSort::SortKeys(tmp, need_b, keys, keys_sorted, n_halo, 0, 64, st);
+    k_halo_rows<<<(unsigned)((n_halo + 255) / 256), 256, 0, st>>>(keys_sorted, n_halo, n_owned, halo_row,
+                                                                   row_global);
+  }
+  // owned edges in global order
+  need_b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need_b, cnt, base, n + 1, st);
+  ensure_tmp(need_b);
+  cub::DeviceScan::ExclusiveSum(tmp, need_b, cnt, base, n + 1, st);
+  int64_t n_e = 0;
+  ESG_CUDA(cudaMemcpyAsync(&n_e, base + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  ESG_CUDA(cudaStreamSynchronize(st));
+  int* edge_index = galloc<int>((size_t)std::max<int64_t>(n_e, 1));
+  int* src_row = galloc<int>((size_t)std::max<int64_t>(n_e, 1));
+  int* dst_row = galloc<int>((size_t)std::max<int64_t>(n_e, 1));
+  if (n) {
+    k_fill_edges<<<bw, 256, 0, st>>>(g->d_off, g->d_src, part, n, rank, base, owned_row, halo_row, edge_index,
+                                      src_row, dst_row);
+    k_send_flags<<<bw, 256, 0, st>>>(g->d_off, g->d_src, part, n, rank, n_parts, sflags);
+  }
+  ESG_CUDA(cudaGetLastError());
+  // to the host: rows, edges, owned-row map, per-peer send lists
+  P->n_owned = n_owned;
+  P->n_rows = n_owned + n_halo;
+  P->row_global.resize(P->n_rows);
+  P->edge_index.resize(n_e);
+  P->src_row.resize(n_e);
+  P->dst_row.resize(n_e);
+  std::vector<int> owned_h(n), halo_keys_owner;
+  if (P->n_rows)
+    ESG_CUDA(cudaMemcpyAsync(P->row_global.data(), row_global, sizeof(int) * P->n_rows, cudaMemcpyDeviceToHost, st));
+  if (n_e) {
+    ESG_CUDA(cudaMemcpyAsync(P->edge_index.data(), edge_index, sizeof(int) * n_e, cudaMemcpyDeviceToHost, st));
+    ESG_CUDA(cudaMemcpyAsync(P->src_row.data(), src_row, sizeof(int) * n_e, cudaMemcpyDeviceToHost, st));
+    ESG_CUDA(cudaMemcpyAsync(P->dst_row.data(), dst_row, sizeof(int) * n_e, cudaMemcpyDeviceToHost, st));
+  }
+  if (n) ESG_CUDA(cudaMemcpyAsync(owned_h.data(), owned_row, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  std::map<int, Neighbor> nb;
+  for (int p = 0; p < n_parts; ++p) {
+    if (p == rank) continue;
+    need_b = 0;
+    cub::DeviceSelect::Flagged(nullptr, need_b, it, sflags + (size_t)p * n, ids, n_sel, n, st);
+    ensure_tmp(need_b);
+    cub::DeviceSelect::Flagged(tmp, need_b, it, sflags + (size_t)p * n, ids, n_sel, n, st);
+    int m = 0;
+    ESG_CUDA(cudaMemcpyAsync(&m, n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+    ESG_CUDA(cudaStreamSynchronize(st));
+    if (!m) continue;
+    std::vector<int> s(m);
+    ESG_CUDA(cudaMemcpy(s.data(), ids, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    Neighbor& x = nb[p];
+    x.peer = p;
+    for (int id : s) x.send_rows.push_back(owned_h[id]);
+  }
+  ESG_CUDA(cudaStreamSynchronize(st));
+  // receive ranges: contiguous halo rows per owner (the halo rows are sorted by owner)
+  int at = n_owned;
+  for (int q = n_owned; q < P->n_rows;) {
+    const int owner = part_h[P->row_global[q]];
+    int r = q;
+    while (r < P->n_rows && part_h[P->row_global[r]] == owner) ++r;
+    Neighbor& x = nb[owner];
+    x.peer = owner;
+    x.recv_row = at;
+    x.recv_count = r - q;
+    at += x.recv_count;
+    q = r;
+  }
+  for (auto& kv : nb) P->nbrs.push_back(kv.second);
+  if (species)
+    for (int r = 0; r < P->n_rows; ++r) P->row_species.push_back(species[P->row_global[r]]);
+  for (void* p : {(void*)part, (void*)flag, (void*)scan, (void*)owned_row, (void*)halo_row, (void*)row_global,
+                  (void*)need, (void*)cnt, (void*)base, (void*)ids, (void*)n_sel, (void*)keys, (void*)keys_sorted,
+                  (void*)sflags, (void*)edge_index, (void*)src_row, (void*)dst_row, tmp})
+    if (p) cudaFree(p);
+  return P;
+}
+
+}  // namespace esg

@@ -11,11 +11,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def n_gpus():
+    """GPUs visible to child processes (torch's count, else nvidia-smi's)."""
+    n = 0
     try:
         import torch
-        return torch.cuda.device_count()
+        n = torch.cuda.device_count()
     except Exception:
-        return 0
+        pass
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=30).stdout
+        n = max(n, sum(1 for line in out.splitlines() if line.startswith("GPU ")))
+    except Exception:
+        pass
+    return n
 
 
 @pytest.mark.parametrize("world", [2, 4])
