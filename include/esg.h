@@ -210,7 +210,25 @@ double esg_adam_lr(const esg_adam* a);
  * check (hash allgather; divergence -> status 4), loss + gradients, Adam
  * step, check again.  timing may be NULL; forward_ms = the forward,
  * message_ms = the backward (CUDA events). */
+/* Optimizer::step (optimizer.h:42-72) with caller-supplied gradients: the
+ * fp64-moment Adam update plus reduce-on-plateau on loss, then the parameter
+ * upload when the model has a device.  esg_train_step is esg_loss_grad
+ * followed by this. */
+int esg_adam_apply(esg_adam* opt, esg_model* m, const float* grads, double loss);
 int esg_train_step(esg_model* m, esg_adam* opt, int64_t n_total, double* loss, esg_timing* timing);
+
+/* ---- checkpoints (checkpoint.h:15-92 + the optimizer state) --
+ * The file is the reference's version-1 container (magic ESGNNCK1, config
+ * text, scalar width 4, named arrays with shapes), so model::load_checkpoint
+ * reads the parameters unchanged.  When opt is given an optimizer section
+ * follows the arrays (magic ESGADAM1: step, lr, best, stale counter, config,
+ * then the fp64 moments m and v), which the reference loader never reads and
+ * esg_checkpoint_load restores for an exact resume. */
+int esg_checkpoint_save(const esg_model* m, const esg_adam* opt, const char* config_text, const char* path);
+/* Loads parameters (uploaded to the device when the model has one) and, if
+ * opt is given, the optimizer section (status 3 if the file has none).
+ * config_out (capacity cap bytes, may be NULL) receives the config text. */
+int esg_checkpoint_load(esg_model* m, esg_adam* opt, const char* path, char* config_out, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <limits>
 #include <map>
 #include <random>
@@ -83,6 +84,34 @@ void check_param_sync(esg_model* m, const char* where) {
 }
 }  // namespace
 
+namespace {
+// checkpoint.h:20-35: little-endian u64 fields
+void ckpt_u64(std::ostream& out, uint64_t v) {
+  unsigned char b[8];
+  for (int i = 0; i < 8; ++i) b[i] = (unsigned char)(v >> (8 * i));
+  out.write(reinterpret_cast<const char*>(b), 8);
+}
+uint64_t ckpt_read_u64(std::istream& in) {
+  unsigned char b[8];
+  in.read(reinterpret_cast<char*>(b), 8);
+  if (!in) esg::data("truncated checkpoint");
+  uint64_t v = 0;
+  for (int i = 0; i < 8; ++i) v |= uint64_t(b[i]) << (8 * i);
+  return v;
+}
+void ckpt_f64(std::ostream& out, double d) {
+  uint64_t v;
+  std::memcpy(&v, &d, 8);
+  ckpt_u64(out, v);
+}
+double ckpt_read_f64(std::istream& in) {
+  const uint64_t v = ckpt_read_u64(in);
+  double d;
+  std::memcpy(&d, &v, 8);
+  return d;
+}
+}  // namespace
+
 #define ESG_API_BEGIN try {
 #define ESG_API_END                       \
   return ESG_OK;                          \
@@ -102,6 +131,32 @@ void check_param_sync(esg_model* m, const char* where) {
 
 #define NEED(p, what) \
   if (!(p)) esg::usage(std::string("null ") + what)
+
+namespace {
+void adam_update(esg_adam* opt, esg_model* m, const float* g, double loss) {
+  // Optimizer::step (optimizer.h:42-59), moments in fp64
+  if (opt->lr < 0) opt->lr = opt->cfg.lr;
+  ++opt->t;
+  const double bc1 = 1.0 - std::pow(opt->cfg.beta1, double(opt->t));
+  const double bc2 = 1.0 - std::pow(opt->cfg.beta2, double(opt->t));
+  for (size_t k = 0; k < m->host_params.size(); ++k) {
+    const double gk = double(g[k]);
+    opt->m[k] = opt->cfg.beta1 * opt->m[k] + (1.0 - opt->cfg.beta1) * gk;
+    opt->v[k] = opt->cfg.beta2 * opt->v[k] + (1.0 - opt->cfg.beta2) * gk * gk;
+    const double mh = opt->m[k] / bc1;
+    const double vh = opt->v[k] / bc2;
+    m->host_params[k] = static_cast<float>(double(m->host_params[k]) - opt->lr * mh / (std::sqrt(vh) + opt->cfg.eps));
+  }
+  // reduce-on-plateau (optimizer.h:62-72)
+  if (loss < opt->best * (1.0 - opt->cfg.threshold)) {
+    opt->best = loss;
+    opt->stale = 0;
+  } else if (++opt->stale >= opt->cfg.patience) {
+    opt->lr = std::max(opt->cfg.min_lr, opt->lr * opt->cfg.factor);
+    opt->stale = 0;
+  }
+}
+}  // namespace
 
 extern "C" {
 
@@ -673,6 +728,20 @@ int esg_adam_create(const esg_model* m, const esg_adam_config* cfg, esg_adam** o
 void esg_adam_destroy(esg_adam* a) { delete a; }
 double esg_adam_lr(const esg_adam* a) { return a ? (a->lr < 0 ? a->cfg.lr : a->lr) : 0.0; }
 
+int esg_adam_apply(esg_adam* opt, esg_model* m, const float* grads, double loss) {
+  ESG_API_BEGIN
+  NEED(opt, "optimizer");
+  NEED(m, "model");
+  NEED(grads, "grads");
+  if (opt->m.size() != m->host_params.size()) usage("optimizer built for another model");
+  adam_update(opt, m, grads, loss);
+  if (m->ctx && m->dev) {
+    ESG_CUDA(cudaSetDevice(m->ctx->device));
+    model_upload_params(m);
+  }
+  ESG_API_END
+}
+
 int esg_train_step(esg_model* m, esg_adam* opt, int64_t n_total, double* loss, esg_timing* timing) {
   ESG_API_BEGIN
   NEED(m, "model");
@@ -685,27 +754,7 @@ int esg_train_step(esg_model* m, esg_adam* opt, int64_t n_total, double* loss, e
   std::vector<float> g(m->host_params.size());
   double partials[3];
   model_loss_grad(m, n_total, partials, loss, g.data());
-  // Optimizer::step (optimizer.h:42-59), moments in fp64
-  if (opt->lr < 0) opt->lr = opt->cfg.lr;
-  ++opt->t;
-  const double bc1 = 1.0 - std::pow(opt->cfg.beta1, double(opt->t));
-  const double bc2 = 1.0 - std::pow(opt->cfg.beta2, double(opt->t));
-  for (size_t k = 0; k < g.size(); ++k) {
-    const double gk = double(g[k]);
-    opt->m[k] = opt->cfg.beta1 * opt->m[k] + (1.0 - opt->cfg.beta1) * gk;
-    opt->v[k] = opt->cfg.beta2 * opt->v[k] + (1.0 - opt->cfg.beta2) * gk * gk;
-    const double mh = opt->m[k] / bc1;
-    const double vh = opt->v[k] / bc2;
-    m->host_params[k] = static_cast<float>(double(m->host_params[k]) - opt->lr * mh / (std::sqrt(vh) + opt->cfg.eps));
-  }
-  // reduce-on-plateau (optimizer.h:62-72)
-  if (*loss < opt->best * (1.0 - opt->cfg.threshold)) {
-    opt->best = *loss;
-    opt->stale = 0;
-  } else if (++opt->stale >= opt->cfg.patience) {
-    opt->lr = std::max(opt->cfg.min_lr, opt->lr * opt->cfg.factor);
-    opt->stale = 0;
-  }
+  adam_update(opt, m, g.data(), *loss);
   model_upload_params(m);
   check_param_sync(m, "after update");
   if (timing) {
@@ -714,6 +763,102 @@ int esg_train_step(esg_model* m, esg_adam* opt, int64_t n_total, double* loss, e
     *timing = esg_timing{};
     timing->forward_ms = f;
     timing->message_ms = b;
+  }
+  ESG_API_END
+}
+
+int esg_checkpoint_save(const esg_model* m, const esg_adam* opt, const char* config_text, const char* path) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  NEED(path, "path");
+  std::ofstream out(path, std::ios::binary);
+  if (!out) data(std::string("cannot open file for writing: ") + path);
+  const std::string cfg = config_text ? config_text : "";
+  out.write("ESGNNCK1", 8);
+  ckpt_u64(out, 1);  // version
+  ckpt_u64(out, cfg.size());
+  out.write(cfg.data(), (std::streamsize)cfg.size());
+  ckpt_u64(out, sizeof(float));
+  ckpt_u64(out, m->params.entries.size());
+  for (const auto& e : m->params.entries) {
+    ckpt_u64(out, e.name.size());
+    out.write(e.name.data(), (std::streamsize)e.name.size());
+    ckpt_u64(out, (uint64_t)e.rows);
+    ckpt_u64(out, (uint64_t)e.cols);
+    out.write(reinterpret_cast<const char*>(m->host_params.data() + e.offset),
+              (std::streamsize)((size_t)e.rows * e.cols * sizeof(float)));
+  }
+  if (opt) {
+    if (opt->m.size() != m->host_params.size()) usage("optimizer built for another model");
+    out.write("ESGADAM1", 8);
+    ckpt_u64(out, (uint64_t)opt->t);
+    ckpt_f64(out, opt->lr);
+    ckpt_f64(out, opt->best);
+    ckpt_u64(out, (uint64_t)opt->stale);
+    out.write(reinterpret_cast<const char*>(&opt->cfg), sizeof(opt->cfg));
+    ckpt_u64(out, opt->m.size());
+    out.write(reinterpret_cast<const char*>(opt->m.data()), (std::streamsize)(opt->m.size() * sizeof(double)));
+    out.write(reinterpret_cast<const char*>(opt->v.data()), (std::streamsize)(opt->v.size() * sizeof(double)));
+  }
+  if (!out) data(std::string("write failed: ") + path);
+  ESG_API_END
+}
+
+int esg_checkpoint_load(esg_model* m, esg_adam* opt, const char* path, char* config_out, int64_t cap) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  NEED(path, "path");
+  std::ifstream in(path, std::ios::binary);
+  if (!in) data(std::string("cannot open file: ") + path);
+  char magic[8];
+  in.read(magic, 8);
+  if (!in || std::memcmp(magic, "ESGNNCK1", 8) != 0) data(std::string("not a checkpoint file: ") + path);
+  if (ckpt_read_u64(in) != 1) data("unsupported checkpoint version");
+  std::string cfg(ckpt_read_u64(in), '\0');
+  in.read(cfg.data(), (std::streamsize)cfg.size());
+  if (ckpt_read_u64(in) != sizeof(float)) data("checkpoint precision does not match the run precision");
+  if (ckpt_read_u64(in) != m->params.entries.size()) data("checkpoint entry count mismatch");
+  std::vector<float> p(m->host_params.size());
+  for (const auto& e : m->params.entries) {
+    std::string name(ckpt_read_u64(in), '\0');
+    in.read(name.data(), (std::streamsize)name.size());
+    if (name != e.name) data("checkpoint entry order mismatch at " + name);
+    const uint64_t rows = ckpt_read_u64(in), cols = ckpt_read_u64(in);
+    if (rows != (uint64_t)e.rows || cols != (uint64_t)e.cols) data("checkpoint shape mismatch at " + name);
+    in.read(reinterpret_cast<char*>(p.data() + e.offset), (std::streamsize)(rows * cols * sizeof(float)));
+    if (!in) data("truncated checkpoint");
+  }
+  if (opt) {
+    char om[8];
+    in.read(om, 8);
+    if (!in || std::memcmp(om, "ESGADAM1", 8) != 0) data("checkpoint has no optimizer state");
+    const long t = (long)ckpt_read_u64(in);
+    const double lr = ckpt_read_f64(in), best = ckpt_read_f64(in);
+    const int stale = (int)ckpt_read_u64(in);
+    esg_adam_config c{};
+    in.read(reinterpret_cast<char*>(&c), sizeof(c));
+    if (ckpt_read_u64(in) != p.size()) data("optimizer state size mismatch");
+    std::vector<double> mm(p.size()), vv(p.size());
+    in.read(reinterpret_cast<char*>(mm.data()), (std::streamsize)(mm.size() * sizeof(double)));
+    in.read(reinterpret_cast<char*>(vv.data()), (std::streamsize)(vv.size() * sizeof(double)));
+    if (!in) data("truncated optimizer state");
+    opt->t = t;
+    opt->lr = lr;
+    opt->best = best;
+    opt->stale = stale;
+    opt->cfg = c;
+    opt->m.swap(mm);
+    opt->v.swap(vv);
+  }
+  m->host_params.swap(p);
+  if (m->ctx && m->dev) {
+    ESG_CUDA(cudaSetDevice(m->ctx->device));
+    model_upload_params(m);
+  }
+  if (config_out && cap > 0) {
+    const size_t n = std::min<size_t>(cfg.size(), (size_t)cap - 1);
+    std::memcpy(config_out, cfg.data(), n);
+    config_out[n] = '\0';
   }
   ESG_API_END
 }

@@ -444,6 +444,19 @@ class Network:
         _check(lib().esg_blocks_uncoupled(self._h, _p(out)))
         return out
 
+    def save_checkpoint(self, path: str, opt: Optional["Adam"] = None, config_text: str = "") -> None:
+        """checkpoint.h save_checkpoint (version-1 container); with opt the
+        optimizer section (step, lr, plateau state, fp64 moments) follows."""
+        _check(lib().esg_checkpoint_save(self._h, opt._h if opt is not None else None,
+                                         config_text.encode(), os.fsencode(path)))
+
+    def load_checkpoint(self, path: str, opt: Optional["Adam"] = None) -> str:
+        """checkpoint.h load_checkpoint; restores opt too when given. Returns the config text."""
+        buf = C.create_string_buffer(1 << 16)
+        _check(lib().esg_checkpoint_load(self._h, opt._h if opt is not None else None,
+                                         os.fsencode(path), buf, C.c_int64(len(buf))))
+        return buf.value.decode()
+
     def close(self) -> None:
         if self._h:
             lib().esg_model_destroy(self._h)
@@ -475,6 +488,12 @@ class Adam:
     @property
     def lr(self) -> float:
         return float(lib().esg_adam_lr(self._h))
+
+    def apply(self, net: Network, grads: np.ndarray, loss: float) -> None:
+        """Optimizer::step with given gradients (optimizer.h:42-72)."""
+        g = np.ascontiguousarray(grads, np.float32)
+        assert g.size == net.n_params
+        _check(lib().esg_adam_apply(self._h, net._h, _p(g), C.c_double(loss)))
 
     def close(self) -> None:
         if self._h:

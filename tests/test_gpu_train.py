@@ -83,3 +83,27 @@ def test_train_step_is_adam_on_the_gradients(gpu_ctx):
     losses = [loss_step] + [net.train_step(opt, n_total)[0] for _ in range(5)]
     assert losses[-1] < losses[0], losses
     assert fwd_ms > 0 and bwd_ms > 0
+
+
+def test_exact_resume_from_checkpoint(gpu_ctx, tmp_path):
+    """§8(f) 2: 4 training steps straight vs 2 steps, checkpoint (params +
+    Adam moments), load into a fresh network and optimizer, 2 more steps:
+    bit-identical parameters and losses (the GPU step is deterministic)."""
+    net, om, view, t32, t64, n_total, g = problem(gpu_ctx, 4, 16)
+    opt = esg.Adam(net)
+    straight = [net.train_step(opt, n_total)[0] for _ in range(4)]
+    p_straight = net.params()
+
+    net2, *_ = problem(gpu_ctx, 4, 16)
+    opt2 = esg.Adam(net2)
+    first = [net2.train_step(opt2, n_total)[0] for _ in range(2)]
+    path = str(tmp_path / "mid.ckpt")
+    net2.save_checkpoint(path, opt2, "l_max=4")
+
+    net3, *_ = problem(gpu_ctx, 4, 16)
+    net3.set_params(np.zeros(net3.n_params, np.float32))
+    opt3 = esg.Adam(net3)
+    assert net3.load_checkpoint(path, opt3) == "l_max=4"
+    second = [net3.train_step(opt3, n_total)[0] for _ in range(2)]
+    assert first + second == straight
+    assert np.array_equal(net3.params().view(np.uint32), p_straight.view(np.uint32))
