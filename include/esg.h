@@ -173,10 +173,40 @@ int esg_forward_outputs(const esg_model* m, const float** node_out, const float*
 /* Node / edge feature tables (n_rows*H*E / n_edges*H*E) to host. */
 int esg_features_export(const esg_model* m, float* nodes, float* edges);
 
-/* model::blocks_to_uncoupled (block_matrix.cpp:66-88) of the last forward:
- * per item a dense n_orb(za) x n_orb(zb) block, concatenated in item order
- * (nodes first, then edges).  sizes: esg_blocks_size. */
-int esg_blocks_size(const esg_model* m, int64_t* n_values);
+/* ---- block export ------------------------
+ * The blocks of the last forward, replacing Network::assemble_blocks
+ * (network.h:168-184), blocks_to_uncoupled (block_matrix.cpp:66-88) and the
+ * text gather to rank 0 (model_run.cpp:103-120).  Items are this rank's
+ * owned atoms (key (g, g, 0)) then its owned edges in global edge order
+ * (key (src, dst, shift)); each block is n_orb(Z_i) x n_orb(Z_j), row-major,
+ * values concatenated in item order.  basis: ESG_BLOCKS_COUPLED (fill_block:
+ * head segments placed per shell-pair rectangle) or ESG_BLOCKS_UNCOUPLED
+ * (to_block per shell pair); symmetrize_onsite (uncoupled only) replaces
+ * (i, i, 0) blocks by 0.5 (B + B^T) (blocks_to_uncoupled's flag). */
+#define ESG_BLOCKS_COUPLED 0
+#define ESG_BLOCKS_UNCOUPLED 1
+typedef struct esg_block_key {
+  int32_t i, j, ix, iy, iz; /* BlockKey (block_matrix.h:21-25) */
+  uint16_t rows, cols;
+} esg_block_key; /* 24 bytes; the shard's key record */
+int esg_blocks_count(esg_model* m, int64_t* n_blocks, int64_t* n_values);
+/* Keys and fp64 values to host memory (either may be NULL). */
+int esg_blocks_export(esg_model* m, int basis, int symmetrize_onsite, esg_block_key* keys, double* values);
+/* The same into device memory (value_bytes 8: fp64, 4: fp32), one launch
+ * each; kernel_ms (may be NULL) receives their device time. */
+int esg_blocks_export_device(esg_model* m, int basis, int symmetrize_onsite, int value_bytes, void* d_keys,
+                             void* d_values, float* kernel_ms);
+/* This rank's shard file (flat block-sparse binary, layout in DESIGN.md §3
+ * and csrc/blocks_io.h), streamed through pinned staging buffers. */
+int esg_blocks_write_shard(esg_model* m, const char* path, int basis, int symmetrize_onsite, int value_bytes);
+/* block_matrix.cpp:90-101 write_blocks of this rank's blocks (BlockKey
+ * order, 17 significant digits): for one rank, model_run's
+ * blocks_coupled.txt / blocks_uncoupled.txt.  Small configurations. */
+int esg_blocks_write_text(esg_model* m, const char* path, int basis, int symmetrize_onsite);
+/* Rank 0's gathered text file from the ranks' shards (no device needed). */
+int esg_blocks_merge_text(const char* const* shard_paths, int n_shards, const char* out_path);
+/* Legacy pair: uncoupled values only, n_values from esg_blocks_count. */
+int esg_blocks_size(esg_model* m, int64_t* n_values);
 int esg_blocks_uncoupled(esg_model* m, double* out);
 
 /* ---- training (config 5) -------------------------- */

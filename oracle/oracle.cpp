@@ -26,6 +26,7 @@
 #include <complex>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <limits>
 #include <map>
 #include <numeric>
@@ -1507,6 +1508,56 @@ void uncoupled_block(const Model<T>& M, int za, int zb, const T* row, double* ou
     }
 }
 
+// network.h:296-315 fill_block: the coupled block (head segments placed
+// row-major into each shell-pair rectangle, L ascending).
+template <typename T>
+void coupled_block(const Model<T>& M, int za, int zb, const T* row, double* out) {
+  const auto& sha = M.basis.shells.at(za);
+  const auto& shb = M.basis.shells.at(zb);
+  const int nb = M.basis.n_orb(zb), na = M.basis.n_orb(za);
+  for (int i = 0; i < na * nb; ++i) out[i] = 0.0;
+  for (size_t a = 0; a < sha.size(); ++a)
+    for (size_t b = 0; b < shb.size(); ++b) {
+      const int la = sha[a], lb = shb[b], db = 2 * lb + 1;
+      const int oa = M.basis.off(za, (int)a), ob = M.basis.off(zb, (int)b);
+      int pos = 0;
+      for (int L = std::abs(la - lb); L <= la + lb; ++L) {
+        const int off = M.heads.segment((int)a, (int)b, L);
+        for (int r = 0; r < 2 * L + 1; ++r, ++pos) out[(oa + pos / db) * nb + ob + pos % db] = double(row[off + r]);
+      }
+    }
+}
+
+// block_matrix.cpp:66-88 blocks_to_uncoupled for one block: per shell pair
+// the rectangle read row-major as the coupled vector, to_block
+// (clebsch_gordan.cpp:157-170) written back into the rectangle.
+template <typename T>
+void uncoupled_from_coupled(const Model<T>& M, int za, int zb, const double* cb, double* out) {
+  const auto& sha = M.basis.shells.at(za);
+  const auto& shb = M.basis.shells.at(zb);
+  const int nb = M.basis.n_orb(zb);
+  for (size_t a = 0; a < sha.size(); ++a)
+    for (size_t b = 0; b < shb.size(); ++b) {
+      const int la = sha[a], lb = shb[b], da = 2 * la + 1, db = 2 * lb + 1;
+      const int oa = M.basis.off(za, (int)a), ob = M.basis.off(zb, (int)b);
+      std::vector<double> c(da * db), flat(da * db, 0.0);
+      for (int r = 0; r < da; ++r)
+        for (int q = 0; q < db; ++q) c[r * db + q] = cb[(oa + r) * nb + ob + q];
+      int o = 0;
+      for (int L = std::abs(la - lb); L <= la + lb; ++L) {
+        const auto& C = coupling(la, lb, L);
+        for (int p = 0; p < da * db; ++p) {
+          double acc = 0.0;
+          for (int r = 0; r < 2 * L + 1; ++r) acc += C[r * da * db + p] * c[o + r];
+          flat[p] += acc;
+        }
+        o += 2 * L + 1;
+      }
+      for (int r = 0; r < da; ++r)
+        for (int q = 0; q < db; ++q) out[(oa + r) * nb + ob + q] = flat[r * db + q];
+    }
+}
+
 }  // namespace orc
 
 // =================================================================== C API
@@ -2062,6 +2113,75 @@ int oracle_backward_f64(void* h, int n_rows, int n_owned, const int* row_species
 // Uncoupled block for one item from a float head row (double output).
 int oracle_uncoupled_block(void* h, int za, int zb, const float* row, double* out) {
   GUARD({ uncoupled_block(((OracleModel*)h)->mf, za, zb, row, out); })
+}
+
+int oracle_coupled_block(void* h, int za, int zb, const float* row, double* out) {
+  GUARD({ coupled_block(((OracleModel*)h)->mf, za, zb, row, out); })
+}
+
+namespace {
+using BlockMap = std::map<std::array<int, 5>, std::pair<std::array<int, 2>, std::vector<double>>>;
+void write_block_map(const BlockMap& bm, const char* path) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot open file for writing");
+  out.precision(17);
+  for (const auto& [key, blk] : bm) {
+    out << key[0] << " " << key[1] << " " << key[2] << " " << key[3] << " " << key[4] << " " << blk.first[0] << " "
+        << blk.first[1];
+    for (double x : blk.second) out << " " << x;
+    out << "\n";
+  }
+}
+}  // namespace
+
+// The reference's forward output stage for one rank (model_run.cpp:141-153):
+// assemble_blocks' map of coupled blocks (network.h:168-184), write_blocks of
+// it, blocks_to_uncoupled (block_matrix.cpp:66-88) into a second map, and
+// write_blocks of that.  The CPU baseline of the block export
+// (tools/blocks_bench.py).  Items: keys5 (i, j, image) with head rows;
+// species per atom index.
+int oracle_export_text(void* h, int64_t n_items, const int32_t* keys5, const float* rows, int out_len,
+                       const int32_t* species, const char* coupled_path, const char* uncoupled_path) {
+  GUARD({
+    const auto& M = ((OracleModel*)h)->mf;
+    BlockMap coupled, uncoupled;
+    for (int64_t it = 0; it < n_items; ++it) {
+      const int32_t* k = keys5 + 5 * it;
+      const int za = species[k[0]], zb = species[k[1]];
+      const int na = M.basis.n_orb(za), nb = M.basis.n_orb(zb);
+      std::vector<double> v((size_t)na * nb);
+      coupled_block(M, za, zb, rows + it * out_len, v.data());
+      coupled.emplace(std::array<int, 5>{k[0], k[1], k[2], k[3], k[4]},
+                      std::make_pair(std::array<int, 2>{na, nb}, std::move(v)));
+    }
+    write_block_map(coupled, coupled_path);
+    for (const auto& [key, blk] : coupled) {
+      std::vector<double> u(blk.second.size());
+      uncoupled_from_coupled(M, species[key[0]], species[key[1]], blk.second.data(), u.data());
+      uncoupled.emplace(key, std::make_pair(blk.first, std::move(u)));
+    }
+    write_block_map(uncoupled, uncoupled_path);
+  })
+}
+
+// block_matrix.cpp:90-101 write_blocks (std::ostream, precision 17) over the
+// std::map that model_run.cpp:103-120 gather_blocks builds: blocks arrive in
+// rank order and insert_or_assign keeps the last of equal keys.  keys7 per
+// block: i j ix iy iz rows cols; values concatenated row-major.
+int oracle_write_blocks(int64_t n_blocks, const int32_t* keys7, const double* values, const char* path) {
+  GUARD({
+    BlockMap bm;
+    int64_t at = 0;
+    for (int64_t b = 0; b < n_blocks; ++b) {
+      const int32_t* k = keys7 + 7 * b;
+      const int rows = k[5], cols = k[6];
+      std::vector<double> v(values + at, values + at + (int64_t)rows * cols);
+      at += (int64_t)rows * cols;
+      bm.insert_or_assign(std::array<int, 5>{k[0], k[1], k[2], k[3], k[4]},
+                          std::make_pair(std::array<int, 2>{rows, cols}, std::move(v)));
+    }
+    write_block_map(bm, path);
+  })
 }
 
 }  // extern "C"

@@ -12,6 +12,7 @@
 #include <map>
 #include <random>
 
+#include "blocks_io.h"
 #include "esg_internal.h"
 
 namespace esg {
@@ -26,8 +27,11 @@ void model_outputs(const esg_model* M, const float** no, const float** eo, const
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
 void model_copy_features(const esg_model* M, float* nodes, float* edges);
 void model_prepared_info(const esg_model* M, int64_t info[3]);
-int64_t model_blocks_size(const esg_model* M);
-void model_blocks(esg_model* M, double* out);
+void blocks_count(esg_model* M, int64_t* n_blocks, int64_t* n_values);
+void blocks_export(esg_model* M, int basis, bool sym, BlockRec* keys, double* values);
+void blocks_export_device(esg_model* M, int basis, bool sym, int vb, void* d_keys, void* d_values, float* kernel_ms);
+void blocks_write_shard(esg_model* M, const char* path, int basis, bool sym, int vb);
+void blocks_write_text(esg_model* M, const char* path, int basis, bool sym);
 
 namespace {
 thread_local std::string g_last;
@@ -668,20 +672,84 @@ int esg_features_export(const esg_model* m, float* nodes, float* edges) {
   ESG_API_END
 }
 
-int esg_blocks_size(const esg_model* m, int64_t* n) {
+namespace {
+esg_model* device_model(esg_model* m) {
+  if (!m) usage("model is NULL");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  return m;
+}
+}  // namespace
+
+int esg_blocks_count(esg_model* m, int64_t* n_blocks, int64_t* n_values) {
   ESG_API_BEGIN
-  NEED(m, "model");
-  *n = model_blocks_size(m);
+  blocks_count(device_model(m), n_blocks, n_values);
+  ESG_API_END
+}
+
+int esg_blocks_export(esg_model* m, int basis, int symmetrize_onsite, esg_block_key* keys, double* values) {
+  ESG_API_BEGIN
+  static_assert(sizeof(esg_block_key) == sizeof(BlockRec), "key record layout");
+  blocks_export(device_model(m), basis, symmetrize_onsite != 0, reinterpret_cast<BlockRec*>(keys), values);
+  ESG_API_END
+}
+
+int esg_blocks_export_device(esg_model* m, int basis, int symmetrize_onsite, int value_bytes, void* d_keys,
+                             void* d_values, float* kernel_ms) {
+  ESG_API_BEGIN
+  blocks_export_device(device_model(m), basis, symmetrize_onsite != 0, value_bytes, d_keys, d_values, kernel_ms);
+  ESG_API_END
+}
+
+int esg_blocks_write_shard(esg_model* m, const char* path, int basis, int symmetrize_onsite, int value_bytes) {
+  ESG_API_BEGIN
+  NEED(path, "path");
+  blocks_write_shard(device_model(m), path, basis, symmetrize_onsite != 0, value_bytes);
+  ESG_API_END
+}
+
+int esg_blocks_write_text(esg_model* m, const char* path, int basis, int symmetrize_onsite) {
+  ESG_API_BEGIN
+  NEED(path, "path");
+  blocks_write_text(device_model(m), path, basis, symmetrize_onsite != 0);
+  ESG_API_END
+}
+
+int esg_blocks_merge_text(const char* const* shard_paths, int n_shards, const char* out_path) {
+  ESG_API_BEGIN
+  NEED(out_path, "out_path");
+  if (n_shards < 0 || (n_shards > 0 && !shard_paths)) usage("shard_paths");
+  std::vector<BlockSet> sets;
+  sets.reserve(n_shards);
+  uint32_t basis0 = 0, flags0 = 0;
+  for (int r = 0; r < n_shards; ++r) {
+    NEED(shard_paths[r], "shard path");
+    ShardHeader h;
+    sets.push_back(read_shard(shard_paths[r], &h));
+    if (r == 0) {
+      basis0 = h.basis;
+      flags0 = h.flags;
+    } else if (h.basis != basis0 || h.flags != flags0) {
+      data("shards mix block bases or on-site symmetrisation");
+    }
+  }
+  std::vector<const BlockSet*> ptrs;
+  for (const auto& s : sets) ptrs.push_back(&s);
+  write_blocks_text(out_path, ptrs);
+  ESG_API_END
+}
+
+int esg_blocks_size(esg_model* m, int64_t* n) {
+  ESG_API_BEGIN
+  NEED(n, "n_values");
+  blocks_count(device_model(m), nullptr, n);
   ESG_API_END
 }
 
 int esg_blocks_uncoupled(esg_model* m, double* out) {
   ESG_API_BEGIN
-  NEED(m, "model");
-  if (!m->ctx || !m->dev) usage("model was created without a device context");
   NEED(out, "out");
-  ESG_CUDA(cudaSetDevice(m->ctx->device));
-  model_blocks(m, out);
+  blocks_export(device_model(m), ESG_BLOCKS_UNCOUPLED, false, nullptr, out);
   ESG_API_END
 }
 

@@ -62,13 +62,16 @@ struct DeviceModel {
   int64_t chunk_cap = 0;
   float* node_out = nullptr;
   float* edge_out = nullptr;
-  // uncoupled block bookkeeping (filled on first use, model_blocks)
-  mutable std::vector<int> h_item_species_a, h_item_species_b;
-  mutable bool item_species_ready = false;
+  // block export (blocks.cu): global ids per row, packed image shift per
+  // view edge, per-item value offsets (built on first export after a prepare)
+  int* row_global = nullptr;
+  uint32_t* eshift = nullptr;
+  struct BlockState* blk = nullptr;
+  bool blk_ready = false;  // blk's per-item offsets match the prepared view
   // allocated elements of the view buffers (grow)
   size_t cap_row_slot = 0, cap_src = 0, cap_dst = 0, cap_dir = 0, cap_dist = 0, cap_seg = 0, cap_nodes = 0,
          cap_nodes_alt = 0, cap_edges = 0, cap_a1 = 0, cap_y = 0, cap_logits = 0, cap_node_out = 0,
-         cap_edge_out = 0, cap_send_rows = 0, cap_send_buf = 0;
+         cap_edge_out = 0, cap_send_rows = 0, cap_send_buf = 0, cap_row_global = 0, cap_eshift = 0;
   bool a1_tc_clean = false;  // A1 holds zeros in every tensor-core K padding slot
   // training (train.cu): the forward saves every block's input tables when
   // save_inputs is set -- the node table after the block's halo exchange
@@ -93,5 +96,6 @@ struct DeviceModel {
 };
 
 void free_ptr(void* p);
+void blocks_free(DeviceModel* D);  // blocks.cu
 
 }  // namespace esg

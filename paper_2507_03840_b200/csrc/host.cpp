@@ -328,42 +328,77 @@ uint64_t param_hash(const ParamSet& p, const std::vector<float>& v) {
 }
 
 // ------------------------------------------------------- coupling tables
-// Complex Clebsch-Gordan <la ma; lb mb | L M> by the Racah closed form
-// (Condon-Shortley: <la la; lb L-la | L L> > 0), then the real-harmonic
-// change of basis with the one fixed phase that makes the block real --
-// the same matrices clebsch_gordan.cpp:90-140 builds by lowering operators.
+// clebsch_gordan.cpp:22-140.  Complex CG vectors per L: the top state
+// |L, L> is the stretched product basis vector orthogonalised (twice) against
+// the |L', L> states of every larger L' and sign-fixed positive on
+// (ma=la, mb=L-la); lower states follow from J- = Ja- + Jb- with a
+// renormalisation at each step.  The real block is then
+// B_L * cg * (B_la (x) B_lb)^H with one fixed phase (imaginary part when
+// la+lb-L is odd).  Same operation order as the CPU oracle, so the tables
+// agree to the bit and block export is bit-exact against it.
 namespace {
-double fact(int n) {
-  double r = 1.0;
-  for (int i = 2; i <= n; ++i) r *= i;
-  return r;
-}
-double cg_racah(int j1, int m1, int j2, int m2, int J, int M) {
-  if (m1 + m2 != M || std::abs(m1) > j1 || std::abs(m2) > j2 || std::abs(M) > J) return 0.0;
-  const double pre = std::sqrt((2 * J + 1) * fact(J + j1 - j2) * fact(J - j1 + j2) * fact(j1 + j2 - J) /
-                               fact(j1 + j2 + J + 1));
-  const double pre2 =
-      std::sqrt(fact(J + M) * fact(J - M) * fact(j1 - m1) * fact(j1 + m1) * fact(j2 - m2) * fact(j2 + m2));
-  double s = 0.0;
-  for (int k = 0; k <= j1 + j2 - J; ++k) {
-    const int a = j1 + j2 - J - k, b = j1 - m1 - k, c = j2 + m2 - k, d = J - j2 + m1 + k, e = J - j1 - m2 + k;
-    if (a < 0 || b < 0 || c < 0 || d < 0 || e < 0) continue;
-    s += ((k % 2) ? -1.0 : 1.0) / (fact(k) * fact(a) * fact(b) * fact(c) * fact(d) * fact(e));
+using cplx = std::complex<double>;
+
+std::vector<std::vector<double>> cg_states(int la, int lb) {
+  const int da = 2 * la + 1, db = 2 * lb + 1, dim = da * db;
+  const int l0 = std::abs(la - lb), l1 = la + lb;
+  auto at = [&](int ma, int mb) { return (ma + la) * db + (mb + lb); };
+  auto norm = [](const std::vector<double>& v) {
+    double s = 0.0;
+    for (double x : v) s += x * x;
+    return std::sqrt(s);
+  };
+  std::vector<std::vector<double>> st(l1 - l0 + 1);  // st[L-l0]: rows M+L, dim columns
+  for (int L = l1; L >= l0; --L) {
+    std::vector<double> v(dim, 0.0), rows((size_t)(2 * L + 1) * dim, 0.0);
+    v[at(la, L - la)] = 1.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int Lq = L + 1; Lq <= l1; ++Lq) {
+        const double* w = &st[Lq - l0][(size_t)(L + Lq) * dim];
+        double d = 0.0;
+        for (int k = 0; k < dim; ++k) d += w[k] * v[k];
+        for (int k = 0; k < dim; ++k) v[k] -= d * w[k];
+      }
+      const double n = norm(v);
+      if (!(n > 1e-12)) data("degenerate coupling state");
+      for (double& x : v) x /= n;
+    }
+    if (v[at(la, L - la)] < 0.0)
+      for (double& x : v) x = -x;
+    std::copy(v.begin(), v.end(), rows.begin() + (size_t)(2 * L) * dim);
+    for (int M = L; M > -L; --M) {
+      std::vector<double> lo(dim, 0.0);
+      for (int ma = -la; ma <= la; ++ma)
+        for (int mb = -lb; mb <= lb; ++mb) {
+          const double c = v[at(ma, mb)];
+          if (c == 0.0) continue;
+          if (ma > -la) lo[at(ma - 1, mb)] += c * std::sqrt(la * (la + 1.0) - ma * (ma - 1.0));
+          if (mb > -lb) lo[at(ma, mb - 1)] += c * std::sqrt(lb * (lb + 1.0) - mb * (mb - 1.0));
+        }
+      const double f = std::sqrt(L * (L + 1.0) - M * (M - 1.0));
+      for (double& x : lo) x /= f;
+      const double n = norm(lo);
+      for (double& x : lo) x /= n;
+      v.swap(lo);
+      std::copy(v.begin(), v.end(), rows.begin() + (size_t)(L + M - 1) * dim);
+    }
+    st[L - l0] = std::move(rows);
   }
-  return pre * pre2 * s;
+  return st;
 }
-// rows: real component m (index m+l); cols: complex m (index m+l).
-std::vector<std::complex<double>> real_basis(int l) {
+
+// rows: real component index m+l; columns: complex m+l
+std::vector<cplx> real_basis(int l) {
   const int d = 2 * l + 1;
-  std::vector<std::complex<double>> b(d * d);
-  const double s = std::sqrt(0.5);
-  b[l * d + l] = 1.0;
+  std::vector<cplx> b((size_t)d * d, cplx(0.0, 0.0));
+  const double s = 1.0 / std::sqrt(2.0);
+  b[(size_t)l * d + l] = 1.0;
   for (int m = 1; m <= l; ++m) {
-    const double ph = (m & 1) ? -1.0 : 1.0;
-    b[(l + m) * d + (l - m)] = s;
-    b[(l + m) * d + (l + m)] = ph * s;
-    b[(l - m) * d + (l - m)] = std::complex<double>(0.0, s);
-    b[(l - m) * d + (l + m)] = std::complex<double>(0.0, -ph * s);
+    const double ph = (m % 2 == 0) ? 1.0 : -1.0;
+    b[(size_t)(l + m) * d + (l - m)] = s;
+    b[(size_t)(l + m) * d + (l + m)] = ph * s;
+    b[(size_t)(l - m) * d + (l - m)] = cplx(0.0, s);
+    b[(size_t)(l - m) * d + (l + m)] = cplx(0.0, -ph * s);
   }
   return b;
 }
@@ -372,26 +407,30 @@ std::vector<std::complex<double>> real_basis(int l) {
 std::vector<double> coupling_matrix(int la, int lb, int L) {
   if (L < std::abs(la - lb) || L > la + lb) data("coupled degree violates the triangle rule");
   const int da = 2 * la + 1, db = 2 * lb + 1, dL = 2 * L + 1, dim = da * db;
+  const auto st = cg_states(la, lb);
   const auto Ba = real_basis(la), Bb = real_basis(lb), BL = real_basis(L);
-  // u[i][q] = sum_M BL[i][M] sum_{ma,mb} cg(ma,mb;M) conj(Ba[qa][ma] Bb[qb][mb])
-  std::vector<double> out(dL * dim);
+  const std::vector<double>& cg = st[L - std::abs(la - lb)];
+  // t = B_L * cg (dL x dim)
+  std::vector<cplx> t((size_t)dL * dim, cplx(0.0, 0.0));
+  for (int i = 0; i < dL; ++i)
+    for (int k = 0; k < dL; ++k) {
+      const cplx a = BL[(size_t)i * dL + k];
+      if (a == cplx(0.0, 0.0)) continue;
+      for (int j = 0; j < dim; ++j) t[(size_t)i * dim + j] += a * cg[(size_t)k * dim + j];
+    }
+  // u = t * K^H with K[(i,j),(k,m)] = Ba[i][k] Bb[j][m]
+  std::vector<double> out((size_t)dL * dim);
   const bool odd = ((la + lb - L) & 1) != 0;
   for (int i = 0; i < dL; ++i)
-    for (int qa = 0; qa < da; ++qa)
-      for (int qb = 0; qb < db; ++qb) {
-        std::complex<double> acc = 0.0;
-        for (int M = -L; M <= L; ++M) {
-          const auto bl = BL[i * dL + (M + L)];
-          if (bl == 0.0) continue;
-          for (int ma = -la; ma <= la; ++ma) {
-            const int mb = M - ma;
-            if (mb < -lb || mb > lb) continue;
-            const double c = cg_racah(la, ma, lb, mb, L, M);
-            acc += bl * c * std::conj(Ba[qa * da + (ma + la)] * Bb[qb * db + (mb + lb)]);
-          }
-        }
-        out[i * dim + qa * db + qb] = odd ? acc.imag() : acc.real();
+    for (int q = 0; q < dim; ++q) {
+      const int qa = q / db, qb = q % db;
+      cplx acc(0.0, 0.0);
+      for (int p = 0; p < dim; ++p) {
+        const cplx kq = Ba[(size_t)qa * da + p / db] * Bb[(size_t)qb * db + p % db];
+        acc += t[(size_t)i * dim + p] * std::conj(kq);
       }
+      out[(size_t)i * dim + q] = odd ? acc.imag() : acc.real();
+    }
   return out;
 }
 

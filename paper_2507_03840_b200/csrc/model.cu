@@ -201,31 +201,6 @@ __global__ void __launch_bounds__(256) k_heads(const float* __restrict__ x, int6
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-// ------------------------------------------------ uncoupled blocks
-// network.h:296-315 fill_block + block_matrix.cpp:66-88 to_block: per item
-// and shell pair, flat = sum_L C_L^T c_L, written row-major into the
-// n_orb(za) x n_orb(zb) block.  Work items are (item, shell pair).
-// Host-built per species pair: block element j = sum over (head index, C
-// coefficient) terms of that element (its shell pair's L segments), in
-// ascending L then r -- the to_block order.  One thread per (item, element).
-__global__ void k_blocks(const float* __restrict__ heads, int out_len, const int* __restrict__ item_pair,
-                         const int64_t* __restrict__ item_off, const int* __restrict__ pair_nelem,
-                         const int* __restrict__ pair_ptr0, const int* __restrict__ elem_ptr,
-                         const int* __restrict__ term_idx, const double* __restrict__ term_coef, int max_elem,
-                         int64_t n_items, double* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t it = t / max_elem;
-  const int j = int(t % max_elem);
-  if (it >= n_items) return;
-  const int sp = item_pair[it];
-  if (j >= pair_nelem[sp]) return;
-  const float* row = heads + it * out_len;
-  const int e = pair_ptr0[sp] + j;
-  double acc = 0.0;
-  for (int q = elem_ptr[e]; q < elem_ptr[e + 1]; ++q) acc += term_coef[q] * (double)row[term_idx[q]];
-  out[item_off[it] + j] = acc;
-}
-
 __global__ void k_pack_rows(const float* __restrict__ nodes, const int* __restrict__ rows, int64_t n_rows, int row_len,
                             float* __restrict__ buf) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -235,7 +210,8 @@ __global__ void k_pack_rows(const float* __restrict__ nodes, const int* __restri
 }
 
 __global__ void k_gather_dirs(const double* __restrict__ disp, const int* __restrict__ eidx, int64_t n,
-                              float* __restrict__ dir, double* __restrict__ dist_in, double* __restrict__ dist_out) {
+                              float* __restrict__ dir, double* __restrict__ dist_in, double* __restrict__ dist_out,
+                              const uint32_t* __restrict__ shift_in, uint32_t* __restrict__ shift_out) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int64_t g = eidx ? eidx[k] : k;
@@ -243,6 +219,7 @@ __global__ void k_gather_dirs(const double* __restrict__ disp, const int* __rest
   dir[3 * k + 1] = (float)disp[3 * g + 1];
   dir[3 * k + 2] = (float)disp[3 * g + 2];
   dist_out[k] = dist_in[g];
+  shift_out[k] = shift_in[g];
 }
 
 }  // namespace
@@ -599,11 +576,12 @@ void model_device_destroy(esg_model* M) {
   DeviceModel* D = M->dev;
   if (!D) return;
   train_free(D);
+  blocks_free(D);
   for (void* p : {(void*)D->params, (void*)D->embed, (void*)D->head_w[0], (void*)D->head_w[1], (void*)D->head_key,
                   (void*)D->head_row, (void*)D->head_hptr, (void*)D->row_slot, (void*)D->src_row, (void*)D->dst_row, (void*)D->dir,
                   (void*)D->dist, (void*)D->seg, (void*)D->send_rows, (void*)D->send_buf, (void*)D->nodes,
                   (void*)D->nodes_alt, (void*)D->edges, D->A1, (void*)D->Y, (void*)D->logits, (void*)D->node_out,
-                  (void*)D->edge_out})
+                  (void*)D->edge_out, (void*)D->row_global, (void*)D->eshift})
     free_ptr(p);
   for (auto p : D->w1t) free_ptr(p);
   for (auto p : D->w2t) free_ptr(p);
@@ -666,14 +644,17 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   D->n_owned = n_owned;
   D->n_edges = ne;
   D->h_seg = seg;
-  D->item_species_ready = false;
+  D->blk_ready = false;
   D->row_slot = grow(D->row_slot, D->cap_row_slot, n_rows);
   D->src_row = grow(D->src_row, D->cap_src, ne);
   D->dst_row = grow(D->dst_row, D->cap_dst, ne);
   D->dir = grow(D->dir, D->cap_dir, 3 * ne);
   D->dist = grow(D->dist, D->cap_dist, ne);
   D->seg = grow(D->seg, D->cap_seg, n_owned + 1);
+  D->eshift = grow(D->eshift, D->cap_eshift, ne);
+  D->row_global = grow(D->row_global, D->cap_row_global, n_rows);
   ESG_CUDA(cudaMemcpyAsync(D->row_slot, slot.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice, st));
+  ESG_CUDA(cudaMemcpyAsync(D->row_global, row_global.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice, st));
   int* d_eidx = nullptr;
   if (plan) {
     ESG_CUDA(cudaMemcpyAsync(D->src_row, plan->src_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
@@ -690,7 +671,8 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     }
   }
   if (ne) {
-    k_gather_dirs<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(g->d_disp, d_eidx, ne, D->dir, g->d_dist, D->dist);
+    k_gather_dirs<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(g->d_disp, d_eidx, ne, D->dir, g->d_dist, D->dist,
+                                                                g->d_shift, D->eshift);
     ++M->ctx->launches;
   }
   // destination-aligned chunks of about chunk_cap edges
@@ -744,28 +726,6 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   free_ptr(d_eidx);
   D->prepared = true;
   D->train_stale = true;
-}
-
-// per-item species for block assembly (nodes: owned rows, edges: view edges),
-// built from the device index arrays the first time blocks are requested
-void ensure_item_species(const esg_model* M) {
-  const DeviceModel* D = M->dev;
-  if (D->item_species_ready) return;
-  const int n_owned = D->n_owned;
-  const int64_t ne = D->n_edges;
-  std::vector<int> src(ne), dst(ne);
-  if (ne) {
-    ESG_CUDA(cudaMemcpy(src.data(), D->src_row, sizeof(int) * ne, cudaMemcpyDeviceToHost));
-    ESG_CUDA(cudaMemcpy(dst.data(), D->dst_row, sizeof(int) * ne, cudaMemcpyDeviceToHost));
-  }
-  D->h_item_species_a.assign(n_owned + ne, 0);
-  D->h_item_species_b.assign(n_owned + ne, 0);
-  for (int i = 0; i < n_owned; ++i) D->h_item_species_a[i] = D->h_item_species_b[i] = D->row_species[i];
-  for (int64_t k = 0; k < ne; ++k) {
-    D->h_item_species_a[n_owned + k] = D->row_species[src[k]];
-    D->h_item_species_b[n_owned + k] = D->row_species[dst[k]];
-  }
-  D->item_species_ready = true;
 }
 
 namespace {
@@ -1066,104 +1026,4 @@ void model_prepared_info(const esg_model* M, int64_t info[3]) {
 }
 
 // Uncoupled blocks of the last forward, items = owned nodes then view edges.
-int64_t model_blocks_size(const esg_model* M) {
-  ensure_item_species(M);
-  const DeviceModel* D = M->dev;
-  int64_t n = 0;
-  for (size_t i = 0; i < D->h_item_species_a.size(); ++i)
-    n += (int64_t)M->basis.n_orb(D->h_item_species_a[i]) * M->basis.n_orb(D->h_item_species_b[i]);
-  return n;
-}
-
-void model_blocks(esg_model* M, double* out_host) {
-  ensure_item_species(M);
-  DeviceModel* D = M->dev;
-  cudaStream_t st = M->ctx->stream;
-  // Per species pair: for every block element (row-major n_orb(za) x
-  // n_orb(zb)) the list of (head index, coupling coefficient) terms.
-  std::map<std::pair<int, int>, int> pair_id;
-  std::vector<int> pair_nelem, pair_ptr0, elem_ptr{0}, term_idx;
-  std::vector<double> term_coef;
-  std::map<std::array<int, 3>, std::vector<double>> cg;
-  for (const auto& ka : M->basis.shells)
-    for (const auto& kb : M->basis.shells) {
-      const int na = M->basis.n_orb(ka.first), nb = M->basis.n_orb(kb.first);
-      std::vector<std::vector<std::pair<int, double>>> terms((size_t)na * nb);
-      for (size_t a = 0; a < ka.second.size(); ++a)
-        for (size_t b = 0; b < kb.second.size(); ++b) {
-          const int la = ka.second[a], lb = kb.second[b], da = 2 * la + 1, db = 2 * lb + 1;
-          const int oa = M->basis.off(ka.first, (int)a), ob = M->basis.off(kb.first, (int)b);
-          for (int L = std::abs(la - lb); L <= la + lb; ++L) {
-            auto key = std::array<int, 3>{la, lb, L};
-            if (!cg.count(key)) cg[key] = coupling_matrix(la, lb, L);
-            const auto& C = cg[key];
-            const int seg = M->heads.segment((int)a, (int)b, L);
-            for (int p = 0; p < da * db; ++p)
-              for (int r = 0; r < 2 * L + 1; ++r)
-                terms[(size_t)(oa + p / db) * nb + ob + p % db].push_back({seg + r, C[(size_t)r * da * db + p]});
-          }
-        }
-      pair_id[{ka.first, kb.first}] = (int)pair_nelem.size();
-      pair_nelem.push_back(na * nb);
-      pair_ptr0.push_back((int)elem_ptr.size() - 1);
-      for (const auto& tl : terms) {
-        for (const auto& t : tl) {
-          term_idx.push_back(t.first);
-          term_coef.push_back(t.second);
-        }
-        elem_ptr.push_back((int)term_idx.size());
-      }
-    }
-  const int64_t n_items = (int64_t)D->h_item_species_a.size();
-  std::vector<int> item_pair(n_items);
-  std::vector<int64_t> off(n_items);
-  int64_t at = 0;
-  int max_elem = 1;
-  for (int64_t i = 0; i < n_items; ++i) {
-    const int pid = pair_id.at({D->h_item_species_a[i], D->h_item_species_b[i]});
-    item_pair[i] = pid;
-    off[i] = at;
-    at += pair_nelem[pid];
-    max_elem = std::max(max_elem, pair_nelem[pid]);
-  }
-  int* d_item_pair = dalloc<int>(n_items);
-  int64_t* d_off = dalloc<int64_t>(n_items);
-  int* d_nelem = dalloc<int>(pair_nelem.size());
-  int* d_ptr0 = dalloc<int>(pair_ptr0.size());
-  int* d_eptr = dalloc<int>(elem_ptr.size());
-  int* d_tidx = dalloc<int>(term_idx.size());
-  double* d_tcoef = dalloc<double>(term_coef.size());
-  double* d_out = dalloc<double>(at);
-  auto up = [&](void* d, const void* h, size_t n) {
-    if (n) ESG_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st));
-  };
-  up(d_item_pair, item_pair.data(), sizeof(int) * n_items);
-  up(d_off, off.data(), sizeof(int64_t) * n_items);
-  up(d_nelem, pair_nelem.data(), sizeof(int) * pair_nelem.size());
-  up(d_ptr0, pair_ptr0.data(), sizeof(int) * pair_ptr0.size());
-  up(d_eptr, elem_ptr.data(), sizeof(int) * elem_ptr.size());
-  up(d_tidx, term_idx.data(), sizeof(int) * term_idx.size());
-  up(d_tcoef, term_coef.data(), sizeof(double) * term_coef.size());
-  const int ol = M->heads.out_len;
-  if (D->n_owned) {
-    const int64_t n = (int64_t)D->n_owned * max_elem;
-    k_blocks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->node_out, ol, d_item_pair, d_off, d_nelem, d_ptr0, d_eptr,
-                                                          d_tidx, d_tcoef, max_elem, D->n_owned, d_out);
-    ++M->ctx->launches;
-  }
-  if (D->n_edges) {
-    const int64_t n = D->n_edges * max_elem;
-    k_blocks<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->edge_out, ol, d_item_pair + D->n_owned,
-                                                          d_off + D->n_owned, d_nelem, d_ptr0, d_eptr, d_tidx, d_tcoef,
-                                                          max_elem, D->n_edges, d_out);
-    ++M->ctx->launches;
-  }
-  ESG_CUDA(cudaGetLastError());
-  ESG_CUDA(cudaMemcpyAsync(out_host, d_out, sizeof(double) * at, cudaMemcpyDeviceToHost, st));
-  ESG_CUDA(cudaStreamSynchronize(st));
-  for (void* q : {(void*)d_item_pair, (void*)d_off, (void*)d_nelem, (void*)d_ptr0, (void*)d_eptr, (void*)d_tidx,
-                  (void*)d_tcoef, (void*)d_out})
-    free_ptr(q);
-}
-
 }  // namespace esg

@@ -332,6 +332,43 @@ class Timing:
     gpu_launches: int
 
 
+# ------------------------------------------------------------- block export
+BLOCKS_COUPLED, BLOCKS_UNCOUPLED = 0, 1
+BLOCK_KEY = np.dtype([("i", "<i4"), ("j", "<i4"), ("ix", "<i4"), ("iy", "<i4"), ("iz", "<i4"),
+                      ("rows", "<u2"), ("cols", "<u2")])  # esg_block_key, 24 bytes
+SHARD_HEADER = np.dtype([("magic", "S8"), ("version", "<u4"), ("basis", "<u4"), ("value_bytes", "<u4"),
+                         ("flags", "<u4"), ("rank", "<u4"), ("world", "<u4"), ("n_blocks", "<u8"),
+                         ("n_values", "<u8"), ("keys_offset", "<u8"), ("values_offset", "<u8")])
+
+
+def _block_arrays(keys, vals):
+    k = np.stack([keys["i"], keys["j"], keys["ix"], keys["iy"], keys["iz"]], axis=1)
+    shp = np.stack([keys["rows"], keys["cols"]], axis=1).astype(np.int64)
+    off = np.zeros(len(keys) + 1, np.int64)
+    np.cumsum(shp[:, 0] * shp[:, 1], out=off[1:])
+    return k, shp, off, vals
+
+
+def read_block_shard(path: str):
+    """A shard file memory-mapped: (header dict, keys (n, 5),
+    shapes (n, 2), value offsets (n + 1), values)."""
+    h = np.fromfile(path, SHARD_HEADER, 1)
+    if h.size != 1 or h["magic"][0] != b"ESGBLKS1" or int(h["version"][0]) != 1:
+        raise DataError(f"not a block shard: {path}")
+    hd = {k: (h[k][0].item() if k != "magic" else h[k][0]) for k in SHARD_HEADER.names}
+    nb, nv = hd["n_blocks"], hd["n_values"]
+    keys = np.memmap(path, BLOCK_KEY, "r", hd["keys_offset"], (nb,)) if nb else np.zeros(0, BLOCK_KEY)
+    vt = np.float64 if hd["value_bytes"] == 8 else np.float32
+    vals = np.memmap(path, vt, "r", hd["values_offset"], (nv,)) if nv else np.zeros(0, vt)
+    return (hd,) + _block_arrays(keys, vals)
+
+
+def merge_block_shards_to_text(shard_paths: Sequence[str], out_path: str) -> None:
+    """model_run's rank-0 text file (block_matrix.cpp:90-101) from shards."""
+    arr = (C.c_char_p * len(shard_paths))(*[os.fsencode(p) for p in shard_paths])
+    _check(lib().esg_blocks_merge_text(arr, C.c_int(len(shard_paths)), os.fsencode(out_path)))
+
+
 class Network:
     """model::Network<float> (network.h:77-228) driven through the C ABI."""
 
@@ -443,6 +480,39 @@ class Network:
         out = np.zeros(n.value)
         _check(lib().esg_blocks_uncoupled(self._h, _p(out)))
         return out
+
+    def blocks_count(self):
+        nb, nv = C.c_int64(), C.c_int64()
+        _check(lib().esg_blocks_count(self._h, C.byref(nb), C.byref(nv)))
+        return nb.value, nv.value
+
+    def blocks(self, basis: int = 1, symmetrize_onsite: bool = False):
+        """This rank's blocks of the last forward: (keys (n, 5) int32 =
+        (i, j, ix, iy, iz), shapes (n, 2), value offsets (n + 1), fp64 values)."""
+        nb, nv = self.blocks_count()
+        keys = np.zeros(nb, BLOCK_KEY)
+        vals = np.zeros(nv)
+        _check(lib().esg_blocks_export(self._h, C.c_int(basis), C.c_int(int(symmetrize_onsite)), _p(keys), _p(vals)))
+        return _block_arrays(keys, vals)
+
+    def blocks_to_device(self, d_keys: int, d_values: int, basis: int = 1, symmetrize_onsite: bool = False,
+                         value_bytes: int = 8) -> float:
+        """Keys/values into caller device buffers (raw pointers, 0 = skip);
+        returns the kernels' device milliseconds."""
+        ms = C.c_float()
+        _check(lib().esg_blocks_export_device(self._h, C.c_int(basis), C.c_int(int(symmetrize_onsite)),
+                                              C.c_int(value_bytes), C.c_void_p(d_keys or None),
+                                              C.c_void_p(d_values or None), C.byref(ms)))
+        return ms.value
+
+    def write_block_shard(self, path: str, basis: int = 1, symmetrize_onsite: bool = False,
+                          value_bytes: int = 8) -> None:
+        _check(lib().esg_blocks_write_shard(self._h, os.fsencode(path), C.c_int(basis),
+                                            C.c_int(int(symmetrize_onsite)), C.c_int(value_bytes)))
+
+    def write_blocks_text(self, path: str, basis: int = 1, symmetrize_onsite: bool = False) -> None:
+        _check(lib().esg_blocks_write_text(self._h, os.fsencode(path), C.c_int(basis),
+                                           C.c_int(int(symmetrize_onsite))))
 
     def save_checkpoint(self, path: str, opt: Optional["Adam"] = None, config_text: str = "") -> None:
         """checkpoint.h save_checkpoint (version-1 container); with opt the

@@ -310,6 +310,32 @@ class Model:
                                          _p(np.ascontiguousarray(row, np.float32)), _p(out)))
         return out.reshape(n_orb_a, n_orb_b)
 
+    def export_text(self, keys, rows, species, coupled_path, uncoupled_path):
+        """model_run.cpp:141-153 for one rank: coupled map, its text,
+        blocks_to_uncoupled, its text (the block export's CPU baseline)."""
+        k = np.ascontiguousarray(keys, np.int32)
+        r = np.ascontiguousarray(rows, np.float32)
+        _ok(lib().oracle_export_text(C.c_void_p(self.h), C.c_int64(len(k)), _p(k), _p(r), C.c_int(r.shape[1]),
+                                     _p(np.ascontiguousarray(species, np.int32)), os.fsencode(str(coupled_path)),
+                                     os.fsencode(str(uncoupled_path))))
+
+    def coupled_block(self, za, zb, row, n_orb_a, n_orb_b):
+        """network.h:296-315 fill_block."""
+        out = np.zeros(n_orb_a * n_orb_b)
+        _ok(lib().oracle_coupled_block(C.c_void_p(self.h), C.c_int(za), C.c_int(zb),
+                                       _p(np.ascontiguousarray(row, np.float32)), _p(out)))
+        return out.reshape(n_orb_a, n_orb_b)
+
+
+def write_blocks(keys, shapes, values, path):
+    """block_matrix.cpp:90-101 write_blocks (std::ostream, precision 17) of the
+    map gather_blocks builds (model_run.cpp:103-120): equal keys keep the last
+    block.  keys (n, 5), shapes (n, 2), values concatenated row-major."""
+    k7 = np.ascontiguousarray(np.concatenate([np.asarray(keys, np.int32).reshape(-1, 5),
+                                              np.asarray(shapes, np.int32).reshape(-1, 2)], axis=1))
+    v = np.ascontiguousarray(values, np.float64)
+    _ok(lib().oracle_write_blocks(C.c_int64(len(k7)), _p(k7), _p(v), os.fsencode(str(path))))
+
 
 def serial_view(n, species, g):
     """model::serial_view (graph_view.h:37-56) as plain arrays."""

@@ -8,7 +8,9 @@ segment-local with a fixed order, so the outputs must agree bit for bit
 import argparse
 import math
 import os
+import shutil
 import sys
+import tempfile
 
 import numpy as np
 import torch
@@ -48,6 +50,12 @@ def main():
     owned = pe["row_global"][:plan.n_owned]
     outs = [None] * world
     dist.all_gather_object(outs, (owned, pe["edge_index"], no, eo, tm.exchanges, tm.halo_ms))
+    # per-rank block shards into a directory rank 0 picks
+    d = [tempfile.mkdtemp(prefix="esg_blk_") if rank == 0 else None]
+    dist.broadcast_object_list(d, src=0)
+    shard = os.path.join(d[0], f"rank{rank}.blk")
+    net.write_block_shard(shard, esg.BLOCKS_UNCOUPLED)
+    dist.barrier()
     ok = True
     if rank == 0:
         ctx1 = esg.Context(local, 0, 1)
@@ -66,6 +74,15 @@ def main():
         print(f"world {world}: exchanges/forward {outs[0][4]}, halo ms {[round(x[5], 3) for x in outs]}, "
               f"bit-exact {same}, max|diff| {max(np.abs(gno - sno).max(), np.abs(geo - seo).max())}")
         ok &= same
+        # rank 0's gathered text from the shards == the 1-GPU text file
+        merged, serial = os.path.join(d[0], "merged.txt"), os.path.join(d[0], "serial.txt")
+        esg.merge_block_shards_to_text([os.path.join(d[0], f"rank{r}.blk") for r in range(world)], merged)
+        net1.write_blocks_text(serial, esg.BLOCKS_UNCOUPLED)
+        with open(merged, "rb") as a, open(serial, "rb") as b:
+            same_txt = a.read() == b.read()
+        print(f"blocks text identical {same_txt} ({os.path.getsize(serial)} bytes)")
+        ok &= same_txt
+        shutil.rmtree(d[0], ignore_errors=True)
     flag = torch.tensor([int(ok)])
     dist.broadcast(flag, 0)
     dist.destroy_process_group()
