@@ -34,10 +34,20 @@ namespace esg {
 // block shape and, per block element (row-major), its terms (head index,
 // coefficient) in to_block order; bit 31 of a term index marks the first
 // term of an L segment.
+// Exactly-zero coefficients are dropped: the running sums start at +0 and
+// never become -0 under round-to-nearest, so adding a zero product cannot
+// change them -- the result is bit-identical for finite heads (a NaN/Inf head
+// no longer reaches elements whose coefficient on it is zero).
+struct __align__(16) BlockTerm {
+  double c;
+  uint32_t idx;  // head index | kSegStart on the first kept term of an L segment
+  uint32_t pad;
+};
+
 struct BlockTables {
   int S = 0, max_elem = 1;
-  int *nelem = nullptr, *rows = nullptr, *cols = nullptr, *ptr0 = nullptr, *eptr = nullptr, *tidx = nullptr;
-  double* coef = nullptr;
+  int *nelem = nullptr, *rows = nullptr, *cols = nullptr, *ptr0 = nullptr, *eptr = nullptr;
+  BlockTerm* terms = nullptr;
 };
 
 struct BlockState {
@@ -125,26 +135,26 @@ __global__ void k_block_keys(int64_t a, int64_t n, int n_owned, const int* __res
 }
 
 __device__ __forceinline__ double uncoupled_value(const float* __restrict__ row, int e, const int* __restrict__ eptr,
-                                                  const int* __restrict__ tidx, const double* __restrict__ coef) {
+                                                  const BlockTerm* __restrict__ terms) {
   // to_block: flat = sum over L of C_L^T c_L, each product summed over r
   // from zero, then added to the running total in L order
   double tot = 0.0, acc = 0.0;
   const int q0 = eptr[e], q1 = eptr[e + 1];
   for (int q = q0; q < q1; ++q) {
-    const uint32_t t = (uint32_t)tidx[q];
-    if ((t & kSegStart) && q > q0) {
+    const BlockTerm t = terms[q];
+    if ((t.idx & kSegStart) && q > q0) {
       tot = __dadd_rn(tot, acc);
       acc = 0.0;
     }
-    acc = __dadd_rn(acc, __dmul_rn(coef[q], (double)row[t & ~kSegStart]));
+    acc = __dadd_rn(acc, __dmul_rn(t.c, (double)row[t.idx & ~kSegStart]));
   }
   return __dadd_rn(tot, acc);
 }
 
 // Values of items [a, a + n) written contiguously from out[0] (= the value
-// offset of item a).  One CTA per tile of kTileItems items; the threads walk
-// the tile's values in order (coalesced stores) and find their item by a
-// binary search over the tile's offsets in shared memory.
+// offset of item a).  One CTA per tile of kTileItems items: the tile's
+// value -> item map is built in shared memory (one byte per value), then the
+// threads walk the tile's values in order (coalesced stores).
 template <bool COUPLED, typename VT>
 __global__ void __launch_bounds__(256) k_block_values(int64_t a, int64_t n, int n_owned, const float* __restrict__ node_out,
                                                       const float* __restrict__ edge_out, int out_len,
@@ -152,51 +162,58 @@ __global__ void __launch_bounds__(256) k_block_values(int64_t a, int64_t n, int 
                                                       const int* __restrict__ dst_row, int S,
                                                       const int64_t* __restrict__ off, const int* __restrict__ cols,
                                                       const int* __restrict__ ptr0, const int* __restrict__ eptr,
-                                                      const int* __restrict__ tidx, const double* __restrict__ coef,
-                                                      int symmetrize, VT* __restrict__ out) {
+                                                      const BlockTerm* __restrict__ terms, int symmetrize,
+                                                      VT* __restrict__ out) {
+  extern __shared__ uint8_t s_item[];  // kTileItems * max_elem bytes
   __shared__ int64_t s_off[kTileItems + 1];
-  __shared__ int s_pair[kTileItems];
+  __shared__ int s_base[kTileItems];  // ptr0 of the item's species pair
+  __shared__ int s_cols[kTileItems];
+  __shared__ const float* s_row[kTileItems];
   const int64_t t0 = a + (int64_t)blockIdx.x * kTileItems;
   const int64_t left = a + n - t0;
   const int nt = left < kTileItems ? (int)left : kTileItems;
   if (nt <= 0) return;
   for (int i = threadIdx.x; i <= nt; i += blockDim.x) {
     s_off[i] = off[t0 + i];
-    if (i < nt) s_pair[i] = item_pair(t0 + i, n_owned, row_slot, src_row, dst_row, S);
+    if (i < nt) {
+      const int64_t it = t0 + i;
+      const int p = item_pair(it, n_owned, row_slot, src_row, dst_row, S);
+      s_base[i] = ptr0[p];
+      s_cols[i] = cols[p];
+      s_row[i] = it < n_owned ? node_out + it * out_len : edge_out + (it - n_owned) * out_len;
+    }
   }
   __syncthreads();
-  const int64_t base = off[a];
-  const int64_t v0 = s_off[0], v1 = s_off[nt];
-  for (int64_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-    int lo = 0, hi = nt - 1;  // last item with s_off[item] <= v
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= v) lo = mid;
-      else hi = mid - 1;
-    }
-    const int64_t it = t0 + lo;
-    const int p = s_pair[lo];
-    const int j = int(v - s_off[lo]);
-    const float* row = it < n_owned ? node_out + it * out_len : edge_out + (it - n_owned) * out_len;
+  const int64_t v0 = s_off[0];
+  const int nv = (int)(s_off[nt] - v0);
+  for (int i = threadIdx.x >> 5; i < nt; i += blockDim.x >> 5)
+    for (int j = (int)(s_off[i] - v0) + (threadIdx.x & 31); j < (int)(s_off[i + 1] - v0); j += 32) s_item[j] = (uint8_t)i;
+  __syncthreads();
+  VT* o = out + (v0 - off[a]);
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    const int i = s_item[v];
+    const int j = v - (int)(s_off[i] - v0);
+    const float* row = s_row[i];
+    const int e = s_base[i] + j;
     double val;
     if (COUPLED) {
-      val = (double)row[(uint32_t)tidx[eptr[ptr0[p] + j]] & ~kSegStart];
+      val = (double)row[terms[e].idx & ~kSegStart];  // one term per element: eptr[e] == e
     } else {
-      val = uncoupled_value(row, ptr0[p] + j, eptr, tidx, coef);
-      if (symmetrize && it < n_owned) {  // block_matrix.cpp:84-85: 0.5 (ub + ub^T) on (i, i, 0)
-        const int nc = cols[p], r = j / nc, c = j % nc;
-        if (r != c) val = __dmul_rn(0.5, __dadd_rn(val, uncoupled_value(row, ptr0[p] + c * nc + r, eptr, tidx, coef)));
+      val = uncoupled_value(row, e, eptr, terms);
+      if (symmetrize && t0 + i < n_owned) {  // block_matrix.cpp:84-85: 0.5 (ub + ub^T) on (i, i, 0)
+        const int nc = s_cols[i], r = j / nc, c = j % nc;
+        if (r != c) val = __dmul_rn(0.5, __dadd_rn(val, uncoupled_value(row, s_base[i] + c * nc + r, eptr, terms)));
       }
     }
-    out[v - base] = (VT)val;
+    o[v] = (VT)val;
   }
 }
 
 BlockTables* build_tables(const esg_model* M, bool coupled, cudaStream_t st) {
   const auto& sl = M->species_list;
   const int S = (int)sl.size();
-  std::vector<int> nelem(S * S), rows(S * S), cols(S * S), ptr0(S * S), eptr{0}, tidx;
-  std::vector<double> coef;
+  std::vector<int> nelem(S * S), rows(S * S), cols(S * S), ptr0(S * S), eptr{0};
+  std::vector<BlockTerm> tl_all;
   std::map<std::array<int, 3>, std::vector<double>> cg;
   int max_elem = 1;
   for (int sa = 0; sa < S; ++sa)
@@ -221,9 +238,15 @@ BlockTables* build_tables(const esg_model* M, bool coupled, cudaStream_t st) {
             auto key = std::array<int, 3>{la, lb, L};
             if (!cg.count(key)) cg[key] = coupling_matrix(la, lb, L);
             const auto& C = cg[key];
-            for (int q = 0; q < da * db; ++q)
-              for (int r = 0; r < 2 * L + 1; ++r)
-                el(q).push_back({(uint32_t)(seg + r) | (r == 0 ? kSegStart : 0u), C[(size_t)r * da * db + q]});
+            for (int q = 0; q < da * db; ++q) {
+              bool first = true;
+              for (int r = 0; r < 2 * L + 1; ++r) {
+                const double c = C[(size_t)r * da * db + q];
+                if (c == 0.0) continue;
+                el(q).push_back({(uint32_t)(seg + r) | (first ? kSegStart : 0u), c});
+                first = false;
+              }
+            }
           }
         }
       nelem[p] = na * nb;
@@ -232,11 +255,8 @@ BlockTables* build_tables(const esg_model* M, bool coupled, cudaStream_t st) {
       ptr0[p] = (int)eptr.size() - 1;
       max_elem = std::max(max_elem, na * nb);
       for (const auto& tl : terms) {
-        for (const auto& t : tl) {
-          tidx.push_back((int)t.first);
-          coef.push_back(t.second);
-        }
-        eptr.push_back((int)tidx.size());
+        for (const auto& t : tl) tl_all.push_back({t.second, t.first, 0u});
+        eptr.push_back((int)tl_all.size());
       }
     }
   auto* T = new BlockTables;
@@ -247,16 +267,14 @@ BlockTables* build_tables(const esg_model* M, bool coupled, cudaStream_t st) {
   T->cols = upload(cols, st);
   T->ptr0 = upload(ptr0, st);
   T->eptr = upload(eptr, st);
-  T->tidx = upload(tidx, st);
-  T->coef = upload(coef, st);
+  T->terms = upload(tl_all, st);
   ESG_CUDA(cudaStreamSynchronize(st));
   return T;
 }
 
 void free_tables(BlockTables* T) {
   if (!T) return;
-  for (void* p : {(void*)T->nelem, (void*)T->rows, (void*)T->cols, (void*)T->ptr0, (void*)T->eptr, (void*)T->tidx,
-                  (void*)T->coef})
+  for (void* p : {(void*)T->nelem, (void*)T->rows, (void*)T->cols, (void*)T->ptr0, (void*)T->eptr, (void*)T->terms})
     free_ptr(p);
   delete T;
 }
@@ -319,12 +337,14 @@ void launch_values(esg_model* M, BlockState& B, int basis, bool sym, int vb, int
   if (n <= 0) return;
   const BlockTables& T = *B.bt[basis];
   const unsigned grid = (unsigned)((n + kTileItems - 1) / kTileItems);
+  const size_t smem = (size_t)kTileItems * T.max_elem;
+  if (smem > 48 * 1024) usage("block too large for the export kernel (max 768 elements per block)");
   cudaStream_t st = M->ctx->stream;
   const int ol = M->heads.out_len;
 #define ESG_BV(C, VT)                                                                                              \
-  k_block_values<C, VT><<<grid, 256, 0, st>>>(a, n, D->n_owned, D->node_out, D->edge_out, ol, D->row_slot,         \
-                                              D->src_row, D->dst_row, T.S, B.off, T.cols, T.ptr0, T.eptr, T.tidx, \
-                                              T.coef, sym ? 1 : 0, (VT*)out)
+  k_block_values<C, VT><<<grid, 256, smem, st>>>(a, n, D->n_owned, D->node_out, D->edge_out, ol, D->row_slot,         \
+                                              D->src_row, D->dst_row, T.S, B.off, T.cols, T.ptr0, T.eptr, T.terms, \
+                                              sym ? 1 : 0, (VT*)out)
   if (basis == 0) {
     if (vb == 8) ESG_BV(true, double);
     else ESG_BV(true, float);

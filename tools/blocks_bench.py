@@ -61,10 +61,28 @@ def main():
     del dk, dv
     torch.cuda.empty_cache()
 
+    # the pipeline's ceiling: pinned device -> host bandwidth (1 GiB, best of 3)
+    src = torch.empty(1 << 30, dtype=torch.uint8, device="cuda:0")
+    dst = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    d2h = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        d2h.append((1 << 30) / e0.elapsed_time(e1) / 1e6)
+    d2h_gbs = max(d2h)
+    del src, dst
+
     file_bytes = 64 + nb * 24 + nv * 8
-    t = time.perf_counter()
-    net.write_block_shard("/dev/null", esg.BLOCKS_UNCOUPLED)
-    null_s = time.perf_counter() - t
+    net.write_block_shard("/dev/null", esg.BLOCKS_UNCOUPLED)  # warm-up: pinned staging buffers
+    null_s = []
+    for _ in range(3):
+        t = time.perf_counter()
+        net.write_block_shard("/dev/null", esg.BLOCKS_UNCOUPLED)
+        null_s.append(time.perf_counter() - t)
+    null_s = min(null_s)
     path = os.path.join(args.dir, "esg_blocks_bench.blk")
     disk_s = None
     try:
@@ -100,7 +118,8 @@ def main():
         "key_kernel": {"ms": keys_ms, "bytes": k_bytes, "gbs": k_bytes / keys_ms / 1e6},
         "shard": {"bytes": file_bytes, "devnull_s": null_s, "devnull_gbs": file_bytes / null_s / 1e9,
                   "disk_s": disk_s, "disk_gbs": file_bytes / disk_s / 1e9 if disk_s else None,
-                  "dir": args.dir, "items_per_s_devnull": nb / null_s},
+                  "dir": args.dir, "items_per_s_devnull": nb / null_s, "pinned_d2h_gbs": d2h_gbs,
+                  "frac_d2h": file_bytes / null_s / 1e9 / d2h_gbs},
         "cpu_baseline": {"items": int(ni), "s": cpu_s, "items_per_s": ni / cpu_s, "cores": 1,
                          "text_bytes": text_bytes, "kind": "port",
                          "what": "coupled map + text + blocks_to_uncoupled + text (model_run.cpp:141-153)"},
