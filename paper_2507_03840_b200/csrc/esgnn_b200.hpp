@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <stdexcept>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -256,6 +257,24 @@ class Network {
     check(esg_blocks_uncoupled(h_, out.data()));
     return out;
   }
+  // ---- block export (model_run.cpp:141-153 output stage)
+  void write_block_shard(const std::string& path, int basis = ESG_BLOCKS_UNCOUPLED, bool symmetrize = false,
+                         int value_bytes = 8) {
+    check(esg_blocks_write_shard(h_, path.c_str(), basis, symmetrize ? 1 : 0, value_bytes));
+  }
+  void write_blocks_text(const std::string& path, int basis = ESG_BLOCKS_UNCOUPLED, bool symmetrize = false) {
+    check(esg_blocks_write_text(h_, path.c_str(), basis, symmetrize ? 1 : 0));
+  }
+  // ---- checkpoints (checkpoint.h:37-92, plus the optimizer state)
+  void save_checkpoint(const std::string& path, const esg_adam* opt = nullptr, const std::string& config = "") const {
+    check(esg_checkpoint_save(h_, opt, config.c_str(), path.c_str()));
+  }
+  std::string load_checkpoint(const std::string& path, esg_adam* opt = nullptr) {
+    std::string cfg(1 << 16, '\0');
+    check(esg_checkpoint_load(h_, opt, path.c_str(), cfg.data(), (int64_t)cfg.size()));
+    cfg.resize(std::strlen(cfg.c_str()));
+    return cfg;
+  }
 
  private:
   esg_model* h_ = nullptr;
@@ -275,6 +294,14 @@ class Adam {
  private:
   esg_adam* h_ = nullptr;
 };
+
+// model_run.cpp:103-120 gather_blocks + write_blocks_file on rank 0, from the
+// ranks' shard files (no device needed)
+inline void merge_block_shards(const std::vector<std::string>& shards, const std::string& out_path) {
+  std::vector<const char*> p;
+  for (const auto& s : shards) p.push_back(s.c_str());
+  check(esg_blocks_merge_text(p.data(), (int)p.size(), out_path.c_str()));
+}
 
 inline std::vector<double> coupling_matrix(int la, int lb, int L) {
   std::vector<double> c((size_t)(2 * L + 1) * (2 * la + 1) * (2 * lb + 1));

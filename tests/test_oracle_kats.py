@@ -270,6 +270,51 @@ def test_coupling_orthonormal_and_intertwining():
                 assert np.abs(C @ kr - D[L] @ C).max() < 1e-10
 
 
+def _racah_cg(j1, m1, j2, m2, J, M):
+    """<j1 m1; j2 m2 | J M> by Racah's closed form (Condon-Shortley)."""
+    from math import factorial as f, sqrt
+    if m1 + m2 != M or abs(m1) > j1 or abs(m2) > j2 or abs(M) > J:
+        return 0.0
+    pre = sqrt((2 * J + 1) * f(J + j1 - j2) * f(J - j1 + j2) * f(j1 + j2 - J) / f(j1 + j2 + J + 1))
+    pre *= sqrt(f(J + M) * f(J - M) * f(j1 - m1) * f(j1 + m1) * f(j2 - m2) * f(j2 + m2))
+    s = 0.0
+    for k in range(j1 + j2 - J + 1):
+        d = (j1 + j2 - J - k, j1 - m1 - k, j2 + m2 - k, J - j2 + m1 + k, J - j1 - m2 + k)
+        if min(d) < 0:
+            continue
+        s += (-1) ** k / (f(k) * f(d[0]) * f(d[1]) * f(d[2]) * f(d[3]) * f(d[4]))
+    return pre * s
+
+
+def _real_basis(l):
+    d = 2 * l + 1
+    b = np.zeros((d, d), complex)
+    b[l, l] = 1.0
+    s = np.sqrt(0.5)
+    for m in range(1, l + 1):
+        ph = -1.0 if m % 2 else 1.0
+        b[l + m, l - m], b[l + m, l + m] = s, ph * s
+        b[l - m, l - m], b[l - m, l + m] = 1j * s, -1j * ph * s
+    return b
+
+
+def test_coupling_matches_racah_closed_form():
+    """An independent construction of clebsch_gordan.cpp's tables: Racah's
+    closed form in the complex basis, the same real-basis change and phase
+    convention, against the oracle's lowering-operator construction (which the
+    product's tables equal bit for bit, tests/test_blocks_cpu.py)."""
+    for la in range(5):
+        for lb in range(5):
+            ba, bb = _real_basis(la), _real_basis(lb)
+            kron = np.kron(ba, bb)
+            for L in range(abs(la - lb), la + lb + 1):
+                cg = np.array([[_racah_cg(la, ma, lb, mb, L, M) for ma in range(-la, la + 1) for mb in range(-lb, lb + 1)]
+                               for M in range(-L, L + 1)])
+                u = _real_basis(L) @ cg @ kron.conj().T
+                want = u.imag if (la + lb - L) % 2 else u.real
+                assert np.abs(want - O.coupling(la, lb, L)).max() < 1e-12, (la, lb, L)
+
+
 # --------------------------------------------------------------- model
 SP_BASIS = {1: [0, 1], 8: [0, 1]}
 
