@@ -95,6 +95,31 @@ int esg_graph_offsets(const esg_graph* g, int64_t* dst_off /* N+1 */);
 int esg_lownn_partition(int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
                         const int32_t* in_degree, int depth, double r_cut, int32_t* node_to_part);
 
+/* ---- partition metrics (partition.h:31-62, metrics.cpp:49-166)
+ * compute_metrics on the device from the graph CSR and an assignment
+ * (n_parts <= 4096).  parts (n_parts entries) and volume (n_parts x n_parts,
+ * volume[from * n_parts + to] = distinct source nodes part `from` packs for
+ * part `to` per exchange, write_dot's edge weights) may be NULL. */
+typedef struct esg_part_stats {
+  int64_t nodes, edges, recv_volume; /* PartStats (partition.h:31-36) */
+  int32_t neighbors, pad;
+} esg_part_stats;
+typedef struct esg_metrics {
+  double node_imbalance, edge_imbalance, mean_neighbors; /* Metrics (partition.h:38-46) */
+  int64_t total_recv, cut_edges;
+  int32_t max_neighbors, n_parts;
+} esg_metrics;
+int esg_partition_metrics(const esg_graph* g, const int32_t* node_to_part, int n_parts, esg_metrics* m,
+                          esg_part_stats* parts, int64_t* volume);
+/* metrics_json (nlohmann dump(2) format) and write_dot text; *len receives
+ * the text length, out (capacity cap, NUL-terminated) may be NULL to size. */
+int esg_metrics_json(const esg_metrics* m, const esg_part_stats* parts, char* out, int64_t cap, int64_t* len);
+int esg_partition_dot(const int64_t* volume, const esg_part_stats* parts, int n_parts, char* out, int64_t cap,
+                      int64_t* len);
+/* write_assignment_file / read_assignment_file ("node part" lines). */
+int esg_assignment_write(const char* path, const int32_t* node_to_part, int64_t n);
+int esg_assignment_read(const char* path, int32_t* node_to_part, int64_t cap, int64_t* n, int* n_parts);
+
 /* ---- runtime::build_comm_plan (comm_plan.h:35, comm_plan.cpp:11-106) -- */
 int esg_plan_build(const esg_graph* g, const int32_t* species, const int32_t* node_to_part,
                    int n_parts, int rank, esg_plan** out);

@@ -1690,6 +1690,95 @@ void oracle_graph_export(int* src, int* dst, int* shift, double* disp, double* d
   }
 }
 
+// metrics.cpp:49-88 compute_metrics over an edge list (src, dst) and an
+// assignment.  parts4: per part nodes, edges, neighbors, recv_volume; dsum:
+// node_imbalance, edge_imbalance, mean_neighbors; isum: max_neighbors,
+// total_recv, cut_edges.
+int oracle_compute_metrics(int n, int64_t E, const int32_t* src, const int32_t* dst, const int32_t* part, int P,
+                           int64_t* parts4, double* dsum, int64_t* isum) {
+  GUARD({
+    for (int i = 0; i < n; ++i)
+      if (part[i] < 0 || part[i] >= P) throw std::runtime_error("part id out of range");
+    std::vector<std::array<long, 4>> st(P, {0, 0, 0, 0});
+    long cut = 0, total_recv = 0;
+    for (int i = 0; i < n; ++i) ++st[part[i]][0];
+    for (int64_t k = 0; k < E; ++k) {
+      ++st[part[dst[k]]][1];
+      if (part[src[k]] != part[dst[k]]) ++cut;
+    }
+    // cross_pairs (metrics.cpp:36-45): distinct (receiving part, source node)
+    std::vector<std::pair<int, int>> pairs;
+    for (int64_t k = 0; k < E; ++k) {
+      const int q = part[dst[k]];
+      if (part[src[k]] != q) pairs.emplace_back(q, src[k]);
+    }
+    std::sort(pairs.begin(), pairs.end());
+    pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
+    std::vector<std::pair<int, int>> pp;
+    for (const auto& [q, sn] : pairs) {
+      ++st[q][3];
+      pp.emplace_back(q, part[sn]);
+      ++total_recv;
+    }
+    std::sort(pp.begin(), pp.end());
+    pp.erase(std::unique(pp.begin(), pp.end()), pp.end());
+    for (const auto& x : pp) ++st[x.first][2];
+    long nbr_sum = 0, max_nbr = 0;
+    for (const auto& x : st) {
+      nbr_sum += x[2];
+      max_nbr = std::max(max_nbr, x[2]);
+    }
+    auto imbalance = [](const std::vector<long>& c) {
+      long total = 0, top = 0;
+      for (long v : c) {
+        total += v;
+        top = std::max(top, v);
+      }
+      if (total == 0) return 1.0;
+      return double(top) * double(c.size()) / double(total);
+    };
+    std::vector<long> nc, ec;
+    for (int q = 0; q < P; ++q) {
+      for (int c = 0; c < 4; ++c) parts4[4 * q + c] = st[q][c];
+      nc.push_back(st[q][0]);
+      ec.push_back(st[q][1]);
+    }
+    dsum[0] = imbalance(nc);
+    dsum[1] = imbalance(ec);
+    dsum[2] = P > 0 ? double(nbr_sum) / double(P) : 0.0;
+    isum[0] = max_nbr;
+    isum[1] = total_recv;
+    isum[2] = cut;
+  })
+}
+
+// metrics.cpp:141-166 write_dot
+int oracle_write_dot(int n, int64_t E, const int32_t* src, const int32_t* dst, const int32_t* part, int P,
+                     const char* path) {
+  GUARD({
+    std::vector<std::pair<std::pair<int, int>, int>> links;
+    for (int64_t k = 0; k < E; ++k) {
+      const int q = part[dst[k]], f = part[src[k]];
+      if (f != q) links.push_back({{f, q}, src[k]});
+    }
+    std::sort(links.begin(), links.end());
+    links.erase(std::unique(links.begin(), links.end()), links.end());
+    std::ofstream out(path);
+    out << "digraph parts {\n";
+    std::vector<long> nodes_per(P, 0);
+    for (int i = 0; i < n; ++i) ++nodes_per[part[i]];
+    for (int q = 0; q < P; ++q) out << "  p" << q << " [label=\"part " << q << "\\n" << nodes_per[q] << " nodes\"];\n";
+    for (size_t k = 0; k < links.size();) {
+      size_t j = k;
+      while (j < links.size() && links[j].first == links[k].first) ++j;
+      out << "  p" << links[k].first.first << " -> p" << links[k].first.second << " [label=\"" << (j - k)
+          << "\"];\n";
+      k = j;
+    }
+    out << "}\n";
+  })
+}
+
 int oracle_lownn(int n, const double* pos, const double* cell, const uint8_t* pbc, const int* in_deg,
                  int depth, double r_cut, int* part_out) {
   GUARD({

@@ -27,6 +27,12 @@ void model_outputs(const esg_model* M, const float** no, const float** eo, const
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
 void model_copy_features(const esg_model* M, float* nodes, float* edges);
 void model_prepared_info(const esg_model* M, int64_t info[3]);
+void partition_metrics_gpu(const esg_graph* g, const int32_t* part, int P, esg_metrics* m, esg_part_stats* parts,
+                           int64_t* vol);
+std::string metrics_json(const esg_metrics& m, const esg_part_stats* parts);
+std::string partition_dot(const int64_t* vol, const esg_part_stats* parts, int P);
+void write_assignment(const std::string& path, const int32_t* part, int64_t n);
+std::vector<int32_t> read_assignment(const std::string& path, int* n_parts);
 void blocks_count(esg_model* M, int64_t* n_blocks, int64_t* n_values);
 void blocks_export(esg_model* M, int basis, bool sym, BlockRec* keys, double* values);
 void blocks_export_device(esg_model* M, int basis, bool sym, int vb, void* d_keys, void* d_values, float* kernel_ms);
@@ -680,6 +686,68 @@ esg_model* device_model(esg_model* m) {
   return m;
 }
 }  // namespace
+
+namespace {
+void put_text(const std::string& t, char* out, int64_t cap, int64_t* len) {
+  if (len) *len = (int64_t)t.size();
+  if (out) {
+    if (cap < (int64_t)t.size() + 1) usage("output buffer too small");
+    std::memcpy(out, t.c_str(), t.size() + 1);
+  }
+}
+}  // namespace
+
+int esg_partition_metrics(const esg_graph* g, const int32_t* node_to_part, int n_parts, esg_metrics* m,
+                          esg_part_stats* parts, int64_t* volume) {
+  ESG_API_BEGIN
+  NEED(g, "graph");
+  NEED(node_to_part, "node_to_part");
+  NEED(m, "metrics");
+  ESG_CUDA(cudaSetDevice(g->ctx->device));
+  partition_metrics_gpu(g, node_to_part, n_parts, m, parts, volume);
+  ESG_API_END
+}
+
+int esg_metrics_json(const esg_metrics* m, const esg_part_stats* parts, char* out, int64_t cap, int64_t* len) {
+  ESG_API_BEGIN
+  NEED(m, "metrics");
+  if (m->n_parts > 0) NEED(parts, "parts");
+  put_text(metrics_json(*m, parts), out, cap, len);
+  ESG_API_END
+}
+
+int esg_partition_dot(const int64_t* volume, const esg_part_stats* parts, int n_parts, char* out, int64_t cap,
+                      int64_t* len) {
+  ESG_API_BEGIN
+  NEED(volume, "volume");
+  NEED(parts, "parts");
+  if (n_parts < 1) usage("n_parts must be positive");
+  put_text(partition_dot(volume, parts, n_parts), out, cap, len);
+  ESG_API_END
+}
+
+int esg_assignment_write(const char* path, const int32_t* node_to_part, int64_t n) {
+  ESG_API_BEGIN
+  NEED(path, "path");
+  if (n > 0) NEED(node_to_part, "node_to_part");
+  write_assignment(path, node_to_part, n);
+  ESG_API_END
+}
+
+int esg_assignment_read(const char* path, int32_t* node_to_part, int64_t cap, int64_t* n, int* n_parts) {
+  ESG_API_BEGIN
+  NEED(path, "path");
+  NEED(n, "n");
+  int np = 0;
+  const auto a = read_assignment(path, &np);
+  *n = (int64_t)a.size();
+  if (n_parts) *n_parts = np;
+  if (node_to_part) {
+    if (cap < (int64_t)a.size()) usage("node_to_part buffer too small");
+    std::copy(a.begin(), a.end(), node_to_part);
+  }
+  ESG_API_END
+}
 
 int esg_blocks_count(esg_model* m, int64_t* n_blocks, int64_t* n_values) {
   ESG_API_BEGIN

@@ -332,6 +332,94 @@ class Timing:
     gpu_launches: int
 
 
+# ------------------------------------------------------- partition metrics
+class _PartStats(C.Structure):
+    _fields_ = [("nodes", C.c_int64), ("edges", C.c_int64), ("recv_volume", C.c_int64), ("neighbors", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class _Metrics(C.Structure):
+    _fields_ = [("node_imbalance", C.c_double), ("edge_imbalance", C.c_double), ("mean_neighbors", C.c_double),
+                ("total_recv", C.c_int64), ("cut_edges", C.c_int64), ("max_neighbors", C.c_int32),
+                ("n_parts", C.c_int32)]
+
+
+@dataclasses.dataclass
+class Metrics:
+    """partition::Metrics (partition.h:38-46) plus write_dot's volume matrix."""
+
+    node_imbalance: float
+    edge_imbalance: float
+    mean_neighbors: float
+    max_neighbors: int
+    total_recv: int
+    cut_edges: int
+    parts: np.ndarray  # (P, 4) int64: nodes, edges, neighbors, recv_volume
+    volume: np.ndarray  # (P, P) int64, [from, to]
+    _m: object = None
+    _p: object = None
+
+    def json(self) -> str:
+        """metrics_json (nlohmann dump(2) format)."""
+        n = C.c_int64()
+        _check(lib().esg_metrics_json(C.byref(self._m), self._p, None, C.c_int64(0), C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().esg_metrics_json(C.byref(self._m), self._p, buf, C.c_int64(len(buf)), C.byref(n)))
+        return buf.value.decode()
+
+    def dot(self) -> str:
+        """write_dot text."""
+        P = len(self.parts)
+        v = np.ascontiguousarray(self.volume, np.int64)
+        n = C.c_int64()
+        _check(lib().esg_partition_dot(_p(v), self._p, C.c_int(P), None, C.c_int64(0), C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().esg_partition_dot(_p(v), self._p, C.c_int(P), buf, C.c_int64(len(buf)), C.byref(n)))
+        return buf.value.decode()
+
+
+def _metrics_from(m, ps, vol):
+    parts = np.array([[p.nodes, p.edges, p.neighbors, p.recv_volume] for p in ps], np.int64)
+    return Metrics(m.node_imbalance, m.edge_imbalance, m.mean_neighbors, m.max_neighbors, m.total_recv,
+                   m.cut_edges, parts, vol, m, ps)
+
+
+def partition_metrics(g: "Graph", node_to_part: np.ndarray, n_parts: int) -> Metrics:
+    """partition::compute_metrics (metrics.cpp:49-88) on the device."""
+    part = np.ascontiguousarray(node_to_part, np.int32)
+    if part.size != g.n_nodes:
+        raise UsageError(f"assignment covers {part.size} nodes, graph has {g.n_nodes}")
+    m = _Metrics()
+    ps = (_PartStats * n_parts)()
+    vol = np.zeros((n_parts, n_parts), np.int64)
+    _check(lib().esg_partition_metrics(g._h, _p(part), C.c_int(n_parts), C.byref(m), ps, _p(vol)))
+    return _metrics_from(m, ps, vol)
+
+
+def metrics_from_arrays(d, i, parts, volume) -> Metrics:
+    """A Metrics value from plain numbers (for the host-side formatters)."""
+    P = len(parts)
+    m = _Metrics(float(d[0]), float(d[1]), float(d[2]), int(i[1]), int(i[2]), int(i[0]), P)
+    ps = (_PartStats * P)()
+    for q in range(P):
+        ps[q].nodes, ps[q].edges, ps[q].neighbors, ps[q].recv_volume = (int(x) for x in parts[q])
+    return _metrics_from(m, ps, np.ascontiguousarray(volume, np.int64))
+
+
+def write_assignment(path: str, node_to_part: np.ndarray) -> None:
+    part = np.ascontiguousarray(node_to_part, np.int32)
+    _check(lib().esg_assignment_write(os.fsencode(path), _p(part), C.c_int64(part.size)))
+
+
+def read_assignment(path: str):
+    """(node_to_part, n_parts) from a write_assignment file."""
+    n, np_ = C.c_int64(), C.c_int()
+    _check(lib().esg_assignment_read(os.fsencode(path), None, C.c_int64(0), C.byref(n), C.byref(np_)))
+    out = np.zeros(n.value, np.int32)
+    _check(lib().esg_assignment_read(os.fsencode(path), _p(out), C.c_int64(out.size), C.byref(n), C.byref(np_)))
+    return out, np_.value
+
+
 # ------------------------------------------------------------- block export
 BLOCKS_COUPLED, BLOCKS_UNCOUPLED = 0, 1
 BLOCK_KEY = np.dtype([("i", "<i4"), ("j", "<i4"), ("ix", "<i4"), ("iy", "<i4"), ("iz", "<i4"),

@@ -110,6 +110,87 @@ def lownn(pos, cell, pbc, deg, depth, r_cut):
     return out
 
 
+def compute_metrics(n, src, dst, part, P):
+    """metrics.cpp:49-88: (parts (P, 4) nodes/edges/neighbors/recv_volume,
+    (node_imbalance, edge_imbalance, mean_neighbors), (max_neighbors,
+    total_recv, cut_edges))."""
+    parts = np.zeros((P, 4), np.int64)
+    d = np.zeros(3)
+    i = np.zeros(3, np.int64)
+    _ok(lib().oracle_compute_metrics(C.c_int(n), C.c_int64(len(src)), _p(np.ascontiguousarray(src, np.int32)),
+                                     _p(np.ascontiguousarray(dst, np.int32)), _p(np.ascontiguousarray(part, np.int32)),
+                                     C.c_int(P), _p(parts), _p(d), _p(i)))
+    return parts, d, i
+
+
+def write_dot(n, src, dst, part, P, path):
+    """metrics.cpp:141-166."""
+    _ok(lib().oracle_write_dot(C.c_int(n), C.c_int64(len(src)), _p(np.ascontiguousarray(src, np.int32)),
+                               _p(np.ascontiguousarray(dst, np.int32)), _p(np.ascontiguousarray(part, np.int32)),
+                               C.c_int(P), os.fsencode(str(path))))
+
+
+def nlohmann_double(v):
+    """nlohmann::json's double output (dtoa_impl::to_chars + format_buffer,
+    min_exp -4, max_exp 15), restated; shortest round-trip digits from repr."""
+    import math
+    if not math.isfinite(v):
+        return "null"
+    sign = "-" if math.copysign(1.0, v) < 0 else ""
+    v = abs(v)
+    if v == 0.0:
+        return sign + "0.0"
+    r = repr(v)
+    if "e" in r:
+        m, e = r.split("e")
+        digits, n = m.replace(".", ""), int(e) + 1
+    else:
+        ip, fp = r.split(".")
+        if ip != "0":
+            digits, n = (ip + fp).rstrip("0") or "0", len(ip)
+        else:
+            z = len(fp) - len(fp.lstrip("0"))
+            digits, n = fp.lstrip("0"), -z
+    digits = digits.lstrip("0") or "0"
+    k = len(digits)
+    if k <= n <= 15:
+        return sign + digits + "0" * (n - k) + ".0"
+    if 0 < n <= 15:
+        return sign + digits[:n] + "." + digits[n:]
+    if -4 < n <= 0:
+        return sign + "0." + "0" * (-n) + digits
+    m = digits[0] + ("." + digits[1:] if k > 1 else "")
+    e = n - 1
+    return sign + m + "e" + ("-" if e < 0 else "+") + f"{abs(e):02d}"
+
+
+def nlohmann_dump2(obj, indent=0):
+    """nlohmann::json::dump(2): std::map key order, ': ' and ',\n'."""
+    pad, inner = " " * indent, " " * (indent + 2)
+    if isinstance(obj, dict):
+        if not obj:
+            return "{}"
+        items = [f'{inner}"{k}": {nlohmann_dump2(obj[k], indent + 2)}' for k in sorted(obj)]
+        return "{\n" + ",\n".join(items) + "\n" + pad + "}"
+    if isinstance(obj, list):
+        if not obj:
+            return "[]"
+        return "[\n" + ",\n".join(inner + nlohmann_dump2(x, indent + 2) for x in obj) + "\n" + pad + "]"
+    if isinstance(obj, float):
+        return nlohmann_double(obj)
+    return str(int(obj))
+
+
+def metrics_json(parts, d, i):
+    """metrics.cpp:124-139 metrics_json."""
+    return nlohmann_dump2({
+        "n_parts": len(parts), "node_imbalance": float(d[0]), "edge_imbalance": float(d[1]),
+        "mean_neighbors": float(d[2]), "max_neighbors": int(i[0]), "total_recv_volume": int(i[1]),
+        "cut_edges": int(i[2]),
+        "parts": [{"nodes": int(p[0]), "edges": int(p[1]), "neighbors": int(p[2]), "recv_volume": int(p[3])}
+                  for p in parts]})
+
+
 def comm_plan(n_nodes, src, dst, part, n_parts, rank):
     E = len(src)
     hdr = np.zeros(4, np.int32)

@@ -1,0 +1,59 @@
+"""Partition metrics on the GPU against the oracle's
+compute_metrics / write_dot: every count, the doubles, the JSON and the DOT
+text must be identical."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2507_03840_b200 import esg
+
+pytestmark = pytest.mark.gpu
+
+
+def check(gpu_ctx, s, r, part, P, tmp_path):
+    g = esg.build_graph(gpu_ctx, s, r)
+    gx = g.export()
+    m = esg.partition_metrics(g, part, P)
+    parts, d, i = O.compute_metrics(s.n_atoms, gx["src"], gx["dst"], part, P)
+    assert np.array_equal(m.parts, parts)
+    assert (m.node_imbalance, m.edge_imbalance, m.mean_neighbors) == tuple(d)
+    assert (m.max_neighbors, m.total_recv, m.cut_edges) == tuple(i)
+    assert m.json() == O.metrics_json(parts, d, i)
+    O.write_dot(s.n_atoms, gx["src"], gx["dst"], part, P, tmp_path / "ref.dot")
+    assert m.dot() == (tmp_path / "ref.dot").read_text()
+    return m
+
+
+@pytest.mark.parametrize("depth", [0, 1, 2, 3])
+def test_lownn_metrics_c2(gpu_ctx, tmp_path, depth):
+    s, r, _, _ = esg.config_structure("C2")
+    g = esg.build_graph(gpu_ctx, s, r)
+    part = esg.lownn_partition(s, g.in_degrees(), depth, r)
+    m = check(gpu_ctx, s, r, part, 1 << depth, tmp_path)
+    if depth == 0:
+        assert m.cut_edges == 0 and m.total_recv == 0 and m.node_imbalance == 1.0
+
+
+def test_arbitrary_assignments(gpu_ctx, tmp_path):
+    s = esg.make_jittered_lattice(300, 2.2, 0.4, [72, 8, 8], 9)
+    rng = np.random.default_rng(4)
+    check(gpu_ctx, s, 5.0, rng.integers(0, 5, s.n_atoms).astype(np.int32), 5, tmp_path)  # not a power of two
+    check(gpu_ctx, s, 5.0, rng.integers(0, 2, s.n_atoms).astype(np.int32), 4, tmp_path)  # empty parts
+    check(gpu_ctx, s, 5.0, np.arange(s.n_atoms, dtype=np.int32) % 97, 97, tmp_path)  # many parts
+
+
+def test_triangle_kat(gpu_ctx, tmp_path):
+    """test_partition.cpp:145-160."""
+    pos = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.5, 0.9, 0.0]])
+    s = esg.AtomicStructure(pos, np.ones(3, np.int32), np.eye(3) * 10.0, np.zeros(3, bool))
+    m = check(gpu_ctx, s, 2.0, np.arange(3, dtype=np.int32), 3, tmp_path)
+    assert (m.parts == [1, 2, 2, 2]).all() and m.total_recv == 6 and m.cut_edges == 6
+
+
+def test_metrics_errors(gpu_ctx):
+    s = esg.make_jittered_lattice(20, 2.2, 0.4, [8], 1)
+    g = esg.build_graph(gpu_ctx, s, 4.0)
+    with pytest.raises(esg.DataError):
+        esg.partition_metrics(g, np.full(20, 3, np.int32), 2)
+    with pytest.raises(esg.UsageError):
+        esg.partition_metrics(g, np.zeros(19, np.int32), 1)
