@@ -95,6 +95,22 @@ int esg_graph_offsets(const esg_graph* g, int64_t* dst_off /* N+1 */);
 int esg_lownn_partition(int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
                         const int32_t* in_degree, int depth, double r_cut, int32_t* node_to_part);
 
+/* ---- partition::mincut_partition (partition.h:26-28, mincut.cpp:183-201;
+ * SURVEY §8(f) 4): the edge-cut baseline for Low-NN comparisons (host). */
+int esg_mincut_partition(const esg_graph* g, int n_parts, uint64_t seed, int32_t* node_to_part);
+/* The same on a host dst-major CSR (dst_off[n+1], src[dst_off[n]]). */
+int esg_mincut_partition_csr(int n, const int64_t* dst_off, const int32_t* src, int n_parts, uint64_t seed,
+                             int32_t* node_to_part);
+
+/* ---- structures::read_extxyz / write_extxyz (extxyz.h:11-18, extxyz.cpp:62-147)
+ * read: pass pos == NULL to get *n_atoms only; otherwise pos (3*cap) and
+ * species (cap) must hold n_atoms entries.  cell is row-major (rows are the
+ * lattice vectors); parse errors are ESG_ERR_DATA with the line number. */
+int esg_extxyz_read(const char* path, int64_t cap, int* n_atoms, double* pos, int32_t* species, double cell[9],
+                    uint8_t pbc[3]);
+int esg_extxyz_write(const char* path, int n_atoms, const double* pos, const int32_t* species, const double cell[9],
+                     const uint8_t pbc[3]);
+
 /* ---- partition metrics (partition.h:31-62, metrics.cpp:49-166)
  * compute_metrics on the device from the graph CSR and an assignment
  * (n_parts <= 4096).  parts (n_parts entries) and volume (n_parts x n_parts,

@@ -80,6 +80,7 @@ struct MLayout {
 MLayout m_layout(int l_max);
 
 std::string element_symbol(int z);
+int atomic_number(const std::string& symbol);
 
 struct ParamEntry {
   std::string name;

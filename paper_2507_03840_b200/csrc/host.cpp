@@ -186,6 +186,13 @@ std::string element_symbol(int z) {
   return t[z];
 }
 
+// elements.cpp:32-36
+int atomic_number(const std::string& symbol) {
+  for (int z = 1; z <= 103; ++z)
+    if (element_symbol(z) == symbol) return z;
+  data("unknown element symbol: '" + symbol + "'");
+}
+
 // ------------------------------------------------------- basis / layouts
 int Basis::n_orb(int z) const {
   auto it = shells.find(z);

@@ -332,6 +332,42 @@ class Timing:
     gpu_launches: int
 
 
+# ------------------------------------------------------------ input side
+def read_extxyz(path: str) -> AtomicStructure:
+    """structures::read_extxyz_file (extxyz.cpp:62-121)."""
+    n = C.c_int()
+    cell = np.zeros(9)
+    pbc = np.zeros(3, np.uint8)
+    _check(lib().esg_extxyz_read(os.fsencode(path), C.c_int64(0), C.byref(n), None, None, _p(cell), _p(pbc)))
+    pos = np.zeros((n.value, 3))
+    sp = np.zeros(n.value, np.int32)
+    _check(lib().esg_extxyz_read(os.fsencode(path), C.c_int64(n.value), C.byref(n), _p(pos), _p(sp), _p(cell),
+                                 _p(pbc)))
+    return AtomicStructure(pos, sp, cell.reshape(3, 3), pbc.astype(bool))
+
+
+def write_extxyz(path: str, s: AtomicStructure) -> None:
+    """structures::write_extxyz_file (extxyz.cpp:125-147)."""
+    _check(lib().esg_extxyz_write(os.fsencode(path), C.c_int(s.n_atoms), _p(np.ascontiguousarray(s.positions, np.float64)),
+                                  _p(np.ascontiguousarray(s.species, np.int32)),
+                                  _p(np.ascontiguousarray(s.cell, np.float64)), _p(s._pbc8())))
+
+
+def mincut_partition(g, n_parts: int, seed: int = 1) -> np.ndarray:
+    """partition::mincut_partition (mincut.cpp:183-201): g is a Graph, or a
+    host (dst_off, src) CSR pair."""
+    if isinstance(g, tuple):
+        off = np.ascontiguousarray(g[0], np.int64)
+        src = np.ascontiguousarray(g[1], np.int32)
+        out = np.zeros(off.size - 1, np.int32)
+        _check(lib().esg_mincut_partition_csr(C.c_int(out.size), _p(off), _p(src), C.c_int(n_parts),
+                                              C.c_uint64(seed), _p(out)))
+        return out
+    out = np.zeros(g.n_nodes, np.int32)
+    _check(lib().esg_mincut_partition(g._h, C.c_int(n_parts), C.c_uint64(seed), _p(out)))
+    return out
+
+
 # ------------------------------------------------------- partition metrics
 class _PartStats(C.Structure):
     _fields_ = [("nodes", C.c_int64), ("edges", C.c_int64), ("recv_volume", C.c_int64), ("neighbors", C.c_int32),

@@ -499,3 +499,221 @@ class Adam:
                 self.lr = max(self.min_lr, self.lr * self.factor)
                 self.stale = 0
         return out
+
+
+# ------------------------------------------------------------ input side
+SYMBOLS = ("", "H", "He", "Li", "Be", "B", "C", "N", "O", "F", "Ne", "Na", "Mg", "Al", "Si", "P", "S", "Cl", "Ar",
+           "K", "Ca", "Sc", "Ti", "V", "Cr", "Mn", "Fe", "Co", "Ni", "Cu", "Zn", "Ga", "Ge", "As", "Se", "Br",
+           "Kr", "Rb", "Sr", "Y", "Zr", "Nb", "Mo", "Tc", "Ru", "Rh", "Pd", "Ag", "Cd", "In", "Sn", "Sb", "Te",
+           "I", "Xe", "Cs", "Ba", "La", "Ce", "Pr", "Nd", "Pm", "Sm", "Eu", "Gd", "Tb", "Dy", "Ho", "Er", "Tm",
+           "Yb", "Lu", "Hf", "Ta", "W", "Re", "Os", "Ir", "Pt", "Au", "Hg", "Tl", "Pb", "Bi", "Po", "At", "Rn",
+           "Fr", "Ra", "Ac", "Th", "Pa", "U", "Np", "Pu", "Am", "Cm", "Bk", "Cf", "Es", "Fm", "Md", "No",
+           "Lr")  # elements.cpp:15-23
+
+
+class ParseError(ValueError):
+    pass
+
+
+def read_extxyz_text(text):
+    """extxyz.cpp:16-121 read_extxyz: (pos (n,3), species, cell (3,3), pbc)."""
+    lines = text.split("\n")
+    if text.endswith("\n"):
+        lines = lines[:-1]
+    if not lines:
+        raise ParseError("empty input")
+    try:
+        natoms = int(lines[0].split()[0])
+    except (IndexError, ValueError):
+        raise ParseError("expected atom count")
+    if natoms < 0:
+        raise ParseError("expected atom count")
+    if len(lines) < 2:
+        raise ParseError("missing comment line")
+    kv, line, i = {}, lines[1], 0
+    while i < len(line):
+        while i < len(line) and line[i].isspace():
+            i += 1
+        if i >= len(line):
+            break
+        k0 = i
+        while i < len(line) and line[i] != "=" and not line[i].isspace():
+            i += 1
+        if i >= len(line) or line[i] != "=":
+            continue
+        key = line[k0:i]
+        i += 1
+        if i < len(line) and line[i] == '"':
+            j = line.find('"', i + 1)
+            if j < 0:
+                raise ParseError("unterminated quote")
+            val, i = line[i + 1:j], j + 1
+        else:
+            j = i
+            while j < len(line) and not line[j].isspace():
+                j += 1
+            val, i = line[i:j], j
+        kv[key] = val
+    cell, pbc = np.eye(3), np.zeros(3, bool)
+    if "Lattice" in kv:
+        t = kv["Lattice"].split()
+        if len(t) < 9:
+            raise ParseError("Lattice needs 9 numbers")
+        cell = np.array([float(x) for x in t[:9]]).reshape(3, 3)
+        pbc[:] = True
+    if "pbc" in kv:
+        t = kv["pbc"].split()
+        if len(t) < 3:
+            raise ParseError("pbc needs 3 flags")
+        for d in range(3):
+            if t[d] in ("T", "true", "True", "1"):
+                pbc[d] = True
+            elif t[d] in ("F", "false", "False", "0"):
+                pbc[d] = False
+            else:
+                raise ParseError("bad pbc flag")
+    if pbc.any() and "Lattice" not in kv:
+        raise ParseError("pbc set but no Lattice given")
+    pos, sp = [], []
+    for k in range(natoms):
+        if 2 + k >= len(lines):
+            raise ParseError("fewer atom lines than declared")
+        t = lines[2 + k].split()
+        if len(t) < 4:
+            raise ParseError("expected 'Symbol x y z'")
+        if t[0] not in SYMBOLS[1:]:
+            raise ValueError("unknown element symbol")
+        sp.append(SYMBOLS.index(t[0]))
+        pos.append([float(x) for x in t[1:4]])
+    return np.array(pos, np.float64).reshape(-1, 3), np.array(sp, np.int32), cell, pbc
+
+
+def write_extxyz_text(pos, species, cell, pbc):
+    """extxyz.cpp:125-140 write_extxyz (std::ostream precision 17 = %.17g)."""
+    out = [f"{len(species)}"]
+    head = ""
+    if any(pbc):
+        head = 'Lattice="' + " ".join("%.17g" % x for x in np.asarray(cell).ravel()) + '" pbc="' + \
+            " ".join("T" if b else "F" for b in pbc) + '"'
+    out.append(head)
+    for z, p in zip(species, pos):
+        out.append(SYMBOLS[z] + " " + " ".join("%.17g" % x for x in p))
+    return "\n".join(out) + "\n"
+
+
+def _splitmix(x):
+    m = (1 << 64) - 1
+    x = (x + 0x9e3779b97f4a7c15) & m
+    x = ((x ^ (x >> 30)) * 0xbf58476d1ce4e5b9) & m
+    x = ((x ^ (x >> 27)) * 0x94d049bb133111eb) & m
+    return x ^ (x >> 31)
+
+
+def mincut(n, dst_off, src, n_parts, seed=1):
+    """mincut.cpp:16-201 mincut_partition, pure Python (small graphs)."""
+    from collections import deque
+    dst = np.repeat(np.arange(n), np.diff(dst_off))
+    pairs = sorted((int(s), int(d)) for s, d in zip(src, dst) if s != d)
+    adj = [[] for _ in range(n)]  # per source: (nbr, multiplicity) in pair order
+    k = 0
+    while k < len(pairs):
+        j = k
+        while j < len(pairs) and pairs[j] == pairs[k]:
+            j += 1
+        adj[pairs[k][0]].append((pairs[k][1], j - k))
+        k = j
+    wt = [max(1, int(dst_off[v + 1] - dst_off[v])) for v in range(n)]
+    wmax = max(wt) if wt else 1
+    out = [0] * n
+
+    def bisect(nodes, np_, base, sd):
+        if np_ == 1:
+            for v in nodes:
+                out[v] = base
+            return
+        npl, npr, m = (np_ + 1) // 2, np_ // 2, len(nodes)
+        local = {v: i for i, v in enumerate(nodes)}
+        total = sum(wt[v] for v in nodes)
+        target = total * npl // np_
+        slack = max(total // 20, wmax)
+
+        def bfs(start):
+            order, seen, q, scan = [], [False] * m, deque(), 0
+            seen[start] = True
+            q.append(start)
+            while len(order) < m:
+                if not q:
+                    while seen[scan]:
+                        scan += 1
+                    seen[scan] = True
+                    q.append(scan)
+                v = q.popleft()
+                order.append(v)
+                for u, _ in adj[nodes[v]]:
+                    lu = local.get(u, -1)
+                    if lu >= 0 and not seen[lu]:
+                        seen[lu] = True
+                        q.append(lu)
+            return order
+
+        far = bfs(_splitmix(sd) % m)[-1]
+        side, lw, taken = [1] * m, 0, 0
+        for v in bfs(far):
+            if taken >= m - 1 or (lw >= target and taken >= 1):
+                break
+            side[v], lw, taken = 0, lw + wt[nodes[v]], taken + 1
+
+        def gain_of(v):
+            g = 0
+            for u, w in adj[nodes[v]]:
+                lu = local.get(u, -1)
+                if lu >= 0:
+                    g += w if side[lu] != side[v] else -w
+            return g
+
+        for _ in range(8):
+            gain = [gain_of(v) for v in range(m)]
+            locked, moves, run, best, best_len, cur = [False] * m, [], 0, 0, 0, lw
+            for _step in range(m):
+                pick = -1
+                for v in range(m):
+                    if locked[v]:
+                        continue
+                    after = cur - wt[nodes[v]] if side[v] == 0 else cur + wt[nodes[v]]
+                    if abs(after - target) > slack:
+                        continue
+                    if pick < 0 or gain[v] > gain[pick]:
+                        pick = v
+                if pick < 0:
+                    break
+                run += gain[pick]
+                cur += -wt[nodes[pick]] if side[pick] == 0 else wt[nodes[pick]]
+                side[pick] ^= 1
+                locked[pick] = True
+                moves.append(pick)
+                gain[pick] = -gain[pick]
+                for u, w in adj[nodes[pick]]:
+                    lu = local.get(u, -1)
+                    if lu < 0 or locked[lu]:
+                        continue
+                    gain[lu] += -2 * w if side[lu] == side[pick] else 2 * w
+                if run > best:
+                    best, best_len = run, len(moves)
+            for v in reversed(moves[best_len:]):
+                side[v] ^= 1
+            lw = sum(wt[nodes[v]] for v in range(m) if side[v] == 0)
+            if best <= 0:
+                break
+        left = [nodes[v] for v in range(m) if side[v] == 0]
+        right = [nodes[v] for v in range(m) if side[v] == 1]
+        if len(left) < npl or len(right) < npr:
+            cut = min(max(m * npl // np_, npl), m - npr)
+            left, right = nodes[:cut], nodes[cut:]
+        bisect(left, npl, base, _splitmix(sd ^ 0x51ed2701))
+        bisect(right, npr, base + npl, _splitmix(sd ^ 0xa24baed4))
+
+    if n_parts < 1 or n_parts > max(1, n):
+        raise ValueError("bad part count")
+    if n_parts > 1 and n > 0:
+        bisect(list(range(n)), n_parts, 0, seed)
+    return np.array(out, np.int32)
