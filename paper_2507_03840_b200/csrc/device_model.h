@@ -92,6 +92,7 @@ struct DeviceModel {
   double prof_ms[ESG_PROF_NCAT] = {0};
   int64_t prof_n[ESG_PROF_NCAT] = {0};
   int precision = ESG_LINEAR_FP32;
+  int prefetch = 1;  // L2 prefetch mode of the rotate kernels (ESG_PREFETCH=0/1/2)
   size_t a1_elem = 4;
 };
 

@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <cmath>
 #include <cstring>
@@ -484,6 +485,7 @@ void model_device_create(esg_model* M) {
     usage("the B200 kernels are instantiated for l_max in {2,4} and e_width in {8,16}; got l_max " +
           std::to_string(L) + ", e_width " + std::to_string(E));
   M->dev = new DeviceModel();
+  if (const char* pf = std::getenv("ESG_PREFETCH")) M->dev->prefetch = std::atoi(pf);
   M->dev->L = L;
   M->dev->E = E;
   M->dev->H = (L + 1) * (L + 1);
@@ -796,7 +798,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
           k_rotate_in<L, E, 64, uint16_t><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
-                                                                         D->dir, e0, n, (uint16_t*)D->A1, D->rc);
+                                                                         D->dir, e0, n, (uint16_t*)D->A1, D->prefetch);
         }
         ++ctx->launches;
         Prof pr(D, st, ESG_PROF_SO2);
@@ -807,7 +809,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
           k_rotate_in<L, E, 1, float><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
-                                                                    D->dir, e0, n, (float*)D->A1, D->rc);
+                                                                    D->dir, e0, n, (float*)D->A1, D->prefetch);
         }
         Prof pr(D, st, ESG_PROF_SO2);
         // CUDA-core SGEMM per order block, gate in place, SGEMM
@@ -824,9 +826,9 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         constexpr int ro_threads = 32 * E / 4 < 128 ? 128 : 32 * E / 4;
         if (tc)
           k_rotate_out_edge<L, E, uint16_t><<<ro_grid, ro_threads, 0, st>>>((const uint16_t*)D->Y, D->dir, e0, n,
-                                                                            D->edges, D->rc);
+                                                                            D->edges, D->prefetch);
         else
-          k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->rc);
+          k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->prefetch);
         ++ctx->launches;
       }
     }

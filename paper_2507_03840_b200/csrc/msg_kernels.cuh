@@ -63,6 +63,33 @@ __device__ __forceinline__ float4 ld4(const uint16_t* p) {
                      __uint_as_float(w.y & 0xffff0000u));
 }
 
+// L2 prefetches: the gathers of a tile are started before its Wigner blocks
+// are computed, so their HBM latency hides behind the recursion.
+// Bulk prefetch of a contiguous range; the instruction takes a uniform
+// address, so only one lane per warp issues it (no per-lane loop).
+__device__ __forceinline__ void prefetch_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Prefetch the bf16 Y values of tile-local edges [el0, el0 + n) (tiled layout
+// [tile][c/8][edge % 128][8]): one contiguous run per 8-channel block and
+// 128-edge tile, issued by lane 0 of warps w, w + nw, ...
+template <int HE>
+__device__ __forceinline__ void prefetch_y(const uint16_t* Y, int64_t el0, int n, int w, int nw) {
+  if (n <= 0 || (threadIdx.x & 31)) return;
+  const int64_t el1 = el0 + n;  // exclusive
+  const int64_t ta = el0 >> 7, tb = (el1 - 1) >> 7;
+  const int runs = (int)(tb - ta + 1) * (HE / 8);
+  for (int u = w; u < runs; u += nw) {
+    const int64_t tile = ta + u / (HE / 8);
+    const int blk = u % (HE / 8);
+    const int64_t a = tile == ta ? el0 : tile << 7, b = tile == tb ? el1 : (tile + 1) << 7;
+    prefetch_bulk(Y + y_index<HE>(Y, a, blk * 8), (uint32_t)(b - a) * 16u);
+  }
+}
+template <int HE>
+__device__ __forceinline__ void prefetch_y(const float*, int64_t, int, int, int) {}
+
 __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
   return make_float4(fmaf(d, x.x, a.x), fmaf(d, x.y, a.y), fmaf(d, x.z, a.z), fmaf(d, x.w, a.w));
 }
@@ -78,7 +105,7 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
                                                              const float* __restrict__ dir, int64_t e0, int64_t n_e,
-                                                             OutT* __restrict__ A1, WigRecipe rc) {
+                                                             OutT* __restrict__ A1, int pf) {
   using G = Geo<L>;
   using Y = Lay1<L, E, KPAD>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
@@ -87,16 +114,23 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
   __shared__ float sdir[TE * 3];
   const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
   const int ne = (int)min64(TE, e0 + n_e - t0);
-  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   const int e = threadIdx.x / TPE, r = threadIdx.x % TPE, p = r / Q, q = r % Q;
+  const float* rowp = nullptr;
+  if (e < ne) {
+    const int64_t k = t0 + e;
+    rowp = p == 0 ? nodes + (int64_t)__ldg(src_row + k) * H * E
+                  : (p == 1 ? nodes + (int64_t)__ldg(dst_row + k) * H * E : edges + k * H * E);
+    // pf 1: the tile's edge rows (contiguous) in one bulk prefetch, source
+    // rows one each (destination rows repeat along the dst-sorted edges);
+    // pf 2: every gathered row
+    if (pf == 2 ? q == 0 : (q == 0 && p == 0 && pf == 1)) prefetch_bulk(rowp, H * E * 4);
+  }
+  if (pf == 1 && threadIdx.x == 0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
+  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   __syncthreads();
   wigner_tile_gen<L, DSP, NG>(sdir, ne, sD);
   if (e < ne) {
-    const int64_t k = t0 + e;
-    const float4* base = reinterpret_cast<const float4*>(
-                             p == 0 ? nodes + (int64_t)__ldg(src_row + k) * H * E
-                                    : (p == 1 ? nodes + (int64_t)__ldg(dst_row + k) * H * E : edges + k * H * E)) +
-                         q;
+    const float4* base = reinterpret_cast<const float4*>(rowp) + q;
     const float* D = sD + e * DSP;
     const int64_t el = t0 + e - e0;
     // A1 element (el, k) with k = K0 + pq, K0 a compile-time multiple of 16
@@ -129,15 +163,19 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
 template <int L, int E, typename YT>
 __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rotate_out_edge(const YT* __restrict__ Yin,
                                                                const float* __restrict__ dir, int64_t e0, int64_t n_e,
-                                                               float* __restrict__ edges, WigRecipe rc) {
+                                                               float* __restrict__ edges, int pf) {
   using G = Geo<L>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, Q = E / 4;
   __shared__ float sD[TE * DSP];
   __shared__ float sdir[TE * 3];
   const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
   const int ne = (int)min64(TE, e0 + n_e - t0);
-  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   const int e = threadIdx.x / Q, q = threadIdx.x % Q;
+  if (pf) {  // the tile's edge rows (contiguous) and its Y runs
+    if (threadIdx.x == 0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
+    prefetch_y<H * E>(Yin, t0 - e0, ne, threadIdx.x >> 5, blockDim.x >> 5);
+  }
+  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   __syncthreads();
   wigner_tile_gen<L, DSP>(sdir, ne, sD);
   if (e < ne) {
