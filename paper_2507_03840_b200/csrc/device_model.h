@@ -15,6 +15,20 @@ namespace esg {
 
 struct TrainState;  // train.cu
 
+// one (order block, <= 256-output tile) of a tf32x3 tensor-core linear
+// (tf32_gemm.cu): A columns [a_col, a_col + K), C columns [c_col, c_col + N),
+// B image chunks at byte b_off
+struct TcTile {
+  int a_col, c_col, K, N;  // N: the MMA width (a multiple of 16)
+  int n_valid;             // output columns actually stored (<= N)
+  int64_t b_off;
+};
+int64_t tf32_tiles(int L, int E, int kind, std::vector<TcTile>* tiles);
+void tf32_pack(const float* params, int L, int E, int li, bool dx, const int64_t* off_a, const int64_t* off_b,
+               uint8_t* img, cudaStream_t st);
+void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t* img, const TcTile* tiles,
+                      int n_tiles, float* C, int64_t ldc, cudaStream_t st);
+
 struct DeviceModel {
   int L = 0, E = 0, H = 0;
   // weights (device)
@@ -25,6 +39,12 @@ struct DeviceModel {
   bool weights_allocated = false;
   struct LinTile* lt[4] = {nullptr, nullptr, nullptr, nullptr};  // k_gemm_m tile lists (lin_kernels.cuh)
   int n_lt[4] = {0, 0, 0, 0};
+  // fp32-accurate linears on the tensor cores (3xTF32): per kind (0 lin1,
+  // 1 lin2, 2 lin2 dx, 3 lin1 dx) one B image per block and a shared tile list
+  std::vector<uint8_t*> wtc[4];
+  TcTile* tct[4] = {nullptr, nullptr, nullptr, nullptr};
+  int n_tct[4] = {0, 0, 0, 0};
+  bool tf32 = true;  // ESG_TF32=0 selects the CUDA-core SGEMM instead
   float* Hbuf = nullptr;  // fp32 path: lin1 output / gated operand of a chunk
   size_t cap_hbuf = 0;
   std::vector<int64_t> att_off;      // per layer offset into params

@@ -416,6 +416,12 @@ void model_upload_params(esg_model* M) {
       D->lt[kind] = dalloc<LinTile>(v.size());
       ESG_CUDA(cudaMemcpy(D->lt[kind], v.data(), sizeof(LinTile) * v.size(), cudaMemcpyHostToDevice));
       D->n_lt[kind] = (int)v.size();
+      std::vector<TcTile> tt;
+      const int64_t img = tf32_tiles(L, E, kind, &tt);
+      D->tct[kind] = dalloc<TcTile>(tt.size());
+      ESG_CUDA(cudaMemcpy(D->tct[kind], tt.data(), sizeof(TcTile) * tt.size(), cudaMemcpyHostToDevice));
+      D->n_tct[kind] = (int)tt.size();
+      for (int b = 0; b < 2 * M->cfg.layers; ++b) D->wtc[kind].push_back(dalloc<uint8_t>(img));
     }
     D->weights_allocated = true;
   }
@@ -443,6 +449,14 @@ void model_upload_params(esg_model* M) {
           dense += (size_t)N * K;
           bf += (size_t)pad64(K) * N;
         }
+        // tf32 hi/lo images, forward and transposed (dx)
+        std::vector<int64_t> oa(L + 1), ob(L + 1);
+        for (int m = 0; m <= L; ++m) {
+          oa[m] = M->params.at(m == 0 ? wb + "/m0" : wb + "/m" + std::to_string(m) + "r").offset;
+          ob[m] = m == 0 ? oa[m] : M->params.at(wb + "/m" + std::to_string(m) + "i").offset;
+        }
+        tf32_pack(D->params, L, E, li, false, oa.data(), ob.data(), D->wtc[li == 0 ? 0 : 1][b], st);
+        tf32_pack(D->params, L, E, li, true, oa.data(), ob.data(), D->wtc[li == 0 ? 3 : 2][b], st);
       }
     }
     D->att_off.push_back(M->params.at("layer" + std::to_string(layer) + "/att").offset);
@@ -486,6 +500,7 @@ void model_device_create(esg_model* M) {
           std::to_string(L) + ", e_width " + std::to_string(E));
   M->dev = new DeviceModel();
   if (const char* pf = std::getenv("ESG_PREFETCH")) M->dev->prefetch = std::atoi(pf);
+  if (const char* tf = std::getenv("ESG_TF32")) M->dev->tf32 = std::atoi(tf) != 0;
   M->dev->L = L;
   M->dev->E = E;
   M->dev->H = (L + 1) * (L + 1);
@@ -588,7 +603,11 @@ void model_device_destroy(esg_model* M) {
   for (auto p : D->w1t) free_ptr(p);
   for (auto p : D->w2t) free_ptr(p);
   for (auto p : D->w1n) free_ptr(p);
-  for (int k = 0; k < 4; ++k) free_ptr(D->lt[k]);
+  for (int k = 0; k < 4; ++k) {
+    free_ptr(D->lt[k]);
+    free_ptr(D->tct[k]);
+    for (auto p : D->wtc[k]) free_ptr(p);
+  }
   free_ptr(D->Hbuf);
   for (auto p : D->w2n) free_ptr(p);
   for (auto p : D->w1b) free_ptr(p);
@@ -814,10 +833,20 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         Prof pr(D, st, ESG_PROF_SO2);
         // CUDA-core SGEMM per order block, gate in place, SGEMM
         D->Hbuf = grow(D->Hbuf, D->cap_hbuf, (size_t)D->chunk_cap * H * 2 * E);
-        lin_launch<L, E>(0, (const float*)D->A1, n, D->w1t[bidx], D->Hbuf, D->lt[0], D->n_lt[0], st);
+        if (D->tf32) {
+          tf32_gemm_launch((const float*)D->A1, (int64_t)H * 3 * E, n, D->wtc[0][bidx], D->tct[0], D->n_tct[0],
+                           D->Hbuf, (int64_t)H * 2 * E, st);
+        } else {
+          lin_launch<L, E>(0, (const float*)D->A1, n, D->w1t[bidx], D->Hbuf, D->lt[0], D->n_lt[0], st);
+        }
         k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(D->Hbuf, 2 * E, n, M->cfg.gate_enabled,
                                                                             D->Hbuf);
-        lin_launch<L, E>(1, D->Hbuf, n, D->w2t[bidx], D->Y, D->lt[1], D->n_lt[1], st);
+        if (D->tf32) {
+          tf32_gemm_launch(D->Hbuf, (int64_t)H * 2 * E, n, D->wtc[1][bidx], D->tct[1], D->n_tct[1], D->Y,
+                           (int64_t)H * E, st);
+        } else {
+          lin_launch<L, E>(1, D->Hbuf, n, D->w2t[bidx], D->Y, D->lt[1], D->n_lt[1], st);
+        }
         ctx->launches += 4;
       }
       if (!node_block) {

@@ -756,8 +756,13 @@ void train_setup(esg_model* M) {
 // kind 0: lin1 forward (3E -> 2E, P = W1^T), 1: lin2 forward (2E -> E, W2^T),
 // 2: lin2 dx (E -> 2E, P = W2), 3: lin1 dx (2E -> 3E, P = W1)
 template <int L, int E>
-void lin(int kind, const float* in, int64_t n, const float* P, float* out, DeviceModel* D, cudaStream_t st) {
-  lin_launch<L, E>(kind, in, n, P, out, D->lt[kind], D->n_lt[kind], st);
+void lin(int kind, const float* in, int64_t n, const float* P, float* out, int b, DeviceModel* D, cudaStream_t st) {
+  constexpr int H = (L + 1) * (L + 1), cin_of[4] = {3 * E, 2 * E, E, 2 * E}, cout_of[4] = {2 * E, E, 2 * E, 3 * E};
+  if (D->tf32)
+    tf32_gemm_launch(in, (int64_t)H * cin_of[kind], n, D->wtc[kind][b], D->tct[kind], D->n_tct[kind], out,
+                     (int64_t)H * cout_of[kind], st);
+  else
+    lin_launch<L, E>(kind, in, n, P, out, D->lt[kind], D->n_lt[kind], st);
 }
 
 constexpr int OUTER_SPLIT = 2048;       // edges per split of a weight-gradient tile
@@ -863,11 +868,11 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     // forward recompute: A1, H, G (+ Y and msg for the attention backward)
     k_rotate_in<L, E, 1, float><<<t32, RI_THREADS, 0, st>>>(nodes, edges, D->src_row, D->dst_row, D->dir, e0, n, T->A1,
                                                             D->prefetch);
-    lin<L, E>(0, T->A1, n, D->w1t[b], T->Hh, D, st);
+    lin<L, E>(0, T->A1, n, D->w1t[b], T->Hh, b, D, st);
     k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, 2 * E, n, M->cfg.gate_enabled, T->Gg);
     const float* g_msg;
     if (node_block) {
-      lin<L, E>(1, T->Gg, n, D->w2t[b], T->Yy, D, st);
+      lin<L, E>(1, T->Gg, n, D->w2t[b], T->Yy, b, D, st);
       k_rot1<L, E, 0><<<t32, 128, 0, st>>>(T->Yy, D->dir, e0, n, T->msg);
       // attention backward into gY's buffer (used as g_msg scratch)
       k_attn_bwd<H, E><<<(unsigned)(ch.second - ch.first), 128, 0, st>>>(
@@ -881,12 +886,12 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     k_rot1<L, E, 1><<<t32, 128, 0, st>>>(g_msg, D->dir, e0, n, T->gY);
     // lin2 adjoint
     outer<L>(T->gY, E, T->Gg, 2 * E, n, T->gacc + T->off_lin2[b], false, T, st);
-    lin<L, E>(2, T->gY, n, D->w2n[b], T->gG, D, st);
+    lin<L, E>(2, T->gY, n, D->w2n[b], T->gG, b, D, st);
     k_gate_bwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, T->gG, 2 * E, n, M->cfg.gate_enabled,
                                                                        T->gH);
     // lin1 adjoint
     outer<L>(T->gH, 2 * E, T->A1, 3 * E, n, T->gacc + T->off_lin1[b], true, T, st);
-    lin<L, E>(3, T->gH, n, D->w1n[b], T->gA1, D, st);
+    lin<L, E>(3, T->gH, n, D->w1n[b], T->gA1, b, D, st);
     // rotate-in / concat adjoint, ordered row reductions
     k_rot_in_bwd<L, E><<<t32, RI_THREADS, 0, st>>>(T->gA1, D->dir, e0, n, T->g_edges, T->gx);
     k_dst_reduce<<<(unsigned)(ch.second - ch.first), 128, 0, st>>>(T->gx, HE, D->seg, ch.first, e0, T->g_nodes);
