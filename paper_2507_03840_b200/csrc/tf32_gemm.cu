@@ -27,7 +27,7 @@ namespace {
 using namespace tc;
 
 constexpr int TM = 128;                  // rows per CTA (UMMA M, one per TMEM lane)
-constexpr int THREADS = 128;
+constexpr int THREADS = 256;
 constexpr int A_BYTES = TM * 128;        // one split of a 32-wide K chunk of A
 constexpr int B_MAX = 256 * 128;         // one split of a K chunk of B (N <= 256)
 constexpr int STAGE = 2 * A_BYTES + 2 * B_MAX;
@@ -94,29 +94,34 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t bbytes = 2u * (uint32_t)t.N * 128u;
   const uint32_t idesc = idesc_tf32(t.N);
   const uint64_t pol = policy_evict_last();
-  const int u = tid & 7;  // 16-byte unit of the K chunk this thread converts
+  const int u = tid & 7;  // 16-byte unit of the K chunk this thread converts (rows tid / 8 + 32 i)
+  auto load = [&](int c, float4* v) {
+    const int k = c * 32 + u * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = r0 + (tid >> 3) + 32 * i;
+      v[i] = (c < nc && row < n_rows && k < t.K)
+                 ? __ldg(reinterpret_cast<const float4*>(A + row * lda + t.a_col + k))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float4 cur[4], nxt[4];
+  load(0, cur);
   for (int c = 0; c < nc; ++c) {
     const int s = c & 1;
     const uint32_t sAh = s0 + s * STAGE, sAl = sAh + A_BYTES, sBh = sAh + 2 * A_BYTES, sBl = sBh + t.N * 128;
+    load(c + 1, nxt);  // next chunk's rows in flight while this one is converted
     if (c >= 2) mbar_wait(bar(2 + s), ((c - 2) >> 1) & 1);  // MMAs of chunk c - 2 released stage s
     if (tid == 0) {
       mbar_expect_tx(bar(s), bbytes);
       bulk_g2s(sBh, Bimg + t.b_off + (int64_t)c * bbytes, bbytes, bar(s), pol);
     }
-    const int k = c * 32 + u * 4;
-    float4 v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int64_t row = r0 + (tid >> 3) + 16 * i;
-      v[i] = (row < n_rows && k < t.K) ? __ldg(reinterpret_cast<const float4*>(A + row * lda + t.a_col + k))
-                                       : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = (tid >> 3) + 16 * i;
-      const float4 h = make_float4(to_tf32(v[i].x), to_tf32(v[i].y), to_tf32(v[i].z), to_tf32(v[i].w));
-      const float4 l = make_float4(to_tf32(v[i].x - h.x), to_tf32(v[i].y - h.y), to_tf32(v[i].z - h.z),
-                                   to_tf32(v[i].w - h.w));
+    for (int i = 0; i < 4; ++i) {
+      const int r = (tid >> 3) + 32 * i;
+      const float4 h = make_float4(to_tf32(cur[i].x), to_tf32(cur[i].y), to_tf32(cur[i].z), to_tf32(cur[i].w));
+      const float4 l = make_float4(to_tf32(cur[i].x - h.x), to_tf32(cur[i].y - h.y), to_tf32(cur[i].z - h.z),
+                                   to_tf32(cur[i].w - h.w));
       const uint32_t o = sw128(r, u);
       asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sAh + o), "f"(h.x), "f"(h.y), "f"(h.z),
                    "f"(h.w)
@@ -124,6 +129,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sAl + o), "f"(l.x), "f"(l.y), "f"(l.z),
                    "f"(l.w)
                    : "memory");
+      cur[i] = nxt[i];
     }
     fence_async_smem();
     __syncthreads();
@@ -145,12 +151,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   mbar_wait(bar(2 + ((nc - 1) & 1)), ((nc - 1) >> 1) & 1);
   tc_fence_after();
-  // epilogue: warp w owns TMEM lanes (rows) 32 w .. 32 w + 31
-  const int64_t row = r0 + warp * 32 + lane;
+  // epilogue: warps w and w + 4 own TMEM lanes (rows) 32 (w % 4) ..; they
+  // take alternate 16-column groups
+  const int quarter = warp & 3;
+  const int64_t row = r0 + quarter * 32 + lane;
   float* out = C + row * ldc + t.c_col;
-  for (int j = 0; j < t.N; j += 16) {
+  for (int j = (warp >> 2) * 16; j < t.N; j += 32) {
     float v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)j, v);
+    tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)j, v);
     if (row < n_rows) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
