@@ -359,6 +359,22 @@ def run_ours(args):
                                            enumerate(("graph_and_plan", "prepare", "forward_and_d2h", "teardown"))},
                "pinned_host_outputs": bool(getattr(torch.from_numpy(edge_out), "is_pinned", lambda: False)())}
 
+    # the fp32-accurate mode on the same graph (3xTF32 tensor-core linears;
+    # Hamiltonian blocks within the fp32 tolerance of tests/test_gpu_parity.py)
+    fp32_mode = None
+    if args.fp32_steps > 0 and prec == esg.LINEAR_BF16:
+        net.set_precision(esg.LINEAR_FP32)
+        net.forward(copy_out=False)
+        barrier()
+        torch.cuda.synchronize()
+        f32 = [net.forward(copy_out=False)[2].forward_ms for _ in range(args.fp32_steps)]
+        ms32 = allmax(float(np.mean(f32)))
+        fp32_mode = {"value": total_edges / (ms32 / 1e3), "unit": "edges/s", "ms_per_step": ms32,
+                     "steps": args.fp32_steps,
+                     "linears": "tcgen05 kind::tf32, 3xTF32 split (hi.hi + hi.lo + lo.hi), fp32 accumulate",
+                     "tolerance": "heads vs fp32 oracle: max-abs <= 2e-4 x max, rel-L2 <= 2e-5"}
+        net.set_precision(prec)
+
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         v, cores, sample = cpu_sample(s, r, layers, basis, target_s=args.cpu_seconds, g=g.export())
@@ -368,10 +384,11 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16" if prec == esg.LINEAR_BF16 else "fp32", "data": "synthetic",
             "config": {"workload": CONFIG_DESC[args.config], "atoms": s.n_atoms, "edges": total_edges,
                        "r_cut": r, "layers": layers, "l_max": 4, "e_width": 16,
-                       "linears": "tcgen05 bf16, fp32 accumulate" if prec == esg.LINEAR_BF16 else "fp32 CUDA cores",
+                       "linears": "tcgen05 bf16, fp32 accumulate" if prec == esg.LINEAR_BF16 else
+                       "tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate",
                        "parallelism": f"graph-partition dp{world} (Low-NN, NCCL halo)",
                        "l2": "inputs larger than L2 (edge table %.0f GB)" % (total_edges * ROW / 1e9)},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "fp32_mode": fp32_mode,
             "gpu_launches": int(allsum(launches)),
             "halo_ms_per_forward": halo_step, "halo_exchanges_per_forward": 2 * layers if world > 1 else 0,
             "message_ms_per_forward": msg_step,
@@ -442,6 +459,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--train-steps", type=int, default=2, help="C2 training steps after the forward (0: skip)")
+    ap.add_argument("--fp32-steps", type=int, default=2, help="forwards timed in the fp32-accurate mode (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

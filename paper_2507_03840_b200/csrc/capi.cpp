@@ -5,6 +5,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -223,6 +226,7 @@ int esg_ctx_destroy(esg_ctx* ctx) {
   ESG_API_BEGIN
   if (!ctx) return ESG_OK;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  ctx->cache.flush();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   ESG_API_END
@@ -306,8 +310,16 @@ int esg_build_graph(esg_ctx* ctx, int n, const double* pos, const double cell[9]
 int esg_graph_destroy(esg_graph* g) {
   ESG_API_BEGIN
   if (!g) return ESG_OK;
+  const bool dbg = std::getenv("ESG_DEBUG_FREE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
+  if (dbg) cudaDeviceSynchronize();
+  auto t1 = now();
   for (void* p : {(void*)g->d_off, (void*)g->d_src, (void*)g->d_shift, (void*)g->d_disp, (void*)g->d_dist})
-    if (p) cudaFree(p);
+    g->ctx->cache.release(p);
+  if (dbg)
+    std::fprintf(stderr, "[esg] graph destroy: device sync %.3f s, frees %.3f s\n",
+                 std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(now() - t1).count());
   delete g;
   ESG_API_END
 }

@@ -105,11 +105,28 @@ std::vector<double> coupling_matrix(int la, int lb, int L);
 }  // namespace esg
 
 // ---- opaque handle bodies -----------------------------------------------
+namespace esg {
+// Device block cache of one context: freed blocks are kept (up to a byte
+// budget) and handed out again by best fit, so a build -> use -> destroy
+// cycle of same-sized graphs does not pay cudaMalloc/cudaFree (a first free
+// of GB-sized blocks costs ~0.6 s of driver unmapping on B200).  A failed
+// cudaMalloc flushes the cache and retries.
+struct BlockCache {
+  std::multimap<size_t, void*> free_blocks;  // capacity -> block
+  std::map<void*, size_t> live;              // handed-out block -> capacity
+  size_t cached = 0, budget = size_t(16) << 30;
+  void* alloc(size_t bytes);
+  void release(void* p);
+  void flush();
+};
+}  // namespace esg
+
 struct esg_ctx {
   int device = 0, rank = 0, world = 1;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   int64_t launches = 0;  // kernels launched by this library
+  esg::BlockCache cache;
 };
 
 struct esg_graph {

@@ -17,6 +17,7 @@
 // HBM layout produced (dst-major CSR, SoA):
 //   d_off[N+1] i64, d_src[E] i32, d_shift[E] u32 packed, d_disp[3E] f64, d_dist[E] f64
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include <algorithm>
 #include <cmath>
@@ -144,13 +145,6 @@ __global__ void k_finalize(const uint64_t* __restrict__ keys, const int32_t* __r
   dist[k] = __dsqrt_rn(q);
 }
 
-template <typename T>
-T* dalloc(size_t n) {
-  T* p = nullptr;
-  if (n) ESG_CUDA(cudaMalloc(&p, n * sizeof(T)));
-  return p;
-}
-
 }  // namespace
 
 esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& cell, const bool pbc[3],
@@ -158,6 +152,11 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   if (!(r_cut > 0.0)) usage("cutoff must be positive");
   if (n < 1) usage("structure has no atoms");
   cudaStream_t st = ctx->stream;
+  // every device buffer through the context's block cache (esg_internal.h)
+  auto dalloc_c = [&](auto* type_tag, size_t n_el) {
+    using T = std::remove_pointer_t<decltype(type_tag)>;
+    return static_cast<T*>(ctx->cache.alloc(n_el * sizeof(T)));
+  };
   std::vector<double> pos(pos_in, pos_in + 3 * (size_t)n);
   wrap_positions(n, pos.data(), cell, pbc);
 
@@ -209,13 +208,13 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   G->n = n;
   for (int d = 0; d < 3; ++d) G->nimg[d] = g.nimg[d];
 
-  double* d_pos = dalloc<double>(3 * (size_t)n);
-  double* d_img = dalloc<double>(off.size());
-  int* d_bin = dalloc<int>(n);
-  int* d_cnt = dalloc<int>(nbins + 1);
-  int* d_start = dalloc<int>(nbins + 1);
-  int* d_cur = dalloc<int>(nbins);
-  int* d_atoms = dalloc<int>(n);
+  double* d_pos = dalloc_c((double*)nullptr, 3 * (size_t)n);
+  double* d_img = dalloc_c((double*)nullptr, off.size());
+  int* d_bin = dalloc_c((int*)nullptr, n);
+  int* d_cnt = dalloc_c((int*)nullptr, nbins + 1);
+  int* d_start = dalloc_c((int*)nullptr, nbins + 1);
+  int* d_cur = dalloc_c((int*)nullptr, nbins);
+  int* d_atoms = dalloc_c((int*)nullptr, n);
   ESG_CUDA(cudaMemcpyAsync(d_pos, pos.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
   ESG_CUDA(cudaMemcpyAsync(d_img, off.data(), sizeof(double) * off.size(), cudaMemcpyHostToDevice, st));
   ESG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int) * (nbins + 1), st));
@@ -225,14 +224,14 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt, d_start, (int)(nbins + 1), st);
   void* d_tmp = nullptr;
-  ESG_CUDA(cudaMalloc(&d_tmp, tmp_bytes));
+  d_tmp = ctx->cache.alloc(tmp_bytes);
   cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_cnt, d_start, (int)(nbins + 1), st);
-  ESG_CUDA(cudaFree(d_tmp));
+  ctx->cache.release(d_tmp);
   k_scatter_atoms<<<(n + 255) / 256, 256, 0, st>>>(d_bin, n, d_start, d_cur, d_atoms);
   ++ctx->launches;
 
-  int64_t* d_cnt_e = dalloc<int64_t>(n + 1);
-  G->d_off = dalloc<int64_t>(n + 1);
+  int64_t* d_cnt_e = dalloc_c((int64_t*)nullptr, n + 1);
+  G->d_off = dalloc_c((int64_t*)nullptr, n + 1);
   ESG_CUDA(cudaMemsetAsync(d_cnt_e, 0, sizeof(int64_t) * (n + 1), st));
   const int threads = 256, warps_per_block = threads / 32;
   const int blocks = (n + warps_per_block - 1) / warps_per_block;
@@ -240,33 +239,33 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   ++ctx->launches;
   tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt_e, G->d_off, n + 1, st);
-  ESG_CUDA(cudaMalloc(&d_tmp, tmp_bytes));
+  d_tmp = ctx->cache.alloc(tmp_bytes);
   cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_cnt_e, G->d_off, n + 1, st);
-  ESG_CUDA(cudaFree(d_tmp));
+  ctx->cache.release(d_tmp);
   int64_t E = 0;
   ESG_CUDA(cudaMemcpyAsync(&E, G->d_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   ESG_CUDA(cudaStreamSynchronize(st));
   if (E > (int64_t)std::numeric_limits<int>::max() - 1) usage("graph exceeds 2^31 edges");
   G->E = E;
 
-  uint64_t* d_keys = dalloc<uint64_t>(E);
-  uint64_t* d_keys_sorted = dalloc<uint64_t>(E);
-  int32_t* d_dst = dalloc<int32_t>(E);
+  uint64_t* d_keys = dalloc_c((uint64_t*)nullptr, E);
+  uint64_t* d_keys_sorted = dalloc_c((uint64_t*)nullptr, E);
+  int32_t* d_dst = dalloc_c((int32_t*)nullptr, E);
   if (E > 0) {
     k_edges<true><<<blocks, threads, 0, st>>>(d_pos, n, g, d_img, d_start, d_atoms, G->d_off, d_keys, d_dst);
     ++ctx->launches;
     tmp_bytes = 0;
     cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
                                        G->d_off + 1, st);
-    ESG_CUDA(cudaMalloc(&d_tmp, tmp_bytes));
+    d_tmp = ctx->cache.alloc(tmp_bytes);
     cub::DeviceSegmentedSort::SortKeys(d_tmp, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off, G->d_off + 1,
                                        st);
-    ESG_CUDA(cudaFree(d_tmp));
+    ctx->cache.release(d_tmp);
   }
-  G->d_src = dalloc<int32_t>(E);
-  G->d_shift = dalloc<uint32_t>(E);
-  G->d_disp = dalloc<double>(3 * (size_t)E);
-  G->d_dist = dalloc<double>(E);
+  G->d_src = dalloc_c((int32_t*)nullptr, E);
+  G->d_shift = dalloc_c((uint32_t*)nullptr, E);
+  G->d_disp = dalloc_c((double*)nullptr, 3 * (size_t)E);
+  G->d_dist = dalloc_c((double*)nullptr, E);
   if (E > 0) {
     k_finalize<<<(unsigned)((E + 255) / 256), 256, 0, st>>>(d_keys_sorted, d_dst, E, d_pos, g, d_img, G->d_src,
                                                            G->d_shift, G->d_disp, G->d_dist);
@@ -276,7 +275,7 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   ESG_CUDA(cudaStreamSynchronize(st));
   for (void* p : {(void*)d_pos, (void*)d_img, (void*)d_bin, (void*)d_cnt, (void*)d_start, (void*)d_cur,
                   (void*)d_atoms, (void*)d_cnt_e, (void*)d_keys, (void*)d_keys_sorted, (void*)d_dst})
-    if (p) cudaFree(p);
+    ctx->cache.release(p);
   return G;
 }
 

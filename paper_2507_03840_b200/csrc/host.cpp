@@ -186,6 +186,59 @@ std::string element_symbol(int z) {
   return t[z];
 }
 
+// ------------------------------------------------------- block cache
+void* BlockCache::alloc(size_t bytes) {
+  if (bytes == 0) return nullptr;
+  auto it = free_blocks.lower_bound(bytes);  // smallest cached block that fits
+  if (it != free_blocks.end() && it->first <= bytes + bytes / 4) {
+    void* p = it->second;
+    live[p] = it->first;
+    cached -= it->first;
+    free_blocks.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    flush();
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(ESG_ERR_OOM, "out of device memory (" + std::to_string(bytes) + " bytes)");
+    }
+  }
+  live[p] = bytes;
+  return p;
+}
+
+void BlockCache::release(void* p) {
+  if (!p) return;
+  auto it = live.find(p);
+  if (it == live.end()) {
+    cudaFree(p);
+    return;
+  }
+  const size_t cap = it->second;
+  live.erase(it);
+  while (cached + cap > budget && !free_blocks.empty()) {  // drop the largest cached blocks first
+    auto big = std::prev(free_blocks.end());
+    cudaFree(big->second);
+    cached -= big->first;
+    free_blocks.erase(big);
+  }
+  if (cached + cap > budget) {
+    cudaFree(p);
+    return;
+  }
+  free_blocks.emplace(cap, p);
+  cached += cap;
+}
+
+void BlockCache::flush() {
+  for (auto& kv : free_blocks) cudaFree(kv.second);
+  free_blocks.clear();
+  cached = 0;
+}
+
 // elements.cpp:32-36
 int atomic_number(const std::string& symbol) {
   for (int z = 1; z <= 103; ++z)
