@@ -25,6 +25,7 @@ void model_device_destroy(esg_model* M);
 void model_upload_params(esg_model* M);
 void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const int32_t* species);
 void model_forward(esg_model* M, esg_timing* tm);
+void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float* edge_out);
 void model_profile(esg_model* M, int enable, double* ms, int64_t* counts);
 void model_outputs(const esg_model* M, const float** no, const float** eo, const float** nf, const float** ef);
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
@@ -667,8 +668,7 @@ int esg_forward(esg_model* m, float* node_out, float* edge_out, esg_timing* timi
   NEED(m, "model");
   if (!m->ctx || !m->dev) usage("model was created without a device context");
   ESG_CUDA(cudaSetDevice(m->ctx->device));
-  model_forward(m, timing);
-  if (node_out || edge_out) model_copy_outputs(m, node_out, edge_out);
+  model_forward_to_host(m, timing, node_out, edge_out);
   ESG_API_END
 }
 

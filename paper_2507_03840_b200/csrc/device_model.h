@@ -111,6 +111,13 @@ struct DeviceModel {
   std::vector<std::pair<int, int>> marks;  // (category, first event index)
   double prof_ms[ESG_PROF_NCAT] = {0};
   int64_t prof_n[ESG_PROF_NCAT] = {0};
+  // streamed outputs (esg_forward with pinned host buffers): heads of the
+  // final tables are computed as soon as they are final and copied on copy_st
+  float* host_node_out = nullptr;
+  float* host_edge_out = nullptr;
+  cudaStream_t copy_st = nullptr;
+  std::vector<cudaEvent_t> out_ev;
+  size_t out_ev_used = 0;
   int precision = ESG_LINEAR_FP32;
   int prefetch = 1;  // L2 prefetch mode of the rotate kernels (ESG_PREFETCH=0/1/2)
   size_t a1_elem = 4;

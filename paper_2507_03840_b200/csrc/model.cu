@@ -613,6 +613,8 @@ void model_device_destroy(esg_model* M) {
   for (auto p : D->w1b) free_ptr(p);
   for (auto p : D->w2b) free_ptr(p);
   for (auto& e : D->ev) cudaEventDestroy(e);
+  for (auto& e : D->out_ev) cudaEventDestroy(e);
+  if (D->copy_st) cudaStreamDestroy(D->copy_st);
   delete D;
   M->dev = nullptr;
 }
@@ -751,6 +753,26 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
 
 namespace {
 
+template <int H, int E>
+void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
+                  float* out, cudaStream_t st);
+
+// Streamed outputs: rows [i0, i0 + n) of a head table are final on st; once
+// they are computed (heads) copy them to the pinned host buffer on copy_st.
+void stream_rows(DeviceModel* D, cudaStream_t st, const float* dev, float* host, int64_t i0, int64_t n, int ol) {
+  if (n <= 0) return;
+  if (D->out_ev_used == D->out_ev.size()) {
+    cudaEvent_t e;
+    ESG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    D->out_ev.push_back(e);
+  }
+  cudaEvent_t e = D->out_ev[D->out_ev_used++];
+  ESG_CUDA(cudaEventRecord(e, st));
+  ESG_CUDA(cudaStreamWaitEvent(D->copy_st, e, 0));
+  ESG_CUDA(cudaMemcpyAsync(host + i0 * ol, dev + i0 * ol, sizeof(float) * (size_t)n * ol, cudaMemcpyDeviceToHost,
+                           D->copy_st));
+}
+
 template <int L, int E>
 void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
   DeviceModel* D = M->dev;
@@ -860,6 +882,15 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
           k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->prefetch);
         ++ctx->launches;
       }
+      if (!node_block && D->host_edge_out && layer == M->cfg.layers - 1) {
+        // the chunk's edge rows are final: its heads now, the copy overlaps the next chunks
+        Prof pr(D, st, ESG_PROF_HEADS);
+        const int ol = M->heads.out_len;
+        launch_heads<H, E>(D->edges + e0 * H * E, n, D->head_w[1], D->head_key, D->head_row, ol,
+                           D->edge_out + e0 * ol, st);
+        ++ctx->launches;
+        stream_rows(D, st, D->edge_out, D->host_edge_out, e0, n, ol);
+      }
     }
     if (node_block && ch.second > ch.first) {
       Prof pr(D, st, ESG_PROF_NODE);
@@ -927,21 +958,29 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   ESG_CUDA(cudaEventRecord(D->ev[1], st));
   float halo_ms = 0.f;
   int64_t exchanges = 0;
+  const int out_len = M->heads.out_len;
+  const bool streamed = D->host_node_out || D->host_edge_out;
+  D->out_ev_used = 0;
   for (int layer = 0; layer < M->cfg.layers; ++layer)
     for (bool nb : {true, false}) {
       run_block<L, E>(M, layer, nb, &halo_ms);
       ++exchanges;
+      if (streamed && nb && layer == M->cfg.layers - 1 && D->n_owned) {
+        // the node table is final after the last node block: its heads and
+        // their copy overlap the last edge block
+        Prof pr(D, st, ESG_PROF_HEADS);
+        launch_heads<H, E>(D->nodes, D->n_owned, D->head_w[0], D->head_key, D->head_row, out_len, D->node_out, st);
+        ++ctx->launches;
+        if (D->host_node_out) stream_rows(D, st, D->node_out, D->host_node_out, 0, D->n_owned, out_len);
+      }
     }
   ESG_CUDA(cudaEventRecord(D->ev[2], st));
-  const int out_len = M->heads.out_len;
-  if (D->n_owned) {
-    const int64_t n = (int64_t)D->n_owned * out_len;
+  if (D->n_owned && !streamed) {
     Prof pr(D, st, ESG_PROF_HEADS);
     launch_heads<H, E>(D->nodes, D->n_owned, D->head_w[0], D->head_key, D->head_row, out_len, D->node_out, st);
     ++ctx->launches;
   }
-  if (D->n_edges) {
-    const int64_t n = D->n_edges * out_len;
+  if (D->n_edges && (!streamed || !D->host_edge_out)) {
     Prof pr(D, st, ESG_PROF_HEADS);
     launch_heads<H, E>(D->edges, D->n_edges, D->head_w[1], D->head_key, D->head_row, out_len, D->edge_out, st);
     ++ctx->launches;
@@ -1030,6 +1069,43 @@ void model_outputs(const esg_model* M, const float** no, const float** eo, const
   if (eo) *eo = D->edge_out;
   if (nf) *nf = D->nodes;
   if (ef) *ef = D->edges;
+}
+
+void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
+
+// esg_forward with host output buffers: when both given buffers are pinned
+// (page-locked or registered), the heads of each final chunk are copied while
+// the rest of the last edge block computes; otherwise the copies follow the
+// forward.
+bool pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float* edge_out) {
+  DeviceModel* D = M->dev;
+  if ((node_out || edge_out) && pinned(node_out) && pinned(edge_out) && !D->save_inputs) {
+    if (!D->copy_st) ESG_CUDA(cudaStreamCreateWithFlags(&D->copy_st, cudaStreamNonBlocking));
+    D->host_node_out = node_out;
+    D->host_edge_out = edge_out;
+    try {
+      model_forward(M, tm);
+    } catch (...) {
+      D->host_node_out = D->host_edge_out = nullptr;
+      cudaStreamSynchronize(D->copy_st);
+      throw;
+    }
+    D->host_node_out = D->host_edge_out = nullptr;
+    ESG_CUDA(cudaStreamSynchronize(D->copy_st));
+    return;
+  }
+  model_forward(M, tm);
+  if (node_out || edge_out) model_copy_outputs(M, node_out, edge_out);
 }
 
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out) {

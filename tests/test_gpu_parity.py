@@ -162,3 +162,27 @@ def test_precision_switch_and_errors(gpu_ctx):
     with pytest.raises(esg.DataError):  # species missing from the basis
         g = esg.build_graph(gpu_ctx, s, 4.5)
         net.prepare(g, np.full(20, 6, np.int32))
+
+
+def test_streamed_outputs_match(gpu_ctx):
+    """esg_forward into pinned host buffers streams the heads of each final
+    chunk while the last edge block runs (C3: several chunks); the outputs
+    are bit-identical to the copy-after-forward path of pageable buffers."""
+    import torch
+    s, r, layers, basis = esg.config_structure("C3")
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=layers, n_radial=32, r_cut=r, seed=1,
+                          linear_precision=esg.LINEAR_BF16)
+    net = esg.Network(gpu_ctx, cfg, basis)
+    net.init_params()
+    g = esg.build_graph(gpu_ctx, s, r)
+    net.prepare(g, s.species)
+    no, eo, _ = net.forward()
+    pn = torch.empty((net.n_owned, net.out_len), dtype=torch.float32, pin_memory=True).numpy()
+    pe = torch.empty((net.n_edges, net.out_len), dtype=torch.float32, pin_memory=True).numpy()
+    pn[:] = np.nan
+    pe[:] = np.nan
+    net.forward_into(pn, pe)
+    assert np.array_equal(pn.view(np.uint32), no.view(np.uint32))
+    assert np.array_equal(pe.view(np.uint32), eo.view(np.uint32))
+    net.close()
+    g.close()
