@@ -26,12 +26,16 @@ namespace esg {
 namespace {
 using namespace tc;
 
-constexpr int TM = 128;                  // rows per CTA (UMMA M, one per TMEM lane)
-constexpr int THREADS = 256;
+constexpr int TM = 128;                  // rows per tile (UMMA M, one per TMEM lane)
 constexpr int A_BYTES = TM * 128;        // one split of a 32-wide K chunk of A
 constexpr int B_MAX = 256 * 128;         // one split of a K chunk of B (N <= 256)
-constexpr int STAGE = 2 * A_BYTES + 2 * B_MAX;
-constexpr int SMEM_BYTES = 1024 + 2 * STAGE + 64;
+// persistent warp-specialised GEMM: warps 0-3 epilogue, 4-11 A producers,
+// warp 12 MMA issuer; rings of A (3 stages) and B (2 stages)
+constexpr int EPI_WARPS = 4, PROD_WARPS = 8, MMA_WARP = EPI_WARPS + PROD_WARPS;
+constexpr int THREADS = 32 * (MMA_WARP + 1);
+constexpr int NA = 3, NB = 2;
+constexpr int A_STAGE = 2 * A_BYTES, B_STAGE = 2 * B_MAX;
+constexpr int SMEM_BYTES = 1024 + NA * A_STAGE + NB * B_STAGE + 256;
 
 __device__ __forceinline__ float to_tf32(float x) {
   uint32_t r;
@@ -66,109 +70,172 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// C[e, c_col + o] = sum_k A[e, a_col + k] B[o, k] over work items (128-row
+// tile, tile-list entry), tile-list major so all SMs stream the same B image.
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tf32x3(const float* __restrict__ A, int64_t lda, int64_t n_rows, const uint8_t* __restrict__ Bimg,
-                  const TcTile* __restrict__ tiles, float* __restrict__ C, int64_t ldc) {
+                  const TcTile* __restrict__ tiles, int n_tiles, float* __restrict__ C, int64_t ldc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t s0 = smem_u32(base);
-  uint64_t* bars = (uint64_t*)(base + 2 * STAGE);  // full[2], done[2]
-  uint32_t* tmem_slot = (uint32_t*)(bars + 4);
+  const uint32_t sA = smem_u32(base), sB = sA + NA * A_STAGE;
+  uint64_t* bars = (uint64_t*)(base + NA * A_STAGE + NB * B_STAGE);
   auto bar = [&](int i) { return smem_u32(&bars[i]); };
-  const TcTile t = tiles[blockIdx.y];
-  const int64_t r0 = (int64_t)blockIdx.x * TM;
+  const int AF = 0, AE = NA, BF = 2 * NA, BE = 2 * NA + NB, CF = 2 * NA + 2 * NB, CE = CF + 2;
+  uint32_t* tmem_slot = (uint32_t*)(bars + CE + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(bar(i), 1);
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(bar(AF + i), PROD_WARPS * 32);
+      mbar_init(bar(AE + i), 1);
+    }
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(bar(BF + i), 1);
+      mbar_init(bar(BE + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(CF + i), 1);
+      mbar_init(bar(CE + i), EPI_WARPS * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tmem_slot)));
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int nc = (t.K + 31) >> 5;
-  const uint32_t bbytes = 2u * (uint32_t)t.N * 128u;
-  const uint32_t idesc = idesc_tf32(t.N);
-  const uint64_t pol = policy_evict_last();
-  const int u = tid & 7;  // 16-byte unit of the K chunk this thread converts (rows tid / 8 + 32 i)
-  auto load = [&](int c, float4* v) {
-    const int k = c * 32 + u * 4;
+  const int64_t n_rt = (n_rows + TM - 1) / TM;
+  const int64_t n_items = n_rt * n_tiles;
+
+  if (warp >= EPI_WARPS && warp < MMA_WARP) {
+    // ---- producers: A chunks split into tf32 hi/lo, B chunks by bulk copy
+    const int pt = tid - EPI_WARPS * 32;  // 0..255
+    const int u = pt & 7;                 // 16-byte unit of the chunk row
+    const uint64_t pol = policy_evict_last();
+    int sa = 0, sb = 0;
+    uint32_t ka = 0, kb = 0;  // ring uses (parity source)
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const TcTile t = tiles[it / n_rt];
+      const int64_t r0 = (it % n_rt) * TM;
+      const int nc = (t.K + 31) >> 5;
+      const uint32_t bbytes = 2u * (uint32_t)t.N * 128u;
+      auto load = [&](int c, float4* v) {
+        const int k = c * 32 + u * 4;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t row = r0 + (tid >> 3) + 32 * i;
-      v[i] = (c < nc && row < n_rows && k < t.K)
-                 ? __ldg(reinterpret_cast<const float4*>(A + row * lda + t.a_col + k))
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  float4 cur[4], nxt[4];
-  load(0, cur);
-  for (int c = 0; c < nc; ++c) {
-    const int s = c & 1;
-    const uint32_t sAh = s0 + s * STAGE, sAl = sAh + A_BYTES, sBh = sAh + 2 * A_BYTES, sBl = sBh + t.N * 128;
-    load(c + 1, nxt);  // next chunk's rows in flight while this one is converted
-    if (c >= 2) mbar_wait(bar(2 + s), ((c - 2) >> 1) & 1);  // MMAs of chunk c - 2 released stage s
-    if (tid == 0) {
-      mbar_expect_tx(bar(s), bbytes);
-      bulk_g2s(sBh, Bimg + t.b_off + (int64_t)c * bbytes, bbytes, bar(s), pol);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = (tid >> 3) + 32 * i;
-      const float4 h = make_float4(to_tf32(cur[i].x), to_tf32(cur[i].y), to_tf32(cur[i].z), to_tf32(cur[i].w));
-      const float4 l = make_float4(to_tf32(cur[i].x - h.x), to_tf32(cur[i].y - h.y), to_tf32(cur[i].z - h.z),
-                                   to_tf32(cur[i].w - h.w));
-      const uint32_t o = sw128(r, u);
-      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sAh + o), "f"(h.x), "f"(h.y), "f"(h.z),
-                   "f"(h.w)
-                   : "memory");
-      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sAl + o), "f"(l.x), "f"(l.y), "f"(l.z),
-                   "f"(l.w)
-                   : "memory");
-      cur[i] = nxt[i];
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (warp == 0) {
-      mbar_wait(bar(s), (c >> 1) & 1);  // B chunk landed
-      tc_fence_after();
-      if (elect_one()) {
-        const uint64_t ah = sdesc(sAh), al = sdesc(sAl), bh = sdesc(sBh), bl = sdesc(sBl);
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 (32 bytes) per instruction
-          mma_tf32(tmem, ah + 2 * ks, bh + 2 * ks, idesc, (c | ks) ? 1u : 0u);
-          mma_tf32(tmem, ah + 2 * ks, bl + 2 * ks, idesc, 1u);
-          mma_tf32(tmem, al + 2 * ks, bh + 2 * ks, idesc, 1u);
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = r0 + (pt >> 3) + 32 * i;
+          v[i] = (c < nc && row < n_rows && k < t.K)
+                     ? __ldg(reinterpret_cast<const float4*>(A + row * lda + t.a_col + k))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        tc_commit(bar(2 + s));
-      }
-      __syncwarp();
-    }
-  }
-  mbar_wait(bar(2 + ((nc - 1) & 1)), ((nc - 1) >> 1) & 1);
-  tc_fence_after();
-  // epilogue: warps w and w + 4 own TMEM lanes (rows) 32 (w % 4) ..; they
-  // take alternate 16-column groups
-  const int quarter = warp & 3;
-  const int64_t row = r0 + quarter * 32 + lane;
-  float* out = C + row * ldc + t.c_col;
-  for (int j = (warp >> 2) * 16; j < t.N; j += 32) {
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)j, v);
-    if (row < n_rows) {
+      };
+      // one chunk: its B bulk copy, then its A rows (loaded a chunk earlier)
+      // split into the ring
+      auto chunk = [&](int c, const float4* v) {
+        if (pt == 0) {
+          mbar_wait(bar(BE + sb), ((kb / NB) & 1) ^ 1);
+          mbar_expect_tx(bar(BF + sb), bbytes);
+          bulk_g2s(sB + sb * B_STAGE, Bimg + t.b_off + (int64_t)c * bbytes, bbytes, bar(BF + sb), pol);
+        }
+        if (++sb == NB) sb = 0;
+        ++kb;
+        mbar_wait(bar(AE + sa), ((ka / NA) & 1) ^ 1);
+        const uint32_t sh = sA + sa * A_STAGE, sl = sh + A_BYTES;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (j + 4 * q < t.n_valid)
-          reinterpret_cast<float4*>(out + j)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int i = 0; i < 4; ++i) {
+          const int r = (pt >> 3) + 32 * i;
+          const float4 h = make_float4(to_tf32(v[i].x), to_tf32(v[i].y), to_tf32(v[i].z), to_tf32(v[i].w));
+          const float4 l = make_float4(to_tf32(v[i].x - h.x), to_tf32(v[i].y - h.y), to_tf32(v[i].z - h.z),
+                                       to_tf32(v[i].w - h.w));
+          const uint32_t o = sw128(r, u);
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sh + o), "f"(h.x), "f"(h.y), "f"(h.z),
+                       "f"(h.w)
+                       : "memory");
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sl + o), "f"(l.x), "f"(l.y), "f"(l.z),
+                       "f"(l.w)
+                       : "memory");
+        }
+        fence_async_smem();
+        mbar_arrive(bar(AF + sa));
+        if (++sa == NA) sa = 0;
+        ++ka;
+      };
+      float4 va[4], vb[4];  // two register buffers: chunk c + 1 loads while chunk c converts
+      load(0, va);
+      for (int c = 0; c < nc; c += 2) {
+        load(c + 1, vb);
+        chunk(c, va);
+        if (c + 1 < nc) {
+          load(c + 2, va);
+          chunk(c + 1, vb);
+        }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ---- MMA issuer: 3 passes per K step into the item's TMEM buffer
+    int sa = 0, sb = 0;
+    uint32_t ka = 0, kb = 0, j = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++j) {
+      const TcTile t = tiles[it / n_rt];
+      const int nc = (t.K + 31) >> 5;
+      const uint32_t idesc = idesc_tf32(t.N);
+      const int ab = j & 1;
+      mbar_wait(bar(CE + ab), ((j >> 1) & 1) ^ 1);  // the epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t acc = tmem + (uint32_t)(ab * 256);
+      for (int c = 0; c < nc; ++c) {
+        mbar_wait(bar(AF + sa), (ka / NA) & 1);
+        mbar_wait(bar(BF + sb), (kb / NB) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t ah_a = sA + sa * A_STAGE, bh_a = sB + sb * B_STAGE;
+          const uint64_t ah = sdesc(ah_a), al = sdesc(ah_a + A_BYTES), bh = sdesc(bh_a), bl = sdesc(bh_a + t.N * 128);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 (32 bytes) per instruction
+            mma_tf32(acc, ah + 2 * ks, bh + 2 * ks, idesc, (c | ks) ? 1u : 0u);
+            mma_tf32(acc, ah + 2 * ks, bl + 2 * ks, idesc, 1u);
+            mma_tf32(acc, al + 2 * ks, bh + 2 * ks, idesc, 1u);
+          }
+          tc_commit(bar(AE + sa));
+          tc_commit(bar(BE + sb));
+          if (c == nc - 1) tc_commit(bar(CF + ab));
+        }
+        __syncwarp();
+        if (++sa == NA) sa = 0;
+        ++ka;
+        if (++sb == NB) sb = 0;
+        ++kb;
+      }
+    }
+  } else {
+    // ---- epilogue: warp w drains TMEM lanes 32 w .. into the output rows
+    uint32_t j = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++j) {
+      const TcTile t = tiles[it / n_rt];
+      const int64_t row = (it % n_rt) * TM + warp * 32 + lane;
+      const int ab = j & 1;
+      mbar_wait(bar(CF + ab), (j >> 1) & 1);
+      tc_fence_after();
+      float* out = C + row * ldc + t.c_col;
+      for (int c0 = 0; c0 < t.N; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(ab * 256 + c0), v);
+        if (row < n_rows) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c0 + 4 * q < t.n_valid)
+              reinterpret_cast<float4*>(out + c0)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bar(CE + ab));
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+  if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
 // the expanded order block W (N x K; m = 0: W0, m >= 1: [[Wr, Wi], [-Wi, Wr]])
@@ -253,8 +320,15 @@ void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t
     init = true;
   }
   if (n_rows <= 0) return;
-  k_gemm_tf32x3<<<dim3((unsigned)((n_rows + TM - 1) / TM), (unsigned)n_tiles), THREADS, SMEM_BYTES, st>>>(
-      A, lda, n_rows, img, tiles, C, ldc);
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    ESG_CUDA(cudaGetDevice(&dev));
+    ESG_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t items = (n_rows + TM - 1) / TM * n_tiles;
+  const int grid = (int)(items < n_sm ? items : n_sm);
+  k_gemm_tf32x3<<<grid, THREADS, SMEM_BYTES, st>>>(A, lda, n_rows, img, tiles, n_tiles, C, ldc);
   ESG_CUDA(cudaGetLastError());
 }
 
