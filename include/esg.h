@@ -187,7 +187,10 @@ int esg_prepare(esg_model* m, const esg_graph* g, const esg_plan* plan, const in
 int esg_prepared_info(const esg_model* m, int64_t info[3]); /* n_rows, n_owned, n_edges */
 
 /* DistributedRunner::forward + heads (distributed.h:193, network.h:115-164).
- * Host outputs may be NULL (results stay on the device). */
+ * Host outputs may be NULL (results stay on the device).  When the given
+ * host buffers are pinned (cudaHostAlloc / cudaHostRegister), the heads of
+ * each final chunk are computed and copied while the last edge block still
+ * runs; pageable buffers are filled after the forward.  Same values either way. */
 int esg_forward(esg_model* m, float* node_out /* n_owned*out_len */,
                 float* edge_out /* n_edges*out_len */, esg_timing* timing);
 /* Per-category kernel timing with CUDA events on the launching stream.

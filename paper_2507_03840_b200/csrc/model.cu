@@ -906,10 +906,10 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       }
       if (tc)
         k_node_update<L, E, uint16_t, true><<<ch.second - ch.first, 128, dyn_bf16, st>>>(
-            (const uint16_t*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->rc);
+            (const uint16_t*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->prefetch);
       else
         k_node_update<L, E, float, false><<<ch.second - ch.first, 128, dyn, st>>>(D->Y, D->dir, D->seg, ch.first, e0, att,
-                                                                          D->nodes, D->nodes_alt, D->logits, D->rc);
+                                                                          D->nodes, D->nodes_alt, D->logits, D->prefetch);
       ++ctx->launches;
     }
   }

@@ -123,9 +123,9 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
     // pf 1: the tile's edge rows (contiguous) in one bulk prefetch, source
     // rows one each (destination rows repeat along the dst-sorted edges);
     // pf 2: every gathered row
-    if (pf == 2 ? q == 0 : (q == 0 && p == 0 && pf == 1)) prefetch_bulk(rowp, H * E * 4);
+    if ((pf & 3) == 2 ? q == 0 : (q == 0 && p == 0 && (pf & 3) == 1)) prefetch_bulk(rowp, H * E * 4);
   }
-  if (pf == 1 && threadIdx.x == 0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
+  if ((pf & 3) == 1 && threadIdx.x == 0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   __syncthreads();
   wigner_tile_gen<L, DSP, NG>(sdir, ne, sD);
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
   const int64_t t0 = e0 + (int64_t)blockIdx.x * TE;
   const int ne = (int)min64(TE, e0 + n_e - t0);
   const int e = threadIdx.x / Q, q = threadIdx.x % Q;
-  if (pf) {  // the tile's edge rows (contiguous) and its Y runs
+  if (pf & 3) {  // the tile's edge rows (contiguous) and its Y runs
     if (threadIdx.x == 0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
     prefetch_y<H * E>(Yin, t0 - e0, ne, threadIdx.x >> 5, blockDim.x >> 5);
   }
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
                                                      const int64_t* __restrict__ seg, int j0, int64_t e0,
                                                      const float* __restrict__ att,
                                                      const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
-                                                     float* __restrict__ logit_scratch, WigRecipe rc) {
+                                                     float* __restrict__ logit_scratch, int pf) {
   using G = Geo<L>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, HE = H * E, Q = E / 4, HQ = H * Q, NSLOT = 32 / Q;
   constexpr bool YSMEM = sizeof(YT) == 2;  // bf16 Y: stage the tile's rows in SMEM
@@ -360,8 +360,11 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
     if ((t & 31) == 0) sred[t >> 5] = z;
     __syncthreads();
     z = (sred[0] + sred[1]) + (sred[2] + sred[3]);
+    if (pf & 4) prefetch_y<HE>(Yin, b - e0, (int)min64(TE, en - b), t >> 5, 4);
     for (int64_t k0 = b; k0 < en; k0 += TE) {
       const int ne = (int)min64(TE, en - k0);
+      // pf & 4: the next tile's Y rows (one lane per warp issues the bulk prefetches)
+      if ((pf & 4) && k0 + TE < en) prefetch_y<HE>(Yin, k0 + TE - e0, (int)min64(TE, en - k0 - TE), t >> 5, 4);
       __syncthreads();  // the previous tile's D is no longer read
       for (int i = t; i < ne * 3; i += 128) sdir[i] = dir[(k0 - e0) * 3 + i];
       for (int i = t; i < ne; i += 128) sA[i] = lg[k0 - b + i] / z;
