@@ -119,7 +119,7 @@ struct DeviceModel {
   std::vector<cudaEvent_t> out_ev;
   size_t out_ev_used = 0;
   int precision = ESG_LINEAR_FP32;
-  int prefetch = 1;  // L2 prefetch flags (ESG_PREFETCH): & 3 rotate kernels mode 0/1/2, & 4 node update Y
+  int prefetch = 1;  // L2 prefetch mode of the rotate kernels (ESG_PREFETCH=0/1/2)
   size_t a1_elem = 4;
 };
 

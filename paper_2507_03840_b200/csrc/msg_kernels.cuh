@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
                                                      const int64_t* __restrict__ seg, int j0, int64_t e0,
                                                      const float* __restrict__ att,
                                                      const float* __restrict__ nodes_in, float* __restrict__ nodes_out,
-                                                     float* __restrict__ logit_scratch, int pf) {
+                                                     float* __restrict__ logit_scratch, int /*pf*/) {
   using G = Geo<L>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, HE = H * E, Q = E / 4, HQ = H * Q, NSLOT = 32 / Q;
   constexpr bool YSMEM = sizeof(YT) == 2;  // bf16 Y: stage the tile's rows in SMEM
@@ -360,11 +360,8 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
     if ((t & 31) == 0) sred[t >> 5] = z;
     __syncthreads();
     z = (sred[0] + sred[1]) + (sred[2] + sred[3]);
-    if (pf & 4) prefetch_y<HE>(Yin, b - e0, (int)min64(TE, en - b), t >> 5, 4);
     for (int64_t k0 = b; k0 < en; k0 += TE) {
       const int ne = (int)min64(TE, en - k0);
-      // pf & 4: the next tile's Y rows (one lane per warp issues the bulk prefetches)
-      if ((pf & 4) && k0 + TE < en) prefetch_y<HE>(Yin, k0 + TE - e0, (int)min64(TE, en - k0 - TE), t >> 5, 4);
       __syncthreads();  // the previous tile's D is no longer read
       for (int i = t; i < ne * 3; i += 128) sdir[i] = dir[(k0 - e0) * 3 + i];
       for (int i = t; i < ne; i += 128) sA[i] = lg[k0 - b + i] / z;
