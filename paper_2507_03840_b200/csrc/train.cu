@@ -206,15 +206,29 @@ __global__ void __launch_bounds__(256) k_outer_tiled(const float* __restrict__ g
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // the next stage's 2 x 4 values are loaded into registers while this
+  // stage's outer products run (TE * 64 / 256 = 4 per thread and operand)
+  float rg[4], rx[4];
+  auto fetch = [&](int64_t e0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = threadIdx.x + 256 * i, e = u / 64, c = u % 64;
+      const int64_t ee = e0 + e;
+      rg[i] = (ee < s1 && t.n0 + c < t.N) ? g[ee * G::H * cg + go + c] : 0.f;
+      rx[i] = (ee < s1 && t.k0 + c < t.K) ? x[ee * G::H * cx + xo + c] : 0.f;
+    }
+  };
+  fetch(s0);
   for (int64_t e0 = s0; e0 < s1; e0 += TE) {
     __syncthreads();
-    for (int u = threadIdx.x; u < TE * 64; u += 256) {
-      const int e = u / 64, c = u % 64;
-      const int64_t ee = e0 + e;
-      sg[e][c] = (ee < s1 && t.n0 + c < t.N) ? g[ee * G::H * cg + go + c] : 0.f;
-      sx[e][c] = (ee < s1 && t.k0 + c < t.K) ? x[ee * G::H * cx + xo + c] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = threadIdx.x + 256 * i;
+      sg[u / 64][u % 64] = rg[i];
+      sx[u / 64][u % 64] = rx[i];
     }
     __syncthreads();
+    if (e0 + TE < s1) fetch(e0 + TE);
 #pragma unroll 4
     for (int e = 0; e < TE; ++e) {
       float a[4], b[4];
