@@ -699,7 +699,9 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     ++M->ctx->launches;
   }
   // destination-aligned chunks of about chunk_cap edges
-  const int64_t cap = std::max<int64_t>(std::min<int64_t>(ne, 2 << 20), 1);
+  int64_t chunk_edges = 2 << 20;  // ESG_CHUNK_EDGES overrides (experiments)
+  if (const char* ce = std::getenv("ESG_CHUNK_EDGES")) chunk_edges = std::max<int64_t>(std::atoll(ce), 1024);
+  const int64_t cap = std::max<int64_t>(std::min<int64_t>(ne, chunk_edges), 1);
   int64_t maxseg = 0;
   for (int j = 0; j < n_owned; ++j) maxseg = std::max(maxseg, seg[j + 1] - seg[j]);
   D->chunk_cap = std::max(cap, maxseg);
