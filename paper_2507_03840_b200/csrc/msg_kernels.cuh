@@ -366,9 +366,9 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
       for (int i = t; i < ne * 3; i += 128) sdir[i] = dir[(k0 - e0) * 3 + i];
       for (int i = t; i < ne; i += 128) sA[i] = lg[k0 - b + i] / z;
       if constexpr (YSMEM) {  // the tile's Y rows arrive while the Wigner blocks are computed
-        for (int u = t; u < (HE / 8) * ne; u += 128) {
-          const int blk = u / ne, i = u - blk * ne;
-          cp_async16(sY + ((blk * TE + i) << 3), Yin + y_index<HE>(Yin, k0 + i - e0, blk * 8));
+        for (int u = t; u < (HE / 8) * TE; u += 128) {  // TE a power of two: no runtime division
+          const int blk = u / TE, i = u % TE;
+          if (i < ne) cp_async16(sY + ((blk * TE + i) << 3), Yin + y_index<HE>(Yin, k0 + i - e0, blk * 8));
         }
       }
       __syncthreads();
