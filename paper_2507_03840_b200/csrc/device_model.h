@@ -102,9 +102,6 @@ struct DeviceModel {
   bool train_stale = true;  // set by every prepare
   int64_t block_values = 0;
   cudaEvent_t ev[8];
-  // expanded Wigner recursion (device copies)
-  WigRecipe rc{};
-  void* rc_mem[4] = {nullptr, nullptr, nullptr, nullptr};
   // optional per-category kernel timing (esg_profile_*): events around launches
   bool profile = false;
   std::vector<cudaEvent_t> pool;

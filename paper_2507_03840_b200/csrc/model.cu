@@ -304,29 +304,6 @@ void prof_collect(DeviceModel* D) {
 }
 
 
-void upload_wigner_coef(int L) {
-  static bool done = false;
-  if (done) return;
-  WignerCoef wc{};
-  auto delta = [](int a, int b) { return a == b ? 1.0 : 0.0; };
-  int off = 0;
-  for (int l = 0; l <= L && l <= 4; ++l) {
-    const int d = 2 * l + 1;
-    if (l >= 2)
-      for (int m = -l; m <= l; ++m)
-        for (int n = -l; n <= l; ++n) {
-          const double denom = (std::abs(n) == l) ? (2.0 * l) * (2.0 * l - 1.0) : double(l + n) * double(l - n);
-          const int q = off + (m + l) * d + (n + l);
-          wc.u[q] = (float)std::sqrt(double(l + m) * double(l - m) / denom);
-          wc.v[q] = (float)(0.5 * std::sqrt((1.0 + delta(m, 0)) * (l + std::abs(m) - 1.0) * (l + std::abs(m)) / denom) *
-                            (1.0 - 2.0 * delta(m, 0)));
-          wc.w[q] = (float)(-0.5 * std::sqrt((l - std::abs(m) - 1.0) * (l - std::abs(m)) / denom) * (1.0 - delta(m, 0)));
-        }
-    off += d * d;
-  }
-  ESG_CUDA(cudaMemcpyToSymbol(c_wig, &wc, sizeof(wc)));
-  done = true;
-}
 
 
 bool supported(int L, int E) { return (L == 4 || L == 2) && (E == 16 || E == 8); }
@@ -505,86 +482,8 @@ void model_device_create(esg_model* M) {
   M->dev->E = E;
   M->dev->H = (L + 1) * (L + 1);
   M->dev->precision = M->cfg.linear_precision;
-  for (auto& e : M->dev->ev) ESG_CUDA(cudaEventCreate(&e));
   ESG_CUDA(cudaSetDevice(M->ctx->device));
-  upload_wigner_coef(L);
-  // wigner.cpp:47-83 multiplied out: entry = sum coef * R[ri] * prev[pi]
-  std::vector<int> start{0};
-  std::vector<float> coef;
-  std::vector<uint8_t> ri;
-  std::vector<uint16_t> pi;
-  auto delta = [](int a, int b) { return a == b ? 1.0 : 0.0; };
-  for (int l = 0; l <= L; ++l) {
-    const int d = 2 * l + 1, dp = 2 * l - 1;
-    for (int m = -l; m <= l; ++m)
-      for (int n = -l; n <= l; ++n) {
-        if (l >= 2) {
-          struct T {
-            double c;
-            int r, p;
-          };
-          auto P = [&](double s, int i, int a, int b, std::vector<T>& out) {
-            auto idx = [&](int x, int y) { return (x + l - 1) * dp + (y + l - 1); };
-            if (b == l) {
-              out.push_back({s, (i + 1) * 3 + 2, idx(a, l - 1)});
-              out.push_back({-s, (i + 1) * 3 + 0, idx(a, -l + 1)});
-            } else if (b == -l) {
-              out.push_back({s, (i + 1) * 3 + 2, idx(a, -l + 1)});
-              out.push_back({s, (i + 1) * 3 + 0, idx(a, l - 1)});
-            } else {
-              out.push_back({s, (i + 1) * 3 + 1, idx(a, b)});
-            }
-          };
-          const double denom = (std::abs(n) == l) ? (2.0 * l) * (2.0 * l - 1.0) : double(l + n) * double(l - n);
-          const double u = std::sqrt(double(l + m) * double(l - m) / denom);
-          const double v = 0.5 * std::sqrt((1.0 + delta(m, 0)) * (l + std::abs(m) - 1.0) * (l + std::abs(m)) / denom) *
-                           (1.0 - 2.0 * delta(m, 0));
-          const double w = -0.5 * std::sqrt((l - std::abs(m) - 1.0) * (l - std::abs(m)) / denom) * (1.0 - delta(m, 0));
-          std::vector<T> terms;
-          if (u != 0.0) P(u, 0, m, n, terms);
-          if (v != 0.0) {
-            if (m == 0) {
-              P(v, 1, 1, n, terms);
-              P(v, -1, -1, n, terms);
-            } else if (m > 0) {
-              P(v * std::sqrt(1.0 + delta(m, 1)), 1, m - 1, n, terms);
-              if (m != 1) P(-v, -1, -m + 1, n, terms);
-            } else {
-              if (m != -1) P(v, 1, m + 1, n, terms);
-              P(v * std::sqrt(1.0 + delta(m, -1)), -1, -m - 1, n, terms);
-            }
-          }
-          if (w != 0.0) {
-            if (m > 0) {
-              P(w, 1, m + 1, n, terms);
-              P(w, -1, -m - 1, n, terms);
-            } else {
-              P(w, 1, m - 1, n, terms);
-              P(-w, -1, -m + 1, n, terms);
-            }
-          }
-          for (const auto& t : terms) {
-            coef.push_back((float)t.c);
-            ri.push_back((uint8_t)t.r);
-            pi.push_back((uint16_t)t.p);
-          }
-        }
-        start.push_back((int)coef.size());
-      }
-    (void)d;
-  }
-  DeviceModel* D = M->dev;
-  auto up = [&](int slot, const void* h, size_t bytes) {
-    void* p = nullptr;
-    ESG_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 4)));
-    if (bytes) ESG_CUDA(cudaMemcpy(p, h, bytes, cudaMemcpyHostToDevice));
-    D->rc_mem[slot] = p;
-    return p;
-  };
-  D->rc.start = (const int*)up(0, start.data(), sizeof(int) * start.size());
-  D->rc.coef = (const float*)up(1, coef.data(), sizeof(float) * coef.size());
-  D->rc.ri = (const uint8_t*)up(2, ri.data(), ri.size());
-  D->rc.pi = (const uint16_t*)up(3, pi.data(), sizeof(uint16_t) * pi.size());
+  for (auto& e : M->dev->ev) ESG_CUDA(cudaEventCreate(&e));
 }
 
 void train_free(DeviceModel* D);  // train.cu

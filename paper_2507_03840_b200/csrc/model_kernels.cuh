@@ -46,12 +46,6 @@ struct Lay1 {
   __host__ __device__ static constexpr int N2(int m) { return Geo<L>::rows(m) * E; }      // lin2 N
 };
 
-// Wigner recursion coefficients u, v, w for l = 2..L (wigner.cpp:64-76),
-// indexed like the stacked blocks; filled by the host.
-struct WignerCoef {
-  float u[165], v[165], w[165];
-};
-static __constant__ WignerCoef c_wig;  // per translation unit; see upload_wigner_coef
 
 // Rotation taking the unit edge direction onto +y: R = Rx(-beta) Ry(-alpha)
 // with alpha = atan2(ux, uz), beta = acos(uy) (align.cpp:32-39), written with
@@ -113,101 +107,6 @@ __device__ void wigner_tile_gen(const float* dirs, int ne, float* D) {
   }
   __syncthreads();
   wigner_levels<L, 2, NG>(act, warp, R, D + lane * DSP);
-}
-
-// Ivanic-Ruedenberg recursion expanded on the host into flat recipes: entry
-// q of degree l (stacked index doff(l) + (m+l)(2l+1) + (n+l)) is
-// sum_t coef[t] * R[ri[t]] * prev[pi[t]] with R the 3x3 band-1 block and prev
-// the degree l-1 block (wigner.cpp:58-81 with the u/v/w/P terms multiplied
-// out; zero-coefficient terms skipped exactly as the reference skips them).
-struct WigRecipe {
-  const int* start;   // per stacked entry (DS + 1)
-  const float* coef;  // per term
-  const uint8_t* ri;  // R index 0..8
-  const uint16_t* pi; // index inside the degree l-1 block
-};
-
-// Branch-free cooperative Wigner blocks for a tile of `ne` edges.
-template <int L, int DSP>
-__device__ void wigner_tile_recipe(const float* dirs, int ne, float* D, WigRecipe rc) {
-  using G = Geo<L>;
-  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    float R[9];
-    align_to_y(dirs[3 * e], dirs[3 * e + 1], dirs[3 * e + 2], R);
-    float* d = D + e * DSP;
-    d[0] = 1.f;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) d[1 + i] = R[i];
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int l = 2; l <= L; ++l) {
-    const int dd = (2 * l + 1) * (2 * l + 1);
-    const int ob = G::doff(l), op = G::doff(l - 1);
-    for (int t = threadIdx.x; t < ne * dd; t += blockDim.x) {
-      const int e = t / dd, q = ob + t % dd;
-      const float* R = D + e * DSP + 1;
-      const float* pv = D + e * DSP + op;
-      float acc = 0.f;
-      const int t1 = __ldg(rc.start + q + 1);
-      for (int k = __ldg(rc.start + q); k < t1; ++k) acc = fmaf(__ldg(rc.coef + k) * R[__ldg(rc.ri + k)], pv[__ldg(rc.pi + k)], acc);
-      D[e * DSP + q] = acc;
-    }
-    __syncthreads();
-  }
-}
-
-// Cooperative Wigner blocks for a tile of `ne` edges: D[e*DSP + doff(l) + ...].
-// dirs: 3 floats per edge (displacement).  All threads of the block call it.
-template <int L, int DSP>
-__device__ void wigner_tile(const float* dirs, int ne, float* D) {
-  using G = Geo<L>;
-  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    float R[9];
-    align_to_y(dirs[3 * e], dirs[3 * e + 1], dirs[3 * e + 2], R);
-    float* d = D + e * DSP;
-    d[0] = 1.f;
-    for (int i = 0; i < 9; ++i) d[1 + i] = R[i];
-  }
-  __syncthreads();
-#pragma unroll 1
-  for (int l = 2; l <= L; ++l) {
-    const int dd = 2 * l + 1, dp = 2 * l - 1;
-    const int cnt = ne * dd * dd;
-    const int ob = G::doff(l), op = G::doff(l - 1);
-    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
-      const int e = t / (dd * dd), q = t % (dd * dd);
-      const int m = q / dd - l, n = q % dd - l;
-      const float* R = D + e * DSP + 1;          // band 1, indices -1..1
-      const float* pv = D + e * DSP + op;        // degree l-1
-      auto pm = [&](int a, int b) { return pv[(a + l - 1) * dp + (b + l - 1)]; };
-      auto P = [&](int i, int a, int b) {
-        const float* r = R + (i + 1) * 3;
-        if (b == l) return r[2] * pm(a, l - 1) - r[0] * pm(a, -l + 1);
-        if (b == -l) return r[2] * pm(a, -l + 1) + r[0] * pm(a, l - 1);
-        return r[1] * pm(a, b);
-      };
-      const float cu = c_wig.u[ob + q], cv = c_wig.v[ob + q], cw = c_wig.w[ob + q];
-      float acc = 0.f;
-      if (cu != 0.f) acc += cu * P(0, m, n);
-      if (cv != 0.f) {
-        float vt;
-        if (m == 0)
-          vt = P(1, 1, n) + P(-1, -1, n);
-        else if (m > 0)
-          vt = P(1, m - 1, n) * (m == 1 ? 1.41421356237f : 1.f) - (m == 1 ? 0.f : P(-1, -m + 1, n));
-        else
-          vt = (m == -1 ? 0.f : P(1, m + 1, n)) + P(-1, -m - 1, n) * (m == -1 ? 1.41421356237f : 1.f);
-        acc += cv * vt;
-      }
-      if (cw != 0.f) {
-        const float wt = m > 0 ? P(1, m + 1, n) + P(-1, -m - 1, n) : P(1, m - 1, n) - P(-1, -m + 1, n);
-        acc += cw * wt;
-      }
-      D[e * DSP + ob + q] = acc;
-    }
-    __syncthreads();
-  }
 }
 
 }  // namespace esg
