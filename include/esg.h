@@ -193,6 +193,13 @@ int esg_prepared_info(const esg_model* m, int64_t info[3]); /* n_rows, n_owned, 
  * runs; pageable buffers are filled after the forward.  Same values either way. */
 int esg_forward(esg_model* m, float* node_out /* n_owned*out_len */,
                 float* edge_out /* n_edges*out_len */, esg_timing* timing);
+/* The same with pinned host buffers, returning once the compute is done and
+ * the output copies are queued; esg_forward_wait completes them (the buffers
+ * must not be read or reused before).  A following forward runs while those
+ * copies drain and waits for them only before its heads overwrite the device
+ * outputs.  Pageable buffers: identical to esg_forward. */
+int esg_forward_async(esg_model* m, float* node_out, float* edge_out, esg_timing* timing);
+int esg_forward_wait(esg_model* m);
 /* Per-category kernel timing with CUDA events on the launching stream.
  * esg_profile(m, enable, ms, counts): copies the accumulated milliseconds
  * and launch counts (ESG_PROF_NCAT entries each, may be NULL), then if

@@ -25,7 +25,8 @@ void model_device_destroy(esg_model* M);
 void model_upload_params(esg_model* M);
 void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const int32_t* species);
 void model_forward(esg_model* M, esg_timing* tm);
-void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float* edge_out);
+void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float* edge_out, bool async);
+void model_outputs_wait(esg_model* M);
 void model_profile(esg_model* M, int enable, double* ms, int64_t* counts);
 void model_outputs(const esg_model* M, const float** no, const float** eo, const float** nf, const float** ef);
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
@@ -228,6 +229,8 @@ int esg_ctx_destroy(esg_ctx* ctx) {
   if (!ctx) return ESG_OK;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   ctx->cache.flush();
+  if (ctx->zc) cudaFreeHost(ctx->zc);
+  if (ctx->up) cudaFreeHost(ctx->up);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   ESG_API_END
@@ -668,7 +671,25 @@ int esg_forward(esg_model* m, float* node_out, float* edge_out, esg_timing* timi
   NEED(m, "model");
   if (!m->ctx || !m->dev) usage("model was created without a device context");
   ESG_CUDA(cudaSetDevice(m->ctx->device));
-  model_forward_to_host(m, timing, node_out, edge_out);
+  model_forward_to_host(m, timing, node_out, edge_out, false);
+  ESG_API_END
+}
+
+int esg_forward_async(esg_model* m, float* node_out, float* edge_out, esg_timing* timing) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_forward_to_host(m, timing, node_out, edge_out, true);
+  ESG_API_END
+}
+
+int esg_forward_wait(esg_model* m) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_outputs_wait(m);
   ESG_API_END
 }
 

@@ -115,6 +115,10 @@ struct DeviceModel {
   cudaStream_t copy_st = nullptr;
   std::vector<cudaEvent_t> out_ev;
   size_t out_ev_used = 0;
+  // copies of a previous call may still read node_out / edge_out (async
+  // forward): heads of the next forward wait on this event first
+  cudaEvent_t copies_done = nullptr;
+  bool copies_pending = false;
   int precision = ESG_LINEAR_FP32;
   int prefetch = 1;  // L2 prefetch mode of the rotate kernels (ESG_PREFETCH=0/1/2)
   size_t a1_elem = 4;

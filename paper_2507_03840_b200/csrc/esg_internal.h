@@ -127,7 +127,21 @@ struct esg_ctx {
   ncclComm_t comm = nullptr;
   int64_t launches = 0;  // kernels launched by this library
   esg::BlockCache cache;
+  // zero-copy readback buffer (pinned, mapped): small device -> host reads
+  // go through a kernel store instead of the copy engine, so they never queue
+  // behind the multi-GB output copies of an async forward
+  void* zc = nullptr;
+  size_t zc_cap = 0;
+  // pinned staging for small host -> device uploads (pageable copies are
+  // synchronous and can serialise behind in-flight async copies)
+  void* up = nullptr;
+  size_t up_cap = 0;
 };
+
+namespace esg {
+void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes);  // graph.cu; bytes % 4 == 0
+void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes);  // graph.cu; synchronous
+}
 
 struct esg_graph {
   esg_ctx* ctx = nullptr;

@@ -20,6 +20,9 @@
 #include <type_traits>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -152,6 +155,15 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   if (!(r_cut > 0.0)) usage("cutoff must be positive");
   if (n < 1) usage("structure has no atoms");
   cudaStream_t st = ctx->stream;
+  const bool dbg = std::getenv("ESG_DEBUG_BUILD") != nullptr;
+  auto tmark = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[esg build] %-24s %.4f s\n", what, std::chrono::duration<double>(now - tmark).count());
+    tmark = now;
+  };
   // every device buffer through the context's block cache (esg_internal.h)
   auto dalloc_c = [&](auto* type_tag, size_t n_el) {
     using T = std::remove_pointer_t<decltype(type_tag)>;
@@ -215,10 +227,12 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   int* d_start = dalloc_c((int*)nullptr, nbins + 1);
   int* d_cur = dalloc_c((int*)nullptr, nbins);
   int* d_atoms = dalloc_c((int*)nullptr, n);
-  ESG_CUDA(cudaMemcpyAsync(d_pos, pos.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
-  ESG_CUDA(cudaMemcpyAsync(d_img, off.data(), sizeof(double) * off.size(), cudaMemcpyHostToDevice, st));
+  mark("host prologue");
+  h2d_staged(ctx, d_pos, pos.data(), sizeof(double) * 3 * n);
+  h2d_staged(ctx, d_img, off.data(), sizeof(double) * off.size());
   ESG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int) * (nbins + 1), st));
   ESG_CUDA(cudaMemsetAsync(d_cur, 0, sizeof(int) * nbins, st));
+  mark("uploads");
   k_bin_atoms<<<(n + 255) / 256, 256, 0, st>>>(d_pos, n, g, d_bin, d_cnt);
   ++ctx->launches;
   size_t tmp_bytes = 0;
@@ -243,8 +257,9 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_cnt_e, G->d_off, n + 1, st);
   ctx->cache.release(d_tmp);
   int64_t E = 0;
-  ESG_CUDA(cudaMemcpyAsync(&E, G->d_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  ESG_CUDA(cudaStreamSynchronize(st));
+  mark("count pass");
+  d2h_small(ctx, &E, G->d_off + n, sizeof(int64_t));
+  mark("edge count readback");
   if (E > (int64_t)std::numeric_limits<int>::max() - 1) usage("graph exceeds 2^31 edges");
   G->E = E;
 
@@ -255,13 +270,20 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
     k_edges<true><<<blocks, threads, 0, st>>>(d_pos, n, g, d_img, d_start, d_atoms, G->d_off, d_keys, d_dst);
     ++ctx->launches;
     tmp_bytes = 0;
-    cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
-                                       G->d_off + 1, st);
+    // one CTA per destination segment, no host readback (DeviceSegmentedSort
+    // reads its segment-size groups back to the host, which would queue behind
+    // in-flight output copies); keys are unique per segment, so the order is
+    // the same as any other sort's.  Bits: packed shift (30) + source index.
+    int end_bit = 32;
+    while ((int64_t(1) << (end_bit - 32)) < n) ++end_bit;
+    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
+                                            G->d_off + 1, 0, end_bit, st);
     d_tmp = ctx->cache.alloc(tmp_bytes);
-    cub::DeviceSegmentedSort::SortKeys(d_tmp, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off, G->d_off + 1,
-                                       st);
+    cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
+                                            G->d_off + 1, 0, end_bit, st);
     ctx->cache.release(d_tmp);
   }
+  mark("sort");
   G->d_src = dalloc_c((int32_t*)nullptr, E);
   G->d_shift = dalloc_c((uint32_t*)nullptr, E);
   G->d_disp = dalloc_c((double*)nullptr, 3 * (size_t)E);
@@ -276,7 +298,50 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   for (void* p : {(void*)d_pos, (void*)d_img, (void*)d_bin, (void*)d_cnt, (void*)d_start, (void*)d_cur,
                   (void*)d_atoms, (void*)d_cnt_e, (void*)d_keys, (void*)d_keys_sorted, (void*)d_dst})
     ctx->cache.release(p);
+  mark("finalize + release");
   return G;
+}
+
+namespace {
+__global__ void k_copy_words(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+}  // namespace
+
+void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes) {
+  if (bytes == 0) return;
+  if (ctx->up_cap < bytes) {
+    if (ctx->up) cudaFreeHost(ctx->up);
+    ctx->up = nullptr;
+    ctx->up_cap = 0;
+    ESG_CUDA(cudaHostAlloc(&ctx->up, bytes, cudaHostAllocDefault));
+    ctx->up_cap = bytes;
+  }
+  ESG_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffer is free
+  std::memcpy(ctx->up, host, bytes);
+  ESG_CUDA(cudaMemcpyAsync(dev, ctx->up, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ESG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  if (bytes == 0) return;
+  if (ctx->zc_cap < bytes) {
+    if (ctx->zc) cudaFreeHost(ctx->zc);
+    ctx->zc = nullptr;
+    ctx->zc_cap = 0;
+    ESG_CUDA(cudaHostAlloc(&ctx->zc, bytes, cudaHostAllocMapped));
+    ctx->zc_cap = bytes;
+  }
+  void* dptr = nullptr;
+  ESG_CUDA(cudaHostGetDevicePointer(&dptr, ctx->zc, 0));
+  const size_t n = bytes / 4;
+  k_copy_words<<<(unsigned)std::min<size_t>((n + 255) / 256, 1024), 256, 0, ctx->stream>>>(
+      static_cast<const uint32_t*>(dev), static_cast<uint32_t*>(dptr), n);
+  ++ctx->launches;
+  ESG_CUDA(cudaGetLastError());
+  ESG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(host, ctx->zc, bytes);
 }
 
 }  // namespace esg
@@ -284,7 +349,7 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
 void esg_graph::host_sync_offsets() const {
   if ((int64_t)h_off.size() == n + 1) return;
   h_off.resize(n + 1);
-  ESG_CUDA(cudaMemcpy(h_off.data(), d_off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+  esg::d2h_small(ctx, h_off.data(), d_off, sizeof(int64_t) * (n + 1));
 }
 void esg_graph::host_sync() const {
   host_sync_offsets();

@@ -512,6 +512,8 @@ void model_device_destroy(esg_model* M) {
   for (auto p : D->w1b) free_ptr(p);
   for (auto p : D->w2b) free_ptr(p);
   for (auto& e : D->ev) cudaEventDestroy(e);
+  if (D->copies_pending) cudaEventSynchronize(D->copies_done);
+  if (D->copies_done) cudaEventDestroy(D->copies_done);
   for (auto& e : D->out_ev) cudaEventDestroy(e);
   if (D->copy_st) cudaStreamDestroy(D->copy_st);
   delete D;
@@ -526,6 +528,8 @@ __global__ void k_fill_dst(const int64_t* __restrict__ off, int n, int* __restri
   if (j >= n) return;
   for (int64_t k = off[j] + (threadIdx.x & 31); k < off[j + 1]; k += 32) dst_row[k] = j;
 }
+
+void model_outputs_wait(esg_model* M);
 
 void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const int32_t* species) {
   DeviceModel* D = M->dev;
@@ -551,7 +555,7 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     row_global.resize(g->n);
     for (int i = 0; i < g->n; ++i) row_global[i] = i;
     seg.resize(g->n + 1);
-    ESG_CUDA(cudaMemcpy(seg.data(), g->d_off, sizeof(int64_t) * (g->n + 1), cudaMemcpyDeviceToHost));
+    d2h_small(M->ctx, seg.data(), g->d_off, sizeof(int64_t) * (g->n + 1));
   }
   std::vector<int> slot(n_rows);
   D->row_species.resize(n_rows);
@@ -575,15 +579,15 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   D->seg = grow(D->seg, D->cap_seg, n_owned + 1);
   D->eshift = grow(D->eshift, D->cap_eshift, ne);
   D->row_global = grow(D->row_global, D->cap_row_global, n_rows);
-  ESG_CUDA(cudaMemcpyAsync(D->row_slot, slot.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice, st));
-  ESG_CUDA(cudaMemcpyAsync(D->row_global, row_global.data(), sizeof(int) * n_rows, cudaMemcpyHostToDevice, st));
+  h2d_staged(M->ctx, D->row_slot, slot.data(), sizeof(int) * n_rows);
+  h2d_staged(M->ctx, D->row_global, row_global.data(), sizeof(int) * n_rows);
   int* d_eidx = nullptr;
   if (plan) {
-    ESG_CUDA(cudaMemcpyAsync(D->src_row, plan->src_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
-    ESG_CUDA(cudaMemcpyAsync(D->dst_row, plan->dst_row.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
-    ESG_CUDA(cudaMemcpyAsync(D->seg, seg.data(), sizeof(int64_t) * (n_owned + 1), cudaMemcpyHostToDevice, st));
+    h2d_staged(M->ctx, D->src_row, plan->src_row.data(), sizeof(int) * ne);
+    h2d_staged(M->ctx, D->dst_row, plan->dst_row.data(), sizeof(int) * ne);
+    h2d_staged(M->ctx, D->seg, seg.data(), sizeof(int64_t) * (n_owned + 1));
     d_eidx = dalloc<int>(ne);
-    ESG_CUDA(cudaMemcpyAsync(d_eidx, plan->edge_index.data(), sizeof(int) * ne, cudaMemcpyHostToDevice, st));
+    h2d_staged(M->ctx, d_eidx, plan->edge_index.data(), sizeof(int) * ne);
   } else {
     if (ne) ESG_CUDA(cudaMemcpyAsync(D->src_row, g->d_src, sizeof(int) * ne, cudaMemcpyDeviceToDevice, st));
     ESG_CUDA(cudaMemcpyAsync(D->seg, g->d_off, sizeof(int64_t) * (n_owned + 1), cudaMemcpyDeviceToDevice, st));
@@ -631,6 +635,9 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   D->Y = (float*)grow((uint8_t*)D->Y, D->cap_y,
                       std::max((size_t)D->chunk_cap * row * 4, (size_t)((D->chunk_cap + 127) / 128) * 128 * row * 2));
   D->logits = grow(D->logits, D->cap_logits, (size_t)D->chunk_cap);
+  if (D->cap_node_out < (size_t)std::max(n_owned, 1) * M->heads.out_len ||
+      D->cap_edge_out < (size_t)std::max<int64_t>(ne, 1) * M->heads.out_len)
+    model_outputs_wait(M);  // pending copies still read the buffers about to be replaced
   D->node_out = grow(D->node_out, D->cap_node_out, (size_t)std::max(n_owned, 1) * M->heads.out_len);
   D->edge_out = grow(D->edge_out, D->cap_edge_out, (size_t)std::max<int64_t>(ne, 1) * M->heads.out_len);
   // halo
@@ -644,7 +651,7 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     D->send_rows = grow(D->send_rows, D->cap_send_rows, all.size());
     D->send_buf = grow(D->send_buf, D->cap_send_buf, all.size() * row);
     if (!all.empty())
-      ESG_CUDA(cudaMemcpyAsync(D->send_rows, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
+      h2d_staged(M->ctx, D->send_rows, all.data(), sizeof(int) * all.size());
   }
   ESG_CUDA(cudaStreamSynchronize(st));  // host vectors above are freed on return
   free_ptr(d_eidx);
@@ -657,6 +664,12 @@ namespace {
 template <int H, int E>
 void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
                   float* out, cudaStream_t st);
+
+// The head tables may still be read by the copies of an earlier async
+// forward: everything after this point on st waits for them.
+void wait_prior_copies(DeviceModel* D, cudaStream_t st) {
+  if (D->copies_pending) ESG_CUDA(cudaStreamWaitEvent(st, D->copies_done, 0));
+}
 
 // Streamed outputs: rows [i0, i0 + n) of a head table are final on st; once
 // they are computed (heads) copy them to the pinned host buffer on copy_st.
@@ -787,6 +800,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         // the chunk's edge rows are final: its heads now, the copy overlaps the next chunks
         Prof pr(D, st, ESG_PROF_HEADS);
         const int ol = M->heads.out_len;
+        wait_prior_copies(D, st);
         launch_heads<H, E>(D->edges + e0 * H * E, n, D->head_w[1], D->head_key, D->head_row, ol,
                            D->edge_out + e0 * ol, st);
         ++ctx->launches;
@@ -870,12 +884,14 @@ void forward_impl(esg_model* M, esg_timing* tm) {
         // the node table is final after the last node block: its heads and
         // their copy overlap the last edge block
         Prof pr(D, st, ESG_PROF_HEADS);
+        wait_prior_copies(D, st);
         launch_heads<H, E>(D->nodes, D->n_owned, D->head_w[0], D->head_key, D->head_row, out_len, D->node_out, st);
         ++ctx->launches;
         if (D->host_node_out) stream_rows(D, st, D->node_out, D->host_node_out, 0, D->n_owned, out_len);
       }
     }
   ESG_CUDA(cudaEventRecord(D->ev[2], st));
+  wait_prior_copies(D, st);
   if (D->n_owned && !streamed) {
     Prof pr(D, st, ESG_PROF_HEADS);
     launch_heads<H, E>(D->nodes, D->n_owned, D->head_w[0], D->head_key, D->head_row, out_len, D->node_out, st);
@@ -988,10 +1004,21 @@ bool pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float* edge_out) {
+void model_outputs_wait(esg_model* M) {
+  DeviceModel* D = M->dev;
+  if (!D || !D->copies_pending) return;
+  ESG_CUDA(cudaEventSynchronize(D->copies_done));
+  D->copies_pending = false;
+}
+
+// async: return once the compute is done and the output copies are queued on
+// copy_st (pinned buffers only); model_outputs_wait completes them.  The next
+// forward overlaps those copies until its first heads launch.
+void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float* edge_out, bool async) {
   DeviceModel* D = M->dev;
   if ((node_out || edge_out) && pinned(node_out) && pinned(edge_out) && !D->save_inputs) {
     if (!D->copy_st) ESG_CUDA(cudaStreamCreateWithFlags(&D->copy_st, cudaStreamNonBlocking));
+    if (!D->copies_done) ESG_CUDA(cudaEventCreateWithFlags(&D->copies_done, cudaEventDisableTiming));
     D->host_node_out = node_out;
     D->host_edge_out = edge_out;
     try {
@@ -999,10 +1026,13 @@ void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float*
     } catch (...) {
       D->host_node_out = D->host_edge_out = nullptr;
       cudaStreamSynchronize(D->copy_st);
+      D->copies_pending = false;
       throw;
     }
     D->host_node_out = D->host_edge_out = nullptr;
-    ESG_CUDA(cudaStreamSynchronize(D->copy_st));
+    ESG_CUDA(cudaEventRecord(D->copies_done, D->copy_st));
+    D->copies_pending = true;
+    if (!async) model_outputs_wait(M);
     return;
   }
   model_forward(M, tm);

@@ -23,10 +23,8 @@ namespace esg {
 namespace {
 
 template <typename T>
-T* galloc(size_t n) {
-  T* p = nullptr;
-  if (n) ESG_CUDA(cudaMalloc(&p, n * sizeof(T)));
-  return p;
+T* galloc_ctx(esg_ctx* ctx, size_t n) {
+  return static_cast<T*>(ctx->cache.alloc(n * sizeof(T)));
 }
 
 __global__ void k_flag_owned(const int* __restrict__ part, int n, int rank, int* __restrict__ flag) {
@@ -111,21 +109,21 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   auto* P = new esg_plan();
   P->rank = rank;
   P->world = n_parts;
-  int* part = galloc<int>(n);
-  int* flag = galloc<int>(n + 1);
-  int* scan = galloc<int>(n + 1);
-  int* owned_row = galloc<int>(n);
-  int* halo_row = galloc<int>(n);
-  int* row_global = galloc<int>(n);
-  uint8_t* need = galloc<uint8_t>(n);
-  int64_t* cnt = galloc<int64_t>(n + 1);
-  int64_t* base = galloc<int64_t>(n + 1);
-  int* ids = galloc<int>(n);
-  int* n_sel = galloc<int>(1);
-  uint64_t* keys = galloc<uint64_t>(n);
-  uint64_t* keys_sorted = galloc<uint64_t>(n);
-  uint8_t* sflags = galloc<uint8_t>((size_t)n * n_parts);
-  ESG_CUDA(cudaMemcpyAsync(part, part_h, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  int* part = galloc_ctx<int>(g->ctx, n);
+  int* flag = galloc_ctx<int>(g->ctx, n + 1);
+  int* scan = galloc_ctx<int>(g->ctx, n + 1);
+  int* owned_row = galloc_ctx<int>(g->ctx, n);
+  int* halo_row = galloc_ctx<int>(g->ctx, n);
+  int* row_global = galloc_ctx<int>(g->ctx, n);
+  uint8_t* need = galloc_ctx<uint8_t>(g->ctx, n);
+  int64_t* cnt = galloc_ctx<int64_t>(g->ctx, n + 1);
+  int64_t* base = galloc_ctx<int64_t>(g->ctx, n + 1);
+  int* ids = galloc_ctx<int>(g->ctx, n);
+  int* n_sel = galloc_ctx<int>(g->ctx, 1);
+  uint64_t* keys = galloc_ctx<uint64_t>(g->ctx, n);
+  uint64_t* keys_sorted = galloc_ctx<uint64_t>(g->ctx, n);
+  uint8_t* sflags = galloc_ctx<uint8_t>(g->ctx, (size_t)n * n_parts);
+  h2d_staged(g->ctx, part, part_h, sizeof(int) * n);
   ESG_CUDA(cudaMemsetAsync(need, 0, n, st));
   ESG_CUDA(cudaMemsetAsync(halo_row, 0xff, sizeof(int) * n, st));
   ESG_CUDA(cudaMemsetAsync(sflags, 0, (size_t)n * n_parts, st));
@@ -135,8 +133,8 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   size_t tmp_bytes = 0;
   auto ensure_tmp = [&](size_t b) {
     if (b > tmp_bytes) {
-      if (tmp) cudaFree(tmp);
-      tmp = galloc<uint8_t>(b);
+      if (tmp) g->ctx->cache.release(tmp);
+      tmp = galloc_ctx<uint8_t>(g->ctx, b);
       tmp_bytes = b;
     }
   };
@@ -149,7 +147,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   cub::DeviceScan::ExclusiveSum(tmp, need_b, flag, scan, n + 1, st);
   k_owned_rows<<<b1, 256, 0, st>>>(part, n, rank, scan, owned_row, row_global);
   int n_owned = 0;
-  ESG_CUDA(cudaMemcpyAsync(&n_owned, scan + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  d2h_small(g->ctx, &n_owned, scan + n, sizeof(int));
   // halo rows, sorted by (owner, id)
   if (n) k_halo_need<<<bw, 256, 0, st>>>(g->d_off, g->d_src, part, n, rank, need, cnt);
   thrust::counting_iterator<int> it(0);
@@ -158,7 +156,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   ensure_tmp(need_b);
   cub::DeviceSelect::Flagged(tmp, need_b, it, need, ids, n_sel, n, st);
   int n_halo = 0;
-  ESG_CUDA(cudaMemcpyAsync(&n_halo, n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+  d2h_small(g->ctx, &n_halo, n_sel, sizeof(int));
   ESG_CUDA(cudaStreamSynchronize(st));
   if (n_halo) {
     k_halo_keys<<<(unsigned)((n_halo + 255) / 256), 256, 0, st>>>(ids, n_halo, part, keys);
@@ -175,11 +173,11 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   ensure_tmp(need_b);
   cub::DeviceScan::ExclusiveSum(tmp, need_b, cnt, base, n + 1, st);
   int64_t n_e = 0;
-  ESG_CUDA(cudaMemcpyAsync(&n_e, base + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  d2h_small(g->ctx, &n_e, base + n, sizeof(int64_t));
   ESG_CUDA(cudaStreamSynchronize(st));
-  int* edge_index = galloc<int>((size_t)std::max<int64_t>(n_e, 1));
-  int* src_row = galloc<int>((size_t)std::max<int64_t>(n_e, 1));
-  int* dst_row = galloc<int>((size_t)std::max<int64_t>(n_e, 1));
+  int* edge_index = galloc_ctx<int>(g->ctx, (size_t)std::max<int64_t>(n_e, 1));
+  int* src_row = galloc_ctx<int>(g->ctx, (size_t)std::max<int64_t>(n_e, 1));
+  int* dst_row = galloc_ctx<int>(g->ctx, (size_t)std::max<int64_t>(n_e, 1));
   if (n) {
     k_fill_edges<<<bw, 256, 0, st>>>(g->d_off, g->d_src, part, n, rank, base, owned_row, halo_row, edge_index,
                                       src_row, dst_row);
@@ -195,13 +193,13 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   P->dst_row.resize(n_e);
   std::vector<int> owned_h(n), halo_keys_owner;
   if (P->n_rows)
-    ESG_CUDA(cudaMemcpyAsync(P->row_global.data(), row_global, sizeof(int) * P->n_rows, cudaMemcpyDeviceToHost, st));
+    d2h_small(g->ctx, P->row_global.data(), row_global, sizeof(int) * P->n_rows);
   if (n_e) {
-    ESG_CUDA(cudaMemcpyAsync(P->edge_index.data(), edge_index, sizeof(int) * n_e, cudaMemcpyDeviceToHost, st));
-    ESG_CUDA(cudaMemcpyAsync(P->src_row.data(), src_row, sizeof(int) * n_e, cudaMemcpyDeviceToHost, st));
-    ESG_CUDA(cudaMemcpyAsync(P->dst_row.data(), dst_row, sizeof(int) * n_e, cudaMemcpyDeviceToHost, st));
+    d2h_small(g->ctx, P->edge_index.data(), edge_index, sizeof(int) * n_e);
+    d2h_small(g->ctx, P->src_row.data(), src_row, sizeof(int) * n_e);
+    d2h_small(g->ctx, P->dst_row.data(), dst_row, sizeof(int) * n_e);
   }
-  if (n) ESG_CUDA(cudaMemcpyAsync(owned_h.data(), owned_row, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  if (n) d2h_small(g->ctx, owned_h.data(), owned_row, sizeof(int) * n);
   std::map<int, Neighbor> nb;
   for (int p = 0; p < n_parts; ++p) {
     if (p == rank) continue;
@@ -210,11 +208,11 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
     ensure_tmp(need_b);
     cub::DeviceSelect::Flagged(tmp, need_b, it, sflags + (size_t)p * n, ids, n_sel, n, st);
     int m = 0;
-    ESG_CUDA(cudaMemcpyAsync(&m, n_sel, sizeof(int), cudaMemcpyDeviceToHost, st));
+    d2h_small(g->ctx, &m, n_sel, sizeof(int));
     ESG_CUDA(cudaStreamSynchronize(st));
     if (!m) continue;
     std::vector<int> s(m);
-    ESG_CUDA(cudaMemcpy(s.data(), ids, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    d2h_small(g->ctx, s.data(), ids, sizeof(int) * m);
     Neighbor& x = nb[p];
     x.peer = p;
     for (int id : s) x.send_rows.push_back(owned_h[id]);
@@ -239,7 +237,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   for (void* p : {(void*)part, (void*)flag, (void*)scan, (void*)owned_row, (void*)halo_row, (void*)row_global,
                   (void*)need, (void*)cnt, (void*)base, (void*)ids, (void*)n_sel, (void*)keys, (void*)keys_sorted,
                   (void*)sflags, (void*)edge_index, (void*)src_row, (void*)dst_row, tmp})
-    if (p) cudaFree(p);
+    g->ctx->cache.release(p);
   return P;
 }
 

@@ -586,6 +586,16 @@ class Network:
         _check(lib().esg_forward(self._h, _p(node_out), _p(edge_out), C.byref(t)))
         return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches)
 
+    def forward_into_async(self, node_out: Optional[np.ndarray], edge_out: Optional[np.ndarray]) -> Timing:
+        """esg_forward_async: with pinned buffers returns once the copies are
+        queued; call wait_outputs() before reading or reusing the buffers."""
+        t = _Timing()
+        _check(lib().esg_forward_async(self._h, _p(node_out), _p(edge_out), C.byref(t)))
+        return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches)
+
+    def wait_outputs(self) -> None:
+        _check(lib().esg_forward_wait(self._h))
+
     def device_outputs(self):
         ptrs = [C.c_void_p() for _ in range(4)]
         _check(lib().esg_forward_outputs(self._h, *[C.byref(p) for p in ptrs]))

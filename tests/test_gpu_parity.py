@@ -186,3 +186,35 @@ def test_streamed_outputs_match(gpu_ctx):
     assert np.array_equal(pe.view(np.uint32), eo.view(np.uint32))
     net.close()
     g.close()
+
+
+def test_async_outputs_do_not_race(gpu_ctx):
+    """esg_forward_async: the next forward runs while the previous outputs
+    drain, but its heads wait for those copies -- two back-to-back async
+    forwards with different parameters deliver their own outputs, bit-exact."""
+    import torch
+    s, r, layers, basis = esg.config_structure("C3")
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=layers, n_radial=32, r_cut=r, seed=1,
+                          linear_precision=esg.LINEAR_BF16)
+    net = esg.Network(gpu_ctx, cfg, basis)
+    net.init_params()
+    g = esg.build_graph(gpu_ctx, s, r)
+    net.prepare(g, s.species)
+    p1 = net.params()
+    p2 = (p1 * 1.01).astype(np.float32)
+    want = []
+    for p in (p1, p2):
+        net.set_params(p)
+        no, eo, _ = net.forward()
+        want.append((no, eo))
+    bufs = [(torch.empty((net.n_owned, net.out_len), dtype=torch.float32, pin_memory=True).numpy(),
+             torch.empty((net.n_edges, net.out_len), dtype=torch.float32, pin_memory=True).numpy()) for _ in range(2)]
+    for p, (bn, be) in zip((p1, p2), bufs):
+        net.set_params(p)
+        net.forward_into_async(bn, be)
+    net.wait_outputs()
+    for (bn, be), (no, eo) in zip(bufs, want):
+        assert np.array_equal(bn.view(np.uint32), no.view(np.uint32))
+        assert np.array_equal(be.view(np.uint32), eo.view(np.uint32))
+    net.close()
+    g.close()
