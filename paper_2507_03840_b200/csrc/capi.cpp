@@ -228,6 +228,24 @@ int esg_ctx_destroy(esg_ctx* ctx) {
   ESG_API_BEGIN
   if (!ctx) return ESG_OK;
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (esg_graph* g : ctx->graphs) {  // detach graphs and plans that outlive their context
+    for (void* p : {(void*)g->d_off, (void*)g->d_src, (void*)g->d_shift, (void*)g->d_disp, (void*)g->d_dist})
+      ctx->cache.release(p);
+    g->d_off = nullptr;
+    g->d_src = nullptr;
+    g->d_shift = nullptr;
+    g->d_disp = g->d_dist = nullptr;
+    g->ctx = nullptr;
+  }
+  for (esg_plan* p : ctx->plans) {
+    for (void* q : {(void*)p->d_edge_index, (void*)p->d_src_row, (void*)p->d_dst_row, (void*)p->d_seg})
+      ctx->cache.release(q);
+    p->d_edge_index = p->d_src_row = p->d_dst_row = nullptr;
+    p->d_seg = nullptr;
+    p->ctx = nullptr;
+  }
+  ctx->graphs.clear();
+  ctx->plans.clear();
   ctx->cache.flush();
   if (ctx->zc) cudaFreeHost(ctx->zc);
   if (ctx->up) cudaFreeHost(ctx->up);
@@ -314,16 +332,11 @@ int esg_build_graph(esg_ctx* ctx, int n, const double* pos, const double cell[9]
 int esg_graph_destroy(esg_graph* g) {
   ESG_API_BEGIN
   if (!g) return ESG_OK;
-  const bool dbg = std::getenv("ESG_DEBUG_FREE") != nullptr;
-  auto now = [] { return std::chrono::steady_clock::now(); };
-  auto t0 = now();
-  if (dbg) cudaDeviceSynchronize();
-  auto t1 = now();
-  for (void* p : {(void*)g->d_off, (void*)g->d_src, (void*)g->d_shift, (void*)g->d_disp, (void*)g->d_dist})
-    g->ctx->cache.release(p);
-  if (dbg)
-    std::fprintf(stderr, "[esg] graph destroy: device sync %.3f s, frees %.3f s\n",
-                 std::chrono::duration<double>(t1 - t0).count(), std::chrono::duration<double>(now() - t1).count());
+  if (g->ctx) {
+    for (void* p : {(void*)g->d_off, (void*)g->d_src, (void*)g->d_shift, (void*)g->d_disp, (void*)g->d_dist})
+      g->ctx->cache.release(p);
+    g->ctx->graphs.erase(g);
+  }
   delete g;
   ESG_API_END
 }
@@ -462,6 +475,7 @@ static esg_plan* plan_from_csr(int n, const int64_t* off, const int32_t* src, co
     q = r;
   }
   for (auto& kv : nb) P->nbrs.push_back(kv.second);
+  P->n_edges = (int64_t)P->src_row.size();
   return P;
 }
 
@@ -497,7 +511,7 @@ int esg_plan_info(const esg_plan* p, int64_t info[5]) {
   NEED(p, "plan");
   info[0] = p->n_rows;
   info[1] = p->n_owned;
-  info[2] = (int64_t)p->src_row.size();
+  info[2] = p->n_edges;
   info[3] = (int64_t)p->nbrs.size();
   int64_t s = 0;
   for (const auto& nb : p->nbrs) s += (int64_t)nb.send_rows.size();
@@ -510,6 +524,7 @@ int esg_plan_export(const esg_plan* p, int32_t* row_global, int32_t* row_species
                     int32_t* nbr_recv_count, int32_t* nbr_send_count, int32_t* send_rows) {
   ESG_API_BEGIN
   NEED(p, "plan");
+  if (edge_index || src_row || dst_row) p->host_sync_edges();
   if (row_global) std::copy(p->row_global.begin(), p->row_global.end(), row_global);
   if (row_species) std::copy(p->row_species.begin(), p->row_species.end(), row_species);
   if (edge_index) std::copy(p->edge_index.begin(), p->edge_index.end(), edge_index);

@@ -7,6 +7,7 @@
 #include <array>
 #include <cstdint>
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -121,8 +122,15 @@ struct BlockCache {
 };
 }  // namespace esg
 
+struct esg_graph;
+struct esg_plan;
+
 struct esg_ctx {
   int device = 0, rank = 0, world = 1;
+  // live objects whose device arrays come from `cache`; a context destroyed
+  // first releases their arrays and detaches them (destroy order is free)
+  std::set<esg_graph*> graphs;
+  std::set<esg_plan*> plans;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   int64_t launches = 0;  // kernels launched by this library
@@ -164,9 +172,17 @@ struct esg_graph {
 struct esg_plan {
   int rank = 0, world = 1;
   int n_rows = 0, n_owned = 0;
+  int64_t n_edges = 0;
   std::vector<int32_t> row_global, row_species;
-  std::vector<int32_t> edge_index, src_row, dst_row;
+  // per owned edge (host); a GPU-built plan keeps them on the device and
+  // fills these only when exported (host_sync_edges)
+  mutable std::vector<int32_t> edge_index, src_row, dst_row;
+  esg_ctx* ctx = nullptr;  // owner of the device arrays (block cache)
+  int32_t *d_edge_index = nullptr, *d_src_row = nullptr, *d_dst_row = nullptr;
+  int64_t* d_seg = nullptr;  // n_owned + 1 destination segment offsets
   std::vector<esg::Neighbor> nbrs;
+  void host_sync_edges() const;  // plan_gpu.cu
+  ~esg_plan();
 };
 
 namespace esg {

@@ -217,6 +217,7 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
 
   auto* G = new esg_graph();
   G->ctx = ctx;
+  ctx->graphs.insert(G);
   G->n = n;
   for (int d = 0; d < 3; ++d) G->nimg[d] = g.nimg[d];
 

@@ -543,10 +543,14 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
     n_rows = plan->n_rows;
     n_owned = plan->n_owned;
     row_global = plan->row_global;
-    ne = (int64_t)plan->src_row.size();
+    ne = plan->n_edges;
     seg.assign(n_owned + 1, 0);
-    for (int64_t k = 0; k < ne; ++k) seg[plan->dst_row[k] + 1]++;
-    for (int j = 0; j < n_owned; ++j) seg[j + 1] += seg[j];
+    if (plan->d_seg) {  // GPU-built plan: the segment offsets are on the device
+      d2h_small(M->ctx, seg.data(), plan->d_seg, sizeof(int64_t) * (n_owned + 1));
+    } else {
+      for (int64_t k = 0; k < ne; ++k) seg[plan->dst_row[k] + 1]++;
+      for (int j = 0; j < n_owned; ++j) seg[j + 1] += seg[j];
+    }
   } else {
     // the whole graph as the view: indices stay on the device (CSR src, the
     // segment offsets are the CSR offsets); only the offsets come to the host
@@ -582,7 +586,14 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   h2d_staged(M->ctx, D->row_slot, slot.data(), sizeof(int) * n_rows);
   h2d_staged(M->ctx, D->row_global, row_global.data(), sizeof(int) * n_rows);
   int* d_eidx = nullptr;
-  if (plan) {
+  if (plan && plan->d_src_row) {
+    if (ne) {
+      ESG_CUDA(cudaMemcpyAsync(D->src_row, plan->d_src_row, sizeof(int) * ne, cudaMemcpyDeviceToDevice, st));
+      ESG_CUDA(cudaMemcpyAsync(D->dst_row, plan->d_dst_row, sizeof(int) * ne, cudaMemcpyDeviceToDevice, st));
+    }
+    ESG_CUDA(cudaMemcpyAsync(D->seg, plan->d_seg, sizeof(int64_t) * (n_owned + 1), cudaMemcpyDeviceToDevice, st));
+    d_eidx = plan->d_edge_index;  // read by k_gather_dirs below, owned by the plan
+  } else if (plan) {
     h2d_staged(M->ctx, D->src_row, plan->src_row.data(), sizeof(int) * ne);
     h2d_staged(M->ctx, D->dst_row, plan->dst_row.data(), sizeof(int) * ne);
     h2d_staged(M->ctx, D->seg, seg.data(), sizeof(int64_t) * (n_owned + 1));
@@ -654,7 +665,7 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
       h2d_staged(M->ctx, D->send_rows, all.data(), sizeof(int) * all.size());
   }
   ESG_CUDA(cudaStreamSynchronize(st));  // host vectors above are freed on return
-  free_ptr(d_eidx);
+  if (!(plan && plan->d_src_row)) free_ptr(d_eidx);
   D->prepared = true;
   D->train_stale = true;
 }

@@ -97,6 +97,15 @@ __global__ void k_send_flags(const int64_t* __restrict__ off, const int* __restr
   }
 }
 
+// seg[r] = first owned edge of owned row r (rows ascend in global id and
+// base is the edge offset per global node), seg[n_owned] = n_e
+__global__ void k_plan_seg(const int64_t* __restrict__ base, const int* __restrict__ row_global, int n_owned,
+                           int64_t n_e, int64_t* __restrict__ seg) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n_owned) seg[r] = base[row_global[r]];
+  if (r == n_owned) seg[r] = n_e;
+}
+
 }  // namespace
 
 esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32_t* part_h, int n_parts,
@@ -187,18 +196,21 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   // to the host: rows, edges, owned-row map, per-peer send lists
   P->n_owned = n_owned;
   P->n_rows = n_owned + n_halo;
+  P->n_edges = n_e;
   P->row_global.resize(P->n_rows);
-  P->edge_index.resize(n_e);
-  P->src_row.resize(n_e);
-  P->dst_row.resize(n_e);
   std::vector<int> owned_h(n), halo_keys_owner;
   if (P->n_rows)
     d2h_small(g->ctx, P->row_global.data(), row_global, sizeof(int) * P->n_rows);
-  if (n_e) {
-    d2h_small(g->ctx, P->edge_index.data(), edge_index, sizeof(int) * n_e);
-    d2h_small(g->ctx, P->src_row.data(), src_row, sizeof(int) * n_e);
-    d2h_small(g->ctx, P->dst_row.data(), dst_row, sizeof(int) * n_e);
-  }
+  // the per-edge arrays stay on the device (prepare copies them device to
+  // device); the host copies are made only if the plan is exported
+  P->ctx = g->ctx;
+  g->ctx->plans.insert(P);
+  P->d_edge_index = edge_index;
+  P->d_src_row = src_row;
+  P->d_dst_row = dst_row;
+  P->d_seg = galloc_ctx<int64_t>(g->ctx, (size_t)n_owned + 1);
+  k_plan_seg<<<(unsigned)((n_owned + 256) / 256), 256, 0, st>>>(base, row_global, n_owned, n_e, P->d_seg);
+  g->ctx->launches += 1;
   if (n) d2h_small(g->ctx, owned_h.data(), owned_row, sizeof(int) * n);
   std::map<int, Neighbor> nb;
   for (int p = 0; p < n_parts; ++p) {
@@ -236,9 +248,27 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
     for (int r = 0; r < P->n_rows; ++r) P->row_species.push_back(species[P->row_global[r]]);
   for (void* p : {(void*)part, (void*)flag, (void*)scan, (void*)owned_row, (void*)halo_row, (void*)row_global,
                   (void*)need, (void*)cnt, (void*)base, (void*)ids, (void*)n_sel, (void*)keys, (void*)keys_sorted,
-                  (void*)sflags, (void*)edge_index, (void*)src_row, (void*)dst_row, tmp})
+                  (void*)sflags, tmp})
     g->ctx->cache.release(p);
   return P;
 }
 
 }  // namespace esg
+
+void esg_plan::host_sync_edges() const {
+  if (!d_src_row || (int64_t)src_row.size() == n_edges) return;
+  edge_index.resize(n_edges);
+  src_row.resize(n_edges);
+  dst_row.resize(n_edges);
+  if (n_edges) {
+    esg::d2h_small(ctx, edge_index.data(), d_edge_index, sizeof(int32_t) * n_edges);
+    esg::d2h_small(ctx, src_row.data(), d_src_row, sizeof(int32_t) * n_edges);
+    esg::d2h_small(ctx, dst_row.data(), d_dst_row, sizeof(int32_t) * n_edges);
+  }
+}
+
+esg_plan::~esg_plan() {
+  if (!ctx) return;
+  for (void* p : {(void*)d_edge_index, (void*)d_src_row, (void*)d_dst_row, (void*)d_seg}) ctx->cache.release(p);
+  ctx->plans.erase(this);
+}
