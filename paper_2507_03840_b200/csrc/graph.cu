@@ -148,6 +148,47 @@ __global__ void k_finalize(const uint64_t* __restrict__ keys, const int32_t* __r
   dist[k] = __dsqrt_rn(q);
 }
 
+// Per-destination sort of the (source, shift) keys: one CTA per segment
+// (grid-strided), bitonic over the next power of two in SMEM, padding keys
+// ~0 sort last.  Keys are unique within a segment.
+constexpr int SEG_SORT_CAP = 4096;
+__global__ void __launch_bounds__(256) k_segment_sort(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                      const int64_t* __restrict__ off, int n) {
+  __shared__ uint64_t sk[SEG_SORT_CAP];
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    const int64_t a = off[j];
+    const int len = (int)(off[j + 1] - a);
+    int P = 1;
+    while (P < len) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) sk[i] = i < len ? in[a + i] : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int h = k >> 1; h > 0; h >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          const int o = i ^ h;
+          if (o > i) {
+            const uint64_t x = sk[i], y = sk[o];
+            if ((x > y) == ((i & k) == 0)) {
+              sk[i] = y;
+              sk[o] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) out[a + i] = sk[i];
+    __syncthreads();
+  }
+}
+
+__global__ void k_max_segment(const int64_t* __restrict__ off, int n, unsigned long long* __restrict__ mx) {
+  unsigned long long m = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)(off[j + 1] - off[j]));
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
 }  // namespace
 
 esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& cell, const bool pbc[3],
@@ -275,14 +316,27 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
     // reads its segment-size groups back to the host, which would queue behind
     // in-flight output copies); keys are unique per segment, so the order is
     // the same as any other sort's.  Bits: packed shift (30) + source index.
-    int end_bit = 32;
-    while ((int64_t(1) << (end_bit - 32)) < n) ++end_bit;
-    cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
-                                            G->d_off + 1, 0, end_bit, st);
-    d_tmp = ctx->cache.alloc(tmp_bytes);
-    cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
-                                            G->d_off + 1, 0, end_bit, st);
-    ctx->cache.release(d_tmp);
+    unsigned long long* d_mx = dalloc_c((unsigned long long*)nullptr, 1);
+    ESG_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
+    k_max_segment<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(G->d_off, n, d_mx);
+    unsigned long long max_seg = 0;
+    d2h_small(ctx, &max_seg, d_mx, sizeof(max_seg));
+    ctx->cache.release(d_mx);
+    int cap = SEG_SORT_CAP;  // ESG_SEG_SORT_CAP=0 forces the cub path (tests)
+    if (const char* e = std::getenv("ESG_SEG_SORT_CAP")) cap = std::min(std::max(std::atoi(e), 0), SEG_SORT_CAP);
+    if (max_seg <= (unsigned long long)cap) {
+      k_segment_sort<<<(unsigned)std::min<int64_t>(n, 148 * 8), 256, 0, st>>>(d_keys, d_keys_sorted, G->d_off, n);
+      ctx->launches += 2;
+    } else {  // very dense graphs: cub's segmented radix sort
+      int end_bit = 32;
+      while ((int64_t(1) << (end_bit - 32)) < n) ++end_bit;
+      cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
+                                              G->d_off + 1, 0, end_bit, st);
+      d_tmp = ctx->cache.alloc(tmp_bytes);
+      cub::DeviceSegmentedRadixSort::SortKeys(d_tmp, tmp_bytes, d_keys, d_keys_sorted, (int)E, n, G->d_off,
+                                              G->d_off + 1, 0, end_bit, st);
+      ctx->cache.release(d_tmp);
+    }
   }
   mark("sort");
   G->d_src = dalloc_c((int32_t*)nullptr, E);

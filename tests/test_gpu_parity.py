@@ -71,6 +71,15 @@ def test_graph_configs_bit_exact(gpu_ctx, name):
                     assert np.array_equal(got[k], want[k])
 
 
+def test_graph_sort_fallback(gpu_ctx, monkeypatch):
+    """The per-destination key sort runs as a shared-memory bitonic sort when
+    every segment fits (the other graph tests) and as cub's segmented radix
+    sort otherwise; ESG_SEG_SORT_CAP=0 forces the latter."""
+    monkeypatch.setenv("ESG_SEG_SORT_CAP", "0")
+    s, r, _, _ = esg.config_structure("C1")
+    same_graph(esg.build_graph(gpu_ctx, s, r).export(), O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r))
+
+
 def test_graph_tiling_x8(gpu_ctx):
     """test_structures.cpp:166-189 on the skewed cell (no exact-cutoff ties)."""
     pos = np.random.default_rng(13).random((5, 3)) @ SKEW
