@@ -465,7 +465,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--train-steps", type=int, default=2, help="C2 training steps after the forward (0: skip)")
     ap.add_argument("--fp32-steps", type=int, default=2, help="forwards timed in the fp32-accurate mode (0: skip)")
