@@ -256,6 +256,15 @@ int esg_blocks_write_shard(esg_model* m, const char* path, int basis, int symmet
 int esg_blocks_write_text(esg_model* m, const char* path, int basis, int symmetrize_onsite);
 /* Rank 0's gathered text file from the ranks' shards (no device needed). */
 int esg_blocks_merge_text(const char* const* shard_paths, int n_shards, const char* out_path);
+/* Network::build_targets (network.h:187-214): head-space targets and masks of
+ * the prepared view (n_owned x out_len, n_edges x out_len, view order) from
+ * uncoupled target blocks (keys + row-major values concatenated, e.g. from a
+ * text file).  Items without a block keep mask 0; *count receives the number
+ * of active entries (TargetBuffers::local_count).  The result feeds
+ * esg_set_targets. */
+int esg_build_targets(esg_model* m, int64_t n_blocks, const esg_block_key* keys, const double* values,
+                      float* node_target, uint8_t* node_mask, float* edge_target, uint8_t* edge_mask,
+                      int64_t* count);
 /* Legacy pair: uncoupled values only, n_values from esg_blocks_count. */
 int esg_blocks_size(esg_model* m, int64_t* n_values);
 int esg_blocks_uncoupled(esg_model* m, double* out);

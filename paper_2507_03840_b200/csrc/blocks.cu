@@ -23,6 +23,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
+#include <array>
+#include <algorithm>
 #include <memory>
 
 #include "blocks_io.h"
@@ -493,6 +496,88 @@ void blocks_write_shard(esg_model* M, const char* path, int basis, bool sym, int
   put(pad.data(), pad.size());
   stream_items(M, B, false, basis, sym, vb, put);
   if (std::fflush(f.get()) != 0) data(std::string("write failed: ") + path);
+}
+
+// Network::build_targets (network.h:187-214) with encode_target
+// (network.h:318-343, clebsch_gordan.cpp:142-155 to_coupled): for every item
+// of the prepared view whose key has a target block, each shell-pair
+// rectangle is mapped to its coupled coefficients c_L = C_L . flat (sums in
+// ascending element order) and placed at the item's head slots; mask 1 there.
+int64_t build_targets(esg_model* M, int64_t n_blocks, const BlockRec* keys, const double* values, float* node_t,
+                      uint8_t* node_m, float* edge_t, uint8_t* edge_m) {
+  BlockState& B = state(M);
+  DeviceModel* D = M->dev;
+  const int ol = M->heads.out_len;
+  std::vector<BlockRec> items(B.n_items);
+  blocks_export(M, ESG_BLOCKS_UNCOUPLED, false, items.data(), nullptr);
+  std::vector<int32_t> src(D->n_edges), dst(D->n_edges);  // the view's endpoint rows (species)
+  if (D->n_edges) {
+    d2h_small(M->ctx, src.data(), D->src_row, sizeof(int32_t) * D->n_edges);
+    d2h_small(M->ctx, dst.data(), D->dst_row, sizeof(int32_t) * D->n_edges);
+  }
+  struct KeyHash {
+    size_t operator()(const std::array<int32_t, 5>& k) const {
+      size_t h = 1469598103934665603ull;
+      for (int32_t v : k) h = (h ^ (uint32_t)v) * 1099511628211ull;
+      return h;
+    }
+  };
+  std::unordered_map<std::array<int32_t, 5>, int64_t, KeyHash> where;
+  where.reserve((size_t)n_blocks * 2);
+  std::vector<int64_t> off((size_t)n_blocks + 1, 0);
+  for (int64_t b = 0; b < n_blocks; ++b) {
+    const BlockRec& k = keys[b];
+    if (k.rows < 1 || k.cols < 1) data("bad target block shape");
+    off[b + 1] = off[b] + (int64_t)k.rows * k.cols;
+    where[{k.i, k.j, k.ix, k.iy, k.iz}] = b;  // BlockMatrix keeps one block per key
+  }
+  std::map<std::array<int, 3>, std::vector<double>> cg;
+  auto coupling_of = [&](int la, int lb, int L) -> const std::vector<double>& {
+    auto key = std::array<int, 3>{la, lb, L};
+    auto it = cg.find(key);
+    if (it == cg.end()) it = cg.emplace(key, coupling_matrix(la, lb, L)).first;
+    return it->second;
+  };
+  int64_t count = 0;
+  for (int64_t it = 0; it < B.n_items; ++it) {
+    const BlockRec& k = items[it];
+    const auto f = where.find({k.i, k.j, k.ix, k.iy, k.iz});
+    const bool node = it < D->n_owned;
+    float* row = node ? (node_t ? node_t + it * ol : nullptr) : (edge_t ? edge_t + (it - D->n_owned) * ol : nullptr);
+    uint8_t* mask = node ? (node_m ? node_m + it * ol : nullptr) : (edge_m ? edge_m + (it - D->n_owned) * ol : nullptr);
+    if (row) std::fill(row, row + ol, 0.f);
+    if (mask) std::fill(mask, mask + ol, (uint8_t)0);
+    if (f == where.end()) continue;
+    const int64_t b = f->second;
+    if (keys[b].rows != k.rows || keys[b].cols != k.cols) data("target block shape does not match the species basis");
+    const double* blk = values + off[b];
+    const int nb = k.cols;
+    const int64_t e = it - D->n_owned;
+    const int zi = node ? D->row_species[it] : D->row_species[src[e]];
+    const int zj = node ? D->row_species[it] : D->row_species[dst[e]];
+    const auto& sha = M->basis.shells.at(zi);
+    const auto& shb = M->basis.shells.at(zj);
+    for (size_t a = 0; a < sha.size(); ++a)
+      for (size_t c = 0; c < shb.size(); ++c) {
+        const int la = sha[a], lb = shb[c], da = 2 * la + 1, db = 2 * lb + 1;
+        const int oa = M->basis.off(zi, (int)a), ob = M->basis.off(zj, (int)c);
+        std::vector<double> flat((size_t)da * db);
+        for (int i = 0; i < da; ++i)
+          for (int j = 0; j < db; ++j) flat[(size_t)i * db + j] = blk[(size_t)(oa + i) * nb + ob + j];
+        for (int L = std::abs(la - lb); L <= la + lb; ++L) {
+          const auto& C = coupling_of(la, lb, L);
+          const int seg = M->heads.segment((int)a, (int)c, L);
+          for (int r = 0; r < 2 * L + 1; ++r) {
+            double acc = 0.0;
+            for (int q = 0; q < da * db; ++q) acc += C[(size_t)r * da * db + q] * flat[q];
+            if (row) row[seg + r] = static_cast<float>(acc);
+            if (mask) mask[seg + r] = 1;
+            ++count;
+          }
+        }
+      }
+  }
+  return count;
 }
 
 void blocks_write_text(esg_model* M, const char* path, int basis, bool sym) {

@@ -49,6 +49,8 @@ void blocks_export(esg_model* M, int basis, bool sym, BlockRec* keys, double* va
 void blocks_export_device(esg_model* M, int basis, bool sym, int vb, void* d_keys, void* d_values, float* kernel_ms);
 void blocks_write_shard(esg_model* M, const char* path, int basis, bool sym, int vb);
 void blocks_write_text(esg_model* M, const char* path, int basis, bool sym);
+int64_t build_targets(esg_model* M, int64_t n_blocks, const BlockRec* keys, const double* values, float* node_t,
+                      uint8_t* node_m, float* edge_t, uint8_t* edge_m);
 
 namespace {
 thread_local std::string g_last;
@@ -898,6 +900,21 @@ int esg_blocks_write_text(esg_model* m, const char* path, int basis, int symmetr
   ESG_API_BEGIN
   NEED(path, "path");
   blocks_write_text(device_model(m), path, basis, symmetrize_onsite != 0);
+  ESG_API_END
+}
+
+int esg_build_targets(esg_model* m, int64_t n_blocks, const esg_block_key* keys, const double* values,
+                      float* node_target, uint8_t* node_mask, float* edge_target, uint8_t* edge_mask,
+                      int64_t* count) {
+  ESG_API_BEGIN
+  if (n_blocks < 0) usage("n_blocks must be non-negative");
+  if (n_blocks > 0) {
+    NEED(keys, "keys");
+    NEED(values, "values");
+  }
+  const int64_t c = build_targets(device_model(m), n_blocks, reinterpret_cast<const BlockRec*>(keys), values,
+                                  node_target, node_mask, edge_target, edge_mask);
+  if (count) *count = c;
   ESG_API_END
 }
 

@@ -629,6 +629,26 @@ class Network:
         _check(lib().esg_blocks_export(self._h, C.c_int(basis), C.c_int(int(symmetrize_onsite)), _p(keys), _p(vals)))
         return _block_arrays(keys, vals)
 
+    def build_targets(self, keys: np.ndarray, shapes: np.ndarray, values: np.ndarray):
+        """Network::build_targets: uncoupled target blocks (keys (n, 5), shapes
+        (n, 2), concatenated row-major values) -> (node_target, node_mask,
+        edge_target, edge_mask, count) in head space, view order."""
+        n = len(keys)
+        rec = np.zeros(n, BLOCK_KEY)
+        k = np.asarray(keys).reshape(-1, 5)
+        for f, col in zip(("i", "j", "ix", "iy", "iz"), k.T):
+            rec[f] = col
+        rec["rows"], rec["cols"] = np.asarray(shapes).reshape(-1, 2).T
+        v = np.ascontiguousarray(values, np.float64)
+        nt = np.zeros((self.n_owned, self.out_len), np.float32)
+        nm = np.zeros((self.n_owned, self.out_len), np.uint8)
+        et = np.zeros((self.n_edges, self.out_len), np.float32)
+        em = np.zeros((self.n_edges, self.out_len), np.uint8)
+        cnt = C.c_int64()
+        _check(lib().esg_build_targets(self._h, C.c_int64(n), _p(rec), _p(v), _p(nt), _p(nm), _p(et), _p(em),
+                                       C.byref(cnt)))
+        return nt, nm, et, em, cnt.value
+
     def blocks_to_device(self, d_keys: int, d_values: int, basis: int = 1, symmetrize_onsite: bool = False,
                          value_bytes: int = 8) -> float:
         """Keys/values into caller device buffers (raw pointers, 0 = skip);

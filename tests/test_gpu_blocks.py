@@ -137,3 +137,30 @@ def test_reference_output_stage(run, tmp_path):
     net.write_blocks_text(str(tmp_path / "u.txt"), esg.BLOCKS_UNCOUPLED)
     assert (tmp_path / "c.txt").read_bytes() == (tmp_path / "ref_c.txt").read_bytes()
     assert (tmp_path / "u.txt").read_bytes() == (tmp_path / "ref_u.txt").read_bytes()
+
+
+def test_build_targets_inverts_blocks(run):
+    """test_model.cpp:472-498: encoding the uncoupled blocks of a forward as
+    targets gives back the head outputs (fp32 heads -> fp64 blocks -> fp32);
+    every slot of an item's species pair is active; items without a block
+    stay masked."""
+    net, s, gx, no, eo, om = run
+    keys, shapes, off, vals = net.blocks(esg.BLOCKS_UNCOUPLED)
+    nt, nm, et, em, cnt = net.build_targets(keys, shapes, vals)
+    for t, m, ref in ((nt, nm, no), (et, em, eo)):
+        sel = m.astype(bool)
+        assert np.abs(t[sel] - ref[sel]).max() <= 1e-5 * np.abs(ref).max()
+    assert cnt == int(nm.sum() + em.sum()) == int((shapes[:, 0] * shapes[:, 1]).sum())
+    # a numpy restatement of encode_target for a few items
+    for b in (0, s.n_atoms, len(keys) - 1):
+        za, zb = (s.species[keys[b, 0]], s.species[keys[b, 1]])
+        blk = vals[off[b]:off[b + 1]].reshape(shapes[b])
+        row = nt[b] if b < s.n_atoms else et[b - s.n_atoms]
+        want = om.uncoupled_block(za, zb, row, *shapes[b])  # encode then decode must round-trip
+        assert np.abs(want - blk).max() <= 1e-5 * max(1.0, np.abs(blk).max())
+    # only half of the blocks given: the others keep mask 0
+    half = np.arange(len(keys)) % 2 == 0
+    hv = np.concatenate([vals[off[b]:off[b + 1]] for b in np.nonzero(half)[0]])
+    nt2, nm2, et2, em2, cnt2 = net.build_targets(keys[half], shapes[half], hv)
+    masks = np.concatenate([nm2.any(axis=1), em2.any(axis=1)])
+    assert np.array_equal(masks, half) and cnt2 == int((shapes[half, 0] * shapes[half, 1]).sum())

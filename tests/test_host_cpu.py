@@ -121,3 +121,15 @@ def test_model_config_validation():
         esg.Network(None, esg.ModelConfig(l_max=2), {72: [0, 2]})
     with pytest.raises(esg.DataError):
         esg.Network(None, esg.ModelConfig(l_max=2), {1: [9]})
+
+
+def test_acceptance_counts():
+    """acceptance.cpp:466-496 criterion 6: 1000 Hf + 2000 O in the SZV basis
+    is an 18,000-orbital Hamiltonian; the generator gives 1000 Hf of 3000;
+    tiling 2x2x2 gives 24,000 atoms; a message row is 3 x 25 x 16 fp32 = 4,800 B."""
+    n_orb = {z: sum(2 * l + 1 for l in ls) for z, ls in esg.BASIS_HFO2.items()}
+    assert 1000 * n_orb[72] + 2000 * n_orb[8] == 18000
+    cell = esg.make_jittered_lattice(3000, 2.4, 0.1, [72, 8, 8], 2)
+    assert cell.n_atoms == 3000 and int((cell.species == 72).sum()) == 1000
+    assert esg.tile(cell, (2, 2, 2)).n_atoms == 24000
+    assert 3 * 25 * 16 * 4 == 4800
