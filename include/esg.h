@@ -254,6 +254,11 @@ int esg_blocks_write_shard(esg_model* m, const char* path, int basis, int symmet
  * order, 17 significant digits): for one rank, model_run's
  * blocks_coupled.txt / blocks_uncoupled.txt.  Small configurations. */
 int esg_blocks_write_text(esg_model* m, const char* path, int basis, int symmetrize_onsite);
+/* block_matrix.cpp:109-128 read_blocks_file (e.g. training targets): pass
+ * keys / values NULL to get the sizes; blocks in BlockKey order; parse errors
+ * are ESG_ERR_DATA with the line number. */
+int esg_blocks_read_text(const char* path, int64_t* n_blocks, int64_t* n_values, esg_block_key* keys,
+                         double* values);
 /* Rank 0's gathered text file from the ranks' shards (no device needed). */
 int esg_blocks_merge_text(const char* const* shard_paths, int n_shards, const char* out_path);
 /* Network::build_targets (network.h:187-214): head-space targets and masks of

@@ -6,6 +6,9 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <sstream>
+#include <map>
+#include <fstream>
 
 #include "esg_internal.h"
 
@@ -113,6 +116,44 @@ void write_blocks_text(const std::string& path, const std::vector<const BlockSet
     if (buf.size() > (1 << 20)) flush();
   }
   flush();
+}
+
+// block_matrix.cpp:109-128 read_blocks: one block per line
+// "i j ix iy iz rows cols v...", blank lines and '#' comments skipped, values
+// parsed as std::istream does; malformed lines, bad shapes, short value lists
+// and duplicate keys are data errors with the line number.  Blocks come back
+// in BlockKey order (the std::map of the reference).
+BlockSet read_blocks_text(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) data("cannot open file: " + path);
+  std::map<std::array<int32_t, 5>, std::pair<std::array<int32_t, 2>, std::vector<double>>> bm;
+  std::string line;
+  long lineno = 0;
+  while (std::getline(in, line)) {
+    ++lineno;
+    if (line.empty() || line[0] == '#') continue;
+    std::istringstream ss(line);
+    int32_t k[5];
+    long rows = 0, cols = 0;
+    if (!(ss >> k[0] >> k[1] >> k[2] >> k[3] >> k[4] >> rows >> cols))
+      data("expected 'i j ix iy iz rows cols values...' (line " + std::to_string(lineno) + ")");
+    if (rows < 1 || cols < 1 || rows > 65535 || cols > 65535)
+      data("bad block shape (line " + std::to_string(lineno) + ")");
+    std::vector<double> v((size_t)rows * cols);
+    for (double& x : v)
+      if (!(ss >> x)) data("short block value list (line " + std::to_string(lineno) + ")");
+    const std::array<int32_t, 5> key{k[0], k[1], k[2], k[3], k[4]};
+    if (!bm.emplace(key, std::make_pair(std::array<int32_t, 2>{(int32_t)rows, (int32_t)cols}, std::move(v))).second)
+      data("duplicate block key (line " + std::to_string(lineno) + ")");
+  }
+  BlockSet s;
+  s.off.push_back(0);
+  for (auto& [key, blk] : bm) {
+    s.keys.push_back({key[0], key[1], key[2], key[3], key[4], (uint16_t)blk.first[0], (uint16_t)blk.first[1]});
+    s.values.insert(s.values.end(), blk.second.begin(), blk.second.end());
+    s.off.push_back((int64_t)s.values.size());
+  }
+  return s;
 }
 
 }  // namespace esg

@@ -55,4 +55,7 @@ BlockSet read_shard(const std::string& path, ShardHeader* hdr = nullptr);
 // (gather_blocks' insert_or_assign, model_run.cpp:108-118).
 void write_blocks_text(const std::string& path, const std::vector<const BlockSet*>& sets);
 
+// block_matrix.cpp:109-128 read_blocks_file
+BlockSet read_blocks_text(const std::string& path);
+
 }  // namespace esg

@@ -918,6 +918,19 @@ int esg_build_targets(esg_model* m, int64_t n_blocks, const esg_block_key* keys,
   ESG_API_END
 }
 
+int esg_blocks_read_text(const char* path, int64_t* n_blocks, int64_t* n_values, esg_block_key* keys,
+                         double* values) {
+  ESG_API_BEGIN
+  NEED(path, "path");
+  const BlockSet s = read_blocks_text(path);
+  if (n_blocks) *n_blocks = (int64_t)s.keys.size();
+  if (n_values) *n_values = (int64_t)s.values.size();
+  static_assert(sizeof(esg_block_key) == sizeof(BlockRec), "key record layout");
+  if (keys) std::memcpy(keys, s.keys.data(), sizeof(BlockRec) * s.keys.size());
+  if (values) std::memcpy(values, s.values.data(), sizeof(double) * s.values.size());
+  ESG_API_END
+}
+
 int esg_blocks_merge_text(const char* const* shard_paths, int n_shards, const char* out_path) {
   ESG_API_BEGIN
   NEED(out_path, "out_path");

@@ -487,6 +487,17 @@ def read_block_shard(path: str):
     return (hd,) + _block_arrays(keys, vals)
 
 
+def read_blocks_text(path: str):
+    """block_matrix.cpp read_blocks_file: (keys (n, 5), shapes (n, 2), value
+    offsets (n + 1), fp64 values), blocks in BlockKey order."""
+    nb, nv = C.c_int64(), C.c_int64()
+    _check(lib().esg_blocks_read_text(os.fsencode(path), C.byref(nb), C.byref(nv), None, None))
+    keys = np.zeros(nb.value, BLOCK_KEY)
+    vals = np.zeros(nv.value)
+    _check(lib().esg_blocks_read_text(os.fsencode(path), C.byref(nb), C.byref(nv), _p(keys), _p(vals)))
+    return _block_arrays(keys, vals)
+
+
 def merge_block_shards_to_text(shard_paths: Sequence[str], out_path: str) -> None:
     """model_run's rank-0 text file (block_matrix.cpp:90-101) from shards."""
     arr = (C.c_char_p * len(shard_paths))(*[os.fsencode(p) for p in shard_paths])

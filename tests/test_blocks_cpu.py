@@ -128,3 +128,27 @@ def test_merge_rejects_bad_shards(tmp_path):
             esg.merge_block_shards_to_text(paths, out)
     esg.merge_block_shards_to_text([], out)  # no shards: empty file
     assert (tmp_path / "o.txt").read_bytes() == b""
+
+
+def test_read_blocks_round_trip_and_errors(tmp_path):
+    """test_blocks.cpp:147-163: write_blocks then read_blocks gives the same
+    blocks (in BlockKey order); malformed lines, short value lists and
+    duplicate keys are data errors."""
+    rng = np.random.default_rng(11)
+    k, s, v = random_set(rng, 40)
+    k[:, 0] = np.arange(40)  # distinct keys
+    write_shard(tmp_path / "a.blk", k, s, v)
+    esg.merge_block_shards_to_text([str(tmp_path / "a.blk")], str(tmp_path / "a.txt"))
+    keys, shapes, off, vals = esg.read_blocks_text(str(tmp_path / "a.txt"))
+    order = np.lexsort(k.T[::-1])  # BlockKey order
+    src_off = np.concatenate([[0], np.cumsum(s[:, 0] * s[:, 1])])
+    assert np.array_equal(keys, k[order]) and np.array_equal(shapes, s[order])
+    want = np.concatenate([v[src_off[b]:src_off[b + 1]] for b in order])
+    assert np.array_equal(vals.view(np.uint64), want.view(np.uint64))
+    (tmp_path / "c.txt").write_text("# comment\n\n0 0 0 0 0 1 1 2.5\n")
+    assert esg.read_blocks_text(str(tmp_path / "c.txt"))[3].tolist() == [2.5]
+    for bad in ("0 0 0 0 0 1\n", "0 0 0 0 0 2 2 1 2 3\n", "0 0 0 0 0 0 1\n", "0 0 0 0 0 1 1 nan\n",
+                "0 0 0 0 0 1 1 1\n0 0 0 0 0 1 1 2\n"):
+        (tmp_path / "b.txt").write_text(bad)
+        with pytest.raises(esg.DataError):
+            esg.read_blocks_text(str(tmp_path / "b.txt"))

@@ -139,7 +139,7 @@ def test_reference_output_stage(run, tmp_path):
     assert (tmp_path / "u.txt").read_bytes() == (tmp_path / "ref_u.txt").read_bytes()
 
 
-def test_build_targets_inverts_blocks(run):
+def test_build_targets_inverts_blocks(run, tmp_path):
     """test_model.cpp:472-498: encoding the uncoupled blocks of a forward as
     targets gives back the head outputs (fp32 heads -> fp64 blocks -> fp32);
     every slot of an item's species pair is active; items without a block
@@ -158,6 +158,12 @@ def test_build_targets_inverts_blocks(run):
         row = nt[b] if b < s.n_atoms else et[b - s.n_atoms]
         want = om.uncoupled_block(za, zb, row, *shapes[b])  # encode then decode must round-trip
         assert np.abs(want - blk).max() <= 1e-5 * max(1.0, np.abs(blk).max())
+    # through the text format, as model_run reads training targets
+    net.write_blocks_text(str(tmp_path / "targets.txt"), esg.BLOCKS_UNCOUPLED)
+    tk, ts, to, tv = esg.read_blocks_text(str(tmp_path / "targets.txt"))
+    nt3, nm3, et3, em3, cnt3 = net.build_targets(tk, ts, tv)
+    assert cnt3 == cnt and np.array_equal(nm3, nm) and np.array_equal(em3, em)
+    assert np.array_equal(nt3, nt) and np.array_equal(et3, et)
     # only half of the blocks given: the others keep mask 0
     half = np.arange(len(keys)) % 2 == 0
     hv = np.concatenate([vals[off[b]:off[b + 1]] for b in np.nonzero(half)[0]])
