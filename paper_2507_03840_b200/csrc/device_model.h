@@ -26,8 +26,10 @@ struct TcTile {
 int64_t tf32_tiles(int L, int E, int kind, std::vector<TcTile>* tiles);
 void tf32_pack(const float* params, int L, int E, int li, bool dx, const int64_t* off_a, const int64_t* off_b,
                uint8_t* img, cudaStream_t st);
+// gate_c2 = 2E: lin2 with the gate of its operand fused into the A load
+// (A holds ungated lin1 outputs); 0: plain product
 void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t* img, const TcTile* tiles,
-                      int n_tiles, float* C, int64_t ldc, cudaStream_t st);
+                      int n_tiles, float* C, int64_t ldc, cudaStream_t st, int gate_c2 = 0);
 
 struct DeviceModel {
   int L = 0, E = 0, H = 0;

@@ -786,12 +786,12 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         } else {
           lin_launch<L, E>(0, (const float*)D->A1, n, D->w1t[bidx], D->Hbuf, D->lt[0], D->n_lt[0], st);
         }
-        k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(D->Hbuf, 2 * E, n, M->cfg.gate_enabled,
-                                                                            D->Hbuf);
-        if (D->tf32) {
+        if (D->tf32) {  // gate fused into lin2's operand load
           tf32_gemm_launch(D->Hbuf, (int64_t)H * 2 * E, n, D->wtc[1][bidx], D->tct[1], D->n_tct[1], D->Y,
-                           (int64_t)H * E, st);
+                           (int64_t)H * E, st, M->cfg.gate_enabled ? 2 * E : 0);
         } else {
+          k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(D->Hbuf, 2 * E, n,
+                                                                              M->cfg.gate_enabled, D->Hbuf);
           lin_launch<L, E>(1, D->Hbuf, n, D->w2t[bidx], D->Y, D->lt[1], D->n_lt[1], st);
         }
         ctx->launches += 4;

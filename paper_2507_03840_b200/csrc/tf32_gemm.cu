@@ -74,7 +74,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 // tile, tile-list entry), tile-list major so all SMs stream the same B image.
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tf32x3(const float* __restrict__ A, int64_t lda, int64_t n_rows, const uint8_t* __restrict__ Bimg,
-                  const TcTile* __restrict__ tiles, int n_tiles, float* __restrict__ C, int64_t ldc) {
+                  const TcTile* __restrict__ tiles, int n_tiles, float* __restrict__ C, int64_t ldc, int gate_c2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sA = smem_u32(base), sB = sA + NA * A_STAGE;
@@ -121,6 +121,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t r0 = (it % n_rt) * TM;
       const int nc = (t.K + 31) >> 5;
       const uint32_t bbytes = 2u * (uint32_t)t.N * 128u;
+      // fused gate (kernels.h:210-226) of lin2's operand: column k of an order
+      // block is channel k % 2E, and a thread always converts the same four
+      // columns of a chunk, so its 4 x 4 scales sigmoid(A[row][c]) (the row's
+      // first 2E values: l = 0, m = 0) are loaded once per item
+      float4 gs[4];
+      if (gate_c2) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t row = r0 + (pt >> 3) + 32 * i;
+          const int c0 = (u * 4) % gate_c2;
+          float4 h = row < n_rows ? __ldg(reinterpret_cast<const float4*>(A + row * lda + c0))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          gs[i] = make_float4(1.f / (1.f + expf(-h.x)), 1.f / (1.f + expf(-h.y)), 1.f / (1.f + expf(-h.z)),
+                              1.f / (1.f + expf(-h.w)));
+        }
+      }
       auto load = [&](int c, float4* v) {
         const int k = c * 32 + u * 4;
 #pragma unroll
@@ -129,6 +145,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           v[i] = (c < nc && row < n_rows && k < t.K)
                      ? __ldg(reinterpret_cast<const float4*>(A + row * lda + t.a_col + k))
                      : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (gate_c2)
+            v[i] = make_float4(v[i].x * gs[i].x, v[i].y * gs[i].y, v[i].z * gs[i].z, v[i].w * gs[i].w);
         }
       };
       // one chunk: its B bulk copy, then its A rows (loaded a chunk earlier)
@@ -313,7 +331,7 @@ void tf32_pack(const float* params, int L, int E, int li, bool dx, const int64_t
 }
 
 void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t* img, const TcTile* tiles,
-                      int n_tiles, float* C, int64_t ldc, cudaStream_t st) {
+                      int n_tiles, float* C, int64_t ldc, cudaStream_t st, int gate_c2) {
   static bool init = false;
   if (!init) {
     ESG_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -328,7 +346,8 @@ void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t
   }
   const int64_t items = (n_rows + TM - 1) / TM * n_tiles;
   const int grid = (int)(items < n_sm ? items : n_sm);
-  k_gemm_tf32x3<<<grid, THREADS, SMEM_BYTES, st>>>(A, lda, n_rows, img, tiles, n_tiles, C, ldc);
+  if (gate_c2 && (32 % gate_c2 != 0 || gate_c2 % 4 != 0)) usage("fused gate needs 2E dividing 32");
+  k_gemm_tf32x3<<<grid, THREADS, SMEM_BYTES, st>>>(A, lda, n_rows, img, tiles, n_tiles, C, ldc, gate_c2);
   ESG_CUDA(cudaGetLastError());
 }
 
