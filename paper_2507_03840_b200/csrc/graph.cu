@@ -381,6 +381,7 @@ void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes) {
 
 void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes) {
   if (bytes == 0) return;
+  if (bytes % 4 != 0) usage("d2h_small copies whole 4-byte words");
   if (ctx->zc_cap < bytes) {
     if (ctx->zc) cudaFreeHost(ctx->zc);
     ctx->zc = nullptr;
