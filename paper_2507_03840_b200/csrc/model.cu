@@ -83,7 +83,7 @@ __global__ void k_init_nodes(const int* __restrict__ row_slot, int n_rows, const
 template <int H, int E, int NG>
 __global__ void __launch_bounds__(256) k_init_edges(const double* __restrict__ dist, int64_t n_e,
                                                     const float* __restrict__ lift, int ng, double spacing,
-                                                    float* __restrict__ edges) {
+                                                    float* __restrict__ edges, int full) {
   constexpr int U = 4;
   const int lane = threadIdx.x & 31;
   float w[NG];  // lane c < E keeps lift row c in registers (zero past ng)
@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(256) k_init_edges(const double* __restrict__ d
         if (e0 + u >= cnt) break;
         const int64_t k = base + e0 + u;
         float4* row = reinterpret_cast<float4*>(edges + k * (H * E));
-        for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (full)  // otherwise layer 0 treats the l > 0 planes as zero without reading them
+          for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (lane < E) edges[k * (H * E) + lane] = acc[u];
       }
     }
@@ -676,6 +677,12 @@ template <int H, int E>
 void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, const int* row_of, int out_len,
                   float* out, cudaStream_t st);
 
+// Layer 0 of a plain forward: k_init_edges writes only the l = 0 plane of the
+// edge rows and the layer-0 kernels read the other planes as zero (layer 0's
+// rotate_out writes the full rows).  Training keeps full rows (its saved
+// inputs are read whole), and so does a zero-layer model (the heads read them).
+bool el0_edges(const esg_model* M) { return !M->dev->save_inputs && M->cfg.layers > 0; }
+
 // The head tables may still be read by the copies of an earlier async
 // forward: everything after this point on st waits for them.
 void wait_prior_copies(DeviceModel* D, cudaStream_t st) {
@@ -704,6 +711,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
   esg_ctx* ctx = M->ctx;
   cudaStream_t st = ctx->stream;
   constexpr int H = (L + 1) * (L + 1);
+  const int el0 = layer == 0 && el0_edges(M) ? 1 : 0;  // the edge table still holds only its l = 0 plane
   const int bidx = 2 * layer + (node_block ? 0 : 1);
   // halo exchange (distributed.h:51-130): pack, grouped send/recv straight
   // into the contiguous halo rows of each peer.
@@ -764,7 +772,8 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
           k_rotate_in<L, E, 64, uint16_t><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
-                                                                         D->dir, e0, n, (uint16_t*)D->A1, D->prefetch);
+                                                                         D->dir, e0, n, (uint16_t*)D->A1, D->prefetch,
+                                                                         el0);
         }
         ++ctx->launches;
         Prof pr(D, st, ESG_PROF_SO2);
@@ -775,7 +784,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
           k_rotate_in<L, E, 1, float><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
-                                                                    D->dir, e0, n, (float*)D->A1, D->prefetch);
+                                                                    D->dir, e0, n, (float*)D->A1, D->prefetch, el0);
         }
         Prof pr(D, st, ESG_PROF_SO2);
         // CUDA-core SGEMM per order block, gate in place, SGEMM
@@ -802,9 +811,10 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         constexpr int ro_threads = 32 * E / 4 < 128 ? 128 : 32 * E / 4;
         if (tc)
           k_rotate_out_edge<L, E, uint16_t><<<ro_grid, ro_threads, 0, st>>>((const uint16_t*)D->Y, D->dir, e0, n,
-                                                                            D->edges, D->prefetch);
+                                                                            D->edges, D->prefetch, el0);
         else
-          k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->prefetch);
+          k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->prefetch,
+                                                                       el0);
         ++ctx->launches;
       }
       if (!node_block && D->host_edge_out && layer == M->cfg.layers - 1) {
@@ -877,7 +887,8 @@ void forward_impl(esg_model* M, esg_timing* tm) {
       const int64_t blocks = std::min<int64_t>((D->n_edges + 255) / 256, 148 * 8);  // 8 warps x 32-edge blocks
       k_init_edges<H, E, 32><<<(unsigned)blocks, 256, 0, st>>>(D->dist, D->n_edges, D->params + D->lift_off,
                                                                 M->cfg.n_radial,
-                                                                M->cfg.r_cut / (M->cfg.n_radial - 1), D->edges);
+                                                                M->cfg.r_cut / (M->cfg.n_radial - 1), D->edges,
+                                                                el0_edges(M) ? 0 : 1);
       ++ctx->launches;
     }
   }
@@ -944,7 +955,7 @@ void model_init_edges(esg_model* M, float* out, cudaStream_t st) {
   auto go = [&](auto h, auto e) {
     constexpr int H = decltype(h)::value, EE = decltype(e)::value;
     k_init_edges<H, EE, 32><<<(unsigned)blocks, 256, 0, st>>>(D->dist, D->n_edges, D->params + D->lift_off,
-                                                               M->cfg.n_radial, spacing, out);
+                                                               M->cfg.n_radial, spacing, out, 1);
   };
   using I25 = std::integral_constant<int, 25>;
   using I9 = std::integral_constant<int, 9>;

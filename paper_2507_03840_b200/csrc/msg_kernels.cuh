@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
                                                              const float* __restrict__ dir, int64_t e0, int64_t n_e,
-                                                             OutT* __restrict__ A1, int pf) {
+                                                             OutT* __restrict__ A1, int pf, int el0) {
   using G = Geo<L>;
   using Y = Lay1<L, E, KPAD>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
     // pf 2: every gathered row
     if ((pf & 3) == 2 ? q == 0 : (q == 0 && p == 0 && (pf & 3) == 1)) prefetch_bulk(rowp, H * E * 4);
   }
-  if ((pf & 3) == 1 && threadIdx.x == 0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
+  if ((pf & 3) == 1 && threadIdx.x == 0 && !el0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   __syncthreads();
   wigner_tile_gen<L, DSP, NG>(sdir, ne, sD);
@@ -137,12 +137,16 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
     // and pq = p * E + 4 q < 48 fixed per thread (a1_index, split once)
     const int pq = p * E + q * 4;
     OutT* a1_row = A1 + a1_index<Y::KTOT, KPAD>(el, 0);
+    // el0: the edge table holds only its l = 0 plane (layer 0 of a forward;
+    // k_init_edges leaves the other planes unwritten): they read as zero
+    const bool zero_l = el0 && p == 2;
 #pragma unroll
     for (int l = 0; l <= L; ++l) {
       const int dd = 2 * l + 1;
       float4 x[2 * L + 1];
 #pragma unroll
-      for (int b = -l; b <= l; ++b) x[b + l] = __ldg(base + (l * l + l + b) * (E / 4));
+      for (int b = -l; b <= l; ++b)
+        x[b + l] = (l > 0 && zero_l) ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(base + (l * l + l + b) * (E / 4));
 #pragma unroll
       for (int a = -l; a <= l; ++a) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
 template <int L, int E, typename YT>
 __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rotate_out_edge(const YT* __restrict__ Yin,
                                                                const float* __restrict__ dir, int64_t e0, int64_t n_e,
-                                                               float* __restrict__ edges, int pf) {
+                                                               float* __restrict__ edges, int pf, int el0) {
   using G = Geo<L>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, Q = E / 4;
   __shared__ float sD[TE * DSP];
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
   const int ne = (int)min64(TE, e0 + n_e - t0);
   const int e = threadIdx.x / Q, q = threadIdx.x % Q;
   if (pf & 3) {  // the tile's edge rows (contiguous) and its Y runs
-    if (threadIdx.x == 0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
+    if (threadIdx.x == 0 && !el0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
     prefetch_y<H * E>(Yin, t0 - e0, ne, threadIdx.x >> 5, blockDim.x >> 5);
   }
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
@@ -189,7 +193,8 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
 #pragma unroll
       for (int b = -l; b <= l; ++b) {
         y[b + l] = ld4(Yin + y_index<H * E>(Yin, el, G::mrow(l, b) * E + 4 * q));  // order-major rows
-        old[b + l] = row[(l * l + l + b) * Q];
+        // el0: only the l = 0 plane of the residual holds data (layer 0)
+        old[b + l] = (l > 0 && el0) ? make_float4(0.f, 0.f, 0.f, 0.f) : row[(l * l + l + b) * Q];
       }
 #pragma unroll
       for (int a = -l; a <= l; ++a) {

@@ -881,7 +881,7 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     constexpr int RI_THREADS = 32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4;
     // forward recompute: A1, H, G (+ Y and msg for the attention backward)
     k_rotate_in<L, E, 1, float><<<t32, RI_THREADS, 0, st>>>(nodes, edges, D->src_row, D->dst_row, D->dir, e0, n, T->A1,
-                                                            D->prefetch);
+                                                            D->prefetch, 0);
     lin<L, E>(0, T->A1, n, D->w1t[b], T->Hh, b, D, st);
     k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, 2 * E, n, M->cfg.gate_enabled, T->Gg);
     const float* g_msg;
