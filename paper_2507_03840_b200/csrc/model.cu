@@ -711,7 +711,10 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
   esg_ctx* ctx = M->ctx;
   cudaStream_t st = ctx->stream;
   constexpr int H = (L + 1) * (L + 1);
-  const int el0 = layer == 0 && el0_edges(M) ? 1 : 0;  // the edge table still holds only its l = 0 plane
+  // layer 0 of a plain forward: the edge table still holds only its l = 0
+  // plane (1), and before the node update so do the node rows (2: k_init_nodes
+  // embeds into l = 0 only)
+  const int el0 = layer == 0 && el0_edges(M) ? (node_block ? 3 : 1) : 0;
   const int bidx = 2 * layer + (node_block ? 0 : 1);
   // halo exchange (distributed.h:51-130): pack, grouped send/recv straight
   // into the contiguous halo rows of each peer.

@@ -123,9 +123,9 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
     // pf 1: the tile's edge rows (contiguous) in one bulk prefetch, source
     // rows one each (destination rows repeat along the dst-sorted edges);
     // pf 2: every gathered row
-    if ((pf & 3) == 2 ? q == 0 : (q == 0 && p == 0 && (pf & 3) == 1)) prefetch_bulk(rowp, H * E * 4);
+    if (((pf & 3) == 2 ? q == 0 : (q == 0 && p == 0 && (pf & 3) == 1)) && !(el0 & 2)) prefetch_bulk(rowp, H * E * 4);
   }
-  if ((pf & 3) == 1 && threadIdx.x == 0 && !el0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
+  if ((pf & 3) == 1 && threadIdx.x == 0 && !(el0 & 1)) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   __syncthreads();
   wigner_tile_gen<L, DSP, NG>(sdir, ne, sD);
@@ -137,9 +137,10 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
     // and pq = p * E + 4 q < 48 fixed per thread (a1_index, split once)
     const int pq = p * E + q * 4;
     OutT* a1_row = A1 + a1_index<Y::KTOT, KPAD>(el, 0);
-    // el0: the edge table holds only its l = 0 plane (layer 0 of a forward;
-    // k_init_edges leaves the other planes unwritten): they read as zero
-    const bool zero_l = el0 && p == 2;
+    // el0 & 1: the edge table holds only its l = 0 plane (layer 0 of a
+    // forward; k_init_edges leaves the other planes unwritten); el0 & 2: so do
+    // the node rows (before layer 0's node update).  Those planes read as zero.
+    const bool zero_l = p == 2 ? (el0 & 1) != 0 : (el0 & 2) != 0;
 #pragma unroll
     for (int l = 0; l <= L; ++l) {
       const int dd = 2 * l + 1;
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
   const int ne = (int)min64(TE, e0 + n_e - t0);
   const int e = threadIdx.x / Q, q = threadIdx.x % Q;
   if (pf & 3) {  // the tile's edge rows (contiguous) and its Y runs
-    if (threadIdx.x == 0 && !el0) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
+    if (threadIdx.x == 0 && !(el0 & 1)) prefetch_bulk(edges + t0 * H * E, (uint32_t)ne * H * E * 4);
     prefetch_y<H * E>(Yin, t0 - e0, ne, threadIdx.x >> 5, blockDim.x >> 5);
   }
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
       for (int b = -l; b <= l; ++b) {
         y[b + l] = ld4(Yin + y_index<H * E>(Yin, el, G::mrow(l, b) * E + 4 * q));  // order-major rows
         // el0: only the l = 0 plane of the residual holds data (layer 0)
-        old[b + l] = (l > 0 && el0) ? make_float4(0.f, 0.f, 0.f, 0.f) : row[(l * l + l + b) * Q];
+        old[b + l] = (l > 0 && (el0 & 1)) ? make_float4(0.f, 0.f, 0.f, 0.f) : row[(l * l + l + b) * Q];
       }
 #pragma unroll
       for (int a = -l; a <= l; ++a) {
