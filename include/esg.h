@@ -94,6 +94,11 @@ int esg_graph_offsets(const esg_graph* g, int64_t* dst_off /* N+1 */);
 /* pos are the UNWRAPPED input positions (model_run.cpp:68 passes in.s). */
 int esg_lownn_partition(int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
                         const int32_t* in_degree, int depth, double r_cut, int32_t* node_to_part);
+/* The same assignment computed on the device of `ctx`: one
+ * pass per bisection level, segmented radix sorts by (coordinate, atom id),
+ * a weight scan and a per-segment first-minimiser split.  Host in / out. */
+int esg_lownn_partition_gpu(esg_ctx* ctx, int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
+                            const int32_t* in_degree, int depth, double r_cut, int32_t* node_to_part);
 
 /* ---- partition::mincut_partition (partition.h:26-28, mincut.cpp:183-201;
  * SURVEY §8(f) 4): the edge-cut baseline for Low-NN comparisons (host). */

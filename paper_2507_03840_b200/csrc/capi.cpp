@@ -77,6 +77,8 @@ struct esg_adam {
 
 namespace esg {
 esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32_t* part, int n_parts, int rank);
+void lownn_gpu(esg_ctx* ctx, int n, const double* pos, const M3& cell, const bool pbc[3], const int32_t* deg, int depth,
+               double r_cut, int32_t* part);  // lownn_gpu.cu
 void model_set_targets(esg_model* M, const float* node_target, const uint8_t* node_mask, const float* edge_target,
                        const uint8_t* edge_mask);
 void model_loss_grad(esg_model* M, int64_t n_total, double partials[3], double* loss, float* grads_out);
@@ -402,6 +404,20 @@ int esg_lownn_partition(int n, const double* pos, const double cell[9], const ui
   bool p[3] = {pbc[0] != 0, pbc[1] != 0, pbc[2] != 0};
   auto a = lownn(n, pos, to_m3(cell), p, deg, depth, r_cut);
   std::copy(a.begin(), a.end(), part);
+  ESG_API_END
+}
+
+// lownn.cpp:23-133 on the device (lownn_gpu.cu): the same assignment as
+// esg_lownn_partition, level by level with segmented radix sorts
+int esg_lownn_partition_gpu(esg_ctx* ctx, int n, const double* pos, const double cell[9], const uint8_t pbc[3],
+                            const int32_t* deg, int depth, double r_cut, int32_t* part) {
+  ESG_API_BEGIN
+  NEED(ctx, "ctx");
+  NEED(pos, "pos");
+  NEED(deg, "in_degree");
+  NEED(part, "node_to_part");
+  bool p[3] = {pbc[0] != 0, pbc[1] != 0, pbc[2] != 0};
+  lownn_gpu(ctx, n, pos, to_m3(cell), p, deg, depth, r_cut, part);
   ESG_API_END
 }
 

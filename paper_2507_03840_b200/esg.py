@@ -257,6 +257,18 @@ def lownn_partition(s: AtomicStructure, in_degrees: np.ndarray, depth: int, r_cu
     return part
 
 
+def lownn_partition_gpu(ctx: "Context", s: AtomicStructure, in_degrees: np.ndarray, depth: int,
+                        r_cut: float) -> np.ndarray:
+    """lownn_partition computed on ctx's device (lownn_gpu.cu); same assignment bit for bit."""
+    part = np.zeros(s.n_atoms, np.int32)
+    _check(lib().esg_lownn_partition_gpu(ctx._h, C.c_int(s.n_atoms),
+                                         _p(np.ascontiguousarray(s.positions, np.float64)),
+                                         _p(np.ascontiguousarray(s.cell, np.float64)), _p(s._pbc8()),
+                                         _p(np.ascontiguousarray(in_degrees, np.int32)), C.c_int(depth),
+                                         C.c_double(r_cut), _p(part)))
+    return part
+
+
 class CommPlan:
     """runtime::CommPlan (comm_plan.h:15-35)."""
 
