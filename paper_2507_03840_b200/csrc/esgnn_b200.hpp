@@ -154,6 +154,17 @@ inline Assignment lownn_partition(const AtomicStructure& s, const Graph& g, int 
                             r_cut, a.node_to_part.data()));
   return a;
 }
+// the same assignment computed on ctx's device (esg_lownn_partition_gpu)
+inline Assignment lownn_partition(const Context& ctx, const AtomicStructure& s, const Graph& g, int depth,
+                                  double r_cut) {
+  Assignment a;
+  a.n_parts = 1 << depth;
+  a.node_to_part.resize(s.n_atoms());
+  const auto deg = g.in_degrees();
+  check(esg_lownn_partition_gpu(ctx.get(), s.n_atoms(), s.positions[0].data(), s.cell.data(), s.pbc8().data(),
+                                deg.data(), depth, r_cut, a.node_to_part.data()));
+  return a;
+}
 
 // runtime::CommPlan (comm_plan.h:15-35)
 class CommPlan {
