@@ -239,11 +239,16 @@ def run_ours(args):
     t0 = time.perf_counter()
     g = esg.build_graph(ctx, s, r)
     t_graph = time.perf_counter() - t0
+    def lownn(ctx, s, deg, depth, r):  # ESG_LOWNN_HOST=1: the host restatement (A/B only)
+        if os.environ.get("ESG_LOWNN_HOST") == "1":
+            return esg.lownn_partition(s, deg, depth, r)
+        return esg.lownn_partition_gpu(ctx, s, deg, depth, r)
+
     t0 = time.perf_counter()
     plan = None
     if world > 1:
         depth = int(round(math.log2(world)))
-        part = esg.lownn_partition(s, g.in_degrees(), depth, r)
+        part = lownn(ctx, s, g.in_degrees(), depth, r)
         plan = esg.build_comm_plan(g, s.species, part, world, rank)
     t_part = time.perf_counter() - t0
     net = esg.Network(ctx, cfg, basis)
@@ -342,7 +347,7 @@ def run_ours(args):
             g2 = esg.build_graph(ctx, s, r)  # H2D of the positions
             plan2 = None
             if world > 1:
-                part2 = esg.lownn_partition(s, g2.in_degrees(), int(round(math.log2(world))), r)
+                part2 = lownn(ctx, s, g2.in_degrees(), int(round(math.log2(world))), r)
                 plan2 = esg.build_comm_plan(g2, s.species, part2, world, rank)
             tb = time.perf_counter()
             net.prepare(g2, s.species, plan2)
