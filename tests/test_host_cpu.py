@@ -65,6 +65,16 @@ def test_lownn_errors_map_to_usage():
         esg.lownn_partition(s, np.ones(4, np.int32), 3, 2.5)  # 8 parts > 4 atoms
 
 
+def test_lownn_gpu_entry_rejects_null_context():
+    # the device Low-NN has no host fallback: without a context it is a usage
+    # error (checked before any device work, so this runs without a GPU)
+    s = esg.make_jittered_lattice(8, 2.0, 0.1, [1], 1)
+    part = np.zeros(8, np.int32)
+    rc = esg.lib().esg_lownn_partition_gpu(None, C.c_int(8), esg._p(s.positions), esg._p(s.cell), esg._p(s._pbc8()),
+                                           esg._p(np.ones(8, np.int32)), C.c_int(1), C.c_double(2.5), esg._p(part))
+    assert rc == 2 and b"ctx" in esg.lib().esg_last_error()
+
+
 @pytest.mark.parametrize("n_parts", [2, 4, 8])
 def test_comm_plan_matches_oracle(n_parts):
     s = esg.make_jittered_lattice(400, 2.2, 0.45, [72, 8, 8], 3)
