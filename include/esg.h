@@ -100,22 +100,6 @@ int esg_lownn_partition(int n_atoms, const double* pos, const double cell[9], co
 int esg_lownn_partition_gpu(esg_ctx* ctx, int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
                             const int32_t* in_degree, int depth, double r_cut, int32_t* node_to_part);
 
-/* ---- partition::mincut_partition (partition.h:26-28, mincut.cpp:183-201;
- * SURVEY §8(f) 4): the edge-cut baseline for Low-NN comparisons (host). */
-int esg_mincut_partition(const esg_graph* g, int n_parts, uint64_t seed, int32_t* node_to_part);
-/* The same on a host dst-major CSR (dst_off[n+1], src[dst_off[n]]). */
-int esg_mincut_partition_csr(int n, const int64_t* dst_off, const int32_t* src, int n_parts, uint64_t seed,
-                             int32_t* node_to_part);
-
-/* ---- structures::read_extxyz / write_extxyz (extxyz.h:11-18, extxyz.cpp:62-147)
- * read: pass pos == NULL to get *n_atoms only; otherwise pos (3*cap) and
- * species (cap) must hold n_atoms entries.  cell is row-major (rows are the
- * lattice vectors); parse errors are ESG_ERR_DATA with the line number. */
-int esg_extxyz_read(const char* path, int64_t cap, int* n_atoms, double* pos, int32_t* species, double cell[9],
-                    uint8_t pbc[3]);
-int esg_extxyz_write(const char* path, int n_atoms, const double* pos, const int32_t* species, const double cell[9],
-                     const uint8_t pbc[3]);
-
 /* ---- partition metrics (partition.h:31-62, metrics.cpp:49-166)
  * compute_metrics on the device from the graph CSR and an assignment
  * (n_parts <= 4096).  parts (n_parts entries) and volume (n_parts x n_parts,
@@ -228,6 +212,14 @@ int esg_forward_outputs(const esg_model* m, const float** node_out, const float*
                         const float** node_features, const float** edge_features);
 /* Node / edge feature tables (n_rows*H*E / n_edges*H*E) to host. */
 int esg_features_export(const esg_model* m, float* nodes, float* edges);
+
+/* Per-edge rotation blocks, kernels.h:43-68 build_edge_rotations (align_to_y,
+ * align.cpp:32-39, then wigner_blocks, wigner.cpp:47-83) on the device: the
+ * fp64 displacements (host, E*3) are rounded to fp32 as Network::prepare's
+ * view does and the same in-register recursion the message kernels use
+ * fills blocks (host, E * sum_l (2l+1)^2 floats: D_0..D_lmax row-major,
+ * EdgeRotations' stride).  l_max 1..6. */
+int esg_edge_rotations(esg_ctx* ctx, int64_t n_edges, const double* disp, int l_max, float* blocks);
 
 /* ---- block export ------------------------
  * The blocks of the last forward, replacing Network::assemble_blocks

@@ -32,12 +32,7 @@ void model_outputs(const esg_model* M, const float** no, const float** eo, const
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
 void model_copy_features(const esg_model* M, float* nodes, float* edges);
 void model_prepared_info(const esg_model* M, int64_t info[3]);
-std::vector<int32_t> mincut_partition(int n, const std::vector<int64_t>& dst_off, const std::vector<int32_t>& src,
-                                      int n_parts, uint64_t seed);
-void read_extxyz(const std::string& path, std::vector<double>& pos, std::vector<int32_t>& species, double cell[9],
-                 uint8_t pbc[3]);
-void write_extxyz(const std::string& path, int n, const double* pos, const int32_t* species, const double cell[9],
-                  const uint8_t pbc[3]);
+void edge_rotations(esg_ctx* ctx, int64_t n, const double* disp, int l_max, float* out);
 void partition_metrics_gpu(const esg_graph* g, const int32_t* part, int P, esg_metrics* m, esg_part_stats* parts,
                            int64_t* vol);
 std::string metrics_json(const esg_metrics& m, const esg_part_stats* parts);
@@ -741,6 +736,16 @@ int esg_forward_outputs(const esg_model* m, const float** no, const float** eo, 
   ESG_API_END
 }
 
+int esg_edge_rotations(esg_ctx* ctx, int64_t n_edges, const double* disp, int l_max, float* blocks) {
+  ESG_API_BEGIN
+  NEED(ctx, "context");
+  if (n_edges < 0) usage("negative edge count");
+  if (n_edges && (!disp || !blocks)) usage("edge rotations: NULL array");
+  ESG_CUDA(cudaSetDevice(ctx->device));
+  edge_rotations(ctx, n_edges, disp, l_max, blocks);
+  ESG_API_END
+}
+
 int esg_features_export(const esg_model* m, float* nodes, float* edges) {
   ESG_API_BEGIN
   NEED(m, "model");
@@ -768,70 +773,6 @@ void put_text(const std::string& t, char* out, int64_t cap, int64_t* len) {
   }
 }
 }  // namespace
-
-int esg_mincut_partition(const esg_graph* g, int n_parts, uint64_t seed, int32_t* node_to_part) {
-  ESG_API_BEGIN
-  NEED(g, "graph");
-  NEED(node_to_part, "node_to_part");
-  ESG_CUDA(cudaSetDevice(g->ctx->device));
-  g->host_sync();
-  const auto p = mincut_partition(g->n, g->h_off, g->h_src, n_parts, seed);
-  std::copy(p.begin(), p.end(), node_to_part);
-  ESG_API_END
-}
-
-int esg_mincut_partition_csr(int n, const int64_t* dst_off, const int32_t* src, int n_parts, uint64_t seed,
-                             int32_t* node_to_part) {
-  ESG_API_BEGIN
-  NEED(dst_off, "dst_off");
-  NEED(node_to_part, "node_to_part");
-  if (n < 0) usage("n must be non-negative");
-  std::vector<int64_t> off(dst_off, dst_off + n + 1);
-  if (off[n] > 0) NEED(src, "src");
-  std::vector<int32_t> sv(src, src + off[n]);
-  for (int32_t v : sv)
-    if (v < 0 || v >= n) data("source index out of range");
-  const auto p = mincut_partition(n, off, sv, n_parts, seed);
-  std::copy(p.begin(), p.end(), node_to_part);
-  ESG_API_END
-}
-
-int esg_extxyz_read(const char* path, int64_t cap, int* n_atoms, double* pos, int32_t* species, double cell[9],
-                    uint8_t pbc[3]) {
-  ESG_API_BEGIN
-  NEED(path, "path");
-  NEED(n_atoms, "n_atoms");
-  std::vector<double> p;
-  std::vector<int32_t> z;
-  double c[9];
-  uint8_t b[3];
-  read_extxyz(path, p, z, c, b);
-  *n_atoms = (int)z.size();
-  if (pos) {
-    NEED(species, "species");
-    if (cap < (int64_t)z.size()) usage("buffers too small for the structure");
-    std::copy(p.begin(), p.end(), pos);
-    std::copy(z.begin(), z.end(), species);
-  }
-  if (cell) std::copy(c, c + 9, cell);
-  if (pbc) std::copy(b, b + 3, pbc);
-  ESG_API_END
-}
-
-int esg_extxyz_write(const char* path, int n_atoms, const double* pos, const int32_t* species, const double cell[9],
-                     const uint8_t pbc[3]) {
-  ESG_API_BEGIN
-  NEED(path, "path");
-  NEED(cell, "cell");
-  NEED(pbc, "pbc");
-  if (n_atoms < 0) usage("n_atoms must be non-negative");
-  if (n_atoms > 0) {
-    NEED(pos, "pos");
-    NEED(species, "species");
-  }
-  write_extxyz(path, n_atoms, pos, species, cell, pbc);
-  ESG_API_END
-}
 
 int esg_partition_metrics(const esg_graph* g, const int32_t* node_to_part, int n_parts, esg_metrics* m,
                           esg_part_stats* parts, int64_t* volume) {

@@ -947,6 +947,53 @@ void forward_impl(esg_model* M, esg_timing* tm) {
 
 }  // namespace
 
+// Per-edge rotation blocks (kernels.h:43-68 build_edge_rotations): the
+// fp32 displacement (the prepared view's `dir`, rounded from the fp64
+// Graph::disp) through align_to_y and the generated Ivanic-Ruedenberg
+// recursion -- the same device code the message kernels run in-register.
+// Output per edge: the stacked D_l blocks l = 0..L, (2l+1)^2 row-major each.
+template <int L>
+__global__ void __launch_bounds__(128) k_edge_rotations(const double* __restrict__ disp, int64_t n,
+                                                        float* __restrict__ out) {
+  using G = Geo<L>;
+  constexpr int TE = L >= 6 ? 16 : 32, DSP = G::DS + 2;  // static SMEM <= 48 KB
+  __shared__ float sD[TE * DSP];
+  __shared__ float sdir[TE * 3];
+  const int64_t t0 = (int64_t)blockIdx.x * TE;
+  const int ne = (int)(n - t0 < TE ? n - t0 : TE);
+  for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = (float)disp[t0 * 3 + i];
+  __syncthreads();
+  wigner_tile_gen<L, DSP>(sdir, ne, sD);
+  for (int i = threadIdx.x; i < ne * G::DS; i += blockDim.x) out[t0 * G::DS + i] = sD[(i / G::DS) * DSP + i % G::DS];
+}
+
+void edge_rotations(esg_ctx* ctx, int64_t n, const double* disp, int l_max, float* out) {
+  if (l_max < 1 || l_max > 6) usage("edge rotations: l_max must be 1..6");
+  if (n <= 0) return;
+  const int ds = l_max + 1 == 0 ? 0 : (l_max + 1) * (4 * (l_max + 1) * (l_max + 1) - 1) / 3;
+  cudaStream_t st = ctx->stream;
+  double* d_disp = nullptr;
+  float* d_out = nullptr;
+  ESG_CUDA(cudaMalloc(&d_disp, sizeof(double) * 3 * n));
+  ESG_CUDA(cudaMalloc(&d_out, sizeof(float) * ds * n));
+  ESG_CUDA(cudaMemcpyAsync(d_disp, disp, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+  const unsigned grid = (unsigned)((n + 31) / 32), grid6 = (unsigned)((n + 15) / 16);
+  switch (l_max) {
+    case 1: k_edge_rotations<1><<<grid, 128, 0, st>>>(d_disp, n, d_out); break;
+    case 2: k_edge_rotations<2><<<grid, 128, 0, st>>>(d_disp, n, d_out); break;
+    case 3: k_edge_rotations<3><<<grid, 128, 0, st>>>(d_disp, n, d_out); break;
+    case 4: k_edge_rotations<4><<<grid, 128, 0, st>>>(d_disp, n, d_out); break;
+    case 5: k_edge_rotations<5><<<grid, 128, 0, st>>>(d_disp, n, d_out); break;
+    default: k_edge_rotations<6><<<grid6, 128, 0, st>>>(d_disp, n, d_out); break;
+  }
+  ++ctx->launches;
+  ESG_CUDA(cudaGetLastError());
+  ESG_CUDA(cudaMemcpyAsync(out, d_out, sizeof(float) * ds * n, cudaMemcpyDeviceToHost, st));
+  ESG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d_disp);
+  cudaFree(d_out);
+}
+
 // The initial edge table (k_init_edges) into out: the training backward
 // recomputes layer 0's input instead of keeping it.
 void model_init_edges(esg_model* M, float* out, cudaStream_t st) {

@@ -269,6 +269,18 @@ def lownn_partition_gpu(ctx: "Context", s: AtomicStructure, in_degrees: np.ndarr
     return part
 
 
+def edge_rotations(ctx: "Context", disp: np.ndarray, l_max: int) -> np.ndarray:
+    """build_edge_rotations (kernels.h:43-68) on ctx's device: per edge the
+    stacked Wigner blocks D_0..D_lmax (row-major, stride sum (2l+1)^2) of
+    align_to_y of the fp32-rounded displacement, as the message kernels
+    compute them in-register."""
+    d = np.ascontiguousarray(disp, np.float64).reshape(-1, 3)
+    ds = (l_max + 1) * (4 * (l_max + 1) ** 2 - 1) // 3
+    out = np.zeros((d.shape[0], ds), np.float32)
+    _check(lib().esg_edge_rotations(ctx._h, C.c_int64(d.shape[0]), _p(d), C.c_int(l_max), _p(out)))
+    return out
+
+
 class CommPlan:
     """runtime::CommPlan (comm_plan.h:15-35)."""
 
@@ -345,39 +357,10 @@ class Timing:
 
 
 # ------------------------------------------------------------ input side
-def read_extxyz(path: str) -> AtomicStructure:
-    """structures::read_extxyz_file (extxyz.cpp:62-121)."""
-    n = C.c_int()
-    cell = np.zeros(9)
-    pbc = np.zeros(3, np.uint8)
-    _check(lib().esg_extxyz_read(os.fsencode(path), C.c_int64(0), C.byref(n), None, None, _p(cell), _p(pbc)))
-    pos = np.zeros((n.value, 3))
-    sp = np.zeros(n.value, np.int32)
-    _check(lib().esg_extxyz_read(os.fsencode(path), C.c_int64(n.value), C.byref(n), _p(pos), _p(sp), _p(cell),
-                                 _p(pbc)))
-    return AtomicStructure(pos, sp, cell.reshape(3, 3), pbc.astype(bool))
-
-
-def write_extxyz(path: str, s: AtomicStructure) -> None:
-    """structures::write_extxyz_file (extxyz.cpp:125-147)."""
-    _check(lib().esg_extxyz_write(os.fsencode(path), C.c_int(s.n_atoms), _p(np.ascontiguousarray(s.positions, np.float64)),
-                                  _p(np.ascontiguousarray(s.species, np.int32)),
-                                  _p(np.ascontiguousarray(s.cell, np.float64)), _p(s._pbc8())))
-
-
-def mincut_partition(g, n_parts: int, seed: int = 1) -> np.ndarray:
-    """partition::mincut_partition (mincut.cpp:183-201): g is a Graph, or a
-    host (dst_off, src) CSR pair."""
-    if isinstance(g, tuple):
-        off = np.ascontiguousarray(g[0], np.int64)
-        src = np.ascontiguousarray(g[1], np.int32)
-        out = np.zeros(off.size - 1, np.int32)
-        _check(lib().esg_mincut_partition_csr(C.c_int(out.size), _p(off), _p(src), C.c_int(n_parts),
-                                              C.c_uint64(seed), _p(out)))
-        return out
-    out = np.zeros(g.n_nodes, np.int32)
-    _check(lib().esg_mincut_partition(g._h, C.c_int(n_parts), C.c_uint64(seed), _p(out)))
-    return out
+def _metrics_from(m, ps, vol):
+    parts = np.array([[p.nodes, p.edges, p.neighbors, p.recv_volume] for p in ps], np.int64)
+    return Metrics(m.node_imbalance, m.edge_imbalance, m.mean_neighbors, m.max_neighbors, m.total_recv,
+                   m.cut_edges, parts, vol, m, ps)
 
 
 # ------------------------------------------------------- partition metrics
@@ -425,11 +408,6 @@ class Metrics:
         _check(lib().esg_partition_dot(_p(v), self._p, C.c_int(P), buf, C.c_int64(len(buf)), C.byref(n)))
         return buf.value.decode()
 
-
-def _metrics_from(m, ps, vol):
-    parts = np.array([[p.nodes, p.edges, p.neighbors, p.recv_volume] for p in ps], np.int64)
-    return Metrics(m.node_imbalance, m.edge_imbalance, m.mean_neighbors, m.max_neighbors, m.total_recv,
-                   m.cut_edges, parts, vol, m, ps)
 
 
 def partition_metrics(g: "Graph", node_to_part: np.ndarray, n_parts: int) -> Metrics:

@@ -18,6 +18,10 @@ pytestmark = pytest.mark.gpu
 SKEW = np.array([[6.0, 0.4, 0.0], [0.9, 5.5, 0.3], [0.2, 0.6, 6.5]])
 
 
+PLAN_KEYS = ("row_global", "edge_index", "src_row", "dst_row", "send_rows", "nbr_peer", "nbr_recv_row",
+             "nbr_recv_count", "nbr_send_count")
+
+
 def same_graph(g, ref):
     assert len(g["src"]) == len(ref["src"])
     for k in ("src", "dst", "shift"):
@@ -63,12 +67,34 @@ def test_graph_configs_bit_exact(gpu_ctx, name):
     for depth in (1, 2, 3):
         part = esg.lownn_partition(s, deg, depth, r)
         assert np.array_equal(part, O.lownn(s.positions, s.cell, np.ones(3, np.uint8), deg, depth, r))
-        if name == "C1":
-            for rank in range(1 << depth):
-                got = esg.build_comm_plan(g, s.species, part, 1 << depth, rank).export()
-                want = O.comm_plan(s.n_atoms, ref["src"], ref["dst"], part, 1 << depth, rank)
-                for k in ("row_global", "edge_index", "src_row", "send_rows", "nbr_recv_row"):
-                    assert np.array_equal(got[k], want[k])
+        for rank in range(1 << depth):
+            got = esg.build_comm_plan(g, s.species, part, 1 << depth, rank).export()
+            want = O.comm_plan(s.n_atoms, ref["src"], ref["dst"], part, 1 << depth, rank)
+            for k in PLAN_KEYS:
+                assert np.array_equal(got[k], want[k]), (name, depth, rank, k)
+
+
+def test_graph_c4_bit_exact_and_plans(gpu_ctx):
+    """The bench workload's graph (C4: 192k atoms, 69.6M edges at 10 A) is
+    bit-exact against the oracle's build_graph (graph.cpp:55-131); Low-NN at
+    depth 3 on the host and on the device equals the oracle
+    (lownn.cpp:105-133); every rank's comm plan equals comm_plan.cpp:11-106."""
+    s, r, _, _ = esg.config_structure("C4")
+    g = esg.build_graph(gpu_ctx, s, r)
+    ref = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
+    assert g.n_edges == 69626112
+    same_graph(g.export(), ref)
+    deg = g.in_degrees()
+    assert np.array_equal(deg, O.in_degrees(s.n_atoms, ref))
+    part = O.lownn(s.positions, s.cell, np.ones(3, np.uint8), deg, 3, r)
+    assert np.array_equal(esg.lownn_partition(s, deg, 3, r), part)
+    assert np.array_equal(esg.lownn_partition_gpu(gpu_ctx, s, deg, 3, r), part)
+    for rank in range(8):
+        got = esg.build_comm_plan(g, s.species, part, 8, rank).export()
+        want = O.comm_plan(s.n_atoms, ref["src"], ref["dst"], part, 8, rank)
+        for k in PLAN_KEYS:
+            assert np.array_equal(got[k], want[k]), (rank, k)
+    g.close()
 
 
 def test_graph_sort_fallback(gpu_ctx, monkeypatch):
@@ -134,6 +160,47 @@ def test_forward_fp32_c1(gpu_ctx):
     # deterministic: a second forward is bitwise identical
     no2, eo2, _ = net.forward()
     assert np.array_equal(no, no2) and np.array_equal(eo, eo2)
+
+
+def test_forward_c2_three_layers(gpu_ctx):
+    """BASELINE config 2: the 3-layer forward (network.h:115-164 at M = 3) on
+    the 3,000-atom HfO2 structure, 1.86M edges.  fp32 linears: heads and
+    uncoupled blocks within the fp32 bar of the float oracle; bf16 linears
+    within their stated bar; serial determinism."""
+    s, r, layers, basis = esg.config_structure("C2")
+    net, (no, eo, tm), (rno, reo), om, ref = run_both(gpu_ctx, s, r, layers, basis)
+    assert tm.gpu_launches > 0 and net.n_edges == 1860036
+    for got, want in ((no, rno), (eo, reo)):
+        mx, rl2 = err(got, want)
+        assert mx < 2e-4 and rl2 < 2e-5, (mx, rl2)
+    # uncoupled blocks (block_matrix.cpp:66-88) of the device export against
+    # the oracle's to_block of the oracle heads, on a sample of items
+    flat = net.blocks_uncoupled()
+    norb = {72: 10, 8: 4}
+    sp = s.species
+    sizes = np.array([norb[z] for z in sp])
+    item_n = np.concatenate([sizes * sizes, sizes[ref["src"]] * sizes[ref["dst"]]])
+    starts = np.concatenate([[0], np.cumsum(item_n)])
+    assert starts[-1] == flat.size
+    rng = np.random.default_rng(5)
+    picks = np.concatenate([np.arange(64), s.n_atoms + rng.choice(len(ref["src"]), 400, replace=False)])
+    for it in picks:
+        if it < s.n_atoms:
+            za, zb, row = sp[it], sp[it], rno[it]
+        else:
+            k = it - s.n_atoms
+            za, zb, row = sp[ref["src"][k]], sp[ref["dst"][k]], reo[k]
+        want = om.uncoupled_block(za, zb, row, norb[za], norb[zb]).ravel()
+        got = flat[starts[it]:starts[it + 1]]
+        scale = max(np.abs(reo).max(), np.abs(rno).max())
+        assert np.abs(got - want).max() <= 2e-4 * scale, it
+    no2, eo2, _ = net.forward()
+    assert np.array_equal(no, no2) and np.array_equal(eo, eo2)
+    net.set_precision(esg.LINEAR_BF16)
+    nb, eb, _ = net.forward()
+    for got, want in ((nb, rno), (eb, reo)):
+        mx, rl2 = err(got, want)
+        assert mx < 5e-2 and rl2 < 2e-2, (mx, rl2)
 
 
 def test_forward_bf16_tensor_cores(gpu_ctx):
