@@ -31,12 +31,35 @@ void tf32_pack(const float* params, int L, int E, int li, bool dx, const int64_t
 void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t* img, const TcTile* tiles,
                       int n_tiles, float* C, int64_t ldc, cudaStream_t st, int gate_c2 = 0);
 
+// Power-of-two scales of the fp16x3 chain (so2_f16x3.cu), per order m: the
+// weight scales of lin1 / lin2 and ||W1_m||_inf (max row sum of |w|), which
+// bounds lin1's output from the message bound
+struct F16x3Scales {
+  float w1[8], w2[8], w1inf[8];
+};
+bool so2_f16x3_available(int L, int E);
+int64_t so2_f16x3_a1_tile_bytes(int L, int E);
+int64_t so2_f16x3_w1_bytes(int L, int E);
+int64_t so2_f16x3_w2_bytes(int L, int E);
+int so2_f16x3_kofs(int m);
+int so2_f16x3_ktot();
+void so2_f16x3_launch(int L, int E, const uint8_t* A1, int64_t n_e, const uint8_t* W1, const uint8_t* W2,
+                      const F16x3Scales& sc, const float* tmax, int edge_slot, float* Y, int gate, const float* att,
+                      float* logits, cudaStream_t st);
+
 struct DeviceModel {
   int L = 0, E = 0, H = 0;
   // weights (device)
   float* params = nullptr;  // raw flat parameters
   std::vector<float*> w1t, w2t;      // per block (2*layers): SIMT packed
   std::vector<uint16_t*> w1b, w2b;   // per block: tcgen05 bf16 packed
+  std::vector<uint8_t*> w1f, w2f;    // per block: fp16x3 split images (so2_f16x3.cu)
+  std::vector<F16x3Scales> f16sc;    // per block: their scales
+  bool f16x3 = true;                 // ESG_F16X3=0: fp32 linears on the tf32 GEMMs instead
+  // |x| maxima of the feature tables for the fp16x3 scale bounds: [0] the
+  // node table entering the current block, [1 + l] the edge table entering
+  // layer l (written by the init / rotate_out kernels)
+  float* tmax = nullptr;
   std::vector<float*> w1n, w2n;      // per block: expanded, not transposed (training dx = W^T g)
   bool weights_allocated = false;
   struct LinTile* lt[4] = {nullptr, nullptr, nullptr, nullptr};  // k_gemm_m tile lists (lin_kernels.cuh)
@@ -95,6 +118,7 @@ struct DeviceModel {
          cap_nodes_alt = 0, cap_edges = 0, cap_a1 = 0, cap_y = 0, cap_logits = 0, cap_node_out = 0,
          cap_edge_out = 0, cap_send_rows = 0, cap_send_buf = 0, cap_row_global = 0, cap_eshift = 0;
   bool a1_tc_clean = false;  // A1 holds zeros in every tensor-core K padding slot
+  int a1_zero_mode = 0;      // which image's padding is zero (1 bf16 tiles, 2 fp16x3 split)
   // training (train.cu): the forward saves every block's input tables when
   // save_inputs is set -- the node table after the block's halo exchange
   // (per block) and the edge table entering each layer (per layer)

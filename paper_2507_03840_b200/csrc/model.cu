@@ -83,8 +83,10 @@ __global__ void k_init_nodes(const int* __restrict__ row_slot, int n_rows, const
 template <int H, int E, int NG>
 __global__ void __launch_bounds__(256) k_init_edges(const double* __restrict__ dist, int64_t n_e,
                                                     const float* __restrict__ lift, int ng, double spacing,
-                                                    float* __restrict__ edges, int full) {
+                                                    float* __restrict__ edges, int full,
+                                                    float* __restrict__ emax = nullptr) {
   constexpr int U = 4;
+  float vmax = 0.f;
   const int lane = threadIdx.x & 31;
   float w[NG];  // lane c < E keeps lift row c in registers (zero past ng)
 #pragma unroll
@@ -113,9 +115,16 @@ __global__ void __launch_bounds__(256) k_init_edges(const double* __restrict__ d
         float4* row = reinterpret_cast<float4*>(edges + k * (H * E));
         if (full)  // otherwise layer 0 treats the l > 0 planes as zero without reading them
           for (int q = E / 4 + lane; q < H * E / 4; q += 32) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (lane < E) edges[k * (H * E) + lane] = acc[u];
+        if (lane < E) {
+          edges[k * (H * E) + lane] = acc[u];
+          vmax = fmaxf(vmax, fabsf(acc[u]));
+        }
       }
     }
+  }
+  if (emax) {  // max |edge row| (the fp16x3 chain's scale bound of layer 0)
+    vmax = warp_max(vmax);
+    if (lane == 0) atomic_max_abs(emax, vmax);
   }
 }
 
@@ -344,6 +353,58 @@ std::vector<float> expanded(const esg_model* M, const std::string& base, int m, 
   return W;
 }
 
+namespace {
+// Power-of-two scale of a split operand bounded by `bound` (host twin of
+// f16s_pow2_scale): every |x| / s < 2^14.
+float pow2_scale_host(double bound) {
+  if (!(bound > 0.0) || !std::isfinite(bound)) return 1.f;
+  int k;
+  std::frexp((float)bound, &k);
+  return std::ldexp(1.f, k - 14);
+}
+uint16_t f16_bits(float x) {
+  const __half h = __float2half_rn(x);
+  uint16_t u;
+  std::memcpy(&u, &h, 2);
+  return u;
+}
+// The fp16x3 split image of one expanded order block W (N x K row-major):
+// per 32-wide K chunk N rows of 128 bytes, [hi(32) | lo(32)] fp16 of W / s,
+// 16-byte units XOR-swizzled by row % 8 (so2_f16x3.cu).  Returns s and
+// ||W||_inf (max row sum of |w|, rounded up).
+void pack_f16x3_block(const std::vector<float>& W, int N, int K, std::vector<uint8_t>& img, float* scale,
+                      float* inf_norm) {
+  double mx = 0.0, inf = 0.0;
+  for (int n = 0; n < N; ++n) {
+    double rs = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double a = std::fabs((double)W[(size_t)n * K + k]);
+      mx = std::max(mx, a);
+      rs += a;
+    }
+    inf = std::max(inf, rs);
+  }
+  const float s = pow2_scale_host(mx), inv = 1.f / s;
+  *scale = s;
+  *inf_norm = std::nextafter((float)inf, INFINITY);
+  const int KP = (K + 31) / 32 * 32;
+  const size_t base = img.size();
+  img.resize(base + (size_t)N * KP * 4, 0);
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < K; ++k) {
+      const float x = W[(size_t)n * K + k] * inv;
+      const uint16_t hb = f16_bits(x);
+      __half hh;
+      std::memcpy(&hh, &hb, 2);
+      const uint16_t lb = f16_bits(x - __half2float(hh));
+      const int c = k >> 5, w = k & 31, u = w >> 3;
+      const size_t row = base + (size_t)c * N * 128 + (size_t)n * 128 + (w & 7) * 2;
+      std::memcpy(&img[row + (((u) ^ (n & 7)) << 4)], &hb, 2);
+      std::memcpy(&img[row + (((4 + u) ^ (n & 7)) << 4)], &lb, 2);
+    }
+}
+}  // namespace
+
 void model_upload_params(esg_model* M) {
   DeviceModel* D = M->dev;
   cudaStream_t st = M->ctx->stream;
@@ -375,6 +436,15 @@ void model_upload_params(esg_model* M) {
       D->w1b[b] = dalloc<uint16_t>(bf1);
       D->w2b[b] = dalloc<uint16_t>(bf2);
     }
+    if (so2_f16x3_available(L, E)) {
+      D->w1f.assign(nb, nullptr);
+      D->w2f.assign(nb, nullptr);
+      for (int b = 0; b < nb; ++b) {
+        D->w1f[b] = dalloc<uint8_t>(so2_f16x3_w1_bytes(L, E));
+        D->w2f[b] = dalloc<uint8_t>(so2_f16x3_w2_bytes(L, E));
+      }
+    }
+    D->tmax = dalloc<float>(16);
     D->embed = dalloc<float>(M->species_list.size() * E);
     D->head_w[0] = dalloc<float>(M->heads.keys.size() * E);
     D->head_w[1] = dalloc<float>(M->heads.keys.size() * E);
@@ -435,6 +505,23 @@ void model_upload_params(esg_model* M) {
         }
         tf32_pack(D->params, L, E, li, false, oa.data(), ob.data(), D->wtc[li == 0 ? 0 : 1][b], st);
         tf32_pack(D->params, L, E, li, true, oa.data(), ob.data(), D->wtc[li == 0 ? 3 : 2][b], st);
+        if (!D->w1f.empty()) {  // fp16x3 split images, packed on the host from the same values
+          std::vector<uint8_t> img;
+          if ((int)D->f16sc.size() < nb) D->f16sc.resize(nb);
+          F16x3Scales& sc = D->f16sc[b];
+          for (int m = 0; m <= L; ++m) {
+            const int rows = m == 0 ? M->lay.nd(0) : 2 * M->lay.nd(m);
+            float sw = 1.f, inf = 0.f;
+            pack_f16x3_block(expanded(M, wb, m, cin, cout), rows * cout, rows * cin, img, &sw, &inf);
+            (li == 0 ? sc.w1 : sc.w2)[m] = sw;
+            if (li == 0) sc.w1inf[m] = inf;
+          }
+          const int64_t want = li == 0 ? so2_f16x3_w1_bytes(L, E) : so2_f16x3_w2_bytes(L, E);
+          if ((int64_t)img.size() != want) usage("fp16x3 weight image size mismatch");
+          ESG_CUDA(cudaMemcpyAsync(li == 0 ? D->w1f[b] : D->w2f[b], img.data(), img.size(), cudaMemcpyHostToDevice,
+                                   st));
+          ESG_CUDA(cudaStreamSynchronize(st));  // img is freed at scope exit
+        }
       }
     }
     D->att_off.push_back(M->params.at("layer" + std::to_string(layer) + "/att").offset);
@@ -479,6 +566,7 @@ void model_device_create(esg_model* M) {
   M->dev = new DeviceModel();
   if (const char* pf = std::getenv("ESG_PREFETCH")) M->dev->prefetch = std::atoi(pf);
   if (const char* tf = std::getenv("ESG_TF32")) M->dev->tf32 = std::atoi(tf) != 0;
+  if (const char* f3 = std::getenv("ESG_F16X3")) M->dev->f16x3 = std::atoi(f3) != 0;
   M->dev->L = L;
   M->dev->E = E;
   M->dev->H = (L + 1) * (L + 1);
@@ -512,6 +600,9 @@ void model_device_destroy(esg_model* M) {
   for (auto p : D->w2n) free_ptr(p);
   for (auto p : D->w1b) free_ptr(p);
   for (auto p : D->w2b) free_ptr(p);
+  for (auto p : D->w1f) free_ptr(p);
+  for (auto p : D->w2f) free_ptr(p);
+  free_ptr(D->tmax);
   for (auto& e : D->ev) cudaEventDestroy(e);
   if (D->copies_pending) cudaEventSynchronize(D->copies_done);
   if (D->copies_done) cudaEventDestroy(D->copies_done);
@@ -640,9 +731,11 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   // fp32 row-major (CUDA-core path) or bf16 tiles of 128 edges (tensor cores)
   const size_t a1_fp32 = (size_t)D->chunk_cap * K1T * 4;
   const size_t a1_bf16 = (size_t)((D->chunk_cap + 127) / 128) * 128 * K1T * 2;
+  const size_t a1_f16s =
+      so2_f16x3_available(D->L, D->E) ? (size_t)((D->chunk_cap + 127) / 128) * so2_f16x3_a1_tile_bytes(D->L, D->E) : 0;
   void* a1_prev = D->A1;
-  D->A1 = (void*)grow((uint8_t*)D->A1, D->cap_a1, std::max(a1_fp32, a1_bf16));
-  if (D->A1 != a1_prev) D->a1_tc_clean = false;  // zeroed before the first tensor-core use (run_block)
+  D->A1 = (void*)grow((uint8_t*)D->A1, D->cap_a1, std::max(std::max(a1_fp32, a1_bf16), a1_f16s));
+  if (D->A1 != a1_prev) D->a1_zero_mode = 0;  // zeroed before the first tensor-core use (run_block)
   // fp32 rows (CUDA-core path) or bf16 tiles of 128 edges (tcgen05 epilogue)
   D->Y = (float*)grow((uint8_t*)D->Y, D->cap_y,
                       std::max((size_t)D->chunk_cap * row * 4, (size_t)((D->chunk_cap + 127) / 128) * 128 * row * 2));
@@ -758,11 +851,24 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     ++ctx->launches;
   }
   const bool tc = D->precision == ESG_LINEAR_BF16 && so2_tc_available(L, E);
-  if (tc && !D->a1_tc_clean) {  // the K padding slots of the tensor-core image are never written by rotate_in
+  // fp32 linears on the tensor cores through the fp16x3 split (so2_f16x3.cu);
+  // training keeps the tf32 GEMMs (its reverse pass shares their images)
+  const bool f3 = !tc && D->f16x3 && !D->save_inputs && !D->w1f.empty();
+  const int zero_mode = tc ? 1 : (f3 ? 2 : 0);
+  if (zero_mode && D->a1_zero_mode != zero_mode) {
+    // the K padding slots of a tensor-core image are never written by rotate_in
     ESG_CUDA(cudaMemsetAsync(D->A1, 0, D->cap_a1, st));
-    D->a1_tc_clean = true;
-  } else if (!tc) {
-    D->a1_tc_clean = false;  // the CUDA-core path writes fp32 rows over the whole buffer
+    D->a1_zero_mode = zero_mode;
+  } else if (!zero_mode) {
+    D->a1_zero_mode = 0;  // the CUDA-core path writes fp32 rows over the whole buffer
+  }
+  const int edge_slot = 1 + layer;  // tmax slot of the edge table entering this layer
+  if (f3) {  // |node table| bound after the exchange (k_abs_max, a 1.6 KB/row read)
+    Prof pr(D, st, ESG_PROF_COPY);
+    ESG_CUDA(cudaMemsetAsync(D->tmax, 0, sizeof(float), st));
+    const int64_t n4 = (int64_t)D->n_rows * H * E / 4;
+    k_abs_max<256><<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 8), 256, 0, st>>>(D->nodes, 4 * n4, D->tmax);
+    ++ctx->launches;
   }
   const float* att = D->params + D->att_off[layer];
   for (const auto& ch : D->chunks) {
@@ -771,7 +877,19 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
     if (n > 0) {
       const unsigned ri_tiles = (unsigned)((n + 31) / 32);
       constexpr int RI_THREADS = 32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4;  // >= 4 warps for the Wigner groups
-      if (tc) {
+      if (f3) {
+        {
+          Prof pr(D, st, ESG_PROF_ROTATE_IN);
+          k_rotate_in<L, E, 32, uint8_t><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
+                                                                        D->dir, e0, n, (uint8_t*)D->A1, D->prefetch,
+                                                                        el0, D->tmax, edge_slot);
+        }
+        ++ctx->launches;
+        Prof pr(D, st, ESG_PROF_SO2);
+        so2_f16x3_launch(L, E, (const uint8_t*)D->A1, n, D->w1f[bidx], D->w2f[bidx], D->f16sc[bidx], D->tmax,
+                         edge_slot, D->Y, M->cfg.gate_enabled, att, node_block ? D->logits : nullptr, st);
+        ++ctx->launches;
+      } else if (tc) {
         {
           Prof pr(D, st, ESG_PROF_ROTATE_IN);
           k_rotate_in<L, E, 64, uint16_t><<<ri_tiles, RI_THREADS, 0, st>>>(D->nodes, D->edges, D->src_row, D->dst_row,
@@ -817,7 +935,7 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
                                                                             D->edges, D->prefetch, el0);
         else
           k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->prefetch,
-                                                                       el0);
+                                                                       el0, f3 ? D->tmax + 2 + layer : nullptr);
         ++ctx->launches;
       }
       if (!node_block && D->host_edge_out && layer == M->cfg.layers - 1) {
@@ -841,9 +959,14 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
                                       dyn));
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, uint16_t, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bf16));
+        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      dyn));
         attr = true;
       }
-      if (tc)
+      if (f3)  // logits from the chain's fp32 accumulator
+        k_node_update<L, E, float, true><<<ch.second - ch.first, 128, dyn, st>>>(
+            D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->prefetch);
+      else if (tc)
         k_node_update<L, E, uint16_t, true><<<ch.second - ch.first, 128, dyn_bf16, st>>>(
             (const uint16_t*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->prefetch);
       else
@@ -882,6 +1005,7 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   {
     const int64_t n = (int64_t)D->n_rows * H * E;
     Prof pr(D, st, ESG_PROF_INIT);
+    ESG_CUDA(cudaMemsetAsync(D->tmax, 0, 16 * sizeof(float), st));  // table maxima of this forward
     k_init_nodes<H, E><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->row_slot, D->n_rows, D->embed, D->nodes);
     ++ctx->launches;
     if (D->n_edges) {
@@ -891,7 +1015,7 @@ void forward_impl(esg_model* M, esg_timing* tm) {
       k_init_edges<H, E, 32><<<(unsigned)blocks, 256, 0, st>>>(D->dist, D->n_edges, D->params + D->lift_off,
                                                                 M->cfg.n_radial,
                                                                 M->cfg.r_cut / (M->cfg.n_radial - 1), D->edges,
-                                                                el0_edges(M) ? 0 : 1);
+                                                                el0_edges(M) ? 0 : 1, D->tmax + 1);
       ++ctx->launches;
     }
   }

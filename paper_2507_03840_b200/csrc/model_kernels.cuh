@@ -47,6 +47,16 @@ struct Lay1 {
 };
 
 
+// Power-of-two scale of an fp16x3 split operand (so2_f16x3.cu) whose values
+// are bounded by `bound`: every |x| / s stays below 2^14 (fp16 max 65504).
+// rotate_in (the A1 image) and the chain evaluate it from the same bound.
+__device__ __forceinline__ float f16s_pow2_scale(float bound) {
+  if (!(bound > 0.f) || !(bound < 3.0e38f)) return 1.f;
+  int k;
+  frexpf(bound, &k);  // bound < 2^k
+  return ldexpf(1.f, k - 14);
+}
+
 // Rotation taking the unit edge direction onto +y: R = Rx(-beta) Ry(-alpha)
 // with alpha = atan2(ux, uz), beta = acos(uy) (align.cpp:32-39), written with
 // cos/sin of alpha and beta taken directly from the displacement (no trig

@@ -4,6 +4,8 @@
 // entry read from SMEM once per 4 FMAs); Wigner blocks are recomputed per
 // tile from the fp32 direction with the host-expanded recursion recipe.
 #pragma once
+#include <cuda_fp16.h>
+
 #include "model_kernels.cuh"
 
 namespace esg {
@@ -90,6 +92,54 @@ __device__ __forceinline__ void prefetch_y(const uint16_t* Y, int64_t el0, int n
 template <int HE>
 __device__ __forceinline__ void prefetch_y(const float*, int64_t, int, int, int) {}
 
+// |v| maxima of the feature tables (the fp16x3 chain's scale bounds): a
+// non-negative float orders like its bit pattern, so an unsigned atomicMax
+// on the bits is a float max (NaN bits sort above +inf and propagate)
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ void atomic_max_abs(float* p, float v) {
+  atomicMax(reinterpret_cast<unsigned int*>(p), __float_as_uint(fabsf(v)));
+}
+__device__ __forceinline__ float max4(float4 v) { return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))); }
+
+// max |x| over n floats (n % 4 == 0, 16-byte aligned) into *out
+template <int BLOCK = 256>
+__global__ void __launch_bounds__(BLOCK) k_abs_max(const float* __restrict__ x, int64_t n, float* __restrict__ out) {
+  float m = 0.f;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, max4(__ldg(x4 + i)));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomic_max_abs(out, m);
+}
+
+// The fp16x3 split image of A1 (so2_f16x3.cu): tiles of 128 edges, per
+// 32-wide K chunk a 16 KB K-major SWIZZLE_128B tile whose 128-byte rows hold
+// [hi(32) | lo(32)] fp16.  Byte offset of (edge el, K index k) in the hi
+// half; the lo value sits 4 units (64 bytes) later, before the swizzle.
+template <int KTOT>
+__device__ __forceinline__ int64_t f16s_hi_off(int64_t el, int k, bool lo) {
+  const int64_t tile = el >> 7;
+  const int r = (int)(el & 127), w = k & 31;
+  const int unit = (w >> 3) + (lo ? 4 : 0);
+  return (tile * (KTOT / 32) + (k >> 5)) * 16384 + r * 128 + ((unit ^ (r & 7)) << 4) + (w & 7) * 2;
+}
+__device__ __forceinline__ void st_f16s(uint8_t* base, int64_t off_hi, int64_t off_lo, float4 v, float inv_s) {
+  const float x[4] = {v.x * inv_s, v.y * inv_s, v.z * inv_s, v.w * inv_s};
+  __half hi[4], lo[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    hi[t] = __float2half_rn(x[t]);
+    lo[t] = __float2half_rn(x[t] - __half2float(hi[t]));
+  }
+  auto pk = [](__half a, __half b) { return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16); };
+  *reinterpret_cast<uint2*>(base + off_hi) = make_uint2(pk(hi[0], hi[1]), pk(hi[2], hi[3]));
+  *reinterpret_cast<uint2*>(base + off_lo) = make_uint2(pk(lo[0], lo[1]), pk(lo[2], lo[3]));
+}
+
 __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
   return make_float4(fmaf(d, x.x, a.x), fmaf(d, x.y, a.y), fmaf(d, x.z, a.z), fmaf(d, x.w, a.w));
 }
@@ -105,7 +155,9 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
                                                              const int* __restrict__ src_row,
                                                              const int* __restrict__ dst_row,
                                                              const float* __restrict__ dir, int64_t e0, int64_t n_e,
-                                                             OutT* __restrict__ A1, int pf, int el0) {
+                                                             OutT* __restrict__ A1, int pf, int el0,
+                                                             const float* __restrict__ tmax = nullptr,
+                                                             int edge_slot = 0) {
   using G = Geo<L>;
   using Y = Lay1<L, E, KPAD>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, C3 = 3 * E, Q = E / 4, TPE = 3 * Q;
@@ -136,7 +188,10 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
     // A1 element (el, k) with k = K0 + pq, K0 a compile-time multiple of 16
     // and pq = p * E + 4 q < 48 fixed per thread (a1_index, split once)
     const int pq = p * E + q * 4;
-    OutT* a1_row = A1 + a1_index<Y::KTOT, KPAD>(el, 0);
+    // KPAD == 32: the fp16x3 split image, values scaled by the message bound
+    float inv_s = 1.f;
+    if constexpr (KPAD == 32) inv_s = 1.f / f16s_pow2_scale(3.f * fmaxf(tmax[0], tmax[edge_slot]));
+    OutT* a1_row = KPAD == 32 ? A1 : A1 + a1_index<Y::KTOT, KPAD>(el, 0);
     // el0 & 1: the edge table holds only its l = 0 plane (layer 0 of a
     // forward; k_init_edges leaves the other planes unwritten); el0 & 2: so do
     // the node rows (before layer 0's node update).  Those planes read as zero.
@@ -155,7 +210,11 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
         for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (a + l) * dd + (b + l)], x[b + l], acc);
         const int m = a < 0 ? -a : a;
         const int k = Y::kofs(m) + (G::mrow(l, a) - G::moff(m)) * C3 + pq;
-        st4(a1_row + a1_offset<KPAD>(el, k), acc);
+        if constexpr (KPAD == 32)
+          st_f16s(reinterpret_cast<uint8_t*>(A1), f16s_hi_off<Y::KTOT>(el, k, false),
+                  f16s_hi_off<Y::KTOT>(el, k, true), acc, inv_s);
+        else
+          st4(a1_row + a1_offset<KPAD>(el, k), acc);
       }
     }
   }
@@ -168,7 +227,8 @@ __global__ void __launch_bounds__(32 * 3 * E / 4 < 128 ? 128 : 32 * 3 * E / 4, 3
 template <int L, int E, typename YT>
 __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rotate_out_edge(const YT* __restrict__ Yin,
                                                                const float* __restrict__ dir, int64_t e0, int64_t n_e,
-                                                               float* __restrict__ edges, int pf, int el0) {
+                                                               float* __restrict__ edges, int pf, int el0,
+                                                               float* __restrict__ emax = nullptr) {
   using G = Geo<L>;
   constexpr int TE = 32, DSP = G::DS + 2, H = G::H, Q = E / 4;
   __shared__ float sD[TE * DSP];
@@ -183,6 +243,7 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
   for (int i = threadIdx.x; i < ne * 3; i += blockDim.x) sdir[i] = dir[t0 * 3 + i];
   __syncthreads();
   wigner_tile_gen<L, DSP>(sdir, ne, sD);
+  float vmax = 0.f;
   if (e < ne) {
     const int64_t el = t0 + e - e0;
     const float* D = sD + e * DSP;
@@ -203,8 +264,13 @@ __global__ void __launch_bounds__(32 * E / 4 < 128 ? 128 : 32 * E / 4, 4) k_rota
 #pragma unroll
         for (int b = -l; b <= l; ++b) acc = fma4(D[G::doff(l) + (b + l) * dd + (a + l)], y[b + l], acc);
         row[(l * l + l + a) * Q] = acc;
+        vmax = fmaxf(vmax, max4(acc));
       }
     }
+  }
+  if (emax) {  // max |new edge row| (the next layer's fp16x3 scale bound)
+    vmax = warp_max(vmax);
+    if ((threadIdx.x & 31) == 0) atomic_max_abs(emax, vmax);
   }
 }
 
