@@ -737,8 +737,7 @@ void model_prepare(esg_model* M, const esg_graph* g, const esg_plan* plan, const
   D->A1 = (void*)grow((uint8_t*)D->A1, D->cap_a1, std::max(std::max(a1_fp32, a1_bf16), a1_f16s));
   if (D->A1 != a1_prev) D->a1_zero_mode = 0;  // zeroed before the first tensor-core use (run_block)
   // fp32 rows (CUDA-core path) or bf16 tiles of 128 edges (tcgen05 epilogue)
-  D->Y = (float*)grow((uint8_t*)D->Y, D->cap_y,
-                      std::max((size_t)D->chunk_cap * row * 4, (size_t)((D->chunk_cap + 127) / 128) * 128 * row * 2));
+  D->Y = (float*)grow((uint8_t*)D->Y, D->cap_y, (size_t)((D->chunk_cap + 127) / 128) * 128 * row * 4);
   D->logits = grow(D->logits, D->cap_logits, (size_t)D->chunk_cap);
   if (D->cap_node_out < (size_t)std::max(n_owned, 1) * M->heads.out_len ||
       D->cap_edge_out < (size_t)std::max<int64_t>(ne, 1) * M->heads.out_len)
@@ -933,9 +932,12 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
         if (tc)
           k_rotate_out_edge<L, E, uint16_t><<<ro_grid, ro_threads, 0, st>>>((const uint16_t*)D->Y, D->dir, e0, n,
                                                                             D->edges, D->prefetch, el0);
+        else if (f3)  // the chain's tiled fp32 Y
+          k_rotate_out_edge<L, E, F32T><<<ro_grid, ro_threads, 0, st>>>((const F32T*)D->Y, D->dir, e0, n, D->edges,
+                                                                      D->prefetch, el0, D->tmax + 2 + layer);
         else
           k_rotate_out_edge<L, E, float><<<ro_grid, ro_threads, 0, st>>>(D->Y, D->dir, e0, n, D->edges, D->prefetch,
-                                                                       el0, f3 ? D->tmax + 2 + layer : nullptr);
+                                                                       el0);
         ++ctx->launches;
       }
       if (!node_block && D->host_edge_out && layer == M->cfg.layers - 1) {
@@ -959,13 +961,13 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
                                       dyn));
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, uint16_t, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bf16));
-        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, F32T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       dyn));
         attr = true;
       }
       if (f3)  // logits from the chain's fp32 accumulator
-        k_node_update<L, E, float, true><<<ch.second - ch.first, 128, dyn, st>>>(
-            D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->prefetch);
+        k_node_update<L, E, F32T, true><<<ch.second - ch.first, 128, dyn, st>>>(
+            (const F32T*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->prefetch);
       else if (tc)
         k_node_update<L, E, uint16_t, true><<<ch.second - ch.first, 128, dyn_bf16, st>>>(
             (const uint16_t*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->prefetch);

@@ -6,6 +6,8 @@
 #pragma once
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "model_kernels.cuh"
 
 namespace esg {
@@ -49,6 +51,17 @@ __device__ __forceinline__ int64_t y_index(const uint16_t*, int64_t el, int c) {
   return (((el >> 7) * (HE / 8) + (c >> 3)) << 10) + ((el & 127) << 3) + (c & 7);
 }
 
+// fp32 Y in tiles of 128 edges, [tile][c / 4][el % 128][c % 4] (the fp16x3
+// chain's drain: every 16-byte store of a warp lands next to its neighbour
+// lane's, 512 contiguous bytes per instruction)
+struct F32T {
+  float x;
+};
+template <int HE>
+__device__ __forceinline__ int64_t y_index(const F32T*, int64_t el, int c) {
+  return (((el >> 7) * (HE / 4) + (c >> 2)) << 9) + ((el & 127) << 2) + (c & 3);
+}
+
 // a1_index(el, k) - a1_index(el, 0): the within-tile-row offset of K index k
 template <int KPAD>
 __device__ __forceinline__ int a1_offset(int64_t el, int k) {
@@ -59,6 +72,7 @@ __device__ __forceinline__ int a1_offset(int64_t el, int k) {
 
 // 4 consecutive Y values as float4 from fp32 or bf16 storage
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4(const F32T* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ float4 ld4(const uint16_t* p) {
   const uint2 w = __ldg(reinterpret_cast<const uint2*>(p));
   return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
@@ -91,6 +105,8 @@ __device__ __forceinline__ void prefetch_y(const uint16_t* Y, int64_t el0, int n
 }
 template <int HE>
 __device__ __forceinline__ void prefetch_y(const float*, int64_t, int, int, int) {}
+template <int HE>
+__device__ __forceinline__ void prefetch_y(const F32T*, int64_t, int, int, int) {}
 
 // |v| maxima of the feature tables (the fp16x3 chain's scale bounds): a
 // non-negative float orders like its bit pattern, so an unsigned atomicMax
@@ -127,17 +143,28 @@ __device__ __forceinline__ int64_t f16s_hi_off(int64_t el, int k, bool lo) {
   const int unit = (w >> 3) + (lo ? 4 : 0);
   return (tile * (KTOT / 32) + (k >> 5)) * 16384 + r * 128 + ((unit ^ (r & 7)) << 4) + (w & 7) * 2;
 }
+// The fp16x3 split of two fp32 values (|x| < 2^14): hi = x truncated to its
+// leading 11 significant bits (mask the low 13 mantissa bits), an fp16
+// number that packs exactly; lo = x - hi is exact in fp32 (< 2^-10 |x|) and
+// rounds to fp16 (11 of its <= 13 bits: error <= 2^-22 |x|).  Two packed
+// conversions (cvt.rn.f16x2.f32) per pair, no scalar ones.
+__device__ __forceinline__ uint32_t pack_f16x2(float lo_half, float hi_half) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi_half), "f"(lo_half));
+  return r;
+}
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const float h0 = __uint_as_float(__float_as_uint(x0) & 0xffffe000u);
+  const float h1 = __uint_as_float(__float_as_uint(x1) & 0xffffe000u);
+  hi = pack_f16x2(h0, h1);
+  lo = pack_f16x2(__fsub_rn(x0, h0), __fsub_rn(x1, h1));
+}
 __device__ __forceinline__ void st_f16s(uint8_t* base, int64_t off_hi, int64_t off_lo, float4 v, float inv_s) {
-  const float x[4] = {v.x * inv_s, v.y * inv_s, v.z * inv_s, v.w * inv_s};
-  __half hi[4], lo[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    hi[t] = __float2half_rn(x[t]);
-    lo[t] = __float2half_rn(x[t] - __half2float(hi[t]));
-  }
-  auto pk = [](__half a, __half b) { return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16); };
-  *reinterpret_cast<uint2*>(base + off_hi) = make_uint2(pk(hi[0], hi[1]), pk(hi[2], hi[3]));
-  *reinterpret_cast<uint2*>(base + off_lo) = make_uint2(pk(lo[0], lo[1]), pk(lo[2], lo[3]));
+  uint32_t h0, l0, h1, l1;
+  split_f16x2(v.x * inv_s, v.y * inv_s, h0, l0);
+  split_f16x2(v.z * inv_s, v.w * inv_s, h1, l1);
+  *reinterpret_cast<uint2*>(base + off_hi) = make_uint2(h0, h1);
+  *reinterpret_cast<uint2*>(base + off_lo) = make_uint2(l0, l1);
 }
 
 __device__ __forceinline__ float4 fma4(float d, float4 x, float4 a) {
@@ -295,9 +322,9 @@ struct NodeSplit {
 
 // Y of one edge: from global memory (fp32 rows) or from the SMEM copy of the
 // edge tile (bf16, [col / 8][edge in tile][col % 8], like the global tiles)
-template <int HE>
+template <int HE, typename YT = float>
 struct YGlobal {
-  const float* Y;
+  const YT* Y;
   int64_t el;
   __device__ __forceinline__ float4 operator()(int c) const { return ld4(Y + y_index<HE>(Y, el, c)); }
 };
@@ -461,7 +488,8 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
             default: node_part<L, E, 3>(ys, q, D, al, acc); break;
           }
         } else {
-          const YGlobal<HE> ys{reinterpret_cast<const float*>(Yin), k0 + i - e0};
+          using YG = typename std::conditional<sizeof(YT) == 2, float, YT>::type;
+          const YGlobal<HE, YG> ys{reinterpret_cast<const YG*>(Yin), k0 + i - e0};
           switch (part) {
             case 0: node_part<L, E, 0>(ys, q, D, al, acc); break;
             case 1: node_part<L, E, 1>(ys, q, D, al, acc); break;

@@ -30,26 +30,29 @@
 //   gate   s = sigmoid(h_0[:, l = 0 channels]) (order 0 first),
 //          G_m = H_m * s[c % 2E] / s2_m, split -> A2 ring (32-column chunks)
 //   lin2   Y_m = A2_m . W2_m^T        chunk-pipelined behind the gate
-//   drain  Y_m -> fp32 order-major rows in HBM (+ attention logits)
+//   drain  Y_m -> fp32 order-major values in HBM, tiles of 128 edges
+//          [c / 4][edge][c % 4] (+ attention logits)
 //
 // Operand images (HBM and SMEM alike): per 32-wide K chunk a K-major
 // SWIZZLE_128B tile whose 128-byte rows hold [hi(32) | lo(32)] fp16, so the
 // hi and lo operands of a K = 16 step are the same descriptor advanced by 0
 // or 64 bytes.  One bulk copy (TMA, 1-D) per chunk, no tensor maps.
 //
-// Warp roles (608 threads, 1 CTA per SM, persistent over tiles):
-//   warp 0      A producer (A1 chunks, 4-stage ring)
-//   warp 18     B producer (weight chunks, 3-stage ring)
-//   warp 1      MMA issuer (one elected lane)
+// Warp roles (544 threads, 1 CTA per SM, persistent over tiles):
+//   warps 0/14  A1 / W1 producers (one lockstep 3-stage ring, L2 prefetch of A1)
+//   warp 15     W2 producer (2-stage ring)
+//   warps 1/16  lin1 / lin2 MMA issuers (one elected lane each): two
+//               independent instruction streams into the tensor pipe
 //   warps 2-9   gate: warp w owns TMEM lanes 32 (w % 4)+, the two halves take
 //               alternate 32-column chunks
-//   warps 10-17 drain
+//   warps 10-13 drain (one per TMEM lane quarter)
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "device_model.h"
+#include "msg_kernels.cuh"
 #include "esg_internal.h"
 #include "model_kernels.cuh"
 #include "tc_common.cuh"
@@ -60,14 +63,19 @@ namespace {
 using namespace tc;
 
 constexpr int TILE_M = 128;
-constexpr int THREADS = 608;
-constexpr int NSA = 4;                 // A1 ring
-constexpr int NSB = 3;                 // weight ring
-constexpr int NS2 = 4;                 // gated-operand ring (>= the Y chunks of any order)
+constexpr int THREADS = 544;  // 17 warps
+constexpr int GATE_PARTS = 2;  // gate warps per TMEM lane quarter (part p takes chunks q = p mod GATE_PARTS)
+constexpr int NSA = 3;                 // A1 + lin1 weight ring (lockstep, one barrier pair per stage)
+constexpr int PFA = 8;                 // L2 prefetch distance of the A1 stream (chunks)
+constexpr int NL1 = 4;                 // lin1 may run NL1 - 1 units ahead of lin2's issue
+constexpr int NB1 = NSA;
+constexpr int NB2 = 2;                 // lin2 weight ring
+constexpr int NS2 = 3;                 // gated-operand ring
 constexpr int CHUNK = TILE_M * 128;    // one 32-wide K chunk of 128 rows, hi | lo: 16 KB
-constexpr int B_STAGE = 256 * 128;     // up to 256 weight rows: 32 KB
-constexpr int GATE_THREADS = 256, DRAIN_THREADS = 256;
-constexpr int SMEM_BYTES = 1024 + NSA * CHUNK + NSB * B_STAGE + NS2 * CHUNK + 512;
+constexpr int B1_STAGE = 256 * 128;    // up to 256 lin1 weight rows: 32 KB
+constexpr int B2_STAGE = 128 * 128;    // up to 128 lin2 weight rows: 16 KB
+constexpr int GATE_THREADS = 128 * GATE_PARTS, DRAIN_THREADS = 128;
+constexpr int SMEM_BYTES = 1024 + NSA * CHUNK + NB1 * B1_STAGE + NB2 * B2_STAGE + NS2 * CHUNK + 512;
 
 template <int L, int E>
 struct S3 {
@@ -113,27 +121,37 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
 }
 // one 32-wide K chunk: two K = 16 steps x (hi.hi, hi.lo, lo.hi); the lo half
 // of a 128-byte row starts 64 bytes in (descriptor start + 4)
-__device__ __forceinline__ void mma_chunk(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, bool first) {
+__device__ __forceinline__ void mma_chunk(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, bool first,
+                                          int nmma = 3) {
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
     mma_f16(tmem_d, da + 2 * ks, db + 2 * ks, idesc, (first && ks == 0) ? 0u : 1u);
-    mma_f16(tmem_d, da + 2 * ks, db + 4 + 2 * ks, idesc, 1u);
-    mma_f16(tmem_d, da + 4 + 2 * ks, db + 2 * ks, idesc, 1u);
+    if (nmma == 3) {
+      mma_f16(tmem_d, da + 2 * ks, db + 4 + 2 * ks, idesc, 1u);
+      mma_f16(tmem_d, da + 4 + 2 * ks, db + 2 * ks, idesc, 1u);
+    }
   }
 }
 
-// TMEM column plan (l_max 4, e_width 16; N1 = 160 256 192 128 64, N2 = N1/2):
-// lin1 of order m accumulates into R_m = [R0[m], R0[m] + N1); lin2 then
-// accumulates Y_m into its head [R0[m], R0[m] + N2), chunk by chunk behind the
-// gate, once the gate has read those leading columns.  Consecutive orders'
-// regions are disjoint (lin1 of order m + 1 runs while order m is gated).
-// lin1 of unit u waits until units < u - LAG[m] are drained: the most recent
-// earlier unit whose Y overlaps R_m (Y2 for m0, Y3 for m1, Y0 for m2, Y1 for
-// m3, the previous tile's Y4 for m4); gate reads of earlier units are ordered
-// by the MMA issue order (lin2 of u - 2 issues its last chunk only after the
-// gate wrote it).
-__device__ __forceinline__ int r0_col(int m) { return m == 1 || m == 3 ? 0 : (m == 4 ? 448 : 256); }
-__device__ __forceinline__ int lag(int m) { return m <= 1 ? 2 : (m <= 3 ? 1 : 4); }
+// TMEM column plan (l_max 4, e_width 16; N1 = 160 256 192 128 64, N2 = N1/2).
+// Units run in the order m = 0, 1, 4, 3, 2 within a tile (order 0 first: it
+// carries the gate scalars).  lin1 of order m accumulates into
+// R_m = [R0[m], R0[m] + N1):  R0 = [0,160)  R1 = [256,512)  R4 = [96,160)
+// R3 = [384,512)  R2 = [160,352); lin2 accumulates Y_m into its head
+// [R0[m], R0[m] + N2), chunk by chunk behind the gate, once the gate has read
+// those columns.  Consecutive units' regions are disjoint (lin1 of the next
+// unit runs while this one is gated), and no Y overlaps the region of the
+// unit two later (found by exhaustive search over 32-column placements and
+// unit orders), so lin1 of unit u waits only for
+//   the gate of unit u - GL[m] to have read its lin1 columns, and
+//   the drain of unit u - DL[m] (the first earlier unit whose Y it overlaps):
+// GL = 3 2 3 2 2, DL = 3 3 3 5 5 for m = 0..4 -- the drain round trip of a
+// unit has two whole lin1 units to hide behind.
+__device__ __constant__ int kSeq[5] = {0, 1, 4, 3, 2};
+__device__ __forceinline__ int order_of(int u) { return kSeq[u % 5]; }
+__device__ __forceinline__ int r0_col(int m) { return m == 0 ? 0 : (m == 1 ? 256 : (m == 2 ? 160 : (m == 3 ? 384 : 96))); }
+__device__ __forceinline__ int gate_lag(int m) { return (m == 0 || m == 2) ? 3 : 2; }
+__device__ __forceinline__ int drain_lag(int m) { return m >= 3 ? 5 : 3; }
 
 __device__ __forceinline__ uint32_t ld_acquire(uint32_t addr) {
   uint32_t v;
@@ -143,8 +161,64 @@ __device__ __forceinline__ uint32_t ld_acquire(uint32_t addr) {
 __device__ __forceinline__ void st_release(uint32_t addr, uint32_t v) {
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint32_t h2(__half a, __half b) {
   return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+}
+
+// F16X3_PROBE (tools/f16x3_probe.cu only): per-role clock64 accounting of
+// every wait and of the MMA issuer's idle time by cause, plus experiment
+// switches (g_probe_mode: 1 gate skips its arithmetic, 2 drain skips its
+// stores, 4 one MMA per K step instead of three); compiled out of the library.
+#ifdef F16X3_PROBE
+__device__ long long g_probe[1024 * 32];
+__device__ int g_probe_mode;
+#define PROBE_ON 1
+#else
+#define PROBE_ON 0
+#endif
+struct Probe {
+#if PROBE_ON
+  long long v[24] = {};
+  __device__ void add(int i, long long d) { v[i] += d; }
+  __device__ void flush(bool cond) {
+    if (cond)
+      for (int i = 0; i < 24; ++i)
+        if (v[i]) atomicAdd((unsigned long long*)&g_probe[blockIdx.x * 32 + i], (unsigned long long)v[i]);
+  }
+#else
+  __device__ void add(int, long long) {}
+  __device__ void flush(bool) {}
+#endif
+};
+__device__ __forceinline__ long long pclock() {
+#if PROBE_ON
+  return clock64();
+#else
+  return 0;
+#endif
+}
+__device__ __forceinline__ int probe_mode() {
+#if PROBE_ON
+  return g_probe_mode;
+#else
+  return 0;
+#endif
 }
 
 template <int L, int E>
@@ -159,37 +233,42 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sA = smem_u32(base);
-  const uint32_t sB = sA + NSA * CHUNK;
-  const uint32_t sA2 = sB + NSB * B_STAGE;
-  uint64_t* bars = (uint64_t*)(base + NSA * CHUNK + NSB * B_STAGE + NS2 * CHUNK);
+  const uint32_t sB1 = sA + NSA * CHUNK;
+  const uint32_t sB2 = sB1 + NB1 * B1_STAGE;
+  const uint32_t sA2 = sB2 + NB2 * B2_STAGE;
+  uint64_t* bars = (uint64_t*)(base + NSA * CHUNK + NB1 * B1_STAGE + NB2 * B2_STAGE + NS2 * CHUNK);
   auto bar = [&](int i) { return smem_u32(&bars[i]); };
-  const int FA = 0, EA = NSA, FB = 2 * NSA, EB = FB + NSB;
-  const int F2 = EB + NSB, E2 = F2 + NS2;  // gated-operand ring
-  const int L1F = E2 + NS2;                // + (u & 1): lin1 of unit u complete
-  const int L2F = L1F + 2;                 // + (u & 1): lin2 of unit u complete
-  const int H1 = L2F + 2;                  // + (u & 1): the gate read the Y head of unit u
-  uint32_t* drained = (uint32_t*)(bars + H1 + 2);
-  uint32_t* tmem_slot = drained + 1;
+  const int FAB = 0, EAB = NSA, FB2 = 2 * NSA, EB2 = FB2 + NB2;
+  const int F2 = EB2 + NB2, E2 = F2 + NS2;  // gated-operand ring
+  const int L1F = E2 + NS2;                 // + (u % NL1): lin1 of unit u complete
+  const int L2F = L1F + NL1;                // + (u % NL1): lin2 of unit u complete
+  const int H1 = L2F + NL1;                 // + (u % NL1): the gate read the Y head of unit u
+  const int GD = H1 + NL1;                  // + (u % NL1): the gate read all of unit u's columns
+  uint32_t* drained = (uint32_t*)(bars + GD + NL1);  // units drained so far
+  uint32_t* l2_issued = drained + 1;               // units whose lin2 is fully issued
+  uint32_t* tmem_slot = drained + 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NSA; ++s) {
-      mbar_init(bar(FA + s), 1);
-      mbar_init(bar(EA + s), 1);
+      mbar_init(bar(FAB + s), 2);  // the A1 and the W1 producer each arrive with their bytes
+      mbar_init(bar(EAB + s), 1);
     }
-    for (int s = 0; s < NSB; ++s) {
-      mbar_init(bar(FB + s), 1);
-      mbar_init(bar(EB + s), 1);
+    for (int s = 0; s < NB2; ++s) {
+      mbar_init(bar(FB2 + s), 1);
+      mbar_init(bar(EB2 + s), 1);
     }
     for (int s = 0; s < NS2; ++s) {
-      mbar_init(bar(F2 + s), GATE_THREADS / 2);  // one half of the gate writes a chunk
+      mbar_init(bar(F2 + s), 128);  // one part of the gate (4 warps, 128 rows) writes a chunk
       mbar_init(bar(E2 + s), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NL1; ++b) {
       mbar_init(bar(L1F + b), 1);
       mbar_init(bar(L2F + b), 1);
       mbar_init(bar(H1 + b), GATE_THREADS);
+      mbar_init(bar(GD + b), GATE_THREADS);
     }
     *drained = 0;
+    *l2_issued = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -201,111 +280,173 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t n_tiles = (n_e + TILE_M - 1) / TILE_M;
+  const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int total = (int)(my_tiles * (L + 1));  // units (tile, order) of this CTA
+  auto spin_until = [&](const uint32_t* ctr, int need) {
+    const uint32_t a = smem_u32(ctr);
+    if (need > 0)
+      while ((int)ld_acquire(a) < need) {
+      }
+  };
 
-  if (warp == 0) {
-    // ---------------------------------------------------------- A producer
+  if (warp == 0 || warp == 14) {
+    // ------------------------------------- A1 / W1 producers (lockstep ring)
+    // A1 chunks in lin1 order, the chunk PFA steps ahead prefetched into L2
+    // (the ring's bulk copies then see L2 latency); W1 chunks in the same
+    // order.  Both arrive on the stage's one full barrier with their bytes.
     if (lane == 0) {
+      const bool is_a = warp == 0;  // else the W1 producer (warp 14)
       int st = 0;
       uint32_t ph = 0;
-      const uint64_t pol = policy_evict_first();
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const uint8_t* a_tile = A1 + (size_t)tile * S::KCH * CHUNK;
-        for (int c = 0; c < S::KCH; ++c) {
-          mbar_wait(bar(EA + st), ph ^ 1);
-          mbar_expect_tx(bar(FA + st), CHUNK);
-          bulk_g2s(sA + st * CHUNK, a_tile + (size_t)c * CHUNK, CHUNK, bar(FA + st), pol);
-          if (++st == NSA) { st = 0; ph ^= 1; }
+      const uint64_t pol = is_a ? policy_evict_first() : policy_evict_last();
+      Probe pr;
+      const long long t_all = pclock();
+      const int64_t total_a = my_tiles * S::KCH;
+      // A1 chunk i of this CTA's stream, in unit order (the image keeps order m
+      // at K offset kofs(m))
+      auto a_chunk = [&](int64_t i) {
+        const int64_t tile = blockIdx.x + (i / S::KCH) * gridDim.x;
+        int r = (int)(i % S::KCH), k = 0;
+        while (r >= S::K1P(order_of(k)) / 32) r -= S::K1P(order_of(k++)) / 32;
+        return A1 + ((size_t)tile * S::KCH + (size_t)(S::kofs(order_of(k)) / 32 + r)) * CHUNK;
+      };
+      if (is_a)
+        for (int64_t i = 0; i < PFA && i < total_a; ++i) prefetch_l2(a_chunk(i), CHUNK);
+      int64_t i = 0;
+      for (int64_t t = 0; t < my_tiles; ++t)
+        for (int k = 0; k <= L; ++k) {
+          const int m = order_of(k);
+          const uint32_t wbytes = (uint32_t)S::N1(m) * 128u;
+          for (int c = 0; c < S::K1P(m) / 32; ++c, ++i) {
+            if (is_a && i + PFA < total_a) prefetch_l2(a_chunk(i + PFA), CHUNK);
+            const long long t0 = pclock();
+            mbar_wait(bar(EAB + st), ph ^ 1);
+            pr.add(is_a ? 15 : 18, pclock() - t0);
+            const bool skip = (probe_mode() & (is_a ? 8 : 32)) != 0;  // probe: no traffic
+            if (skip) {
+              mbar_arrive(bar(FAB + st));
+            } else if (is_a) {
+              mbar_expect_tx(bar(FAB + st), CHUNK);
+              bulk_g2s(sA + st * CHUNK, a_chunk(i), CHUNK, bar(FAB + st), pol);
+            } else {
+              mbar_expect_tx(bar(FAB + st), wbytes);
+              bulk_g2s(sB1 + st * B1_STAGE, W1 + S::w1_off(m) + (size_t)c * wbytes, wbytes, bar(FAB + st), pol);
+            }
+            if (++st == NSA) { st = 0; ph ^= 1; }
+          }
         }
-      }
+      pr.add(is_a ? 16 : 19, pclock() - t_all);
+      pr.flush(true);
     }
-  } else if (warp == 18) {
-    // ---------------------------------------------------------- B producer
-    // weights in MMA issue order: lin1 of unit u, then lin2 of unit u - 1
+  } else if (warp == 15) {
+    // ---------------------------------------------------------- W2 producer
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
       const uint64_t pol = policy_evict_last();
-      auto load = [&](const uint8_t* src, uint32_t bytes) {
-        mbar_wait(bar(EB + st), ph ^ 1);
-        mbar_expect_tx(bar(FB + st), bytes);
-        bulk_g2s(sB + st * B_STAGE, src, bytes, bar(FB + st), pol);
-        if (++st == NSB) { st = 0; ph ^= 1; }
-      };
-      auto load_w2 = [&](int m) {
-        const uint8_t* w2 = W2 + S::w2_off(m);
-        for (int j = 0; j < S::N1(m) / 32; ++j) load(w2 + (size_t)j * S::N2(m) * 128, S::N2(m) * 128);
-      };
-      int prev = -1;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
-        for (int m = 0; m <= L; ++m) {
-          const uint8_t* w1 = W1 + S::w1_off(m);
-          for (int c = 0; c < S::K1P(m) / 32; ++c) load(w1 + (size_t)c * S::N1(m) * 128, S::N1(m) * 128);
-          if (prev >= 0) load_w2(prev);
-          prev = m;
+      for (int64_t t = 0; t < my_tiles; ++t)
+        for (int k = 0; k <= L; ++k) {
+          const int m = order_of(k);
+          const uint32_t bytes = (uint32_t)S::N2(m) * 128u;
+          for (int c = 0; c < S::N1(m) / 32; ++c) {
+            mbar_wait(bar(EB2 + st), ph ^ 1);
+            if (probe_mode() & 32) {
+              mbar_arrive(bar(FB2 + st));
+            } else {
+              mbar_expect_tx(bar(FB2 + st), bytes);
+              bulk_g2s(sB2 + st * B2_STAGE, W2 + S::w2_off(m) + (size_t)c * bytes, bytes, bar(FB2 + st), pol);
+            }
+            if (++st == NB2) { st = 0; ph ^= 1; }
+          }
         }
-      if (prev >= 0) load_w2(prev);
     }
   } else if (warp == 1) {
-    // ---------------------------------------------------------- MMA issuer
-    int sa = 0, sb = 0;
-    uint32_t pa = 0, pb = 0;
-    uint32_t g2 = 0;  // gated-operand chunks consumed so far
-    const uint32_t drained_addr = smem_u32(drained);
-    auto wait_drained = [&](int need) {
-      if (need > 0)
-        while ((int)ld_acquire(drained_addr) < need) {
-        }
-    };
-    auto lin2 = [&](int m, int u) {
-      wait_drained(u - 1);  // Y of unit u - 2 drained: L2F[u & 1] cannot run ahead
-      mbar_wait(bar(H1 + (u & 1)), (u >> 1) & 1);  // the gate read the columns Y_m overwrites
-      tc_fence_after();
-      const uint32_t id2 = idesc_f16(S::N2(m));
-      const uint32_t t_y = tmem + r0_col(m);
-      for (int j = 0; j < S::N1(m) / 32; ++j, ++g2) {
-        const int s2 = (int)(g2 % NS2);
-        mbar_wait(bar(F2 + s2), (g2 / NS2) & 1);
-        mbar_wait(bar(FB + sb), pb);
+    // ------------------------------------------------------- lin1 issuer
+    // MMA issue is close to synchronous (a shallow queue): the handshakes of
+    // one stream leave bubbles that a second, independent stream fills, so
+    // lin1 and lin2 have one issuing warp each (each commit tracks its own
+    // thread's MMAs).  Unit u's lin1 starts once lin2 of u - 2 is issued (the
+    // L1F phase it reuses has been consumed) and the TMEM plan's drain guard
+    // holds.  The whole warp runs the loop; one elected lane issues.
+    Probe pr;
+    const long long t_all = pclock();
+    const int nmma = (probe_mode() & 4) ? 1 : 3;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int u = 0; u < total; ++u) {
+      const int m = order_of(u);
+      long long t0 = pclock();
+      spin_until(l2_issued, u - (NL1 - 1));  // the L1F / H1 phases of unit u - NL1 are consumed
+      pr.add(4, pclock() - t0);
+      t0 = pclock();
+      const int gu = u - gate_lag(m);  // the gate of unit gu has read R_m's columns
+      if (gu >= 0) mbar_wait(bar(GD + gu % NL1), (gu / NL1) & 1);
+      spin_until(drained, u - drain_lag(m) + 1);  // Y of unit u - DL[m] drained
+      pr.add(1, pclock() - t0);
+      const uint32_t id1 = idesc_f16(S::N1(m)), t_r = tmem + r0_col(m);
+      const int nch = S::K1P(m) / 32;
+      for (int c = 0; c < nch; ++c) {
+        t0 = pclock();
+        mbar_wait(bar(FAB + st), ph);
+        pr.add(2, pclock() - t0);
         tc_fence_after();
         if (elect_one()) {
-          mma_chunk(t_y, sdesc(sA2 + s2 * CHUNK), sdesc(sB + sb * B_STAGE), id2, j == 0);
-          tc_commit(bar(E2 + s2));
-          tc_commit(bar(EB + sb));
+          mma_chunk(t_r, sdesc(sA + st * CHUNK), sdesc(sB1 + st * B1_STAGE), id1, c == 0, nmma);
+          tc_commit(bar(EAB + st));
+          if (c == nch - 1) tc_commit(bar(L1F + u % NL1));
         }
         __syncwarp();
-        if (++sb == NSB) { sb = 0; pb ^= 1; }
+        if (++st == NSA) { st = 0; ph ^= 1; }
       }
-      if (elect_one()) tc_commit(bar(L2F + (u & 1)));
-      __syncwarp();
-    };
-    int u = 0, prev_m = -1;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
-      for (int m = 0; m <= L; ++m, ++u) {
-        wait_drained(u - lag(m));
+    }
+    pr.add(9, pclock() - t_all);
+    pr.flush(lane == 0);
+  } else if (warp == 16) {
+    // ------------------------------------------------------- lin2 issuer
+    // lin2 of unit u: once Y of unit u - 2 is drained (the L2F phase it
+    // reuses) and the gate has read Y_m's columns (H1), one chunk per gated
+    // operand chunk as the gate delivers them.
+    Probe pr;
+    const long long t_all = pclock();
+    const int nmma = (probe_mode() & 4) ? 1 : 3;
+    int sb = 0;
+    uint32_t pb = 0, g2 = 0;
+    for (int u = 0; u < total; ++u) {
+      const int m = order_of(u);
+      long long t0 = pclock();
+      spin_until(drained, u - (NL1 - 1));  // the L2F phase of unit u - NL1 is consumed
+      pr.add(5, pclock() - t0);
+      t0 = pclock();
+      mbar_wait(bar(H1 + u % NL1), (u / NL1) & 1);
+      pr.add(6, pclock() - t0);
+      const uint32_t id2 = idesc_f16(S::N2(m)), t_y = tmem + r0_col(m);
+      const int nch = S::N1(m) / 32;
+      for (int j = 0; j < nch; ++j, ++g2) {
+        const int s2 = (int)(g2 % NS2);
+        t0 = pclock();
+        mbar_wait(bar(F2 + s2), (g2 / NS2) & 1);
+        pr.add(7, pclock() - t0);
+        t0 = pclock();
+        mbar_wait(bar(FB2 + sb), pb);
+        pr.add(8, pclock() - t0);
         tc_fence_after();
-        const uint32_t id1 = idesc_f16(S::N1(m)), t_r = tmem + r0_col(m);
-        for (int c = 0; c < S::K1P(m) / 32; ++c) {
-          mbar_wait(bar(FA + sa), pa);
-          mbar_wait(bar(FB + sb), pb);
-          tc_fence_after();
-          if (elect_one()) {
-            mma_chunk(t_r, sdesc(sA + sa * CHUNK), sdesc(sB + sb * B_STAGE), id1, c == 0);
-            tc_commit(bar(EA + sa));
-            tc_commit(bar(EB + sb));
-          }
-          __syncwarp();
-          if (++sa == NSA) { sa = 0; pa ^= 1; }
-          if (++sb == NSB) { sb = 0; pb ^= 1; }
+        if (elect_one()) {
+          mma_chunk(t_y, sdesc(sA2 + s2 * CHUNK), sdesc(sB2 + sb * B2_STAGE), id2, j == 0, nmma);
+          tc_commit(bar(E2 + s2));
+          tc_commit(bar(EB2 + sb));
+          if (j == nch - 1) tc_commit(bar(L2F + u % NL1));
         }
-        if (elect_one()) tc_commit(bar(L1F + (u & 1)));
         __syncwarp();
-        if (prev_m >= 0) lin2(prev_m, u - 1);
-        prev_m = m;
+        if (++sb == NB2) { sb = 0; pb ^= 1; }
       }
-    if (prev_m >= 0) lin2(prev_m, u - 1);
+      if (lane == 0) st_release(smem_u32(l2_issued), (uint32_t)(u + 1));
+      __syncwarp();
+    }
+    pr.add(17, pclock() - t_all);
+    pr.flush(lane == 0);
   } else if (warp >= 2 && warp <= 9) {
     // ---------------------------------------------------------------- gate
-    const int quad = warp & 3, half = (warp - 2) >> 2;
+    const int quad = warp & 3, half = (warp - 2) >> 2;  // the part: chunks q = half mod GATE_PARTS
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float bound_a = 3.f * fmaxf(tmax[0], tmax[edge_slot]);
@@ -313,14 +454,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     float sg[32];
     uint32_t gbase = 0;
     int u = 0;
+    Probe pr;
+    const long long t_all = pclock();
+    const bool skip_math = probe_mode() & 1;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
-      for (int m = 0; m <= L; ++m, ++u) {
+      for (int k = 0; k <= L; ++k, ++u) {
+        const int m = order_of(k);
         const uint32_t t_r = tmem + lane_off + r0_col(m);
         const int nch = S::N1(m) / 32, ych = S::ych(m);
         const float sc1 = sa_scale * sc.w1[m];  // lin1 accumulator -> fp32 units
         const float s2 = f16s_pow2_scale(sc.w1inf[m] * bound_a);
         const float inv_s2 = 1.f / s2;  // a power of two: exact
-        mbar_sleep(bar(L1F + (u & 1)), (u >> 1) & 1);
+        long long t0 = pclock();
+        mbar_wait(bar(L1F + u % NL1), (u / NL1) & 1);
+        pr.add(10, pclock() - t0);
         tc_fence_after();
         if (m == 0) {  // gate scalars from the l = 0 channels of order 0 (kernels.h:210-226)
           float v[32];
@@ -328,62 +475,81 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) sg[i] = gate ? 1.f / (1.f + expf(-v[i] * sc1)) : 1.f;
         }
+        // accumulator -> split operand: (v * sg) * scl with scl = sc1 / s2 a
+        // power of two, bit-identical to ((v * sc1) * sg) / s2
+        const float scl = sc1 * inv_s2;
         bool head_done = false;
-        for (int q = half; q < nch; q += 2) {
-          if (!head_done && q >= ych) {
-            tc_fence_before();
-            mbar_arrive(bar(H1 + (u & 1)));
-            head_done = true;
-          }
+        for (int q = half; q < nch; q += GATE_PARTS) {
           float v[32];
           tmem_ld32(t_r + q * 32, v);
+          if (!head_done && q + GATE_PARTS >= ych) {  // this thread's last read of Y_m's columns
+            tc_fence_before();
+            mbar_arrive(bar(H1 + u % NL1));
+            head_done = true;
+          }
           const uint32_t gq = gbase + (uint32_t)q, s2i = gq % NS2;
-          mbar_sleep(bar(E2 + s2i), ((gq / NS2) & 1) ^ 1);  // lin2 finished reading this stage
+          t0 = pclock();
+          // lin2 finished reading this stage.  With two parts and three stages
+          // the stage is at most one phase behind here (a part writes chunk g
+          // only after g - 3 is consumed, which needs g - 4, the other part's,
+          // written), so the parity test cannot alias.
+          static_assert(GATE_PARTS == 2 && NS2 == 3, "the parity argument above is for two parts, three stages");
+          mbar_wait(bar(E2 + s2i), ((gq / NS2) & 1) ^ 1);
+          pr.add(11, pclock() - t0);
           const uint32_t cb = sA2 + s2i * CHUNK;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            __half hi[8], lo[8];
+            if (probe_mode() & 16) continue;  // probe: no gated-operand stores
+            uint32_t hi[4], lo[4];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const float x = v[8 * j + t] * sc1 * sg[8 * j + t] * inv_s2;
-              hi[t] = __float2half_rn(x);
-              lo[t] = __float2half_rn(x - __half2float(hi[t]));
-            }
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, j)), "r"(h2(hi[0], hi[1])),
-                         "r"(h2(hi[2], hi[3])), "r"(h2(hi[4], hi[5])), "r"(h2(hi[6], hi[7]))
+            for (int t = 0; t < 4; ++t)
+              if (skip_math)
+                hi[t] = lo[t] = __float_as_uint(v[8 * j + 2 * t]);
+              else
+                split_f16x2((v[8 * j + 2 * t] * sg[8 * j + 2 * t]) * scl, (v[8 * j + 2 * t + 1] * sg[8 * j + 2 * t + 1]) * scl,
+                          hi[t], lo[t]);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, j)), "r"(hi[0]), "r"(hi[1]),
+                         "r"(hi[2]), "r"(hi[3])
                          : "memory");
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, 4 + j)), "r"(h2(lo[0], lo[1])),
-                         "r"(h2(lo[2], lo[3])), "r"(h2(lo[4], lo[5])), "r"(h2(lo[6], lo[7]))
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(cb + sw128(row, 4 + j)), "r"(lo[0]),
+                         "r"(lo[1]), "r"(lo[2]), "r"(lo[3])
                          : "memory");
           }
           fence_async_smem();
           mbar_arrive(bar(F2 + s2i));
         }
-        if (!head_done) {
-          tc_fence_before();
-          mbar_arrive(bar(H1 + (u & 1)));
-        }
+        tc_fence_before();
+        if (!head_done) mbar_arrive(bar(H1 + u % NL1));
+        mbar_arrive(bar(GD + u % NL1));  // every lin1 column of unit u read
         gbase += (uint32_t)nch;
       }
-  } else if (warp >= 10 && warp <= 17) {
+    pr.add(12, pclock() - t_all);
+    pr.flush(warp == 2 && lane == 0);
+  } else if (warp >= 10 && warp <= 13) {
     // --------------------------------------------------------------- drain
-    const int quad = warp & 3, half = (warp - 10) >> 2;
+    const int quad = warp & 3;  // one drain warp per TMEM lane quarter
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const float bound_a = 3.f * fmaxf(tmax[0], tmax[edge_slot]);
     int u = 0;
+    Probe pr;
+    const long long t_all = pclock();
+    const bool skip_st = probe_mode() & 2;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int64_t e0 = tile * TILE_M;
       const bool valid = e0 + row < n_e;
-      float* yrow = Y + (e0 + row) * (int64_t)(G::H * E);
-      for (int m = 0; m <= L; ++m, ++u) {
+      float* ytile = Y + tile * (int64_t)TILE_M * (G::H * E) + row * 4;  // [c / 4][row][4] (F32T)
+      for (int k = 0; k <= L; ++k, ++u) {
+        const int m = order_of(k);
         const int N2 = S::N2(m);
         const uint32_t t_y = tmem + lane_off + r0_col(m);
         const float sy = f16s_pow2_scale(sc.w1inf[m] * bound_a) * sc.w2[m];
-        mbar_sleep(bar(L2F + (u & 1)), (u >> 1) & 1);
+        const long long t0 = pclock();
+        mbar_sleep(bar(L2F + u % NL1), (u / NL1) & 1);
+        pr.add(13, pclock() - t0);
         tc_fence_after();
         const int c0 = G::moff(m) * E;
-        for (int q = half; q * 32 < N2; q += 2) {
+        for (int q = 0; q * 32 < N2; ++q) {
           float v[32];
           tmem_ld32(t_y + q * 32, v);
 #pragma unroll
@@ -396,12 +562,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int c = 0; c < E; ++c) lg = fmaf(__ldg(att + c), v[c], lg);
             logits[e0 + row] = lg;
           }
-          if (valid) {
+          if (valid && !skip_st) {
             const int nv = (N2 - q * 32) < 32 ? (N2 - q * 32) : 32;
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
               if (i < nv)
-                *reinterpret_cast<float4*>(yrow + c0 + q * 32 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                *reinterpret_cast<float4*>(ytile + (int64_t)((c0 + q * 32 + i) >> 2) * (TILE_M * 4)) =
+                    make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
           }
         }
         tc_fence_before();
@@ -409,6 +576,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (warp == 10 && lane == 0) st_release(smem_u32(drained), (uint32_t)(u + 1));
       }
     }
+    pr.add(14, pclock() - t_all);
+    pr.flush(warp == 10 && lane == 0);
   }
   tc_fence_before();
   __syncthreads();
