@@ -39,24 +39,38 @@ CONFIG_DESC = {
 # per-edge compulsory HBM bytes of each kernel category
 H, E = 25, 16
 ROW = H * E * 4  # 1600 B fp32 feature row
-A1_BYTES = 1280 * 2  # bf16 order-major operand, m-blocks padded to 64
 PROF_NAMES = ["init", "rotate_in", "so2_linears", "rotate_out_edge", "node_update", "heads", "halo", "copy"]
-Y_BF16 = H * E * 2  # lin2 output, bf16 in the tensor-core path
-BYTES_PER_EDGE = {
-    "rotate_in": ROW + 12 + 8 + A1_BYTES,        # edge row + dir + indices + A1 write
-    "so2_linears": A1_BYTES + Y_BF16,             # A1 read + Y write
-    "rotate_out_edge": Y_BF16 + 12 + 2 * ROW,     # Y read + dir + edge row RMW
-    "node_update": Y_BF16 + 12,                   # Y read + dir (+ node rows, amortised)
+# fp32 (the headline): rotate_in writes the fp16x3 split image of A1 (1216
+# K slots x hi|lo fp16 = 4,864 B per edge), the fp16x3 chain reads it and
+# writes fp32 Y (1,600 B) and the attention logit
+A1_F16S = 1216 * 4
+BYTES_PER_EDGE_FP32 = {
+    "rotate_in": ROW + 12 + 8 + A1_F16S,         # edge row + dir + indices + A1 write
+    "so2_linears": A1_F16S + ROW + 4,             # A1 read + Y write + logit
+    "rotate_out_edge": ROW + 12 + 2 * ROW,        # Y read + dir + edge row RMW
+    "node_update": ROW + 12 + 4,                  # Y read + dir + logit (+ node rows, amortised)
 }
+A1_BF16 = 1280 * 2  # bf16 order-major operand, m-blocks padded to 64
+Y_BF16 = H * E * 2
+BYTES_PER_EDGE_BF16 = {
+    "rotate_in": ROW + 12 + 8 + A1_BF16,
+    "so2_linears": A1_BF16 + Y_BF16,
+    "rotate_out_edge": Y_BF16 + 12 + 2 * ROW,
+    "node_update": Y_BF16 + 12,
+}
+# SO(2) linear FLOPs per edge-block (lin1 445,440 + lin2 148,480)
+SO2_FLOPS_PER_EDGE = 593920
+# fused-minimum bytes per edge-layer and per node-layer
+ALG_EDGE_LAYER, ALG_NODE_LAYER = 4832, 4800
 
 
-def measured_traffic(name):
+def measured_traffic(name, prec):
     """ncu dram__bytes_read.sum + dram__bytes_write.sum per edge of a kernel
-    category, from the committed capture summary (profiles/traffic.json), or
-    None when that kernel has not been captured."""
+    category in one precision mode, from the committed capture summary
+    (profiles/traffic.json), or None when that kernel has not been captured."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(name)
+            return json.load(f).get(prec, {}).get(name)
     except (OSError, ValueError):
         return None
 
@@ -129,13 +143,27 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def tensor_peak():
+    """Sustained dense fp16/bf16 TFLOP/s (kind::f16, the fp16x3 chain's MMA kind)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops_sustained"]), "measured (cuBLAS bf16, sustained)"
+    except Exception:
+        return 1400.0, "fallback (B200_PROFILING.md sustained)"
+
+
 # ------------------------------------------------------------------ CPU leg
-def cpu_sample(s, r, layers, basis, target_s=15.0, threads=None, g=None):
-    """Times the CPU restatement of the reference forward on a bounded
-    destination sample of the workload: all incoming edges of the first K
-    owned destinations, full 3-layer forward + heads.  Returns edges/s.
-    g: the graph arrays (the oracle builds them when None; the GPU arm passes
-    its bit-identical export to skip the CPU graph build)."""
+CPU_SAMPLE_DST = 512  # destinations in the CPU sample (both arms: the same workload slice)
+
+
+def cpu_sample(s, r, layers, basis, k=CPU_SAMPLE_DST, threads=None, g=None, reps=1):
+    """Times the CPU restatement of the reference forward on a fixed sample of
+    the workload: all incoming edges of the first k destinations, the full
+    M-layer forward + heads in float32 (the reference's --precision single
+    path).  Returns (edges/s, threads, sample text).  g: the graph arrays (the
+    oracle builds them when None; the GPU arm passes its bit-identical
+    export to skip the CPU graph build)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle as O
 
@@ -147,34 +175,33 @@ def cpu_sample(s, r, layers, basis, target_s=15.0, threads=None, g=None):
     om = O.Model(4, 16, layers, 32, r, 1, basis)
     deg = np.bincount(g["dst"], minlength=s.n_atoms)
     off = np.concatenate([[0], np.cumsum(deg)])
-
-    def sub_view(k):
-        e1 = int(off[k])
-        src = g["src"][:e1]
-        rows = np.unique(np.concatenate([np.arange(k), src]))
-        # owned rows first (0..k-1 are the destinations), then the other sources
-        order = np.concatenate([np.arange(k), np.setdiff1d(rows, np.arange(k))])
-        pos_of = np.full(s.n_atoms, -1, np.int64)
-        pos_of[order] = np.arange(len(order))
-        return dict(n_rows=len(order), n_owned=k, row_species=s.species[order], src_row=pos_of[src].astype(np.int32),
-                    dst_row=g["dst"][:e1].astype(np.int32), disp=g["disp"][:e1], dist=g["dist"][:e1]), e1
-
-    k = max(1, min(s.n_atoms, 64))
-    while True:
-        v, ne = sub_view(k)
+    k = min(k, s.n_atoms)
+    e1 = int(off[k])
+    src = g["src"][:e1]
+    rows = np.unique(np.concatenate([np.arange(k), src]))
+    # owned rows first (0..k-1 are the destinations), then the other sources
+    order = np.concatenate([np.arange(k), np.setdiff1d(rows, np.arange(k))])
+    pos_of = np.full(s.n_atoms, -1, np.int64)
+    pos_of[order] = np.arange(len(order))
+    v = dict(n_rows=len(order), n_owned=k, row_species=s.species[order], src_row=pos_of[src].astype(np.int32),
+             dst_row=g["dst"][:e1].astype(np.int32), disp=g["disp"][:e1], dist=g["dist"][:e1])
+    dts = []
+    for _ in range(reps):
         t0 = time.perf_counter()
         om.forward(v, np.float32)
-        dt = time.perf_counter() - t0
-        if dt > 2.0 or k >= s.n_atoms:
-            break
-        k = min(s.n_atoms, int(k * max(2.0, 2.5 / max(dt, 1e-3))))
-    if dt < target_s and k < s.n_atoms:
-        k = min(s.n_atoms, max(k, int(k * target_s / dt)))
-        v, ne = sub_view(k)
-        t0 = time.perf_counter()
-        om.forward(v, np.float32)
-        dt = time.perf_counter() - t0
-    return ne / dt, nthreads, f"all incoming edges of the first {k} destinations ({ne} edges), {layers}-layer forward + heads, float32"
+        dts.append(time.perf_counter() - t0)
+    dt = float(np.median(dts))
+    return e1 / dt, nthreads, (f"all incoming edges of the first {k} destinations ({e1} edges), {layers}-layer "
+                               f"forward + heads, float32, median of {reps}")
+
+
+def config_dict(name, atoms, edges, r, layers, world, prec):
+    return {"workload": CONFIG_DESC[name], "atoms": atoms, "edges": edges, "r_cut": r, "layers": layers, "l_max": 4,
+            "e_width": 16,
+            "linears": ("tcgen05 kind::f16 fp16x3 split (hi.hi + hi.lo + lo.hi, power-of-two scales), fp32 accumulate"
+                        if prec == "fp32" else "tcgen05 bf16, fp32 accumulate"),
+            "parallelism": f"graph-partition dp{world} (Low-NN, NCCL halo)",
+            "l2": "inputs larger than L2 (edge table %.0f GB)" % (edges * ROW / 1e9)}
 
 
 def run_reference(args):
@@ -197,17 +224,15 @@ def run_reference(args):
     r, layers, basis = spec[6], spec[7], spec[8]
     s = esg.AtomicStructure(pos, sp, cell, np.ones(3, bool))
     g = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
-    vals = []
-    info = None
-    for i in range(max(1, args.steps)):
-        v, cores, sample = cpu_sample(s, r, layers, basis, target_s=args.cpu_seconds / max(1, args.steps), g=g)
-        vals.append(v)
-        info = (cores, sample)
-    val = float(np.median(vals))
+    # one timed sample forward per step after the warm-up ones: the same
+    # destination sample as the GPU arm's cpu_baseline
+    cpu_sample(s, r, layers, basis, g=g, reps=max(1, args.warmup))
+    val, cores, sample = cpu_sample(s, r, layers, basis, g=g, reps=max(1, args.steps))
+    info = (cores, sample)
     line = {"metric": METRIC, "value": val, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": CONFIG_DESC[args.config], "atoms": s.n_atoms, "r_cut": r, "layers": layers},
+            "config": config_dict(args.config, s.n_atoms, len(g["src"]), r, layers, 1, "fp32"),
             "cpu_baseline": {"value": val, "unit": "edges/s", "cores": info[0], "kind": "port", "sample": info[1]},
             "e2e": {"value": val, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -305,25 +330,43 @@ def run_ours(args):
     value = total_edges / (ms_step / 1e3)
 
     # roofline of the dominant kernel category (this rank's live CUDA events)
+    prec_name = "fp32" if prec == esg.LINEAR_FP32 else "bf16"
+    bytes_tab = BYTES_PER_EDGE_FP32 if prec == esg.LINEAR_FP32 else BYTES_PER_EDGE_BF16
     dom = int(np.argmax(ms_cat[:6]))
     name = PROF_NAMES[dom]
     roof = None
     hbm, peak_kind = peaks()
-    if name in BYTES_PER_EDGE and ms_cat[dom] > 0:
+    tpk, tpk_kind = tensor_peak()
+    if name in bytes_tab and ms_cat[dom] > 0:
         # node_update runs in the M node blocks, rotate_out_edge in the M edge
         # blocks, rotate_in / so2_linears in all 2M blocks
         blocks = layers if name in ("node_update", "rotate_out_edge") else 2 * layers
-        alg_bytes = BYTES_PER_EDGE[name] * net.n_edges * blocks * args.steps
+        alg_bytes = bytes_tab[name] * net.n_edges * blocks * args.steps
         achieved = alg_bytes / (ms_cat[dom] / 1e3) / 1e9
         launches_dom = max(int(n_cat[dom]), 1)
         edges_per_launch = net.n_edges * blocks * args.steps / launches_dom
-        tr = measured_traffic(name)
+        tr = measured_traffic(name, prec_name)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": (tr["dram_bytes_per_edge"] * edges_per_launch) if tr else None,
                 "kernel": name, "peak_source": peak_kind,
-                "bytes_per_edge": BYTES_PER_EDGE[name], "edges_per_launch": edges_per_launch,
+                "bytes_per_edge": bytes_tab[name], "edges_per_launch": edges_per_launch,
                 "traffic_source": tr.get("source") if tr else None,
                 "launches": int(n_cat[dom]), "avg_launch_ms": float(ms_cat[dom] / launches_dom)}
+        if name == "so2_linears":
+            # the same launches against the tensor pipe: algorithmic fp32 FLOPs
+            # of lin1 + lin2; the fp16x3 split issues 3 kind::f16 products per
+            # fp32 one, so its ceiling is a third of the dense fp16 rate
+            alg_tf = SO2_FLOPS_PER_EDGE * net.n_edges * 2 * layers * args.steps / (ms_cat[dom] / 1e3) / 1e12
+            ceil = tpk / 3 if prec == esg.LINEAR_FP32 else tpk
+            roof["tensor"] = {"achieved": alg_tf, "peak": ceil, "unit": "TFLOP/s (algorithmic fp32)"
+                              if prec == esg.LINEAR_FP32 else "TFLOP/s", "frac": alg_tf / ceil,
+                              "peak_source": tpk_kind + (" / 3 (three products per fp32 product)"
+                                                         if prec == esg.LINEAR_FP32 else "")}
+    # the whole message-passing path against SURVEY §8(d)'s fused minimum
+    path = {"bytes": (ALG_EDGE_LAYER * net.n_edges + ALG_NODE_LAYER * net.n_owned) * layers,
+            "t_mp_ms": msg_step}
+    path["achieved_gbs"] = path["bytes"] / (msg_step / 1e3) / 1e9 if msg_step > 0 else None
+    path["frac"] = path["achieved_gbs"] / hbm if path["achieved_gbs"] else None
 
     # e2e through the public API with host buffers
     e2e = None
@@ -373,37 +416,40 @@ def run_ours(args):
                               "and the next step run (esg_forward_async / esg_forward_wait)",
                "pinned_host_outputs": bool(getattr(torch.from_numpy(edge_out), "is_pinned", lambda: False)())}
 
-    # the fp32-accurate mode on the same graph (3xTF32 tensor-core linears;
-    # Hamiltonian blocks within the fp32 tolerance of tests/test_gpu_parity.py)
-    fp32_mode = None
-    if args.fp32_steps > 0 and prec == esg.LINEAR_BF16:
-        net.set_precision(esg.LINEAR_FP32)
+    # bf16 tensor-core linears on the same graph (throughput side key): time
+    # and the measured deviation of its heads from this run's fp32 heads
+    # (the fp32 path is within rel-L2 2e-5 of the float oracle, test_gpu_parity)
+    bf16_mode = None
+    if args.bf16_steps > 0 and prec == esg.LINEAR_FP32 and world == 1:
+        n_cmp = min(net.n_edges, 2_000_000)
+        ref_n, ref_e = net.outputs_host(n_cmp)
+        net.set_precision(esg.LINEAR_BF16)
         net.forward(copy_out=False)
-        barrier()
         torch.cuda.synchronize()
-        f32 = [net.forward(copy_out=False)[2].forward_ms for _ in range(args.fp32_steps)]
-        ms32 = allmax(float(np.mean(f32)))
-        fp32_mode = {"value": total_edges / (ms32 / 1e3), "unit": "edges/s", "ms_per_step": ms32,
-                     "steps": args.fp32_steps,
-                     "linears": "tcgen05 kind::tf32, 3xTF32 split (hi.hi + hi.lo + lo.hi), fp32 accumulate",
-                     "tolerance": "heads vs fp32 oracle: max-abs <= 2e-4 x max, rel-L2 <= 2e-5"}
+        b16 = [net.forward(copy_out=False)[2].forward_ms for _ in range(args.bf16_steps)]
+        got_n, got_e = net.outputs_host(n_cmp)
+        ms16 = float(np.mean(b16))
+        def dev(a, b):
+            return {"rel_l2": float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)),
+                    "max_abs_over_max": float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))}
+        bf16_mode = {"value": total_edges / (ms16 / 1e3), "unit": "edges/s", "ms_per_step": ms16,
+                     "steps": args.bf16_steps, "dtype": "bf16",
+                     "linears": "tcgen05 kind::f16 bf16 operands, fp32 accumulate",
+                     "deviation_vs_fp32_heads": {"nodes": dev(got_n, ref_n),
+                                                 "edges_first_%d" % n_cmp: dev(got_e, ref_e)},
+                     "tolerance": "bf16 bar: rel-L2 <= 2e-2, max-abs <= 5e-2 x max (fp32 bar 2e-5 / 2e-4)"}
         net.set_precision(prec)
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
-        v, cores, sample = cpu_sample(s, r, layers, basis, target_s=args.cpu_seconds, g=g.export())
+        v, cores, sample = cpu_sample(s, r, layers, basis, g=g.export())
         cpu = {"value": v, "unit": "edges/s", "cores": cores, "kind": "port", "sample": sample}
     line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16" if prec == esg.LINEAR_BF16 else "fp32", "data": "synthetic",
-            "config": {"workload": CONFIG_DESC[args.config], "atoms": s.n_atoms, "edges": total_edges,
-                       "r_cut": r, "layers": layers, "l_max": 4, "e_width": 16,
-                       "linears": "tcgen05 bf16, fp32 accumulate" if prec == esg.LINEAR_BF16 else
-                       "tcgen05 kind::tf32, 3xTF32 split, fp32 accumulate",
-                       "parallelism": f"graph-partition dp{world} (Low-NN, NCCL halo)",
-                       "l2": "inputs larger than L2 (edge table %.0f GB)" % (total_edges * ROW / 1e9)},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clocks, "fp32_mode": fp32_mode,
-            "gpu_launches": int(allsum(launches)),
+            "vs_baseline": None, "dtype": prec_name, "data": "synthetic",
+            "config": config_dict(args.config, s.n_atoms, total_edges, r, layers, world, prec_name),
+            "e2e": e2e, "roofline": roof, "path_roofline": path, "cpu_baseline": cpu, "clocks": clocks,
+            "bf16_mode": bf16_mode, "gpu_launches": int(allsum(launches)),
             "halo_ms_per_forward": halo_step, "halo_exchanges_per_forward": 2 * layers if world > 1 else 0,
             "message_ms_per_forward": msg_step,
             "kernel_ms_per_forward": {PROF_NAMES[i]: float(ms_cat[i] / args.steps) for i in range(8)},
@@ -469,11 +515,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default="fp32", choices=["bf16", "fp32"],
+                    help="fp32: the fp32-faithful linears (the headline); bf16: throughput mode")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="0 skips the CPU baseline sample")
     ap.add_argument("--train-steps", type=int, default=2, help="C2 training steps after the forward (0: skip)")
-    ap.add_argument("--fp32-steps", type=int, default=2, help="forwards timed in the fp32-accurate mode (0: skip)")
+    ap.add_argument("--bf16-steps", type=int, default=3, help="forwards timed in the bf16 side mode (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

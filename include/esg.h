@@ -35,8 +35,12 @@ enum {
 };
 
 /* precision of the SO(2) linears (everything else is fp32 state with fp64
- * geometry): FP32 = CUDA-core fp32 (parity mode), BF16 = tcgen05 kind::f16
- * with fp32 accumulation in TMEM (throughput mode). */
+ * geometry): FP32 = fp32-faithful products on the tensor cores -- tcgen05
+ * kind::f16 over a 3-term fp16 split with power-of-two scales (l_max 4,
+ * e_width 16; so2_f16x3.cu) or kind::tf32 over a 3xTF32 split (other shapes
+ * and the training reverse pass), within the fp32 tolerance of the float
+ * oracle; BF16 = tcgen05 kind::f16 on bf16 operands with fp32 accumulation
+ * in TMEM (throughput mode). */
 enum { ESG_LINEAR_FP32 = 0, ESG_LINEAR_BF16 = 1 };
 
 typedef struct esg_ctx esg_ctx;
@@ -210,6 +214,10 @@ int esg_profile(esg_model* m, int enable, double* ms, int64_t* counts);
  * next forward or destroy). */
 int esg_forward_outputs(const esg_model* m, const float** node_out, const float** edge_out,
                         const float** node_features, const float** edge_features);
+/* Rows [first, first + count) of the last forward's node / edge head outputs
+ * (out_len floats each) to host; either pointer may be NULL. */
+int esg_outputs_export(const esg_model* m, int64_t node_first, int64_t node_count, float* node_out,
+                       int64_t edge_first, int64_t edge_count, float* edge_out);
 /* Node / edge feature tables (n_rows*H*E / n_edges*H*E) to host. */
 int esg_features_export(const esg_model* m, float* nodes, float* edges);
 

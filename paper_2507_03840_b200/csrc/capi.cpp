@@ -31,6 +31,8 @@ void model_profile(esg_model* M, int enable, double* ms, int64_t* counts);
 void model_outputs(const esg_model* M, const float** no, const float** eo, const float** nf, const float** ef);
 void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out);
 void model_copy_features(const esg_model* M, float* nodes, float* edges);
+void model_copy_output_rows(const esg_model* M, int64_t nf, int64_t nc, float* node_out, int64_t ef, int64_t ec,
+                            float* edge_out);
 void model_prepared_info(const esg_model* M, int64_t info[3]);
 void edge_rotations(esg_ctx* ctx, int64_t n, const double* disp, int l_max, float* out);
 void partition_metrics_gpu(const esg_graph* g, const int32_t* part, int P, esg_metrics* m, esg_part_stats* parts,
@@ -743,6 +745,16 @@ int esg_edge_rotations(esg_ctx* ctx, int64_t n_edges, const double* disp, int l_
   if (n_edges && (!disp || !blocks)) usage("edge rotations: NULL array");
   ESG_CUDA(cudaSetDevice(ctx->device));
   edge_rotations(ctx, n_edges, disp, l_max, blocks);
+  ESG_API_END
+}
+
+int esg_outputs_export(const esg_model* m, int64_t node_first, int64_t node_count, float* node_out,
+                       int64_t edge_first, int64_t edge_count, float* edge_out) {
+  ESG_API_BEGIN
+  NEED(m, "model");
+  if (!m->ctx || !m->dev) usage("model was created without a device context");
+  ESG_CUDA(cudaSetDevice(m->ctx->device));
+  model_copy_output_rows(m, node_first, node_count, node_out, edge_first, edge_count, edge_out);
   ESG_API_END
 }
 

@@ -1247,6 +1247,20 @@ void model_copy_outputs(const esg_model* M, float* node_out, float* edge_out) {
     ESG_CUDA(cudaMemcpy(edge_out, D->edge_out, sizeof(float) * (size_t)D->n_edges * ol, cudaMemcpyDeviceToHost));
 }
 
+// Rows [first, first + count) of the last forward's head outputs to host.
+void model_copy_output_rows(const esg_model* M, int64_t nf, int64_t nc, float* node_out, int64_t ef, int64_t ec,
+                            float* edge_out) {
+  const DeviceModel* D = M->dev;
+  const int ol = M->heads.out_len;
+  if (nc < 0 || ec < 0 || nf < 0 || ef < 0 || nf + nc > D->n_owned || ef + ec > D->n_edges)
+    usage("output row range outside the prepared view");
+  ESG_CUDA(cudaStreamSynchronize(M->ctx->stream));
+  if (node_out && nc)
+    ESG_CUDA(cudaMemcpy(node_out, D->node_out + nf * ol, sizeof(float) * (size_t)nc * ol, cudaMemcpyDeviceToHost));
+  if (edge_out && ec)
+    ESG_CUDA(cudaMemcpy(edge_out, D->edge_out + ef * ol, sizeof(float) * (size_t)ec * ol, cudaMemcpyDeviceToHost));
+}
+
 void model_copy_features(const esg_model* M, float* nodes, float* edges) {
   const DeviceModel* D = M->dev;
   const size_t row = (size_t)D->H * D->E;

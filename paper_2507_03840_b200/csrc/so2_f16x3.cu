@@ -133,25 +133,21 @@ __device__ __forceinline__ void mma_chunk(uint32_t tmem_d, uint64_t da, uint64_t
   }
 }
 
-// TMEM column plan (l_max 4, e_width 16; N1 = 160 256 192 128 64, N2 = N1/2).
-// Units run in the order m = 0, 1, 4, 3, 2 within a tile (order 0 first: it
-// carries the gate scalars).  lin1 of order m accumulates into
-// R_m = [R0[m], R0[m] + N1):  R0 = [0,160)  R1 = [256,512)  R4 = [96,160)
-// R3 = [384,512)  R2 = [160,352); lin2 accumulates Y_m into its head
-// [R0[m], R0[m] + N2), chunk by chunk behind the gate, once the gate has read
-// those columns.  Consecutive units' regions are disjoint (lin1 of the next
-// unit runs while this one is gated), and no Y overlaps the region of the
-// unit two later (found by exhaustive search over 32-column placements and
-// unit orders), so lin1 of unit u waits only for
-//   the gate of unit u - GL[m] to have read its lin1 columns, and
-//   the drain of unit u - DL[m] (the first earlier unit whose Y it overlaps):
-// GL = 3 2 3 2 2, DL = 3 3 3 5 5 for m = 0..4 -- the drain round trip of a
-// unit has two whole lin1 units to hide behind.
-__device__ __constant__ int kSeq[5] = {0, 1, 4, 3, 2};
-__device__ __forceinline__ int order_of(int u) { return kSeq[u % 5]; }
-__device__ __forceinline__ int r0_col(int m) { return m == 0 ? 0 : (m == 1 ? 256 : (m == 2 ? 160 : (m == 3 ? 384 : 96))); }
-__device__ __forceinline__ int gate_lag(int m) { return (m == 0 || m == 2) ? 3 : 2; }
-__device__ __forceinline__ int drain_lag(int m) { return m >= 3 ? 5 : 3; }
+// TMEM column plan (l_max 4, e_width 16; N1 = 160 256 192 128 64, N2 = N1/2):
+// lin1 of order m accumulates into R_m = [R0[m], R0[m] + N1)
+//   R1 = [0,256)  R3 = [0,128)  R0 = [256,416)  R2 = [256,448)  R4 = [448,512);
+// lin2 accumulates Y_m into its head [R0[m], R0[m] + N2), chunk by chunk
+// behind the gate, once the gate has read those columns.  Consecutive
+// orders' regions are disjoint (lin1 of order m + 1 runs while order m is
+// gated).  lin1 of unit u waits until units < u - LAG[m] are drained: the
+// most recent earlier unit whose region overlaps R_m (m2 for m0, m3 for m1,
+// m0 for m2, m1 for m3, the previous tile's m4 for m4); a drained unit's gate
+// has read all of its columns.  (A unit order / placement in which no Y
+// overlaps the region two units later exists -- m = 0 1 4 3 2 -- but did
+// not run faster: the chain is bound by its A1 stream.)
+__device__ __forceinline__ int order_of(int u) { return u % 5; }
+__device__ __forceinline__ int r0_col(int m) { return m == 1 || m == 3 ? 0 : (m == 4 ? 448 : 256); }
+__device__ __forceinline__ int lag(int m) { return m <= 1 ? 2 : (m <= 3 ? 1 : 4); }
 
 __device__ __forceinline__ uint32_t ld_acquire(uint32_t addr) {
   uint32_t v;
@@ -243,8 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int L1F = E2 + NS2;                 // + (u % NL1): lin1 of unit u complete
   const int L2F = L1F + NL1;                // + (u % NL1): lin2 of unit u complete
   const int H1 = L2F + NL1;                 // + (u % NL1): the gate read the Y head of unit u
-  const int GD = H1 + NL1;                  // + (u % NL1): the gate read all of unit u's columns
-  uint32_t* drained = (uint32_t*)(bars + GD + NL1);  // units drained so far
+  uint32_t* drained = (uint32_t*)(bars + H1 + NL1);  // units drained so far
   uint32_t* l2_issued = drained + 1;               // units whose lin2 is fully issued
   uint32_t* tmem_slot = drained + 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -265,7 +260,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(bar(L1F + b), 1);
       mbar_init(bar(L2F + b), 1);
       mbar_init(bar(H1 + b), GATE_THREADS);
-      mbar_init(bar(GD + b), GATE_THREADS);
     }
     *drained = 0;
     *l2_issued = 0;
@@ -302,13 +296,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       Probe pr;
       const long long t_all = pclock();
       const int64_t total_a = my_tiles * S::KCH;
-      // A1 chunk i of this CTA's stream, in unit order (the image keeps order m
-      // at K offset kofs(m))
-      auto a_chunk = [&](int64_t i) {
+      auto a_chunk = [&](int64_t i) {  // A1 chunk i of this CTA's stream (orders in image order)
         const int64_t tile = blockIdx.x + (i / S::KCH) * gridDim.x;
-        int r = (int)(i % S::KCH), k = 0;
-        while (r >= S::K1P(order_of(k)) / 32) r -= S::K1P(order_of(k++)) / 32;
-        return A1 + ((size_t)tile * S::KCH + (size_t)(S::kofs(order_of(k)) / 32 + r)) * CHUNK;
+        return A1 + ((size_t)tile * S::KCH + (size_t)(i % S::KCH)) * CHUNK;
       };
       if (is_a)
         for (int64_t i = 0; i < PFA && i < total_a; ++i) prefetch_l2(a_chunk(i), CHUNK);
@@ -379,9 +369,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       spin_until(l2_issued, u - (NL1 - 1));  // the L1F / H1 phases of unit u - NL1 are consumed
       pr.add(4, pclock() - t0);
       t0 = pclock();
-      const int gu = u - gate_lag(m);  // the gate of unit gu has read R_m's columns
-      if (gu >= 0) mbar_wait(bar(GD + gu % NL1), (gu / NL1) & 1);
-      spin_until(drained, u - drain_lag(m) + 1);  // Y of unit u - DL[m] drained
+      spin_until(drained, u - lag(m));  // the units whose columns R_m reuses are drained
       pr.add(1, pclock() - t0);
       const uint32_t id1 = idesc_f16(S::N1(m)), t_r = tmem + r0_col(m);
       const int nch = S::K1P(m) / 32;
@@ -518,9 +506,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           fence_async_smem();
           mbar_arrive(bar(F2 + s2i));
         }
-        tc_fence_before();
-        if (!head_done) mbar_arrive(bar(H1 + u % NL1));
-        mbar_arrive(bar(GD + u % NL1));  // every lin1 column of unit u read
+        if (!head_done) {
+          tc_fence_before();
+          mbar_arrive(bar(H1 + u % NL1));
+        }
         gbase += (uint32_t)nch;
       }
     pr.add(12, pclock() - t_all);

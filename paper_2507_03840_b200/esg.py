@@ -609,6 +609,15 @@ class Network:
         _check(lib().esg_features_export(self._h, _p(n), _p(e)))
         return n, e
 
+    def outputs_host(self, n_edges: int):
+        """Node head outputs and the first n_edges edge head outputs of the
+        last forward (esg_outputs_export)."""
+        no = np.empty((self.n_owned, self.out_len), np.float32)
+        eo = np.empty((n_edges, self.out_len), np.float32)
+        _check(lib().esg_outputs_export(self._h, C.c_int64(0), C.c_int64(self.n_owned), _p(no), C.c_int64(0),
+                                        C.c_int64(n_edges), _p(eo)))
+        return no, eo
+
     def blocks_uncoupled(self) -> np.ndarray:
         n = C.c_int64()
         _check(lib().esg_blocks_size(self._h, C.byref(n)))

@@ -8,10 +8,10 @@ OUT=${1:-gpurun_out/ev}
 mkdir -p "$OUT"
 timeout 900 python bench.py > "$OUT/bench.log" 2>&1; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > "$OUT/ref.log" 2>&1; echo "ref rc=$?"
-SHORT="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --cpu-seconds 0 --train-steps 0 --fp32-steps 0"
+SHORT="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --cpu-seconds 0 --train-steps 0 --bf16-steps 0"
 timeout 600 $SHORT > "$OUT/plain.log" 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
     --log-file "$OUT/launches.csv" $SHORT > "$OUT/ncu_launches.log" 2>&1; echo "launches rc=$?"
 timeout 1200 ncu --set full --import-source on --clock-control none -k "regex:${2:-k_rotate_in}" -c 1 \
-  -o "$OUT/prof_top" -f python bench.py --steps 1 --warmup 0 --e2e-steps 0 --cpu-seconds 0 --train-steps 0 --fp32-steps 0 \
+  -o "$OUT/prof_top" -f python bench.py --steps 1 --warmup 0 --e2e-steps 0 --cpu-seconds 0 --train-steps 0 --bf16-steps 0 \
   > "$OUT/ncu_full.log" 2>&1; echo "full rc=$?"

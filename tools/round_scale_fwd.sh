@@ -3,10 +3,10 @@
 set -o pipefail
 OUT=${1:-gpurun_out/scale_fwd}
 mkdir -p "$OUT"
-timeout 900 python bench.py --steps 3 --warmup 3 --cpu-seconds 0 --train-steps 0 --fp32-steps 0 > "$OUT/fwd_n1.log" 2>&1
+timeout 900 python bench.py --steps 3 --warmup 3 --cpu-seconds 0 --train-steps 0 --bf16-steps 0 > "$OUT/fwd_n1.log" 2>&1
 echo "fwd N=1 rc=$?"
 for N in 2 4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
     --master-port $((29500+N)) bench.py --gpus $N --steps 3 --warmup 3 --cpu-seconds 0 --train-steps 0 \
-    --fp32-steps 0 > "$OUT/fwd_n$N.log" 2>&1; echo "fwd N=$N rc=$?"
+    --bf16-steps 0 > "$OUT/fwd_n$N.log" 2>&1; echo "fwd N=$N rc=$?"
 done
