@@ -1,0 +1,125 @@
+"""The oracle pinned to the REFERENCE code.
+
+oracle/_ref/libesgnn_ref.so is the reference implementation itself -- the
+/root/reference/proj library sources compiled unmodified against
+oracle/eigen_shim (oracle/ref.mk) -- and oracle/_ref/ref_acceptance its own
+acceptance binary.  These CPU tests check that the CPU restatement the GPU
+parity tests compare against (oracle/oracle.cpp) reproduces the reference's
+outputs: graph, Low-NN, comm plans, the taped Network<T>::build_forward heads
+(network.h:115-164) and the forward output stage's text files
+(model_run.cpp:141-151).  Skipped when the reference was not built (no
+/root/reference where build() ran).
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+import ref as R
+from paper_2507_03840_b200 import esg
+
+pytestmark = pytest.mark.skipif(not R.available(), reason="oracle/_ref not built (no /root/reference)")
+
+SKEW = np.array([[6.0, 0.4, 0.0], [0.9, 5.5, 0.3], [0.2, 0.6, 6.5]])
+PBC1 = np.ones(3, np.uint8)
+
+
+def same_graph(a, b):
+    for k in ("src", "dst", "shift"):
+        assert np.array_equal(np.asarray(a[k]).reshape(-1), np.asarray(b[k]).reshape(-1)), k
+    for k in ("disp", "dist"):
+        assert np.array_equal(np.asarray(a[k]).view(np.uint64), np.asarray(b[k]).view(np.uint64)), k
+
+
+def test_reference_acceptance_criteria():
+    """acceptance.cpp criteria 1 (equivariance), 2 (harmonics oracles), 5
+    (Low-NN structure) and 6 (exact counts), run by the reference's own code."""
+    out = subprocess.run([R.ACCEPTANCE, "1", "2", "5", "6"], capture_output=True, text=True, timeout=600)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("criterion")]
+    assert len(lines) == 4 and all(": PASS" in l for l in lines), out.stdout + out.stderr
+    assert out.returncode == 0
+
+
+def test_synthetic_inputs_equal_reference():
+    for args in ((512, 2.71, 0.30, [14], 1), (3000, 2.20, 0.45, [72, 8, 8], 2), (200, 2.0, 0.0, [1], 1)):
+        a, b = R.jittered_lattice(*args), O.jittered_lattice(*args)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("pbc", [(1, 1, 1), (0, 0, 0), (1, 0, 1)])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_graph_kats_equal_reference(pbc, seed):
+    pos = np.random.default_rng(seed).random((8, 3)) @ SKEW
+    sp = np.ones(8, np.int32)
+    same_graph(O.build_graph(pos, SKEW, np.array(pbc, np.uint8), 4.0),
+               R.build_graph(pos, sp, SKEW, np.array(pbc, np.uint8), 4.0))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_graph_partition_plans_equal_reference(name):
+    s, r, _, _ = esg.config_structure(name)
+    g = R.build_graph(s.positions, s.species, s.cell, PBC1, r)
+    go = O.build_graph(s.positions, s.cell, PBC1, r)
+    same_graph(go, g)
+    deg = O.in_degrees(s.n_atoms, go)
+    for depth in (1, 2, 3):
+        part = R.lownn(s.positions, s.species, s.cell, PBC1, depth, r)
+        assert np.array_equal(O.lownn(s.positions, s.cell, PBC1, deg, depth, r), part), depth
+        # the product's host Low-NN too
+        assert np.array_equal(esg.lownn_partition(s, deg, depth, r), part), depth
+    part = R.lownn(s.positions, s.species, s.cell, PBC1, 2, r)
+    for rank in range(4):
+        want = R.comm_plan(s.species, part, 4, rank)
+        got = O.comm_plan(s.n_atoms, go["src"], go["dst"], part, 4, rank)
+        for k in ("row_global", "src_row", "dst_row", "nbr_peer", "nbr_recv_row", "nbr_recv_count", "send_rows"):
+            assert np.array_equal(got[k], want[k]), (name, rank, k)
+
+
+@pytest.mark.parametrize("prec,dtype", [(4, np.float32), (8, np.float64)])
+def test_forward_equals_reference_small(prec, dtype):
+    """The restated forward against the reference's taped
+    Network<T>::build_forward: 40-atom HfO2, 2 layers, l_max 4, E 16."""
+    s = esg.make_jittered_lattice(40, 2.2, 0.45, [72, 8, 8], 4)
+    no, eo, g = R.forward(s.positions, s.species, s.cell, PBC1, 4.5, esg.BASIS_HFO2, layers=2, precision=prec)
+    om = O.Model(4, 16, 2, 32, 4.5, 1, esg.BASIS_HFO2)
+    rno, reo = om.forward(O.serial_view(s.n_atoms, s.species, O.build_graph(s.positions, s.cell, PBC1, 4.5)), dtype)
+    for a, b in ((rno, no), (reo, eo)):
+        assert np.abs(a - b).max() <= 1e-6 * np.abs(b).max()
+        assert np.array_equal(a.astype(np.float64), b), "restatement is bit-identical to the reference"
+
+
+def test_forward_equals_reference_c1():
+    """BASELINE config 1 (512-atom Si, 8 A, 1 layer, DZVP-like basis) in
+    float: the restated forward reproduces the reference's taped forward."""
+    s, r, layers, basis = esg.config_structure("C1")
+    no, eo, g = R.forward(s.positions, s.species, s.cell, PBC1, r, basis, layers=layers, precision=4)
+    om = O.Model(4, 16, layers, 32, r, 1, basis)
+    rno, reo = om.forward(O.serial_view(s.n_atoms, s.species, O.build_graph(s.positions, s.cell, PBC1, r)),
+                          np.float32)
+    for a, b in ((rno, no), (reo, eo)):
+        assert np.abs(a - b).max() <= 1e-6 * np.abs(b).max(), np.abs(a - b).max() / np.abs(b).max()
+
+
+def test_output_stage_text_equals_reference(tmp_path):
+    """model_run.cpp:141-151 (assemble_blocks, blocks_to_uncoupled,
+    write_blocks_file) by the reference against the oracle's restated output
+    stage on the same heads: blocks_coupled.txt and blocks_uncoupled.txt are
+    byte-identical."""
+    s = esg.make_jittered_lattice(24, 2.2, 0.45, [72, 8, 8], 5)
+    rc, ru = str(tmp_path / "ref_coupled.txt"), str(tmp_path / "ref_uncoupled.txt")
+    no, eo, g = R.forward(s.positions, s.species, s.cell, PBC1, 4.0, esg.BASIS_HFO2, layers=1, precision=4,
+                          coupled_path=rc, uncoupled_path=ru)
+    om = O.Model(4, 16, 1, 32, 4.0, 1, esg.BASIS_HFO2)
+    go = O.build_graph(s.positions, s.cell, PBC1, 4.0)
+    rno, reo = om.forward(O.serial_view(s.n_atoms, s.species, go), np.float32)
+    keys = np.concatenate([np.stack([np.arange(s.n_atoms), np.arange(s.n_atoms), np.zeros(s.n_atoms, int),
+                                     np.zeros(s.n_atoms, int), np.zeros(s.n_atoms, int)], 1),
+                           np.concatenate([np.stack([go["src"], go["dst"]], 1), go["shift"]], 1)]).astype(np.int32)
+    rows = np.concatenate([rno, reo]).astype(np.float32)
+    oc, ou = str(tmp_path / "oracle_coupled.txt"), str(tmp_path / "oracle_uncoupled.txt")
+    om.export_text(keys, rows, s.species, oc, ou)
+    assert open(oc, "rb").read() == open(rc, "rb").read()
+    assert open(ou, "rb").read() == open(ru, "rb").read()
