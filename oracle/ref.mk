@@ -17,7 +17,7 @@ FLAGS    := -std=c++20 -O2 -fPIC -ffp-contract=off -Ieigen_shim -I$(JSON) -I$(RE
 LIB_SRC  := $(shell find $(REF)/src -name '*.cpp' 2>/dev/null | sort)
 LIB_OBJ  := $(patsubst $(REF)/src/%.cpp,$(OUT)/obj/%.o,$(LIB_SRC))
 
-all: $(OUT)/libesgnn_ref.so $(OUT)/ref_acceptance
+all: $(OUT)/libesgnn_ref.so $(OUT)/ref_acceptance $(OUT)/forward_rank_b200
 
 $(OUT)/obj/%.o: $(REF)/src/%.cpp eigen_shim/Eigen/Dense
 	@mkdir -p $(dir $@)
@@ -43,3 +43,15 @@ $(OUT)/ref_acceptance: $(LIB_OBJ) $(OUT)/obj/model_run.o $(OUT)/obj/ref_acceptan
 
 clean:
 	rm -rf $(OUT)
+
+# INTEGRATION.md's forward_rank patch, compiled against the reference headers
+# and linked with libesg_b200.so (tests/test_gpu_integration.py runs it)
+B200     := ../paper_2507_03840_b200
+$(OUT)/obj/forward_rank_b200.o: ../tools/integration/forward_rank_b200.cpp $(B200)/csrc/esgnn_b200.hpp eigen_shim/Eigen/Dense
+	@mkdir -p $(dir $@)
+	$(CXX) $(FLAGS) -I$(B200)/csrc -c $< -o $@
+
+$(OUT)/forward_rank_b200: $(LIB_OBJ) $(OUT)/obj/forward_rank_b200.o $(B200)/libesg_b200.so
+	$(CXX) -o $@ $(LIB_OBJ) $(OUT)/obj/forward_rank_b200.o -L$(B200) -lesg_b200 -lpthread -Wl,-rpath,'$$ORIGIN/../../paper_2507_03840_b200'
+
+integration: $(OUT)/forward_rank_b200

@@ -9,7 +9,11 @@
 //   esgnn::runtime::DistributedRunner   (distributed.h:183)   -> Network::forward on a plan
 //   esgnn::harmonics::coupling_matrix   (clebsch_gordan.h:19) -> esgnn::b200::coupling_matrix
 //
-// Errors are rethrown as the esgnn::Error taxonomy (core/error.h:11-51).
+// Errors are rethrown as the esgnn::Error taxonomy (core/error.h:11-51) --
+// the reference's own classes when its headers are on the include path.
+// With the reference headers present, to_b200(...) converts its
+// AtomicStructure, Assignment and ModelConfig, to_map its BasisSet, and
+// to_reference returns a device graph as a structures::Graph.
 #pragma once
 
 #include <array>
@@ -23,8 +27,16 @@
 
 #include "../../include/esg.h"
 
+
+// The error taxonomy is the reference's own (core/error.h:11-51) whenever its
+// headers are on the include path -- the drop-in case, so reference call
+// sites catch the same types -- and a same-named standalone copy otherwise.
+#if __has_include(<esgnn/core/error.h>)
+#include <esgnn/core/error.h>
+#define ESGNN_B200_REFERENCE_TYPES 1
+#else
+#define ESGNN_B200_REFERENCE_TYPES 0
 namespace esgnn {
-#ifndef ESGNN_CORE_ERROR_H_DEFINED
 class Error : public std::runtime_error {
  public:
   explicit Error(const std::string& m) : std::runtime_error(m) {}
@@ -49,8 +61,10 @@ class DivergenceError : public Error {
  public:
   using Error::Error;
 };
+}  // namespace esgnn
 #endif
 
+namespace esgnn {
 namespace b200 {
 
 inline void check(int rc) {
@@ -319,6 +333,56 @@ inline std::vector<double> coupling_matrix(int la, int lb, int L) {
   check(esg_coupling_matrix(la, lb, L, c.data()));
   return c;
 }
+
+#if ESGNN_B200_REFERENCE_TYPES && __has_include(<esgnn/structures/structure.h>) && \
+    __has_include(<esgnn/model/network.h>) && __has_include(<esgnn/partition/partition.h>)
+// ---- converters from the reference's own types (drop-in call sites)
+inline AtomicStructure to_b200(const esgnn::structures::AtomicStructure& s) {
+  AtomicStructure o;
+  o.positions.reserve(s.positions.size());
+  for (const auto& p : s.positions) o.positions.push_back({p(0), p(1), p(2)});
+  o.species = s.species;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) o.cell[3 * i + j] = s.cell(i, j);  // rows are lattice vectors, as the reference's
+  o.pbc = {s.pbc[0], s.pbc[1], s.pbc[2]};
+  return o;
+}
+inline Assignment to_b200(const esgnn::partition::Assignment& a) {
+  Assignment o;
+  o.n_parts = a.n_parts;
+  o.node_to_part = a.node_to_part;
+  return o;
+}
+inline ModelConfig to_b200(const esgnn::model::ModelConfig& c, int linear_precision = ESG_LINEAR_FP32) {
+  ModelConfig o;
+  o.l_max = c.l_max;
+  o.e_width = c.e_width;
+  o.layers = c.layers;
+  o.n_radial = c.n_radial;
+  o.r_cut = c.r_cut;
+  o.seed = c.seed;
+  o.gate_enabled = c.gate_enabled;
+  o.linear_precision = linear_precision;
+  return o;
+}
+inline std::map<int, std::vector<int>> to_map(const esgnn::structures::BasisSet& b) { return b.all(); }
+// Graph::edges in the reference's value type, for call sites that keep
+// using a structures::Graph (the device graph is bit-identical to it)
+inline esgnn::structures::Graph to_reference(const Graph& g) {
+  esgnn::structures::Graph r;
+  r.n_nodes = g.n_nodes;
+  for (const auto& e : g.edges()) {
+    esgnn::structures::Edge x;
+    x.src = e.src;
+    x.dst = e.dst;
+    x.shift = e.shift;
+    x.displacement = Eigen::Vector3d(e.displacement[0], e.displacement[1], e.displacement[2]);
+    x.distance = e.distance;
+    r.edges.push_back(x);
+  }
+  return r;
+}
+#endif
 
 }  // namespace b200
 }  // namespace esgnn
