@@ -310,6 +310,7 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     fwd_ms, msg_ms, halo_ms, launches = [], [], [], 0
+    halo_skew, halo_xch, halo_bytes = [], [], []
     with Clocks(local) as clk:
         w0 = time.perf_counter()
         for _ in range(args.steps):
@@ -317,6 +318,9 @@ def run_ours(args):
             fwd_ms.append(tm.forward_ms)
             msg_ms.append(tm.message_ms)
             halo_ms.append(tm.halo_ms)
+            halo_skew.append(tm.halo_skew_ms)
+            halo_xch.append(tm.halo_exchange_ms)
+            halo_bytes.append(tm.halo_bytes)
             launches += tm.gpu_launches
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
@@ -325,6 +329,22 @@ def run_ours(args):
     clocks = clk.summary()
     ms_step = allmax(float(np.mean(fwd_ms)))
     halo_step = allmax(float(np.mean(halo_ms)))
+    halo = None
+    if world > 1:
+        # per forward, max over ranks: the 2M exchanges' total, the part spent
+        # waiting for the slowest rank (a one-float allreduce lines the ranks
+        # up before each exchange while profiling) and the exchange proper
+        # (pack start -> last recv); NVLink GB/s = this rank's sent + received
+        # bytes over its exchange time
+        xch = float(np.mean(halo_xch))
+        gbs = float(np.mean(halo_bytes)) / (xch / 1e3) / 1e9 if xch > 0 else None
+        halo = {"ms_per_forward": halo_step, "exchanges_per_forward": 2 * layers,
+                "ms_per_exchange": halo_step / (2 * layers),
+                "skew_ms_per_forward": allmax(float(np.mean(halo_skew))),
+                "exchange_ms_per_forward": allmax(xch),
+                "bytes_per_forward_max_rank": allmax(float(np.mean(halo_bytes))),
+                "nvlink_gbs_min_over_ranks": -allmax(-gbs) if gbs else None,
+                "method": "CUDA events around each exchange, no host sync inside the forward; max over ranks"}
     msg_step = allmax(float(np.mean(msg_ms)))
     total_edges = g.n_edges
     value = total_edges / (ms_step / 1e3)
@@ -451,6 +471,7 @@ def run_ours(args):
             "e2e": e2e, "roofline": roof, "path_roofline": path, "cpu_baseline": cpu, "clocks": clocks,
             "bf16_mode": bf16_mode, "gpu_launches": int(allsum(launches)),
             "halo_ms_per_forward": halo_step, "halo_exchanges_per_forward": 2 * layers if world > 1 else 0,
+            "halo": halo,
             "message_ms_per_forward": msg_step,
             "kernel_ms_per_forward": {PROF_NAMES[i]: float(ms_cat[i] / args.steps) for i in range(8)},
             "setup_s": {"graph": t_graph, "partition_plan": t_part, "prepare": t_prep},

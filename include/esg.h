@@ -51,10 +51,17 @@ typedef struct esg_model esg_model;
 typedef struct esg_timing {
   double forward_ms;      /* first init kernel -> last head kernel (CUDA events) */
   double message_ms;      /* message passing only (all 2*M blocks) */
-  double halo_ms;         /* sum over the 2*M exchanges: pack start -> last recv */
+  double halo_ms;         /* sum over the 2*M exchanges: start -> last recv, rank skew included */
   double heads_ms;
   int64_t exchanges;      /* exactly 2*M per forward (acceptance.cpp:298) */
   int64_t gpu_launches;   /* kernels this library launched in the call */
+  /* with esg_profile on, a one-float allreduce lines the ranks up before each
+   * exchange: halo_skew_ms is the waiting for the slowest rank, and
+   * halo_exchange_ms pack start -> last recv after it (otherwise -1 and
+   * halo_ms); halo_bytes: the bytes this rank sent plus received */
+  double halo_skew_ms;
+  double halo_exchange_ms;
+  int64_t halo_bytes;
 } esg_timing;
 
 const char* esg_last_error(void);

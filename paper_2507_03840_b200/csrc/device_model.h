@@ -128,6 +128,11 @@ struct DeviceModel {
   bool train_stale = true;  // set by every prepare
   int64_t block_values = 0;
   cudaEvent_t ev[8];
+  // per-exchange events of the last forward (start, lined up, done) and the
+  // halo bytes it sent + received
+  std::vector<cudaEvent_t> halo_ev;
+  std::vector<int> halo_marks;
+  int64_t halo_bytes = 0;
   // optional per-category kernel timing (esg_profile_*): events around launches
   bool profile = false;
   std::vector<cudaEvent_t> pool;

@@ -604,6 +604,7 @@ void model_device_destroy(esg_model* M) {
   for (auto p : D->w2f) free_ptr(p);
   free_ptr(D->tmax);
   for (auto& e : D->ev) cudaEventDestroy(e);
+  for (auto& e : D->halo_ev) cudaEventDestroy(e);
   if (D->copies_pending) cudaEventSynchronize(D->copies_done);
   if (D->copies_done) cudaEventDestroy(D->copies_done);
   for (auto& e : D->out_ev) cudaEventDestroy(e);
@@ -798,7 +799,7 @@ void stream_rows(DeviceModel* D, cudaStream_t st, const float* dev, float* host,
 }
 
 template <int L, int E>
-void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
+void run_block(esg_model* M, int layer, bool node_block) {
   DeviceModel* D = M->dev;
   esg_ctx* ctx = M->ctx;
   cudaStream_t st = ctx->stream;
@@ -809,9 +810,23 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
   const int el0 = layer == 0 && el0_edges(M) ? (node_block ? 3 : 1) : 0;
   const int bidx = 2 * layer + (node_block ? 0 : 1);
   // halo exchange (distributed.h:51-130): pack, grouped send/recv straight
-  // into the contiguous halo rows of each peer.
+  // into the contiguous halo rows of each peer.  No host synchronisation: the
+  // exchange's events are read after the forward's final one.  With
+  // profiling on, a one-float allreduce first lines the ranks up, so the
+  // exchange time (pack start -> last recv) is separated from rank skew.
   if (ctx->world > 1) {
-    ESG_CUDA(cudaEventRecord(D->ev[4], st));
+    const int x = (int)D->halo_marks.size();
+    while ((int)D->halo_ev.size() < 3 * (x + 1)) {
+      cudaEvent_t e;
+      ESG_CUDA(cudaEventCreate(&e));
+      D->halo_ev.push_back(e);
+    }
+    D->halo_marks.push_back(x);
+    ESG_CUDA(cudaEventRecord(D->halo_ev[3 * x], st));
+    if (D->profile) {
+      ESG_NCCL(ncclAllReduce(D->tmax + 15, D->tmax + 15, 1, ncclFloat, ncclMax, ctx->comm, st));
+    }
+    ESG_CUDA(cudaEventRecord(D->halo_ev[3 * x + 1], st));
     const int row = H * E;
     if (D->n_send) {
       Prof pr(D, st, ESG_PROF_HALO);
@@ -827,13 +842,10 @@ void run_block(esg_model* M, int layer, bool node_block, float* halo_ms) {
       so += (int64_t)nb.send_rows.size();
       ESG_NCCL(ncclRecv(D->nodes + (int64_t)nb.recv_row * row, (int64_t)nb.recv_count * row, ncclFloat, nb.peer,
                         ctx->comm, st));
+      D->halo_bytes += (int64_t)(nb.send_rows.size() + nb.recv_count) * row * (int64_t)sizeof(float);
     }
     ESG_NCCL(ncclGroupEnd());
-    ESG_CUDA(cudaEventRecord(D->ev[5], st));
-    ESG_CUDA(cudaEventSynchronize(D->ev[5]));
-    float ms = 0.f;
-    ESG_CUDA(cudaEventElapsedTime(&ms, D->ev[4], D->ev[5]));
-    *halo_ms += ms;
+    ESG_CUDA(cudaEventRecord(D->halo_ev[3 * x + 2], st));
   }
   if (D->save_inputs) {  // training: this block's input tables (after the exchange)
     const size_t row_bytes = sizeof(float) * H * E;
@@ -1022,14 +1034,15 @@ void forward_impl(esg_model* M, esg_timing* tm) {
     }
   }
   ESG_CUDA(cudaEventRecord(D->ev[1], st));
-  float halo_ms = 0.f;
   int64_t exchanges = 0;
+  D->halo_marks.clear();
+  D->halo_bytes = 0;
   const int out_len = M->heads.out_len;
   const bool streamed = D->host_node_out || D->host_edge_out;
   D->out_ev_used = 0;
   for (int layer = 0; layer < M->cfg.layers; ++layer)
     for (bool nb : {true, false}) {
-      run_block<L, E>(M, layer, nb, &halo_ms);
+      run_block<L, E>(M, layer, nb);
       ++exchanges;
       if (streamed && nb && layer == M->cfg.layers - 1 && D->n_owned) {
         // the node table is final after the last node block: its heads and
@@ -1065,7 +1078,19 @@ void forward_impl(esg_model* M, esg_timing* tm) {
     tm->forward_ms = a;
     tm->message_ms = b;
     tm->heads_ms = c;
-    tm->halo_ms = halo_ms;
+    double halo = 0, skew = 0, xch = 0;
+    for (int x : D->halo_marks) {
+      float t0 = 0, t1 = 0;
+      ESG_CUDA(cudaEventElapsedTime(&t0, D->halo_ev[3 * x], D->halo_ev[3 * x + 1]));
+      ESG_CUDA(cudaEventElapsedTime(&t1, D->halo_ev[3 * x + 1], D->halo_ev[3 * x + 2]));
+      halo += t0 + t1;
+      skew += t0;
+      xch += t1;
+    }
+    tm->halo_ms = halo;
+    tm->halo_skew_ms = D->profile ? skew : -1.0;  // measured only with the lining-up allreduce
+    tm->halo_exchange_ms = D->profile ? xch : halo;
+    tm->halo_bytes = D->halo_bytes;
     tm->exchanges = ctx->world > 1 ? exchanges : 0;
     tm->gpu_launches = ctx->launches - launches0;
   }

@@ -65,6 +65,9 @@ class _Timing(C.Structure):
         ("heads_ms", C.c_double),
         ("exchanges", C.c_int64),
         ("gpu_launches", C.c_int64),
+        ("halo_skew_ms", C.c_double),
+        ("halo_exchange_ms", C.c_double),
+        ("halo_bytes", C.c_int64),
     ]
 
 
@@ -354,6 +357,9 @@ class Timing:
     heads_ms: float
     exchanges: int
     gpu_launches: int
+    halo_skew_ms: float = -1.0
+    halo_exchange_ms: float = 0.0
+    halo_bytes: int = 0
 
 
 # ------------------------------------------------------------ input side
@@ -579,20 +585,23 @@ class Network:
             no = np.zeros((self.n_owned, self.out_len), np.float32)
             eo = np.zeros((self.n_edges, self.out_len), np.float32)
         _check(lib().esg_forward(self._h, _p(no), _p(eo), C.byref(t)))
-        return no, eo, Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches)
+        return no, eo, Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches, t.halo_skew_ms,
+                      t.halo_exchange_ms, t.halo_bytes)
 
     def forward_into(self, node_out: Optional[np.ndarray], edge_out: Optional[np.ndarray]) -> Timing:
         """Forward with caller-owned (ideally pinned) host output buffers."""
         t = _Timing()
         _check(lib().esg_forward(self._h, _p(node_out), _p(edge_out), C.byref(t)))
-        return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches)
+        return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches, t.halo_skew_ms,
+                      t.halo_exchange_ms, t.halo_bytes)
 
     def forward_into_async(self, node_out: Optional[np.ndarray], edge_out: Optional[np.ndarray]) -> Timing:
         """esg_forward_async: with pinned buffers returns once the copies are
         queued; call wait_outputs() before reading or reusing the buffers."""
         t = _Timing()
         _check(lib().esg_forward_async(self._h, _p(node_out), _p(edge_out), C.byref(t)))
-        return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches)
+        return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches, t.halo_skew_ms,
+                      t.halo_exchange_ms, t.halo_bytes)
 
     def wait_outputs(self) -> None:
         _check(lib().esg_forward_wait(self._h))
