@@ -66,7 +66,10 @@ using namespace esg;
 
 struct esg_adam {
   esg_adam_config cfg{};
-  std::vector<double> m, v;
+  std::vector<double> m, v;  // host moments (the host path; checkpoint mirror of the device ones)
+  double *d_m = nullptr, *d_v = nullptr;  // device moments (a model with a device context)
+  int device = -1;
+  bool host_current = true;  // m / v hold the current moments (else d_m / d_v do)
   double lr = -1.0, best = std::numeric_limits<double>::infinity();
   long t = 0;
   int stale = 0;
@@ -154,22 +157,60 @@ double ckpt_read_f64(std::istream& in) {
 #define NEED(p, what) \
   if (!(p)) esg::usage(std::string("null ") + what)
 
+namespace esg {
+void model_adam_device(esg_model* M, double* d_m, double* d_v, const float* grads, double b1, double b2, double lr,
+                       double bc1, double bc2, double eps);  // train.cu
+}
+
 namespace {
+// device moments of opt, uploaded from the host mirror when they are stale
+void adam_device_moments(esg_adam* opt, esg_model* m) {
+  const size_t n = opt->m.size();
+  if (!opt->d_m) {
+    ESG_CUDA(cudaMalloc(&opt->d_m, sizeof(double) * n));
+    ESG_CUDA(cudaMalloc(&opt->d_v, sizeof(double) * n));
+    opt->device = m->ctx->device;
+    opt->host_current = true;
+  }
+  if (opt->host_current) {
+    ESG_CUDA(cudaMemcpy(opt->d_m, opt->m.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    ESG_CUDA(cudaMemcpy(opt->d_v, opt->v.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    opt->host_current = false;
+  }
+}
+// the host mirror of the moments (checkpoints)
+void adam_host_moments(const esg_adam* opt) {
+  esg_adam* o = const_cast<esg_adam*>(opt);
+  if (o->host_current || !o->d_m) return;
+  ESG_CUDA(cudaSetDevice(o->device));
+  ESG_CUDA(cudaMemcpy(o->m.data(), o->d_m, sizeof(double) * o->m.size(), cudaMemcpyDeviceToHost));
+  ESG_CUDA(cudaMemcpy(o->v.data(), o->d_v, sizeof(double) * o->v.size(), cudaMemcpyDeviceToHost));
+  o->host_current = true;
+}
+
 void adam_update(esg_adam* opt, esg_model* m, const float* g, double loss) {
-  // Optimizer::step (optimizer.h:42-59), moments in fp64
+  // Optimizer::step (optimizer.h:42-59), moments in fp64: on the device when
+  // the model has one (k_adam, bit-identical to the host loop below)
   if (opt->lr < 0) opt->lr = opt->cfg.lr;
   ++opt->t;
   const double bc1 = 1.0 - std::pow(opt->cfg.beta1, double(opt->t));
   const double bc2 = 1.0 - std::pow(opt->cfg.beta2, double(opt->t));
-  for (size_t k = 0; k < m->host_params.size(); ++k) {
+  if (m->ctx && m->dev) {
+    adam_device_moments(opt, m);
+    esg::model_adam_device(m, opt->d_m, opt->d_v, g, opt->cfg.beta1, opt->cfg.beta2, opt->lr, bc1, bc2,
+                           opt->cfg.eps);
+  } else {
+    adam_host_moments(opt);
+    for (size_t k = 0; k < m->host_params.size(); ++k) {
     const double gk = double(g[k]);
     opt->m[k] = opt->cfg.beta1 * opt->m[k] + (1.0 - opt->cfg.beta1) * gk;
     opt->v[k] = opt->cfg.beta2 * opt->v[k] + (1.0 - opt->cfg.beta2) * gk * gk;
     const double mh = opt->m[k] / bc1;
     const double vh = opt->v[k] / bc2;
     m->host_params[k] = static_cast<float>(double(m->host_params[k]) - opt->lr * mh / (std::sqrt(vh) + opt->cfg.eps));
+    }
   }
-  // reduce-on-plateau (optimizer.h:62-72)
+  // reduce-on-plateau (optimizer.h:62-72), a scalar rule: on the host
   if (loss < opt->best * (1.0 - opt->cfg.threshold)) {
     opt->best = loss;
     opt->stale = 0;
@@ -978,7 +1019,14 @@ int esg_adam_create(const esg_model* m, const esg_adam_config* cfg, esg_adam** o
   *out = a;
   ESG_API_END
 }
-void esg_adam_destroy(esg_adam* a) { delete a; }
+void esg_adam_destroy(esg_adam* a) {
+  if (a && a->d_m) {
+    cudaSetDevice(a->device);
+    cudaFree(a->d_m);
+    cudaFree(a->d_v);
+  }
+  delete a;
+}
 double esg_adam_lr(const esg_adam* a) { return a ? (a->lr < 0 ? a->cfg.lr : a->lr) : 0.0; }
 
 int esg_adam_apply(esg_adam* opt, esg_model* m, const float* grads, double loss) {
@@ -987,11 +1035,8 @@ int esg_adam_apply(esg_adam* opt, esg_model* m, const float* grads, double loss)
   NEED(m, "model");
   NEED(grads, "grads");
   if (opt->m.size() != m->host_params.size()) usage("optimizer built for another model");
-  adam_update(opt, m, grads, loss);
-  if (m->ctx && m->dev) {
-    ESG_CUDA(cudaSetDevice(m->ctx->device));
-    model_upload_params(m);
-  }
+  if (m->ctx && m->dev) ESG_CUDA(cudaSetDevice(m->ctx->device));
+  adam_update(opt, m, grads, loss);  // the device step repacks the weights itself
   ESG_API_END
 }
 
@@ -1007,8 +1052,7 @@ int esg_train_step(esg_model* m, esg_adam* opt, int64_t n_total, double* loss, e
   std::vector<float> g(m->host_params.size());
   double partials[3];
   model_loss_grad(m, n_total, partials, loss, g.data());
-  adam_update(opt, m, g.data(), *loss);
-  model_upload_params(m);
+  adam_update(opt, m, g.data(), *loss);  // on the device; refreshes the host parameters
   check_param_sync(m, "after update");
   if (timing) {
     double f = 0, b = 0;
@@ -1049,6 +1093,7 @@ int esg_checkpoint_save(const esg_model* m, const esg_adam* opt, const char* con
     ckpt_f64(out, opt->best);
     ckpt_u64(out, (uint64_t)opt->stale);
     out.write(reinterpret_cast<const char*>(&opt->cfg), sizeof(opt->cfg));
+    adam_host_moments(opt);
     ckpt_u64(out, opt->m.size());
     out.write(reinterpret_cast<const char*>(opt->m.data()), (std::streamsize)(opt->m.size() * sizeof(double)));
     out.write(reinterpret_cast<const char*>(opt->v.data()), (std::streamsize)(opt->v.size() * sizeof(double)));
@@ -1102,6 +1147,7 @@ int esg_checkpoint_load(esg_model* m, esg_adam* opt, const char* path, char* con
     opt->cfg = c;
     opt->m.swap(mm);
     opt->v.swap(vv);
+    opt->host_current = true;  // uploaded before the next device step
   }
   m->host_params.swap(p);
   if (m->ctx && m->dev) {

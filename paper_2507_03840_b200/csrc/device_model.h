@@ -55,6 +55,7 @@ struct DeviceModel {
   std::vector<uint16_t*> w1b, w2b;   // per block: tcgen05 bf16 packed
   std::vector<uint8_t*> w1f, w2f;    // per block: fp16x3 split images (so2_f16x3.cu)
   std::vector<F16x3Scales> f16sc;    // per block: their scales
+  bool f16_stale = true;             // the images predate the current parameters
   bool f16x3 = true;                 // ESG_F16X3=0: fp32 linears on the tf32 GEMMs instead
   // |x| maxima of the feature tables for the fp16x3 scale bounds: [0] the
   // node table entering the current block, [1 + l] the edge table entering

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <nccl.h>
 
 #include <array>
@@ -15,6 +17,34 @@
 #include "../../include/esg.h"
 
 namespace esg {
+
+// Function attributes (dynamic SMEM caps) and SM counts belong to a device,
+// not the process: these helpers keep them per device, so a
+// context on a second GPU of the same process configures its own.
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+  return d & 63;
+}
+// runs f once per device for this flag word (idempotent if two threads race)
+template <typename F>
+inline void once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  const uint64_t bit = 1ull << current_device();
+  if (done.load(std::memory_order_acquire) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_release);
+}
+inline int sm_count() {
+  static std::atomic<int> cache[64];
+  const int d = current_device();
+  int n = cache[d].load(std::memory_order_relaxed);
+  if (!n) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n <= 0) n = 148;
+    cache[d].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
 
 // ---- error taxonomy (core/error.h:11-51) mapped to ESG_* codes ----------
 struct Error : std::runtime_error {

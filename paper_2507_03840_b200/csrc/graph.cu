@@ -325,7 +325,7 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
     int cap = SEG_SORT_CAP;  // ESG_SEG_SORT_CAP=0 forces the cub path (tests)
     if (const char* e = std::getenv("ESG_SEG_SORT_CAP")) cap = std::min(std::max(std::atoi(e), 0), SEG_SORT_CAP);
     if (max_seg <= (unsigned long long)cap) {
-      k_segment_sort<<<(unsigned)std::min<int64_t>(n, 148 * 8), 256, 0, st>>>(d_keys, d_keys_sorted, G->d_off, n);
+      k_segment_sort<<<(unsigned)std::min<int64_t>(n, (int64_t)sm_count() * 8), 256, 0, st>>>(d_keys, d_keys_sorted, G->d_off, n);
       ctx->launches += 2;
     } else {  // very dense graphs: cub's segmented radix sort
       int end_bit = 32;

@@ -405,6 +405,40 @@ void pack_f16x3_block(const std::vector<float>& W, int N, int K, std::vector<uin
 }
 }  // namespace
 
+// The fp16x3 split images of every block, packed on the host from the host
+// parameters; run before the first fp16x3 forward after a parameter change
+// (model_upload_params marks them stale), so training steps never pay it.
+void pack_f16x3_images(esg_model* M) {
+  DeviceModel* D = M->dev;
+  if (D->w1f.empty() || !D->f16_stale) return;
+  cudaStream_t st = M->ctx->stream;
+  const int L = M->cfg.l_max, E = M->cfg.e_width, nb = 2 * M->cfg.layers;
+  D->f16sc.resize(nb);
+  for (int b = 0; b < nb; ++b) {
+    const std::string base = "layer" + std::to_string(b / 2) + (b % 2 == 0 ? "/node" : "/edge");
+    F16x3Scales& sc = D->f16sc[b];
+    for (int li = 0; li < 2; ++li) {
+      const int cin = li == 0 ? 3 * E : 2 * E, cout = li == 0 ? 2 * E : E;
+      const std::string wb = base + (li == 0 ? "/lin1" : "/lin2");
+      std::vector<uint8_t> img;
+      for (int m = 0; m <= L; ++m) {
+        const int rows = m == 0 ? M->lay.nd(0) : 2 * M->lay.nd(m);
+        float sw = 1.f, inf = 0.f;
+        pack_f16x3_block(expanded(M, wb, m, cin, cout), rows * cout, rows * cin, img, &sw, &inf);
+        (li == 0 ? sc.w1 : sc.w2)[m] = sw;
+        if (li == 0) sc.w1inf[m] = inf;
+      }
+      const int64_t want = li == 0 ? so2_f16x3_w1_bytes(L, E) : so2_f16x3_w2_bytes(L, E);
+      if ((int64_t)img.size() != want) usage("fp16x3 weight image size mismatch");
+      ESG_CUDA(cudaMemcpyAsync(li == 0 ? D->w1f[b] : D->w2f[b], img.data(), img.size(), cudaMemcpyHostToDevice, st));
+      ESG_CUDA(cudaStreamSynchronize(st));  // img is freed at scope exit
+    }
+  }
+  D->f16_stale = false;
+}
+
+void model_repack_params(esg_model* M);
+
 void model_upload_params(esg_model* M) {
   DeviceModel* D = M->dev;
   cudaStream_t st = M->ctx->stream;
@@ -475,6 +509,17 @@ void model_upload_params(esg_model* M) {
   }
   ESG_CUDA(cudaMemcpyAsync(D->params, M->host_params.data(), sizeof(float) * M->host_params.size(),
                            cudaMemcpyHostToDevice, st));
+  model_repack_params(M);
+}
+
+// Every packed image of the linears (tf32 / bf16 / SIMT forms) and the
+// embedding / head tables from the device parameters D->params (after an
+// upload or a device optimizer step); the fp16x3 images are repacked lazily.
+void model_repack_params(esg_model* M) {
+  DeviceModel* D = M->dev;
+  cudaStream_t st = M->ctx->stream;
+  const int L = M->cfg.l_max, E = M->cfg.e_width;
+  auto pad64 = [](int x) { return (x + 63) / 64 * 64; };
   // every linear's three images from the device parameters
   D->att_off.clear();
   for (int layer = 0; layer < M->cfg.layers; ++layer) {
@@ -505,23 +550,6 @@ void model_upload_params(esg_model* M) {
         }
         tf32_pack(D->params, L, E, li, false, oa.data(), ob.data(), D->wtc[li == 0 ? 0 : 1][b], st);
         tf32_pack(D->params, L, E, li, true, oa.data(), ob.data(), D->wtc[li == 0 ? 3 : 2][b], st);
-        if (!D->w1f.empty()) {  // fp16x3 split images, packed on the host from the same values
-          std::vector<uint8_t> img;
-          if ((int)D->f16sc.size() < nb) D->f16sc.resize(nb);
-          F16x3Scales& sc = D->f16sc[b];
-          for (int m = 0; m <= L; ++m) {
-            const int rows = m == 0 ? M->lay.nd(0) : 2 * M->lay.nd(m);
-            float sw = 1.f, inf = 0.f;
-            pack_f16x3_block(expanded(M, wb, m, cin, cout), rows * cout, rows * cin, img, &sw, &inf);
-            (li == 0 ? sc.w1 : sc.w2)[m] = sw;
-            if (li == 0) sc.w1inf[m] = inf;
-          }
-          const int64_t want = li == 0 ? so2_f16x3_w1_bytes(L, E) : so2_f16x3_w2_bytes(L, E);
-          if ((int64_t)img.size() != want) usage("fp16x3 weight image size mismatch");
-          ESG_CUDA(cudaMemcpyAsync(li == 0 ? D->w1f[b] : D->w2f[b], img.data(), img.size(), cudaMemcpyHostToDevice,
-                                   st));
-          ESG_CUDA(cudaStreamSynchronize(st));  // img is freed at scope exit
-        }
       }
     }
     D->att_off.push_back(M->params.at("layer" + std::to_string(layer) + "/att").offset);
@@ -556,6 +584,7 @@ void model_upload_params(esg_model* M) {
   ESG_CUDA(cudaMemcpyAsync(D->head_key, key_of.data(), sizeof(int) * key_of.size(), cudaMemcpyHostToDevice, st));
   ESG_CUDA(cudaMemcpyAsync(D->head_row, row_of.data(), sizeof(int) * row_of.size(), cudaMemcpyHostToDevice, st));
   ESG_CUDA(cudaStreamSynchronize(st));  // the host staging vectors go out of scope
+  D->f16_stale = true;  // pack_f16x3_images before the next fp16x3 forward
 }
 
 void model_device_create(esg_model* M) {
@@ -873,13 +902,18 @@ void run_block(esg_model* M, int layer, bool node_block) {
   } else if (!zero_mode) {
     D->a1_zero_mode = 0;  // the CUDA-core path writes fp32 rows over the whole buffer
   }
+  if (f3) pack_f16x3_images(M);
   const int edge_slot = 1 + layer;  // tmax slot of the edge table entering this layer
   if (f3) {  // |node table| bound after the exchange (k_abs_max, a 1.6 KB/row read)
     Prof pr(D, st, ESG_PROF_COPY);
     ESG_CUDA(cudaMemsetAsync(D->tmax, 0, sizeof(float), st));
     const int64_t n4 = (int64_t)D->n_rows * H * E / 4;
-    k_abs_max<256><<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 8), 256, 0, st>>>(D->nodes, 4 * n4, D->tmax);
+    k_abs_max<256><<<(unsigned)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8), 256, 0, st>>>(D->nodes, 4 * n4, D->tmax);
     ++ctx->launches;
+    // P ranks: the maxima over all ranks' rows and edges are the serial run's,
+    // so every rank splits with the serial scales (partitioned == serial, bit
+    // for bit).  One 64-byte allreduce per block.
+    if (ctx->world > 1) ESG_NCCL(ncclAllReduce(D->tmax, D->tmax, 16, ncclFloat, ncclMax, ctx->comm, st));
   }
   const float* att = D->params + D->att_off[layer];
   for (const auto& ch : D->chunks) {
@@ -967,16 +1001,15 @@ void run_block(esg_model* M, int layer, bool node_block) {
       Prof pr(D, st, ESG_PROF_NODE);
       constexpr int dyn = node_update_smem_floats<L, E, float>() * (int)sizeof(float);
       constexpr int dyn_bf16 = node_update_smem_floats<L, E, uint16_t>() * (int)sizeof(float);
-      static bool attr = false;
-      if (!attr) {
+      static std::atomic<uint64_t> attr{0};
+      once_per_device(attr, [&] {
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       dyn));
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, uint16_t, true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bf16));
         ESG_CUDA(cudaFuncSetAttribute(k_node_update<L, E, F32T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       dyn));
-        attr = true;
-      }
+      });
       if (f3)  // logits from the chain's fp32 accumulator
         k_node_update<L, E, F32T, true><<<ch.second - ch.first, 128, dyn, st>>>(
             (const F32T*)D->Y, D->dir, D->seg, ch.first, e0, att, D->nodes, D->nodes_alt, D->logits, D->prefetch);
@@ -998,13 +1031,12 @@ void launch_heads(const float* x, int64_t n, const float* W, const int* key_of, 
                   float* out, cudaStream_t st) {
   if (out_len > 256) usage("head layout wider than 256 outputs");
   constexpr int smem = heads_smem_bytes<H, E>();
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     ESG_CUDA(cudaFuncSetAttribute(k_heads<H, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  });
   const int threads = ((out_len + 31) / 32) * 32;
-  const unsigned blocks = (unsigned)std::min<int64_t>((n + HT - 1) / HT, 148 * 3);  // 3 x 64 KB per SM
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + HT - 1) / HT, sm_count() * 3);  // 3 x 64 KB per SM
   k_heads<H, E><<<blocks, threads, smem, st>>>(x, n, W, key_of, row_of, out_len, out);
 }
 
@@ -1025,7 +1057,7 @@ void forward_impl(esg_model* M, esg_timing* tm) {
     if (D->n_edges) {
       Prof pr2(D, st, ESG_PROF_INIT);
       if (M->cfg.n_radial > 32) usage("the GPU radial lift supports up to 32 Gaussians");
-      const int64_t blocks = std::min<int64_t>((D->n_edges + 255) / 256, 148 * 8);  // 8 warps x 32-edge blocks
+      const int64_t blocks = std::min<int64_t>((D->n_edges + 255) / 256, (int64_t)sm_count() * 8);  // 8 warps x 32-edge blocks
       k_init_edges<H, E, 32><<<(unsigned)blocks, 256, 0, st>>>(D->dist, D->n_edges, D->params + D->lift_off,
                                                                 M->cfg.n_radial,
                                                                 M->cfg.r_cut / (M->cfg.n_radial - 1), D->edges,
@@ -1151,7 +1183,7 @@ void model_init_edges(esg_model* M, float* out, cudaStream_t st) {
   DeviceModel* D = M->dev;
   const int L = D->L, E = D->E;
   if (!D->n_edges) return;
-  const int64_t blocks = std::min<int64_t>((D->n_edges + 255) / 256, 148 * 8);
+  const int64_t blocks = std::min<int64_t>((D->n_edges + 255) / 256, (int64_t)sm_count() * 8);
   const double spacing = M->cfg.r_cut / (M->cfg.n_radial - 1);
   auto go = [&](auto h, auto e) {
     constexpr int H = decltype(h)::value, EE = decltype(e)::value;

@@ -105,8 +105,21 @@ __device__ __forceinline__ void prefetch_y(const uint16_t* Y, int64_t el0, int n
 }
 template <int HE>
 __device__ __forceinline__ void prefetch_y(const float*, int64_t, int, int, int) {}
+// fp32 tiles [tile][c/4][edge % 128][4]: one run of (b - a) x 16 bytes per
+// 4-channel block and 128-edge tile
 template <int HE>
-__device__ __forceinline__ void prefetch_y(const F32T*, int64_t, int, int, int) {}
+__device__ __forceinline__ void prefetch_y(const F32T* Y, int64_t el0, int n, int w, int nw) {
+  if (n <= 0 || (threadIdx.x & 31)) return;
+  const int64_t el1 = el0 + n;  // exclusive
+  const int64_t ta = el0 >> 7, tb = (el1 - 1) >> 7;
+  const int runs = (int)(tb - ta + 1) * (HE / 4);
+  for (int u = w; u < runs; u += nw) {
+    const int64_t tile = ta + u / (HE / 4);
+    const int blk = u % (HE / 4);
+    const int64_t a = tile == ta ? el0 : tile << 7, b = tile == tb ? el1 : (tile + 1) << 7;
+    prefetch_bulk(Y + y_index<HE>(Y, a, blk * 4), (uint32_t)(b - a) * 16u);
+  }
+}
 
 // |v| maxima of the feature tables (the fp16x3 chain's scale bounds): a
 // non-negative float orders like its bit pattern, so an unsigned atomicMax
@@ -424,6 +437,7 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
 #pragma unroll
   for (int r = 0; r < NodeSplit<L>::RMAX; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (b < en) {
+    if constexpr (std::is_same<YT, F32T>::value) prefetch_y<HE>(Yin, b - e0, (int)min64(TE, en - b), t >> 5, 4);
     float* lg = logit_scratch + (b - e0);
     float mx = -INFINITY;
     for (int64_t k = b + t; k < en; k += 128) {
@@ -461,8 +475,12 @@ __global__ void __launch_bounds__(128, 4) k_node_update(const YT* __restrict__ Y
     z = (sred[0] + sred[1]) + (sred[2] + sred[3]);
     for (int64_t k0 = b; k0 < en; k0 += TE) {
       const int ne = (int)min64(TE, en - k0);
+      // fp32 tiles (the fp16x3 chain's Y): the next edge tile's runs go to L2
+      // while this one is computed
+      if constexpr (std::is_same<YT, F32T>::value)
+        if (k0 + TE < en) prefetch_y<HE>(Yin, k0 + TE - e0, (int)min64(TE, en - k0 - TE), t >> 5, 4);
       __syncthreads();  // the previous tile's D is no longer read
-      for (int i = t; i < ne * 3; i += 128) sdir[i] = dir[(k0 - e0) * 3 + i];
+      for (int i = t; i < ne * 3; i += 128) sdir[i] = dir[k0 * 3 + i];  // dir: global edge index
       for (int i = t; i < ne; i += 128) sA[i] = lg[k0 - b + i] / z;
       if constexpr (YSMEM) {  // the tile's Y rows arrive while the Wigner blocks are computed
         for (int u = t; u < (HE / 8) * TE; u += 128) {  // TE a power of two: no runtime division

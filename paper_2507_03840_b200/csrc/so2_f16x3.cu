@@ -588,16 +588,13 @@ void so2_f16x3_launch(int L, int E, const uint8_t* A1, int64_t n_e, const uint8_
                       const F16x3Scales& sc, const float* tmax, int edge_slot, float* Y, int gate, const float* att,
                       float* logits, cudaStream_t st) {
   if (!so2_f16x3_available(L, E)) usage("fp16x3 SO(2) chain is instantiated for l_max 4, e_width 16");
-  int dev = 0;
-  ESG_CUDA(cudaGetDevice(&dev));
-  static int n_sm[64] = {0};
-  if (dev < 0 || dev >= 64) usage("device index out of range");
-  if (!n_sm[dev]) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     ESG_CUDA(cudaFuncSetAttribute(k_so2_f16x3<4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    ESG_CUDA(cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev));
-  }
+  });
+  const int n_sm = sm_count();
   const int64_t tiles = (n_e + TILE_M - 1) / TILE_M;
-  const int grid = (int)(tiles < n_sm[dev] ? tiles : n_sm[dev]);
+  const int grid = (int)(tiles < n_sm ? tiles : n_sm);
   if (grid > 0)
     k_so2_f16x3<4, 16><<<grid, THREADS, SMEM_BYTES, st>>>(A1, n_e, W1, W2, sc, tmax, edge_slot, Y, gate, att,
                                                           logits);

@@ -433,13 +433,11 @@ bool so2_tc_available(int L, int E) { return L == 4 && E == 16; }
 void so2_tc_launch(int L, int E, const uint16_t* A1, int64_t n_e, const uint16_t* W1, const uint16_t* W2,
                    uint16_t* Y, int gate, const float* att, float* logits, cudaStream_t st) {
   if (!so2_tc_available(L, E)) usage("tcgen05 SO(2) chain is instantiated for l_max 4, e_width 16");
-  static int n_sm = 0;
-  if (!n_sm) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     ESG_CUDA(cudaFuncSetAttribute(k_so2_tc<4, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    int dev = 0;
-    ESG_CUDA(cudaGetDevice(&dev));
-    ESG_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  }
+  });
+  const int n_sm = sm_count();
   const int64_t tiles = (n_e + TILE_M - 1) / TILE_M;
   const int grid = (int)(tiles < n_sm ? tiles : n_sm);
   if (grid > 0)

@@ -332,18 +332,12 @@ void tf32_pack(const float* params, int L, int E, int li, bool dx, const int64_t
 
 void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t* img, const TcTile* tiles,
                       int n_tiles, float* C, int64_t ldc, cudaStream_t st, int gate_c2) {
-  static bool init = false;
-  if (!init) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
     ESG_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    init = true;
-  }
+  });
   if (n_rows <= 0) return;
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    ESG_CUDA(cudaGetDevice(&dev));
-    ESG_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  }
+  const int n_sm = sm_count();
   const int64_t items = (n_rows + TM - 1) / TM * n_tiles;
   const int grid = (int)(items < n_sm ? items : n_sm);
   if (gate_c2 && (32 % gate_c2 != 0 || gate_c2 % 4 != 0)) usage("fused gate needs 2E dividing 32");

@@ -41,6 +41,8 @@ struct OuterTile {
 };
 
 struct TrainState {
+  float* adam_g = nullptr;  // device Adam: this step's gradients
+  int64_t adam_g_n = 0;
   // loss targets in head space, view order (network.h:187-214)
   float* node_target = nullptr;
   uint8_t* node_mask = nullptr;
@@ -539,7 +541,8 @@ void train_free(DeviceModel* D) {
                   (void*)T->Hh, (void*)T->Gg, (void*)T->Yy, (void*)T->msg, (void*)T->gY, (void*)T->gG, (void*)T->gH,
                   (void*)T->gA1, (void*)T->gx, (void*)T->gacc, (void*)T->part, (void*)T->plane_ptr,
                   (void*)T->plane_out, (void*)T->out_plane, (void*)T->out_key, (void*)T->rbf_scratch,
-                  (void*)T->halo_send, (void*)T->halo_recv, (void*)T->tiles1, (void*)T->tiles2, (void*)T->opart})
+                  (void*)T->halo_send, (void*)T->halo_recv, (void*)T->tiles1, (void*)T->tiles2, (void*)T->opart,
+                  (void*)T->adam_g})
     free_ptr(p);
   for (auto* v : {&T->src_perm, &T->src_off, &T->src_row_u})
     for (int* p : *v) free_ptr(p);
@@ -1134,4 +1137,60 @@ void model_train_timing(const esg_model* M, double* fwd_ms, double* bwd_ms) {
   *bwd_ms = T ? T->last_backward_ms : 0.0;
 }
 
+}  // namespace esg
+
+namespace esg {
+namespace {
+// Optimizer::step (optimizer.h:42-59) per parameter, moments in fp64, the
+// host expression order with explicit round-to-nearest operations (no FMA
+// contraction), so the new parameters equal the host Adam's bit for bit.
+__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, double* __restrict__ m,
+                       double* __restrict__ v, int64_t n, double b1, double omb1, double b2, double omb2, double lr,
+                       double bc1, double bc2, double eps) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double gk = (double)g[k];
+  const double mk = __dadd_rn(__dmul_rn(b1, m[k]), __dmul_rn(omb1, gk));
+  const double vk = __dadd_rn(__dmul_rn(b2, v[k]), __dmul_rn(__dmul_rn(omb2, gk), gk));
+  m[k] = mk;
+  v[k] = vk;
+  const double mh = __ddiv_rn(mk, bc1), vh = __ddiv_rn(vk, bc2);
+  const double step = __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), eps));
+  p[k] = __double2float_rn(__dadd_rn((double)p[k], -step));
+}
+}  // namespace
+
+void model_repack_params(esg_model* M);  // model.cu
+
+// The Adam step on the device: gradients (host, float) in, moments stay in
+// device memory, the parameters are updated in D->params and repacked there;
+// the host copy is refreshed for the parameter hash and checkpoints.
+void model_adam_device(esg_model* M, double* d_m, double* d_v, const float* grads, double b1, double b2, double lr,
+                       double bc1, double bc2, double eps) {
+  DeviceModel* D = M->dev;
+  cudaStream_t st = M->ctx->stream;
+  const int64_t n = (int64_t)M->host_params.size();
+  TrainState* T = D->train;
+  float* g = nullptr;
+  if (T) {
+    if (T->adam_g_n < n) {
+      free_ptr(T->adam_g);
+      T->adam_g = talloc<float>(n);
+      T->adam_g_n = n;
+    }
+    g = T->adam_g;
+  } else {
+    ESG_CUDA(cudaMalloc(&g, sizeof(float) * n));
+  }
+  h2d_staged(M->ctx, g, grads, sizeof(float) * n);
+  k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(D->params, g, d_m, d_v, n, b1, 1.0 - b1, b2, 1.0 - b2, lr, bc1,
+                                                       bc2, eps);
+  ++M->ctx->launches;
+  ESG_CUDA(cudaGetLastError());
+  // the host mirror first: the embedding and head tables are packed from it
+  ESG_CUDA(cudaMemcpyAsync(M->host_params.data(), D->params, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+  ESG_CUDA(cudaStreamSynchronize(st));
+  model_repack_params(M);
+  if (!T) cudaFree(g);
+}
 }  // namespace esg

@@ -203,6 +203,35 @@ def test_forward_c2_three_layers(gpu_ctx):
         assert mx < 5e-2 and rl2 < 2e-2, (mx, rl2)
 
 
+@pytest.mark.parametrize("prec", [esg.LINEAR_FP32, esg.LINEAR_BF16])
+def test_forward_chunking_is_invisible(gpu_ctx, monkeypatch, prec):
+    """The forward runs in destination-aligned edge chunks (model.cu
+    model_prepare); every reduction is segment-local, so the chunk size must
+    not change a bit.  C2 (1.86M edges) in one chunk against ~15 chunks, and
+    a 300-atom case in 1,024-edge chunks against the oracle."""
+    s, r, layers, basis = esg.config_structure("C2")
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=layers, n_radial=32, r_cut=r, seed=1, linear_precision=prec)
+    g = esg.build_graph(gpu_ctx, s, r)
+    outs = []
+    for chunk in (None, "131072"):
+        if chunk:
+            monkeypatch.setenv("ESG_CHUNK_EDGES", chunk)
+        net = esg.Network(gpu_ctx, cfg, basis)
+        net.init_params()
+        net.prepare(g, s.species)
+        outs.append(net.forward()[:2])
+        net.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    monkeypatch.setenv("ESG_CHUNK_EDGES", "1024")
+    sm = esg.make_jittered_lattice(300, 2.2, 0.45, [72, 8, 8], 4)
+    net, (no, eo, tm), (rno, reo), _, _ = run_both(gpu_ctx, sm, 4.5, 2, esg.BASIS_HFO2, prec=prec)
+    assert net.n_edges > 4 * 1024
+    bar = (2e-4, 2e-5) if prec == esg.LINEAR_FP32 else (5e-2, 2e-2)
+    for got, want in ((no, rno), (eo, reo)):
+        mx, rl2 = err(got, want)
+        assert mx < bar[0] and rl2 < bar[1], (mx, rl2)
+
+
 def test_forward_bf16_tensor_cores(gpu_ctx):
     s, r, layers, basis = esg.config_structure("C1")
     net, (no, eo, tm), (rno, reo), _, _ = run_both(gpu_ctx, s, r, layers, basis, prec=esg.LINEAR_BF16)

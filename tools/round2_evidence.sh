@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round-2 evidence on one B200 (run through gpurun): GPU test suite, smoke,
+# the default bench line (fp32 headline), the reference arm, the ncu launch
+# list of a short bench, and full ncu captures of the two dominant fp32
+# kernels (layer-1 launches: -s 68 skips layer 0's 2 x 34 chunk launches).
+#   tools/round2_evidence.sh OUTDIR
+set -o pipefail
+OUT=${1:-gpurun_out/r02}
+mkdir -p "$OUT"
+nvidia-smi -L > "$OUT/gpu.txt"; nproc >> "$OUT/gpu.txt"; free -g >> "$OUT/gpu.txt"
+timeout 1500 python -m pytest tests -m gpu -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?"
+timeout 900 python bench.py > "$OUT/bench.log" 2>&1; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference > "$OUT/ref.log" 2>&1; echo "ref rc=$?"
+SHORT="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --cpu-seconds 0 --train-steps 0 --bf16-steps 0"
+timeout 600 $SHORT > "$OUT/plain.log" 2>&1 && \
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
+    --log-file "$OUT/launches.csv" $SHORT > "$OUT/ncu_launches.log" 2>&1; echo "launches rc=$?"
+ONE="python bench.py --steps 1 --warmup 0 --e2e-steps 0 --cpu-seconds 0 --train-steps 0 --bf16-steps 0"
+for K in so2_f16x3 "k_rotate_in<4, 16, 32"; do
+  TAG=$(echo "$K" | tr -cd 'a-z0-9_')
+  timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$K" -s 68 -c 1 \
+    -o "$OUT/prof_$TAG" -f $ONE > "$OUT/ncu_full_$TAG.log" 2>&1; echo "full $TAG rc=$?"
+done
