@@ -11,9 +11,10 @@ halos through NCCL inside libesg_b200.so (strong scaling on the same graph).
 `value` is whole-job edges/s from device time (CUDA events, max over ranks);
 `e2e` is the same metric through the public API with host buffers
 (H2D of the atom positions, graph build + prepare + forward, D2H of every
-Hamiltonian head output).  `--impl reference` times the CPU restatement of
-the reference (oracle/, all host threads) on a bounded sample of the same
-workload.
+Hamiltonian head output).  `--impl reference` times the reference's own CPU
+forward (oracle/_ref: the unmodified reference sources built by oracle/ref.mk;
+the oracle/ restatement when that was not built) on all host threads, on a
+bounded sample of the same workload.
 """
 import argparse
 import json
@@ -154,25 +155,27 @@ def tensor_peak():
 
 
 # ------------------------------------------------------------------ CPU leg
-CPU_SAMPLE_DST = 512  # destinations in the CPU sample (both arms: the same workload slice)
+CPU_SAMPLE_DST = 128  # destinations in the CPU sample (both arms: the same workload slice)
 
 
-def cpu_sample(s, r, layers, basis, k=CPU_SAMPLE_DST, threads=None, g=None, reps=1):
-    """Times the CPU restatement of the reference forward on a fixed sample of
-    the workload: all incoming edges of the first k destinations, the full
-    M-layer forward + heads in float32 (the reference's --precision single
-    path).  Returns (edges/s, threads, sample text).  g: the graph arrays (the
-    oracle builds them when None; the GPU arm passes its bit-identical
-    export to skip the CPU graph build)."""
+def cpu_sample(s, r, layers, basis, k=CPU_SAMPLE_DST, g=None, reps=1, warmup=0):
+    """Times the reference's CPU forward on a fixed sample of the workload:
+    all incoming edges of the first k destinations, the full M-layer forward
+    + heads in float32 (the reference's --precision single path), on all host
+    threads.  kind "reference": the reference's own code (oracle/_ref, its
+    Network<float>::build_forward per thread on a destination group; prepare
+    -- edge rotations and radial features -- is not timed); kind "port": the
+    CPU restatement (oracle/) when the reference was not built.  Returns
+    (edges/s, threads, sample text, kind).  g: the graph arrays (the oracle
+    builds them when None; the GPU arm passes its bit-identical export)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle as O
+    import ref as R
 
-    if threads:
-        O.set_threads(threads)
-    nthreads = O.num_threads()
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
     if g is None:
         g = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
-    om = O.Model(4, 16, layers, 32, r, 1, basis)
     deg = np.bincount(g["dst"], minlength=s.n_atoms)
     off = np.concatenate([[0], np.cumsum(deg)])
     k = min(k, s.n_atoms)
@@ -185,14 +188,25 @@ def cpu_sample(s, r, layers, basis, k=CPU_SAMPLE_DST, threads=None, g=None, reps
     pos_of[order] = np.arange(len(order))
     v = dict(n_rows=len(order), n_owned=k, row_species=s.species[order], src_row=pos_of[src].astype(np.int32),
              dst_row=g["dst"][:e1].astype(np.int32), disp=g["disp"][:e1], dist=g["dist"][:e1])
-    dts = []
-    for _ in range(reps):
+    kind = "reference" if R.available() else "port"
+    if kind == "port":
+        om = O.Model(4, 16, layers, 32, r, 1, basis)
+
+    def once():
+        if kind == "reference":
+            return R.forward_view_timed(v, basis, layers, r, threads)[1]
         t0 = time.perf_counter()
         om.forward(v, np.float32)
-        dts.append(time.perf_counter() - t0)
-    dt = float(np.median(dts))
-    return e1 / dt, nthreads, (f"all incoming edges of the first {k} destinations ({e1} edges), {layers}-layer "
-                               f"forward + heads, float32, median of {reps}")
+        return time.perf_counter() - t0
+
+    for _ in range(warmup):
+        once()
+    dt = float(np.median([once() for _ in range(max(1, reps))]))
+    what = ("the reference's Network<float>::build_forward (oracle/_ref, unmodified reference sources), "
+            f"destinations split over {threads} threads" if kind == "reference" else
+            f"the CPU restatement (oracle/), {threads} threads")
+    return e1 / dt, threads, (f"all incoming edges of the first {k} destinations ({e1} edges), {layers}-layer "
+                              f"forward + heads, float32, {what}, median of {max(1, reps)}"), kind
 
 
 def config_dict(name, atoms, edges, r, layers, world, prec):
@@ -226,14 +240,13 @@ def run_reference(args):
     g = O.build_graph(s.positions, s.cell, np.ones(3, np.uint8), r)
     # one timed sample forward per step after the warm-up ones: the same
     # destination sample as the GPU arm's cpu_baseline
-    cpu_sample(s, r, layers, basis, g=g, reps=max(1, args.warmup))
-    val, cores, sample = cpu_sample(s, r, layers, basis, g=g, reps=max(1, args.steps))
+    val, cores, sample, kind = cpu_sample(s, r, layers, basis, g=g, reps=max(1, args.steps), warmup=args.warmup)
     info = (cores, sample)
     line = {"metric": METRIC, "value": val, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic", "impl": "reference",
             "config": config_dict(args.config, s.n_atoms, len(g["src"]), r, layers, 1, "fp32"),
-            "cpu_baseline": {"value": val, "unit": "edges/s", "cores": info[0], "kind": "port", "sample": info[1]},
+            "cpu_baseline": {"value": val, "unit": "edges/s", "cores": info[0], "kind": kind, "sample": info[1]},
             "e2e": {"value": val, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -462,8 +475,8 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
-        v, cores, sample = cpu_sample(s, r, layers, basis, g=g.export())
-        cpu = {"value": v, "unit": "edges/s", "cores": cores, "kind": "port", "sample": sample}
+        v, cores, sample, kind = cpu_sample(s, r, layers, basis, g=g.export())
+        cpu = {"value": v, "unit": "edges/s", "cores": cores, "kind": kind, "sample": sample}
     line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": prec_name, "data": "synthetic",

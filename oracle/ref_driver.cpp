@@ -10,10 +10,16 @@
 // tape (network.h:98-164) and the forward output stage of
 // tools/model_run.cpp:129-156 (assemble_blocks, blocks_to_uncoupled,
 // write_blocks_file).  Every call reports errors through ref_last_error().
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "esgnn/model/block_matrix.h"
@@ -196,6 +202,122 @@ int ref_forward(int n, const double* pos, const int* species, const double* cell
       forward<float>(s, basis, cfg, node_out, edge_out, coupled_path, uncoupled_path);
     else
       forward<double>(s, basis, cfg, node_out, edge_out, coupled_path, uncoupled_path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// The reference forward timed on a view (the benchmark's CPU arm): the owned
+// destinations [0, n_owned) of the given view are split into n_threads
+// contiguous groups of about equal edge count; each thread runs the
+// reference's own Network<float>::prepare(GraphView) (network.h:98-105) and
+// build_forward (network.h:115-164) on its group's view -- owned rows the
+// group's destinations, halo rows every other source it reads, like one rank
+// of the reference's distributed run without the exchange.  Times (max over
+// threads, seconds, a barrier before each phase): secs[0] prepare, secs[1]
+// build_forward.  Edges processed: all of the view's edges.
+int ref_forward_view_timed(int n_rows, int n_owned, const int* row_species, int64_t n_edges, const int* src_row,
+                           const int* dst_row, const double* disp, const double* dist, int n_species, const int* z,
+                           const int* n_shells, const int* shells, int l_max, int e_width, int layers, int n_radial,
+                           double r_cut, uint64_t seed, int n_threads, double* secs) {
+  try {
+    model::ModelConfig cfg;
+    cfg.l_max = l_max;
+    cfg.e_width = e_width;
+    cfg.layers = layers;
+    cfg.n_radial = n_radial;
+    cfg.r_cut = r_cut;
+    cfg.seed = seed;
+    const auto basis = make_basis(n_species, z, n_shells, shells);
+    if (n_threads < 1) n_threads = 1;
+    // destination groups of about n_edges / n_threads edges (dst-sorted edges)
+    std::vector<int64_t> first(n_owned + 1, 0);
+    for (int64_t k = 0; k < n_edges; ++k) first[dst_row[k] + 1]++;
+    for (int j = 0; j < n_owned; ++j) first[j + 1] += first[j];
+    std::vector<int> cut{0};
+    for (int t = 1; t < n_threads; ++t) {
+      const int64_t want = n_edges * t / n_threads;
+      int j = cut.back();
+      while (j < n_owned && first[j] < want) ++j;
+      cut.push_back(j);
+    }
+    cut.push_back(n_owned);
+    std::vector<model::GraphView> views(n_threads);
+    for (int t = 0; t < n_threads; ++t) {
+      model::GraphView& v = views[t];
+      const int j0 = cut[t], j1 = cut[t + 1];
+      std::vector<int> row_of(n_rows, -1);
+      for (int j = j0; j < j1; ++j) {
+        row_of[j] = j - j0;
+        v.row_global.push_back(j);
+      }
+      for (int64_t k = first[j0]; k < first[j1]; ++k)
+        if (row_of[src_row[k]] < 0) {
+          row_of[src_row[k]] = (int)v.row_global.size();
+          v.row_global.push_back(src_row[k]);
+        }
+      v.n_owned = j1 - j0;
+      v.n_rows = (int)v.row_global.size();
+      for (int r : v.row_global) v.row_species.push_back(row_species[r]);
+      for (int j = j0; j < j1; ++j)
+        v.dst_ranges.push_back({(int)(first[j] - first[j0]), (int)(first[j + 1] - first[j0])});
+      for (int64_t k = first[j0]; k < first[j1]; ++k) {
+        model::ViewEdge e;
+        e.src_row = row_of[src_row[k]];
+        e.dst_row = row_of[dst_row[k]];
+        e.src_global = src_row[k];
+        e.dst_global = dst_row[k];
+        e.displacement = Eigen::Vector3d(disp[3 * k], disp[3 * k + 1], disp[3 * k + 2]);
+        e.distance = dist[k];
+        v.edges.push_back(e);
+      }
+    }
+    std::vector<double> t_prep(n_threads, 0.0), t_fwd(n_threads, 0.0);
+    std::vector<std::string> errs(n_threads);
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0, generation = 0;
+    auto barrier = [&] {
+      std::unique_lock<std::mutex> lk(mu);
+      const int gen = generation;
+      if (++arrived == n_threads) {
+        arrived = 0;
+        ++generation;
+        cv.notify_all();
+      } else {
+        cv.wait(lk, [&] { return generation != gen; });
+      }
+    };
+    auto work = [&](int t) {
+      int passed = 0;  // barriers passed: a failing thread still passes both
+      try {
+        model::Network<float> net(cfg, basis);
+        net.init_params();
+        barrier();
+        ++passed;
+        auto t0 = std::chrono::steady_clock::now();
+        const model::Prepared<float> prep = net.prepare(views[t]);
+        t_prep[t] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        barrier();
+        ++passed;
+        t0 = std::chrono::steady_clock::now();
+        model::Tape<float> tape;
+        net.build_forward(tape, prep);
+        t_fwd[t] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      } catch (const std::exception& e) {
+        errs[t] = e.what();
+        for (; passed < 2; ++passed) barrier();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < n_threads; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+    for (const auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+    secs[0] = *std::max_element(t_prep.begin(), t_prep.end());
+    secs[1] = *std::max_element(t_fwd.begin(), t_fwd.end());
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -127,3 +127,20 @@ def forward(pos, species, cell, pbc, r_cut, basis, l_max=4, e_width=16, layers=1
                           coupled_path.encode() if coupled_path else None,
                           uncoupled_path.encode() if uncoupled_path else None))
     return no, eo, g
+
+
+def forward_view_timed(view, basis, layers, r_cut, threads, l_max=4, e_width=16, n_radial=32, seed=1):
+    """The reference's Network<float>::prepare + build_forward on a view
+    (dict as oracle.serial_view / bench.cpu_sample build it), the owned
+    destinations split over `threads` threads.  Returns (prepare s, forward s),
+    each the max over threads."""
+    arrs = [np.ascontiguousarray(view["row_species"], np.int32), np.ascontiguousarray(view["src_row"], np.int32),
+            np.ascontiguousarray(view["dst_row"], np.int32), np.ascontiguousarray(view["disp"], np.float64),
+            np.ascontiguousarray(view["dist"], np.float64)]
+    bargs, keep = _basis_args(basis)
+    secs = np.zeros(2)
+    _ok(lib().ref_forward_view_timed(C.c_int(int(view["n_rows"])), C.c_int(int(view["n_owned"])), _p(arrs[0]),
+                                     C.c_int64(len(arrs[1])), _p(arrs[1]), _p(arrs[2]), _p(arrs[3]), _p(arrs[4]),
+                                     *bargs, C.c_int(l_max), C.c_int(e_width), C.c_int(layers), C.c_int(n_radial),
+                                     C.c_double(r_cut), C.c_uint64(seed), C.c_int(threads), _p(secs)))
+    return float(secs[0]), float(secs[1])

@@ -127,3 +127,18 @@ def test_output_stage_text_equals_reference(tmp_path):
     om.export_text(keys, rows, s.species, oc, ou)
     assert open(oc, "rb").read() == open(rc, "rb").read()
     assert open(ou, "rb").read() == open(ru, "rb").read()
+
+
+def test_reference_view_forward_timing_and_bench_sample():
+    """bench.py's CPU arm: the reference's own build_forward on a destination
+    sample, split over threads (ref_driver.cpp ref_forward_view_timed); the
+    sample is the same slice cpu_sample gives the GPU arm."""
+    import bench
+    s = esg.make_jittered_lattice(60, 2.2, 0.45, [72, 8, 8], 4)
+    v, cores, sample, kind = bench.cpu_sample(s, 4.0, 1, esg.BASIS_HFO2, k=12)
+    assert kind == "reference" and v > 0 and cores >= 1 and "first 12 destinations" in sample
+    g = O.build_graph(s.positions, s.cell, PBC1, 4.0)
+    view = O.serial_view(s.n_atoms, s.species, g)
+    for threads in (1, 3):
+        prep, fwd = R.forward_view_timed(view, esg.BASIS_HFO2, 1, 4.0, threads)
+        assert prep >= 0 and fwd > 0
