@@ -23,6 +23,18 @@ struct TcTile {
   int n_valid;             // output columns actually stored (<= N)
   int64_t b_off;
 };
+// one output tile of a weight-gradient product (dw_tc.cu): g channels
+// [goff, goff + nN) x x channels [xoff, xoff + nK) of an order block whose
+// expanded gradient (N x K, row-major) starts at acc_off
+struct DwTile {
+  int goff, xoff, n0, k0, nN, nK, nKp, K;  // nKp: the MMA width (multiple of 16)
+  int64_t acc_off;
+};
+int dw_tiles(int L, int E, int which, std::vector<DwTile>* tiles);
+int64_t dw_part_floats(int n_tiles, int n_split);
+void dw_tf32x3_launch(const float* g, int64_t ldg, const float* x, int64_t ldx, int64_t n_e, const DwTile* tiles,
+                      int n_tiles, int split_e, float* part, double* acc, cudaStream_t st,
+                      const float* gscale = nullptr, int gate_c2 = 0);
 int64_t tf32_tiles(int L, int E, int kind, std::vector<TcTile>* tiles);
 void tf32_pack(const float* params, int L, int E, int li, bool dx, const int64_t* off_a, const int64_t* off_b,
                uint8_t* img, cudaStream_t st);

@@ -34,12 +34,6 @@ namespace esg {
 
 std::vector<float> expanded(const esg_model* M, const std::string& base, int m, int cin, int cout);  // model.cu
 
-// one 64 x 64 output tile of a weight-gradient product (k_outer_tiled)
-struct OuterTile {
-  int m, n0, k0, N, K;  // order, tile origin, block dims
-  int64_t acc_off;      // offset of the order block in the accumulator
-};
-
 struct TrainState {
   float* adam_g = nullptr;  // device Adam: this step's gradients
   int64_t adam_g_n = 0;
@@ -73,10 +67,10 @@ struct TrainState {
   double* part = nullptr;
   int64_t part_n = 0;
   // tiled dW: tile lists of lin1 (g 2E x A1 3E) and lin2 (g E x G 2E), split partials
-  OuterTile* tiles1 = nullptr;
-  OuterTile* tiles2 = nullptr;
+  DwTile* tiles1 = nullptr;
+  DwTile* tiles2 = nullptr;
   int n_tiles1 = 0, n_tiles2 = 0;
-  double* opart = nullptr;
+  float* opart = nullptr;  // dW partial tiles (dw_tc.cu)
   int64_t opart_n = 0;
   // per head output j: its harmonic plane, and per plane the outputs (in key order)
   int* plane_ptr = nullptr;
@@ -184,82 +178,12 @@ __global__ void k_reduce_parts(const double* __restrict__ part, int n_parts, int
 // (forward and dx products: lin_kernels.cuh k_gemm_m)
 
 
-// dWexp_m[o][k] += sum_e g_m[e][o] x_m[e][k] over the chunk's edges as a
-// tiled NT GEMM: CTA (tile, split) accumulates a 64 x 64 output tile of
-// order block m over its edge split [s0, s1) -- thread (ty, tx) a 4 x 4
-// block, 16 edges per SMEM stage, fp32 fmaf in edge order within the split
-// (<= 2048 edges) -- and writes the tile to its split's partial slot;
-// k_outer_reduce then adds the splits in order in fp64.
-template <int L>
-__global__ void __launch_bounds__(256) k_outer_tiled(const float* __restrict__ g, int cg, const float* __restrict__ x,
-                                                     int cx, int64_t n_e, const OuterTile* __restrict__ tiles,
-                                                     int n_tiles, int64_t per_split, double* __restrict__ part) {
-  using G = Geo<L>;
-  constexpr int TE = 16;
-  __shared__ float sg[TE][64];
-  __shared__ float sx[TE][64];
-  const OuterTile t = tiles[blockIdx.x];
-  const int split = blockIdx.y;
-  const int64_t s0 = split * per_split, s1 = s0 + per_split < n_e ? s0 + per_split : n_e;
-  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-  const int go = G::moff(t.m) * cg + t.n0, xo = G::moff(t.m) * cx + t.k0;
-  float acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  // the next stage's 2 x 4 values are loaded into registers while this
-  // stage's outer products run (TE * 64 / 256 = 4 per thread and operand)
-  float rg[4], rx[4];
-  auto fetch = [&](int64_t e0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int u = threadIdx.x + 256 * i, e = u / 64, c = u % 64;
-      const int64_t ee = e0 + e;
-      rg[i] = (ee < s1 && t.n0 + c < t.N) ? g[ee * G::H * cg + go + c] : 0.f;
-      rx[i] = (ee < s1 && t.k0 + c < t.K) ? x[ee * G::H * cx + xo + c] : 0.f;
-    }
-  };
-  fetch(s0);
-  for (int64_t e0 = s0; e0 < s1; e0 += TE) {
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int u = threadIdx.x + 256 * i;
-      sg[u / 64][u % 64] = rg[i];
-      sx[u / 64][u % 64] = rx[i];
-    }
-    __syncthreads();
-    if (e0 + TE < s1) fetch(e0 + TE);
-#pragma unroll 4
-    for (int e = 0; e < TE; ++e) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = sg[e][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sx[e][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-  }
-  double* out = part + ((int64_t)split * n_tiles + blockIdx.x) * 4096;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) out[(ty * 4 + i) * 64 + tx * 4 + j] = acc[i][j];
-}
-__global__ void k_outer_reduce(const double* __restrict__ part, int n_tiles, int n_split,
-                               const OuterTile* __restrict__ tiles, double* __restrict__ acc) {
-  const OuterTile t = tiles[blockIdx.x];
-  for (int u = threadIdx.x; u < 4096; u += blockDim.x) {
-    const int n = t.n0 + u / 64, k = t.k0 + u % 64;
-    if (n >= t.N || k >= t.K) continue;
-    double s = 0.0;
-    for (int sp = 0; sp < n_split; ++sp) s += part[((int64_t)sp * n_tiles + blockIdx.x) * 4096 + u];
-    acc[t.acc_off + (int64_t)n * t.K + k] += s;
-  }
+// sg[e][c] = sigmoid(h[e][row 0][c]), the gate's per-edge scalars (c < c2),
+// in the forward's rounding (1 / (1 + exp(-h)))
+__global__ void k_gate_scale(const float* __restrict__ h, int64_t ldh, int c2, int64_t n_e, float* __restrict__ sg) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_e * c2) return;
+  sg[t] = 1.f / (1.f + expf(-h[(t / c2) * ldh + t % c2]));
 }
 
 // gate (kernels.h:210-226) and its backward (kernels.h:228-250); rows are
@@ -782,44 +706,33 @@ void lin(int kind, const float* in, int64_t n, const float* P, float* out, int b
     lin_launch<L, E>(kind, in, n, P, out, D->lt[kind], D->n_lt[kind], st);
 }
 
-constexpr int OUTER_SPLIT = 2048;       // edges per split of a weight-gradient tile
-constexpr int OUTER_SPLIT_MAX = 128;    // splits per tile (chunk cap 256k edges)
+constexpr int DW_SPLIT = 4096;  // edges per split of a weight-gradient tile (256 chunks of 16, dw_tc.cu)
 
+// dWexp_m += g_m^T x_m over the chunk's edges on the tensor cores (dw_tc.cu)
+// (gscale: x is the pre-gate hidden h, each channel scaled by its edge's gate)
 template <int L>
 void outer(const float* g, int cg, const float* x, int cx, int64_t n, double* acc, bool lin1, TrainState* T,
-           cudaStream_t st) {
-  if (n <= 0) return;
-  const int n_tiles = lin1 ? T->n_tiles1 : T->n_tiles2;
-  const OuterTile* tiles = lin1 ? T->tiles1 : T->tiles2;
-  const int split = (int)std::min<int64_t>(OUTER_SPLIT_MAX, (n + OUTER_SPLIT - 1) / OUTER_SPLIT);
-  const int64_t per = (n + split - 1) / split;
-  k_outer_tiled<L><<<dim3((unsigned)n_tiles, (unsigned)split), 256, 0, st>>>(g, cg, x, cx, n, tiles, n_tiles, per,
-                                                                             T->opart);
-  k_outer_reduce<<<(unsigned)n_tiles, 256, 0, st>>>(T->opart, n_tiles, split, tiles, acc);
+           cudaStream_t st, const float* gscale = nullptr) {
+  constexpr int H = (L + 1) * (L + 1);
+  dw_tf32x3_launch(g, (int64_t)H * cg, x, (int64_t)H * cx, n, lin1 ? T->tiles1 : T->tiles2,
+                   lin1 ? T->n_tiles1 : T->n_tiles2, DW_SPLIT, T->opart, acc, st, gscale, cx);
 }
 
-// tile lists of the two dW products (per order block: N x K outputs)
+// tile lists of the two dW products and their partial-tile scratch
 void outer_tiles(esg_model* M, TrainState* T) {
   const int L = M->cfg.l_max, E = M->cfg.e_width;
   for (int which = 0; which < 2; ++which) {
-    const int cg = which == 0 ? 2 * E : E, cx = which == 0 ? 3 * E : 2 * E;
-    std::vector<OuterTile> v;
-    int64_t off = 0;
-    for (int m = 0; m <= L; ++m) {
-      const int rows = m == 0 ? L + 1 : 2 * (L - m + 1), N = rows * cg, K = rows * cx;
-      for (int n0 = 0; n0 < N; n0 += 64)
-        for (int k0 = 0; k0 < K; k0 += 64) v.push_back({m, n0, k0, N, K, off});
-      off += (int64_t)N * K;
-    }
-    OuterTile*& dst = which == 0 ? T->tiles1 : T->tiles2;
+    std::vector<DwTile> v;
+    dw_tiles(L, E, which, &v);
+    DwTile*& dst = which == 0 ? T->tiles1 : T->tiles2;
     free_ptr(dst);
-    dst = talloc<OuterTile>(v.size());
-    ESG_CUDA(cudaMemcpy(dst, v.data(), sizeof(OuterTile) * v.size(), cudaMemcpyHostToDevice));
+    dst = talloc<DwTile>(v.size());
+    ESG_CUDA(cudaMemcpy(dst, v.data(), sizeof(DwTile) * v.size(), cudaMemcpyHostToDevice));
     (which == 0 ? T->n_tiles1 : T->n_tiles2) = (int)v.size();
   }
   free_ptr(T->opart);
-  T->opart_n = (int64_t)OUTER_SPLIT_MAX * std::max(T->n_tiles1, T->n_tiles2) * 4096;
-  T->opart = talloc<double>(T->opart_n);
+  T->opart_n = dw_part_floats(std::max(T->n_tiles1, T->n_tiles2), (int)((T->cap + DW_SPLIT - 1) / DW_SPLIT));
+  T->opart = talloc<float>(T->opart_n);
 }
 
 // reverse of the forward's exchange: halo-row gradients go back to their
@@ -886,10 +799,22 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     k_rotate_in<L, E, 1, float><<<t32, RI_THREADS, 0, st>>>(nodes, edges, D->src_row, D->dst_row, D->dir, e0, n, T->A1,
                                                             D->prefetch, 0);
     lin<L, E>(0, T->A1, n, D->w1t[b], T->Hh, b, D, st);
-    k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, 2 * E, n, M->cfg.gate_enabled, T->Gg);
+    // the gated hidden G: materialised only on the CUDA-core path; the tensor
+    // cores gate h on the fly in lin2's and dW2's operand loads
+    const bool gate_fused = D->tf32;
+    const int gc2 = gate_fused && M->cfg.gate_enabled ? 2 * E : 0;
+    const float* Gx = gate_fused ? T->Hh : T->Gg;
+    if (!gate_fused)
+      k_gate_fwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, 2 * E, n, M->cfg.gate_enabled, T->Gg);
+    else if (gc2)  // the gate scalars sigmoid(h[row 0]) per edge (2E floats) for dW2's operand
+      k_gate_scale<<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, (int64_t)H * 2 * E, 2 * E, n, T->Gg);
     const float* g_msg;
     if (node_block) {
-      lin<L, E>(1, T->Gg, n, D->w2t[b], T->Yy, b, D, st);
+      if (gate_fused)
+        tf32_gemm_launch(T->Hh, (int64_t)H * 2 * E, n, D->wtc[1][b], D->tct[1], D->n_tct[1], T->Yy, (int64_t)H * E, st,
+                         gc2);
+      else
+        lin<L, E>(1, T->Gg, n, D->w2t[b], T->Yy, b, D, st);
       k_rot1<L, E, 0><<<t32, 128, 0, st>>>(T->Yy, D->dir, e0, n, T->msg);
       // attention backward into gY's buffer (used as g_msg scratch)
       k_attn_bwd<H, E><<<(unsigned)(ch.second - ch.first), 128, 0, st>>>(
@@ -902,7 +827,7 @@ void block_backward(esg_model* M, int layer, bool node_block) {
     }
     k_rot1<L, E, 1><<<t32, 128, 0, st>>>(g_msg, D->dir, e0, n, T->gY);
     // lin2 adjoint
-    outer<L>(T->gY, E, T->Gg, 2 * E, n, T->gacc + T->off_lin2[b], false, T, st);
+    outer<L>(T->gY, E, Gx, 2 * E, n, T->gacc + T->off_lin2[b], false, T, st, gc2 ? T->Gg : nullptr);
     lin<L, E>(2, T->gY, n, D->w2n[b], T->gG, b, D, st);
     k_gate_bwd<H><<<(unsigned)((n * 2 * E + 255) / 256), 256, 0, st>>>(T->Hh, T->gG, 2 * E, n, M->cfg.gate_enabled,
                                                                        T->gH);

@@ -323,3 +323,28 @@ def test_async_outputs_do_not_race(gpu_ctx):
         assert np.array_equal(be.view(np.uint32), eo.view(np.uint32))
     net.close()
     g.close()
+
+
+def test_forward_c3_golden_sample(gpu_ctx):
+    """BASELINE config 3 (20,000-atom HfO2, 12.8M edges, 3 layers, seven
+    edge chunks): the fp32 heads against the float oracle's on the committed
+    sample (tests/golden/c3_heads_sample.npz, tools/make_c3_golden.py), fp32
+    bar on the sample."""
+    import os
+    gd = np.load(os.path.join(os.path.dirname(__file__), "golden", "c3_heads_sample.npz"))
+    s, r, layers, basis = esg.config_structure("C3")
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=layers, n_radial=32, r_cut=r, seed=1,
+                          linear_precision=esg.LINEAR_FP32)
+    net = esg.Network(gpu_ctx, cfg, basis)
+    net.init_params()
+    g = esg.build_graph(gpu_ctx, s, r)
+    assert g.n_edges == int(gd["n_edges"])
+    net.prepare(g, s.species)
+    no, eo, _ = net.forward()
+    got = np.concatenate([no[gd["node_index"]], eo[gd["edge_index"]]]).astype(np.float64)
+    want = np.concatenate([gd["node_heads"], gd["edge_heads"]]).astype(np.float64)
+    mx = np.abs(got - want).max() / max(float(gd["node_max"]), float(gd["edge_max"]))
+    rl2 = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert mx < 2e-4 and rl2 < 2e-5, (mx, rl2)
+    net.close()
+    g.close()

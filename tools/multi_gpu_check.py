@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--config", default="small")
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--oracle", action="store_true", help="rank 0 also checks the serial heads against the oracle")
+    ap.add_argument("--golden", action="store_true",
+                    help="C3: every rank checks its partitioned heads against tests/golden/c3_heads_sample.npz")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -50,6 +52,29 @@ def main():
     pe = plan.export()
     owned = pe["row_global"][:plan.n_owned]
     ok = tm.exchanges == 2 * layers
+    if args.golden:
+        # the committed float-oracle heads of C3 on a fixed sample
+        # (tools/make_c3_golden.py): this rank's sampled rows, fp32 bar
+        gd = np.load(os.path.join(ROOT, "tests", "golden", "c3_heads_sample.npz"))
+        assert args.config == "C3" and int(gd["n_edges"]) == g.n_edges
+        loc_n = {int(v): i for i, v in enumerate(owned)}
+        loc_e = {int(v): i for i, v in enumerate(pe["edge_index"])}
+        pairs = [(no[loc_n[int(v)]], gd["node_heads"][i]) for i, v in enumerate(gd["node_index"]) if int(v) in loc_n]
+        pairs += [(eo[loc_e[int(v)]], gd["edge_heads"][i]) for i, v in enumerate(gd["edge_index"]) if int(v) in loc_e]
+        d2 = sum(float(np.sum((a.astype(np.float64) - b) ** 2)) for a, b in pairs)
+        r2 = sum(float(np.sum(b.astype(np.float64) ** 2)) for a, b in pairs)
+        mx = max([float(np.abs(a.astype(np.float64) - b).max()) for a, b in pairs] or [0.0])
+        got = [None] * world
+        dist.all_gather_object(got, (len(pairs), d2, r2, mx))
+        if rank == 0:
+            n = sum(x[0] for x in got)
+            scale = max(float(gd["node_max"]), float(gd["edge_max"]))
+            mxr = max(x[3] for x in got) / scale
+            rl2 = (sum(x[1] for x in got) / sum(x[2] for x in got)) ** 0.5
+            passed = n == len(gd["node_index"]) + len(gd["edge_index"]) and mxr < 2e-4 and rl2 < 2e-5
+            print(f"partitioned heads vs C3 float-oracle sample ({n} rows over {world} ranks): "
+                  f"max-abs/max {mxr:.3e} rel-L2 {rl2:.3e} pass {passed}")
+            ok &= passed
     if args.config != "small":
         # large configs: every rank runs the serial forward of the same graph on
         # its own GPU and compares its slice locally (no multi-GB gathers)

@@ -9,7 +9,7 @@ mkdir -p $OUT
 nvidia-smi -L > $OUT/gpus.txt; nproc >> $OUT/gpus.txt; free -g >> $OUT/gpus.txt
 for W in 2 4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $W --master-addr 127.0.0.1 \
-    --master-port $((29500 + W)) tools/multi_gpu_check.py --config C3 > $OUT/c3_w$W.log 2>&1
+    --master-port $((29500 + W)) tools/multi_gpu_check.py --config C3 --golden > $OUT/c3_w$W.log 2>&1
   echo "c3 w$W rc=$?" >> $OUT/rc.txt
 done
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
