@@ -891,9 +891,10 @@ void run_block(esg_model* M, int layer, bool node_block) {
     ++ctx->launches;
   }
   const bool tc = D->precision == ESG_LINEAR_BF16 && so2_tc_available(L, E);
-  // fp32 linears on the tensor cores through the fp16x3 split (so2_f16x3.cu);
-  // training keeps the tf32 GEMMs (its reverse pass shares their images)
-  const bool f3 = !tc && D->f16x3 && !D->save_inputs && !D->w1f.empty();
+  // fp32 linears on the tensor cores through the fp16x3 split (so2_f16x3.cu),
+  // the training forward included (its reverse pass recomputes the block from
+  // the saved inputs with the 3xTF32 GEMMs)
+  const bool f3 = !tc && D->f16x3 && !D->w1f.empty();
   const int zero_mode = tc ? 1 : (f3 ? 2 : 0);
   if (zero_mode && D->a1_zero_mode != zero_mode) {
     // the K padding slots of a tensor-core image are never written by rotate_in

@@ -4,18 +4,22 @@
 //
 //   C[e, o] = sum_k A[e, k] B[o, k]       per order block, 128 rows per CTA
 //
-// A (activations, fp32 rows) is split on the fly into tf32 hi = rna(a) and
-// lo = rna(a - hi); B (weights) is split once at pack time into the same two
-// images.  Three tcgen05.mma kind::tf32 passes hi.hi + hi.lo + lo.hi
+// A (activations, fp32 rows) arrives by TMA (boxes of 32 columns x 128 rows,
+// SWIZZLE_128B: the K-major layout the MMA reads) and is split in place by
+// converter warps into tf32 hi = rna(a) and lo = rna(a - hi); B (weights)
+// is split once at pack time into the same two images.  Three tcgen05.mma kind::tf32 passes hi.hi + hi.lo + lo.hi
 // accumulate in one fp32 TMEM accumulator (the dropped lo.lo term and the
 // rounding of lo are ~2^-22 relative), so the result tracks an fp32 SGEMM.
 // Operands sit in SMEM as K-major SWIZZLE_128B tiles (32 tf32 per 128-byte
-// row); B chunks arrive by one bulk copy each, A chunks are converted by the
-// CTA's four warps while the previous chunk's MMAs run.  The epilogue reads
+// row); B chunks arrive by one bulk copy each, A chunks by one TMA box each,
+// and are converted while the previous chunk's MMAs run.  The epilogue reads
 // TMEM rows (one per lane) straight into the fp32 output rows.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "device_model.h"
@@ -29,10 +33,11 @@ using namespace tc;
 constexpr int TM = 128;                  // rows per tile (UMMA M, one per TMEM lane)
 constexpr int A_BYTES = TM * 128;        // one split of a 32-wide K chunk of A
 constexpr int B_MAX = 256 * 128;         // one split of a K chunk of B (N <= 256)
-// persistent warp-specialised GEMM: warps 0-3 epilogue, 4-11 A producers,
-// warp 12 MMA issuer; rings of A (3 stages) and B (2 stages)
-constexpr int EPI_WARPS = 4, PROD_WARPS = 8, MMA_WARP = EPI_WARPS + PROD_WARPS;
-constexpr int THREADS = 32 * (MMA_WARP + 1);
+// persistent warp-specialised GEMM: warps 0-3 epilogue, 4-11 A converters,
+// warp 12 MMA issuer, warp 13 loader (A by TMA, B by bulk copy); rings of A
+// (3 stages) and B (2 stages)
+constexpr int EPI_WARPS = 4, PROD_WARPS = 8, MMA_WARP = EPI_WARPS + PROD_WARPS, LOAD_WARP = MMA_WARP + 1;
+constexpr int THREADS = 32 * (LOAD_WARP + 1);
 constexpr int NA = 3, NB = 2;
 constexpr int A_STAGE = 2 * A_BYTES, B_STAGE = 2 * B_MAX;
 constexpr int SMEM_BYTES = 1024 + NA * A_STAGE + NB * B_STAGE + 256;
@@ -70,21 +75,41 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
 // C[e, c_col + o] = sum_k A[e, a_col + k] B[o, k] over work items (128-row
 // tile, tile-list entry), tile-list major so all SMs stream the same B image.
 __global__ void __launch_bounds__(THREADS, 1)
-    k_gemm_tf32x3(const float* __restrict__ A, int64_t lda, int64_t n_rows, const uint8_t* __restrict__ Bimg,
-                  const TcTile* __restrict__ tiles, int n_tiles, float* __restrict__ C, int64_t ldc, int gate_c2) {
+    k_gemm_tf32x3(const __grid_constant__ CUtensorMap tm_a, const float* __restrict__ A, int64_t lda, int64_t n_rows,
+                  const uint8_t* __restrict__ Bimg, const TcTile* __restrict__ tiles, int n_tiles, float* __restrict__ C,
+                  int64_t ldc, int gate_c2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sA = smem_u32(base), sB = sA + NA * A_STAGE;
   uint64_t* bars = (uint64_t*)(base + NA * A_STAGE + NB * B_STAGE);
   auto bar = [&](int i) { return smem_u32(&bars[i]); };
-  const int AF = 0, AE = NA, BF = 2 * NA, BE = 2 * NA + NB, CF = 2 * NA + 2 * NB, CE = CF + 2;
+  // A: landed (TMA tx), converted, free; B: landed, free; accumulators
+  const int AL = 0, AF = NA, AE = 2 * NA, BF = 3 * NA, BE = 3 * NA + NB, CF = 3 * NA + 2 * NB, CE = CF + 2;
   uint32_t* tmem_slot = (uint32_t*)(bars + CE + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < NA; ++i) {
+      mbar_init(bar(AL + i), 1);
       mbar_init(bar(AF + i), PROD_WARPS * 32);
       mbar_init(bar(AE + i), 1);
     }
@@ -109,86 +134,77 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t n_rt = (n_rows + TM - 1) / TM;
   const int64_t n_items = n_rt * n_tiles;
 
-  if (warp >= EPI_WARPS && warp < MMA_WARP) {
-    // ---- producers: A chunks split into tf32 hi/lo, B chunks by bulk copy
+  if (warp == LOAD_WARP) {
+    // ---- loader: per K chunk one TMA box of A (32 columns x 128 rows; rows
+    // past n_rows arrive as zeros) and one bulk copy of the B chunk
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      int sa = 0, sb = 0;
+      uint32_t ka = 0, kb = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const TcTile t = tiles[it / n_rt];
+        const int r0 = (int)((it % n_rt) * TM);
+        const int nc = (t.K + 31) >> 5;
+        const uint32_t bbytes = 2u * (uint32_t)t.N * 128u;
+        for (int c = 0; c < nc; ++c) {
+          mbar_wait(bar(BE + sb), ((kb / NB) & 1) ^ 1);
+          mbar_expect_tx(bar(BF + sb), bbytes);
+          bulk_g2s(sB + sb * B_STAGE, Bimg + t.b_off + (int64_t)c * bbytes, bbytes, bar(BF + sb), pol);
+          if (++sb == NB) sb = 0;
+          ++kb;
+          mbar_wait(bar(AE + sa), ((ka / NA) & 1) ^ 1);
+          mbar_expect_tx(bar(AL + sa), A_BYTES);
+          tma_2d(sA + sa * A_STAGE, &tm_a, t.a_col + 32 * c, r0, bar(AL + sa));
+          if (++sa == NA) sa = 0;
+          ++ka;
+        }
+      }
+    }
+  } else if (warp >= EPI_WARPS && warp < MMA_WARP) {
+    // ---- converters: the A box (raw fp32) split in place into tf32 hi and
+    // the lo image at the same swizzled offsets.  Columns past the block's K
+    // meet zero rows of the B image.
     const int pt = tid - EPI_WARPS * 32;  // 0..255
-    const int u = pt & 7;                 // 16-byte unit of the chunk row
-    const uint64_t pol = policy_evict_last();
-    int sa = 0, sb = 0;
-    uint32_t ka = 0, kb = 0;  // ring uses (parity source)
+    int sa = 0;
+    uint32_t ka = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const TcTile t = tiles[it / n_rt];
       const int64_t r0 = (it % n_rt) * TM;
       const int nc = (t.K + 31) >> 5;
-      const uint32_t bbytes = 2u * (uint32_t)t.N * 128u;
       // fused gate (kernels.h:210-226) of lin2's operand: column k of an order
       // block is channel k % 2E, and a thread always converts the same four
-      // columns of a chunk, so its 4 x 4 scales sigmoid(A[row][c]) (the row's
-      // first 2E values: l = 0, m = 0) are loaded once per item
+      // 16-byte units of a chunk (fixed row, fixed logical columns), so its
+      // 4 x 4 scales sigmoid(A[row][c]) (the row's first 2E values: l = 0,
+      // m = 0) are loaded once per item
       float4 gs[4];
       if (gate_c2) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int64_t row = r0 + (pt >> 3) + 32 * i;
-          const int c0 = (u * 4) % gate_c2;
+          const int u = pt + 256 * i, r = u >> 3, pos = u & 7;
+          const int64_t row = r0 + r;
+          const int c0 = (((pos ^ (r & 7)) * 4)) % gate_c2;
           float4 h = row < n_rows ? __ldg(reinterpret_cast<const float4*>(A + row * lda + c0))
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
           gs[i] = make_float4(1.f / (1.f + expf(-h.x)), 1.f / (1.f + expf(-h.y)), 1.f / (1.f + expf(-h.z)),
                               1.f / (1.f + expf(-h.w)));
         }
       }
-      auto load = [&](int c, float4* v) {
-        const int k = c * 32 + u * 4;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int64_t row = r0 + (pt >> 3) + 32 * i;
-          v[i] = (c < nc && row < n_rows && k < t.K)
-                     ? __ldg(reinterpret_cast<const float4*>(A + row * lda + t.a_col + k))
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (gate_c2)
-            v[i] = make_float4(v[i].x * gs[i].x, v[i].y * gs[i].y, v[i].z * gs[i].z, v[i].w * gs[i].w);
-        }
-      };
-      // one chunk: its B bulk copy, then its A rows (loaded a chunk earlier)
-      // split into the ring
-      auto chunk = [&](int c, const float4* v) {
-        if (pt == 0) {
-          mbar_wait(bar(BE + sb), ((kb / NB) & 1) ^ 1);
-          mbar_expect_tx(bar(BF + sb), bbytes);
-          bulk_g2s(sB + sb * B_STAGE, Bimg + t.b_off + (int64_t)c * bbytes, bbytes, bar(BF + sb), pol);
-        }
-        if (++sb == NB) sb = 0;
-        ++kb;
-        mbar_wait(bar(AE + sa), ((ka / NA) & 1) ^ 1);
+      for (int c = 0; c < nc; ++c) {
+        mbar_wait(bar(AL + sa), (ka / NA) & 1);
         const uint32_t sh = sA + sa * A_STAGE, sl = sh + A_BYTES;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int r = (pt >> 3) + 32 * i;
-          const float4 h = make_float4(to_tf32(v[i].x), to_tf32(v[i].y), to_tf32(v[i].z), to_tf32(v[i].w));
-          const float4 l = make_float4(to_tf32(v[i].x - h.x), to_tf32(v[i].y - h.y), to_tf32(v[i].z - h.z),
-                                       to_tf32(v[i].w - h.w));
-          const uint32_t o = sw128(r, u);
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sh + o), "f"(h.x), "f"(h.y), "f"(h.z),
-                       "f"(h.w)
-                       : "memory");
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(sl + o), "f"(l.x), "f"(l.y), "f"(l.z),
-                       "f"(l.w)
-                       : "memory");
+          const uint32_t o = (uint32_t)(pt + 256 * i) * 16u;
+          float4 v = lds4(sh + o);
+          if (gate_c2) v = make_float4(v.x * gs[i].x, v.y * gs[i].y, v.z * gs[i].z, v.w * gs[i].w);
+          const float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+          sts4(sh + o, h);
+          sts4(sl + o, make_float4(to_tf32(v.x - h.x), to_tf32(v.y - h.y), to_tf32(v.z - h.z), to_tf32(v.w - h.w)));
         }
         fence_async_smem();
         mbar_arrive(bar(AF + sa));
         if (++sa == NA) sa = 0;
         ++ka;
-      };
-      float4 va[4], vb[4];  // two register buffers: chunk c + 1 loads while chunk c converts
-      load(0, va);
-      for (int c = 0; c < nc; c += 2) {
-        load(c + 1, vb);
-        chunk(c, va);
-        if (c + 1 < nc) {
-          load(c + 2, va);
-          chunk(c + 1, vb);
-        }
       }
     }
   } else if (warp == MMA_WARP) {
@@ -337,11 +353,26 @@ void tf32_gemm_launch(const float* A, int64_t lda, int64_t n_rows, const uint8_t
     ESG_CUDA(cudaFuncSetAttribute(k_gemm_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
   });
   if (n_rows <= 0) return;
+  if (gate_c2 && (32 % gate_c2 != 0 || gate_c2 % 4 != 0)) usage("fused gate needs 2E dividing 32");
+  // A as TMA sees it: n_rows rows of lda floats, boxes of 32 columns x 128 rows, SWIZZLE_128B
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    ESG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !encode) usage("cuTensorMapEncodeTiled unavailable");
+  }
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)lda, (cuuint64_t)n_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
+  const cuuint32_t box[2] = {32, (cuuint32_t)TM}, es[2] = {1, 1};
+  const CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) usage("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   const int n_sm = sm_count();
   const int64_t items = (n_rows + TM - 1) / TM * n_tiles;
   const int grid = (int)(items < n_sm ? items : n_sm);
-  if (gate_c2 && (32 % gate_c2 != 0 || gate_c2 % 4 != 0)) usage("fused gate needs 2E dividing 32");
-  k_gemm_tf32x3<<<grid, THREADS, SMEM_BYTES, st>>>(A, lda, n_rows, img, tiles, n_tiles, C, ldc, gate_c2);
+  k_gemm_tf32x3<<<grid, THREADS, SMEM_BYTES, st>>>(tm, A, lda, n_rows, img, tiles, n_tiles, C, ldc, gate_c2);
   ESG_CUDA(cudaGetLastError());
 }
 

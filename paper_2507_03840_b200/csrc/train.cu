@@ -148,22 +148,48 @@ __global__ void k_heads_bwd_x(const float* __restrict__ g_out, int out_len, int6
   }
   g_x[t] = acc;
 }
-// S[j][c] = sum_i g_out[i][j] x[i][plane(j)][c]: CTA partials over item ranges
+// S[j][c] = sum_i g_out[i][j] x[i][plane(j)][c]: CTA partials over item
+// ranges.  Tiles of TI items go through SMEM (their head gradients and
+// feature rows, coalesced), then thread u = (j, c) pairs accumulate over the
+// tile in item order (fp64: the same sum and order as one item at a time).
 template <int H, int E>
-__global__ void k_heads_bwd_w(const float* __restrict__ g_out, int out_len, int64_t n_items,
-                              const float* __restrict__ x, const int* __restrict__ out_plane,
-                              double* __restrict__ part) {
+__global__ void __launch_bounds__(256) k_heads_bwd_w(const float* __restrict__ g_out, int out_len, int64_t n_items,
+                                                     const float* __restrict__ x, const int* __restrict__ out_plane,
+                                                     double* __restrict__ part) {
+  constexpr int TI = 16, UMAX = 16;  // out_len * E <= 256 * UMAX
+  __shared__ float s_g[TI * 256];
+  __shared__ float s_x[TI * H * E];
   const int64_t per = (n_items + gridDim.x - 1) / gridDim.x;
   const int64_t i0 = blockIdx.x * per, i1 = i0 + per < n_items ? i0 + per : n_items;
-  for (int u = threadIdx.x; u < out_len * E; u += blockDim.x) {
-    const int j = u / E, c = u % E, p = out_plane[j];
-    double acc = 0.0;
-    for (int64_t i = i0; i < i1; ++i) {
-      const float up = g_out[i * out_len + j];
-      if (up != 0.f) acc += double(up) * double(x[(i * H + p) * E + c]);
-    }
-    part[(int64_t)blockIdx.x * out_len * E + u] = acc;
+  const int nu = out_len * E;
+  double acc[UMAX];
+  int off_x[UMAX], off_g[UMAX];
+#pragma unroll
+  for (int q = 0; q < UMAX; ++q) {
+    acc[q] = 0.0;
+    const int u = threadIdx.x + 256 * q, j = u / E, c = u % E;
+    off_g[q] = u < nu ? j : 0;
+    off_x[q] = u < nu ? out_plane[j] * E + c : 0;
   }
+  for (int64_t t0 = i0; t0 < i1; t0 += TI) {
+    const int ni = (int)(i1 - t0 < TI ? i1 - t0 : TI);
+    __syncthreads();
+    for (int v = threadIdx.x; v < ni * out_len; v += blockDim.x) s_g[(v / out_len) * 256 + v % out_len] = g_out[t0 * out_len + v];
+    for (int v = threadIdx.x; v < ni * H * E; v += blockDim.x) s_x[v] = x[t0 * H * E + v];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < UMAX; ++q) {
+      if (threadIdx.x + 256 * q < nu) {
+        for (int ii = 0; ii < ni; ++ii) {
+          const float up = s_g[ii * 256 + off_g[q]];
+          if (up != 0.f) acc[q] += double(up) * double(s_x[ii * H * E + off_x[q]]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < UMAX; ++q)
+    if (threadIdx.x + 256 * q < nu) part[(int64_t)blockIdx.x * nu + threadIdx.x + 256 * q] = acc[q];
 }
 // out[u] += sum over the parts in order
 __global__ void k_reduce_parts(const double* __restrict__ part, int n_parts, int64_t n, double* __restrict__ out) {
@@ -433,22 +459,46 @@ __global__ void k_add_rows(const float* __restrict__ src, const int* __restrict_
 // lift backward (ops.h:52-60): S[c][g] = sum_e g_edges[e][0][c] rbf[e][g],
 // CTA partials over edge ranges (fp64), radial features as the forward
 template <int H, int E>
-__global__ void k_lift_bwd(const float* __restrict__ g_edges, const double* __restrict__ dist, int64_t n_e, int ng,
-                           double spacing, double* __restrict__ part) {
+__global__ void __launch_bounds__(256) k_lift_bwd(const float* __restrict__ g_edges, const double* __restrict__ dist,
+                                                  int64_t n_e, int ng, double spacing, double* __restrict__ part) {
+  // tiles of 64 edges: the Gaussians rbf[k][g] (fp64 exp rounded to float,
+  // as the forward lift) once per tile into SMEM, then thread (c, g) pairs
+  // accumulate up * rbf over the tile in edge order (fp64)
+  constexpr int TK = 64;
+  __shared__ float s_rbf[TK * 32];
+  __shared__ float s_up[TK * E];
   const int64_t per = (n_e + gridDim.x - 1) / gridDim.x;
   const int64_t k0 = blockIdx.x * per, k1 = k0 + per < n_e ? k0 + per : n_e;
-  for (int u = threadIdx.x; u < E * ng; u += blockDim.x) {
-    const int c = u / ng, g = u % ng;
-    double acc = 0.0;
-    const double inv_den = 2.0 * spacing * spacing;
-    for (int64_t k = k0; k < k1; ++k) {
-      const float up = g_edges[k * H * E + c];
-      if (up == 0.f) continue;
-      const double d = dist[k] - g * spacing;
-      const float rbf = (float)exp(-d * d / inv_den);
-      acc += double(up) * double(rbf);
+  const double inv_den = 2.0 * spacing * spacing;
+  double acc[(E * 32 + 255) / 256];
+#pragma unroll
+  for (int i = 0; i < (E * 32 + 255) / 256; ++i) acc[i] = 0.0;
+  for (int64_t t0 = k0; t0 < k1; t0 += TK) {
+    const int nk = (int)(k1 - t0 < TK ? k1 - t0 : TK);
+    __syncthreads();
+    for (int v = threadIdx.x; v < nk * ng; v += blockDim.x) {
+      const int kk = v / ng, g = v % ng;
+      const double d = dist[t0 + kk] - g * spacing;
+      s_rbf[kk * 32 + g] = (float)exp(-d * d / inv_den);
     }
-    part[(int64_t)blockIdx.x * E * ng + u] = acc;
+    for (int v = threadIdx.x; v < nk * E; v += blockDim.x) s_up[v] = g_edges[(t0 + v / E) * H * E + v % E];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < (E * 32 + 255) / 256; ++i) {
+      const int u = threadIdx.x + 256 * i;
+      if (u < E * ng) {
+        const int c = u / ng, g = u % ng;
+        for (int kk = 0; kk < nk; ++kk) {
+          const float up = s_up[kk * E + c];
+          if (up != 0.f) acc[i] += double(up) * double(s_rbf[kk * 32 + g]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < (E * 32 + 255) / 256; ++i) {
+    const int u = threadIdx.x + 256 * i;
+    if (u < E * ng) part[(int64_t)blockIdx.x * E * ng + u] = acc[i];
   }
 }
 
