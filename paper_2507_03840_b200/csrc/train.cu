@@ -756,7 +756,19 @@ void lin(int kind, const float* in, int64_t n, const float* P, float* out, int b
     lin_launch<L, E>(kind, in, n, P, out, D->lt[kind], D->n_lt[kind], st);
 }
 
-constexpr int DW_SPLIT = 4096;  // edges per split of a weight-gradient tile (256 chunks of 16, dw_tc.cu)
+// edges per split of a weight-gradient tile (dw_tc.cu).  The tensor cores'
+// fp32 accumulation is biased: the dW error grows linearly with the number
+// of MMAs accumulated (measured on the smoke problem: gradient rel-L2 4.6e-6
+// at 256 edges per split, 6.5e-6 at 512, 1.0e-5 at 1,024, 2.6e-5 at 4,096),
+// so the splits stay short and are added in fp64 (ESG_DW_SPLIT overrides)
+int dw_split() {
+  static const int v = [] {
+    const char* e = std::getenv("ESG_DW_SPLIT");
+    const int x = e ? std::atoi(e) : 512;
+    return x >= 16 ? x / 16 * 16 : 16;
+  }();
+  return v;
+}
 
 // dWexp_m += g_m^T x_m over the chunk's edges on the tensor cores (dw_tc.cu)
 // (gscale: x is the pre-gate hidden h, each channel scaled by its edge's gate)
@@ -765,7 +777,7 @@ void outer(const float* g, int cg, const float* x, int cx, int64_t n, double* ac
            cudaStream_t st, const float* gscale = nullptr) {
   constexpr int H = (L + 1) * (L + 1);
   dw_tf32x3_launch(g, (int64_t)H * cg, x, (int64_t)H * cx, n, lin1 ? T->tiles1 : T->tiles2,
-                   lin1 ? T->n_tiles1 : T->n_tiles2, DW_SPLIT, T->opart, acc, st, gscale, cx);
+                   lin1 ? T->n_tiles1 : T->n_tiles2, dw_split(), T->opart, acc, st, gscale, cx);
 }
 
 // tile lists of the two dW products and their partial-tile scratch
@@ -781,7 +793,7 @@ void outer_tiles(esg_model* M, TrainState* T) {
     (which == 0 ? T->n_tiles1 : T->n_tiles2) = (int)v.size();
   }
   free_ptr(T->opart);
-  T->opart_n = dw_part_floats(std::max(T->n_tiles1, T->n_tiles2), (int)((T->cap + DW_SPLIT - 1) / DW_SPLIT));
+  T->opart_n = dw_part_floats(std::max(T->n_tiles1, T->n_tiles2), (int)((T->cap + dw_split() - 1) / dw_split()));
   T->opart = talloc<float>(T->opart_n);
 }
 

@@ -28,7 +28,7 @@ int main(int argc, char** argv) {
   float *dg, *dx, *part;
   double* dacc;
   esg::DwTile* dt;
-  const int split = 4096;
+  const int split = getenv("ESG_DW_SPLIT") ? atoi(getenv("ESG_DW_SPLIT")) : 512;
   const int ns = (int)((n + split - 1) / split);
   cudaMalloc(&dg, g.size() * 4);
   cudaMalloc(&dx, x.size() * 4);

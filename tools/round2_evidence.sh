@@ -22,3 +22,10 @@ for K in so2_f16x3 "k_rotate_in<4, 16, 32"; do
   timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$K" -s 68 -c 1 \
     -o "$OUT/prof_$TAG" -f $ONE > "$OUT/ncu_full_$TAG.log" 2>&1; echo "full $TAG rc=$?"
 done
+# training step (C2): launch list of one step after a warm-up one
+timeout 600 python tools/train_profile.py --steps 3 > "$OUT/train.log" 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file "$OUT/train_launches.csv" python tools/train_profile.py --steps 1 > "$OUT/ncu_train.log" 2>&1
+echo "train rc=$?"
+# chunking invariance and the tf32 cross-check at C3
+timeout 600 python tools/f3_chunk_check.py --config C3 > "$OUT/chunk_c3.log" 2>&1; echo "chunk rc=$?"
