@@ -135,28 +135,32 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t n_items = n_rt * n_tiles;
 
   if (warp == LOAD_WARP) {
-    // ---- loader: per K chunk one TMA box of A (32 columns x 128 rows; rows
-    // past n_rows arrive as zeros) and one bulk copy of the B chunk
-    if (lane == 0) {
+    // ---- loader: lane 0 streams A (per K chunk one TMA box of 32 columns x
+    // 128 rows; rows past n_rows arrive as zeros), lane 1 streams B (one bulk
+    // copy per chunk), each at its own ring's pace
+    if (lane < 2) {
+      const bool is_a = lane == 0;
       const uint64_t pol = policy_evict_last();
-      int sa = 0, sb = 0;
-      uint32_t ka = 0, kb = 0;
+      int s = 0;
+      uint32_t k = 0;
+      const int ns = is_a ? NA : NB;
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const TcTile t = tiles[it / n_rt];
         const int r0 = (int)((it % n_rt) * TM);
         const int nc = (t.K + 31) >> 5;
         const uint32_t bbytes = 2u * (uint32_t)t.N * 128u;
         for (int c = 0; c < nc; ++c) {
-          mbar_wait(bar(BE + sb), ((kb / NB) & 1) ^ 1);
-          mbar_expect_tx(bar(BF + sb), bbytes);
-          bulk_g2s(sB + sb * B_STAGE, Bimg + t.b_off + (int64_t)c * bbytes, bbytes, bar(BF + sb), pol);
-          if (++sb == NB) sb = 0;
-          ++kb;
-          mbar_wait(bar(AE + sa), ((ka / NA) & 1) ^ 1);
-          mbar_expect_tx(bar(AL + sa), A_BYTES);
-          tma_2d(sA + sa * A_STAGE, &tm_a, t.a_col + 32 * c, r0, bar(AL + sa));
-          if (++sa == NA) sa = 0;
-          ++ka;
+          if (is_a) {
+            mbar_wait(bar(AE + s), ((k / NA) & 1) ^ 1);
+            mbar_expect_tx(bar(AL + s), A_BYTES);
+            tma_2d(sA + s * A_STAGE, &tm_a, t.a_col + 32 * c, r0, bar(AL + s));
+          } else {
+            mbar_wait(bar(BE + s), ((k / NB) & 1) ^ 1);
+            mbar_expect_tx(bar(BF + s), bbytes);
+            bulk_g2s(sB + s * B_STAGE, Bimg + t.b_off + (int64_t)c * bbytes, bbytes, bar(BF + s), pol);
+          }
+          if (++s == ns) s = 0;
+          ++k;
         }
       }
     }

@@ -940,7 +940,7 @@ void loss_grad_impl(esg_model* M, int64_t n_total, double partials[3], double* l
   double sums[3] = {0, 0, 0};
   auto loss_part = [&](const float* pred, const float* tgt, const uint8_t* mask, int64_t n, float* g_out) {
     if (n <= 0) return;
-    const int blocks = 148;
+    const int blocks = sm_count() * 8;  // latency-bound: 8 CTAs per SM; partials summed on the host in block order
     k_loss<<<blocks, 256, 0, st>>>(pred, tgt, mask, n, inv_total, g_out, T->part);
     std::vector<double> h(blocks * 3);
     ESG_CUDA(cudaMemcpyAsync(h.data(), T->part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
