@@ -1,6 +1,7 @@
 // dw_probe.cu -- checks the tensor-core weight-gradient kernel (dw_tc.cu)
 // against a host fp64 sum on random rows: per tile max |err| / max |ref|.
-//   sh tools/build_dw_probe.sh && tools/bin/dw_probe [n_edges] [which] [probe mode] [timing only]
+//   sh tools/build_dw_probe.sh && tools/bin/dw_probe [n_edges] [which: 0 lin1, 1 lin2] [unused] [timing only]
+//   (ESG_DW_SPLIT sets the edge split, default 512)
 #include <cuda_runtime.h>
 
 #include <cmath>

@@ -17,10 +17,12 @@ timeout 600 $SHORT > "$OUT/plain.log" 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
     --log-file "$OUT/launches.csv" $SHORT > "$OUT/ncu_launches.log" 2>&1; echo "launches rc=$?"
 ONE="python bench.py --steps 1 --warmup 0 --e2e-steps 0 --cpu-seconds 0 --train-steps 0 --bf16-steps 0"
-for K in so2_f16x3 "k_rotate_in<4, 16, 32"; do
-  TAG=$(echo "$K" | tr -cd 'a-z0-9_')
-  timeout 1200 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$K" -s 68 -c 1 \
-    -o "$OUT/prof_$TAG" -f $ONE > "$OUT/ncu_full_$TAG.log" 2>&1; echo "full $TAG rc=$?"
+# layer-1 launches: -s skips layer 0's launches of the kernel (2 x 34 chunk
+# launches for rotate_in / the chain, 34 for the node update)
+for KS in "so2_f16x3 68" "k_rotate_in 68" "k_node_update 34"; do
+  set -- $KS
+  timeout 1200 ncu --set full --import-source on --clock-control none -k "regex:$1" -s $2 -c 1 \
+    -o "$OUT/prof_$1" -f $ONE > "$OUT/ncu_full_$1.log" 2>&1; echo "full $1 rc=$?"
 done
 # training step (C2): launch list of one step after a warm-up one
 timeout 600 python tools/train_profile.py --steps 3 > "$OUT/train.log" 2>&1 && \
