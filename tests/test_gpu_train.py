@@ -62,6 +62,21 @@ def test_loss_and_gradients_match_oracle(gpu_ctx, L, E):
             assert rel(a, b) <= 1e-4, (name, rel(a, b))
 
 
+def test_gradients_many_splits_and_chunks(gpu_ctx, monkeypatch):
+    """A graph of ~6k edges: the tensor-core weight gradients run over a dozen
+    512-edge splits (dw_tc.cu, fp64 split sum) and the training forward over
+    several 1,024-edge chunks -- same bars as the small problem."""
+    monkeypatch.setenv("ESG_CHUNK_EDGES", "1024")
+    net, om, view, t32, t64, n_total, g = problem(gpu_ctx, 4, 16, n=240, r_cut=4.5, seed=7)
+    assert len(view["src_row"]) > 12 * 512
+    loss, partials, grads = net.loss_grad(n_total)
+    (sa, sq, cnt), ref = O.loss_grad(om, view, t64, n_total, np.float64)
+    assert abs(loss - (sa + sq) / n_total) <= 1e-5 * abs(loss)
+    r = rel(grads, ref)
+    mx = float(np.abs(grads.astype(np.float64) - ref).max() / np.abs(ref).max())
+    assert r <= 1e-5 and mx <= 1e-4, (r, mx)
+
+
 def test_gradients_deterministic(gpu_ctx):
     net, *_, n_total, g = problem(gpu_ctx, 4, 16)
     l1, _, g1 = net.loss_grad(n_total)
