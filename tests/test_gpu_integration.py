@@ -47,3 +47,14 @@ def test_patched_forward_rank(tmp_path, case):
         k2, sh2, o2, v2 = esg.read_blocks_text(theirs)
         assert np.array_equal(k1, k2) and np.array_equal(sh1, sh2), mine
         assert np.abs(v1 - v2).max() <= 2e-4 * np.abs(v2).max(), mine
+
+
+DEMO = os.path.join(R.ROOT, "paper_2507_03840_b200", "facade_demo")
+
+
+@pytest.mark.skipif(not os.path.exists(DEMO), reason="facade_demo not built")
+def test_facade_demo_runs_on_gpu():
+    """The façade's own demo (csrc/facade_demo.cpp): model_run.cpp's
+    forward_rank call sequence written against esgnn_b200.hpp, on the GPU."""
+    out = subprocess.run([DEMO], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr

@@ -143,3 +143,17 @@ def test_acceptance_counts():
     assert cell.n_atoms == 3000 and int((cell.species == 72).sum()) == 1000
     assert esg.tile(cell, (2, 2, 2)).n_atoms == 24000
     assert 3 * 25 * 16 * 4 == 4800
+
+
+def test_facade_demo_host_only():
+    """csrc/facade_demo.cpp through esgnn_b200.hpp without a GPU: parameter
+    store, coupling tables and the error mapping (UsageError)."""
+    import os
+    import subprocess
+    demo = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2507_03840_b200",
+                        "facade_demo")
+    if not os.path.exists(demo):
+        pytest.skip("facade_demo not built")
+    out = subprocess.run([demo, "--host-only"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "usage error mapped" in out.stdout and "out_len 160" in out.stdout
