@@ -330,12 +330,21 @@ __global__ void __launch_bounds__(384) k_rot_in_bwd(const float* __restrict__ gA
 // g_nodes[dst] += its segment's dst-part rows in edge order (owned rows j0..j1)
 __global__ void k_dst_reduce(const float* __restrict__ gx, int row, const int64_t* __restrict__ seg, int j0,
                              int64_t e0, float* __restrict__ g_nodes) {
+  // float4 columns; the adds stay in edge order (the loads run ahead)
   const int j = j0 + blockIdx.x;
   const int64_t b = seg[j], en = seg[j + 1];
-  for (int t = threadIdx.x; t < row; t += blockDim.x) {
-    float acc = g_nodes[(int64_t)j * row + t];
-    for (int64_t k = b; k < en; ++k) acc += gx[((k - e0) * 2 + 1) * row + t];
-    g_nodes[(int64_t)j * row + t] = acc;
+  const int r4 = row >> 2;
+  for (int t = threadIdx.x; t < r4; t += blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(g_nodes + (int64_t)j * row)[t];
+#pragma unroll 8
+    for (int64_t k = b; k < en; ++k) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(gx + ((k - e0) * 2 + 1) * row) + t);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(g_nodes + (int64_t)j * row)[t] = acc;
   }
 }
 // g_nodes[src] += the src-part rows of its chunk edges in edge order
@@ -343,10 +352,18 @@ __global__ void k_src_reduce(const float* __restrict__ gx, int row, const int* _
                              const int* __restrict__ off, const int* __restrict__ rows, float* __restrict__ g_nodes) {
   const int u = blockIdx.x;
   const int i = rows[u];
-  for (int t = threadIdx.x; t < row; t += blockDim.x) {
-    float acc = g_nodes[(int64_t)i * row + t];
-    for (int q = off[u]; q < off[u + 1]; ++q) acc += gx[((int64_t)perm[q] * 2 + 0) * row + t];
-    g_nodes[(int64_t)i * row + t] = acc;
+  const int r4 = row >> 2;
+  for (int t = threadIdx.x; t < r4; t += blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(g_nodes + (int64_t)i * row)[t];
+#pragma unroll 8
+    for (int q = off[u]; q < off[u + 1]; ++q) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(gx + ((int64_t)perm[q] * 2 + 0) * row) + t);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(g_nodes + (int64_t)i * row)[t] = acc;
   }
 }
 
