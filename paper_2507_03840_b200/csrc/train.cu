@@ -136,17 +136,26 @@ __global__ void k_heads_bwd_x(const float* __restrict__ g_out, int out_len, int6
                               const float* __restrict__ W, const int* __restrict__ plane_ptr,
                               const int* __restrict__ plane_out, const int* __restrict__ out_key,
                               float* __restrict__ g_x) {
+  // thread = (item, plane, 4-channel quad); the same per-channel sum order
+  constexpr int Q = E / 4;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_items * H * E) return;
-  const int64_t i = t / (H * E);
-  const int p = (int)(t % (H * E)) / E, c = (int)(t % E);
-  float acc = g_x[t];
-  for (int q = plane_ptr[p]; q < plane_ptr[p + 1]; ++q) {
-    const int j = plane_out[q];
+  if (t >= n_items * H * Q) return;
+  const int64_t i = t / (H * Q);
+  const int p = (int)(t % (H * Q)) / Q, q = (int)(t % Q);
+  float4* gx4 = reinterpret_cast<float4*>(g_x) + t;
+  float4 acc = *gx4;
+  for (int r = plane_ptr[p]; r < plane_ptr[p + 1]; ++r) {
+    const int j = plane_out[r];
     const float up = g_out[i * out_len + j];
-    if (up != 0.f) acc += up * W[out_key[j] * E + c];
+    if (up != 0.f) {
+      const float4 w = __ldg(reinterpret_cast<const float4*>(W + out_key[j] * E) + q);
+      acc.x += up * w.x;
+      acc.y += up * w.y;
+      acc.z += up * w.z;
+      acc.w += up * w.w;
+    }
   }
-  g_x[t] = acc;
+  *gx4 = acc;
 }
 // S[j][c] = sum_i g_out[i][j] x[i][plane(j)][c]: CTA partials over item
 // ranges.  Tiles of TI items go through SMEM (their head gradients and
@@ -976,7 +985,7 @@ void loss_grad_impl(esg_model* M, int64_t n_total, double partials[3], double* l
   // heads backward (final tables are D->nodes / D->edges)
   auto heads_bwd = [&](int set, const float* x, int64_t n_items, const float* g_out, float* g_x) {
     if (n_items <= 0) return;
-    k_heads_bwd_x<H, E><<<(unsigned)((n_items * HE + 255) / 256), 256, 0, st>>>(
+    k_heads_bwd_x<H, E><<<(unsigned)((n_items * HE / 4 + 255) / 256), 256, 0, st>>>(
         g_out, ol, n_items, D->head_w[set], T->plane_ptr, T->plane_out, T->out_key, g_x);
     const int parts = (int)std::min<int64_t>(296, n_items);
     k_heads_bwd_w<H, E><<<parts, 256, 0, st>>>(g_out, ol, n_items, x, T->out_plane, T->part);
