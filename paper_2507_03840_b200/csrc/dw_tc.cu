@@ -15,10 +15,10 @@
 // tcgen05.mma kind::tf32 passes (hi.hi + hi.lo + lo.hi) accumulate a
 // 128 x N tile in TMEM (fp32), as tf32_gemm.cu does for the forward.
 //
-// Determinism: work item = (output tile, edge split of DW_SPLIT edges); the
-// split's sum is accumulated in a fixed chunk / instruction order, written
-// to its partial slot, and k_dw_reduce adds the splits in split order in
-// fp64 into the gradient accumulator -- the same bits every run.
+// Determinism: work item = (output tile, edge split); the split's sum is
+// accumulated in a fixed chunk / instruction order, written to its partial
+// slot, and k_dw_reduce adds the splits in a fixed order in fp64 into the
+// gradient accumulator -- the same bits every run.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -289,19 +289,32 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-// the splits of each tile in split order, fp64, into the accumulator: one
-// thread per output element (grid: tiles x element blocks), the split loop
-// reading consecutive columns across the warp
-__global__ void k_dw_reduce(const float* __restrict__ part, const DwTile* __restrict__ tiles, int n_tiles, int n_split,
-                            double* __restrict__ acc) {
+// the splits of each tile into the accumulator, fp64, in a fixed order: a
+// block takes 32 output elements of one tile; its 8 warps-worth of split
+// groups (lane = element, group = warp) each sum a contiguous run of splits
+// in split order, and the 8 group sums are added in group order
+__global__ void __launch_bounds__(256) k_dw_reduce(const float* __restrict__ part, const DwTile* __restrict__ tiles,
+                                                   int n_tiles, int n_split, double* __restrict__ acc) {
+  __shared__ double red[8][32];
   const DwTile t = tiles[blockIdx.y];
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int u = blockIdx.x * 32 + lane;  // element n * 256 + k of the partial tile
   const int n = u >> 8, k = u & 255;
-  if (n >= t.nN || k >= t.nK) return;
-  const float* p = part + (int64_t)blockIdx.y * PART_STRIDE + u;
+  const bool valid = n < t.nN && k < t.nK;
+  const int per = (n_split + 7) / 8, s0 = grp * per, s1 = s0 + per < n_split ? s0 + per : n_split;
   double s = 0.0;
-  for (int sp = 0; sp < n_split; ++sp) s += (double)p[(int64_t)sp * n_tiles * PART_STRIDE];
-  acc[t.acc_off + (int64_t)(t.n0 + n) * t.K + (t.k0 + k)] += s;
+  if (valid) {
+    const float* p = part + (int64_t)blockIdx.y * PART_STRIDE + u;
+    for (int sp = s0; sp < s1; ++sp) s += (double)__ldg(p + (int64_t)sp * n_tiles * PART_STRIDE);
+  }
+  red[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && valid) {
+    double tot = red[0][lane];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) tot += red[g][lane];
+    acc[t.acc_off + (int64_t)(t.n0 + n) * t.K + (t.k0 + k)] += tot;
+  }
 }
 
 // a 2D fp32 tensor map over rows of `row` floats (stride ld floats), n rows;
@@ -374,7 +387,7 @@ void dw_tf32x3_launch(const float* g, int64_t ldg, const float* x, int64_t ldx, 
   const int grid = (int)std::min<int64_t>(items, sm_count());
   k_dw_tf32x3<<<grid, THREADS, SMEM_BYTES, st>>>(tg, tx, ts, n_e, tiles, n_tiles, n_split, split_e, part,
                                                  gscale ? gate_c2 : 0);
-  k_dw_reduce<<<dim3(PART_STRIDE / 256, (unsigned)n_tiles), 256, 0, st>>>(part, tiles, n_tiles, n_split, acc);
+  k_dw_reduce<<<dim3(PART_STRIDE / 32, (unsigned)n_tiles), 256, 0, st>>>(part, tiles, n_tiles, n_split, acc);
   ESG_CUDA(cudaGetLastError());
 }
 
