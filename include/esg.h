@@ -82,6 +82,17 @@ int esg_wrap_positions(int n_atoms, double* pos /* n*3, in place */, const doubl
 /* model::make_jittered_lattice (synthetic.cpp:17-41), host input generator. */
 int esg_jittered_lattice(int n_atoms, double spacing, double jitter, int n_cycle, const int* cycle,
                          uint64_t seed, double* pos_out, double cell_out[9], int* species_out);
+/* structures::read_extxyz_file (extxyz.h:17, extxyz.cpp:62-126): atom count,
+ * Cartesian positions (n*3), atomic numbers, cell rows (Lattice; the
+ * identity when absent, as AtomicStructure's default) and pbc.  Pass pos / species / cell / pbc NULL to get the count
+ * only.  Malformed files: ESG_ERR_DATA with the line number (ParseError,
+ * core/error.h:27-35). */
+int esg_extxyz_read(const char* path, int64_t* n_atoms, double* pos, int32_t* species, double cell[9],
+                    uint8_t pbc[3]);
+/* structures::write_extxyz_file (extxyz.h:20, extxyz.cpp:128-151): the same
+ * text, %.17g numbers (exact round trip). */
+int esg_extxyz_write(const char* path, int64_t n_atoms, const double* pos, const int32_t* species,
+                     const double cell[9], const uint8_t pbc[3]);
 /* structures::tile (structure.cpp:40-63), host. */
 int esg_tile(int n_atoms, const double* pos, const double cell[9], const uint8_t pbc[3],
              const int* species, const int reps[3], double* pos_out, double cell_out[9],

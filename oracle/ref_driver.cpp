@@ -27,6 +27,7 @@
 #include "esgnn/model/synthetic.h"
 #include "esgnn/partition/partition.h"
 #include "esgnn/runtime/comm_plan.h"
+#include "esgnn/structures/extxyz.h"
 #include "esgnn/structures/graph.h"
 #include "esgnn/structures/structure.h"
 
@@ -318,6 +319,37 @@ int ref_forward_view_timed(int n_rows, int n_owned, const int* row_species, int6
       if (!e.empty()) throw std::runtime_error(e);
     secs[0] = *std::max_element(t_prep.begin(), t_prep.end());
     secs[1] = *std::max_element(t_fwd.begin(), t_fwd.end());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// structures::read_extxyz_file (extxyz.h:17): the count first (arrays may be
+// NULL), then the arrays; errors through ref_last_error
+int ref_read_extxyz(const char* path, int64_t* n, double* pos, int* species, double* cell, uint8_t* pbc) {
+  try {
+    const auto s = structures::read_extxyz_file(path);
+    *n = s.n_atoms();
+    for (int i = 0; i < s.n_atoms() && pos; ++i)
+      for (int d = 0; d < 3; ++d) pos[3 * i + d] = s.positions[i](d);
+    for (int i = 0; i < s.n_atoms() && species; ++i) species[i] = s.species[i];
+    for (int i = 0; i < 3 && cell; ++i)
+      for (int j = 0; j < 3; ++j) cell[3 * i + j] = s.cell(i, j);
+    for (int d = 0; d < 3 && pbc; ++d) pbc[d] = s.pbc[d] ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// structures::write_extxyz_file (extxyz.h:20)
+int ref_write_extxyz(const char* path, int n, const double* pos, const int* species, const double* cell,
+                     const uint8_t* pbc) {
+  try {
+    structures::write_extxyz_file(path, make_structure(n, pos, species, cell, pbc));
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -8,6 +8,7 @@
 //   esgnn::model::Network<float>        (network.h:77-228)    -> esgnn::b200::Network
 //   esgnn::runtime::DistributedRunner   (distributed.h:183)   -> Network::forward on a plan
 //   esgnn::harmonics::coupling_matrix   (clebsch_gordan.h:19) -> esgnn::b200::coupling_matrix
+//   esgnn::structures::read_extxyz_file (extxyz.h:17)         -> esgnn::b200::read_extxyz_file
 //
 // Errors are rethrown as the esgnn::Error taxonomy (core/error.h:11-51) --
 // the reference's own classes when its headers are on the include path.
@@ -88,6 +89,30 @@ struct AtomicStructure {
   int n_atoms() const { return (int)positions.size(); }
   std::array<uint8_t, 3> pbc8() const { return {uint8_t(pbc[0]), uint8_t(pbc[1]), uint8_t(pbc[2])}; }
 };
+
+// structures::read_extxyz_file / write_extxyz_file (extxyz.h:17-20)
+inline AtomicStructure read_extxyz_file(const std::string& path) {
+  int64_t n = 0;
+  check(esg_extxyz_read(path.c_str(), &n, nullptr, nullptr, nullptr, nullptr));
+  std::vector<double> pos((size_t)n * 3);
+  std::vector<int32_t> sp((size_t)n);
+  AtomicStructure s;
+  uint8_t pbc[3];
+  check(esg_extxyz_read(path.c_str(), &n, pos.data(), sp.data(), s.cell.data(), pbc));
+  s.positions.resize((size_t)n);
+  for (int64_t i = 0; i < n; ++i) s.positions[i] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+  s.species.assign(sp.begin(), sp.end());
+  for (int d = 0; d < 3; ++d) s.pbc[d] = pbc[d] != 0;
+  return s;
+}
+inline void write_extxyz_file(const std::string& path, const AtomicStructure& s) {
+  std::vector<double> pos;
+  pos.reserve(3 * s.positions.size());
+  for (const auto& p : s.positions) pos.insert(pos.end(), p.begin(), p.end());
+  const std::vector<int32_t> sp(s.species.begin(), s.species.end());
+  const auto pbc = s.pbc8();
+  check(esg_extxyz_write(path.c_str(), (int64_t)s.n_atoms(), pos.data(), sp.data(), s.cell.data(), pbc.data()));
+}
 
 // structures::Edge (graph.h:14-20)
 struct Edge {

@@ -36,6 +36,22 @@ int main(int argc, char** argv) {
       std::printf("usage error mapped: %s\n", e.what());
     }
   }
+  {  // extxyz round trip (read_extxyz_file / write_extxyz_file, extxyz.h:17-20)
+    b200::AtomicStructure a;
+    a.positions = {{0.0, 0.1, 0.2}, {1.25, -0.0, 3e-9}};
+    a.species = {72, 8};
+    a.cell = {4, 0, 0, 0, 4.5, 0, 0.25, 0, 5};
+    a.pbc = {true, false, true};
+    const std::string path = "facade_demo_roundtrip.xyz";
+    b200::write_extxyz_file(path, a);
+    const b200::AtomicStructure b = b200::read_extxyz_file(path);
+    std::remove(path.c_str());
+    if (b.positions != a.positions || b.species != a.species || b.cell != a.cell || b.pbc != a.pbc) {
+      std::printf("extxyz round trip differs\n");
+      return 1;
+    }
+    std::printf("extxyz round trip exact\n");
+  }
   if (host_only) return 0;
   b200::Context ctx(0);
   b200::AtomicStructure s;

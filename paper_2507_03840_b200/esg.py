@@ -153,6 +153,25 @@ def tile(s: AtomicStructure, reps: Sequence[int]) -> AtomicStructure:
     return AtomicStructure(pos, sp, cell.reshape(3, 3), np.array(s.pbc, dtype=bool))
 
 
+def read_extxyz(path: str) -> AtomicStructure:
+    """structures::read_extxyz_file (extxyz.h:17)."""
+    n = C.c_int64()
+    _check(lib().esg_extxyz_read(path.encode(), C.byref(n), None, None, None, None))
+    pos = np.zeros((n.value, 3))
+    sp = np.zeros(n.value, dtype=np.int32)
+    cell = np.zeros(9)
+    pbc = np.zeros(3, dtype=np.uint8)
+    _check(lib().esg_extxyz_read(path.encode(), C.byref(n), _p(pos), _p(sp), _p(cell), _p(pbc)))
+    return AtomicStructure(pos, sp, cell.reshape(3, 3), pbc.astype(bool))
+
+
+def write_extxyz(path: str, s: AtomicStructure) -> None:
+    """structures::write_extxyz_file (extxyz.h:20)."""
+    _check(lib().esg_extxyz_write(path.encode(), C.c_int64(s.n_atoms), _p(np.ascontiguousarray(s.positions)),
+                                  _p(np.ascontiguousarray(s.species, dtype=np.int32)),
+                                  _p(np.ascontiguousarray(s.cell, dtype=np.float64)), _p(s._pbc8())))
+
+
 def wrap_positions(s: AtomicStructure) -> np.ndarray:
     """AtomicStructure::wrap (structure.cpp:26-38) on a copy of the positions."""
     pos = np.ascontiguousarray(s.positions, dtype=np.float64).copy()

@@ -144,3 +144,20 @@ def forward_view_timed(view, basis, layers, r_cut, threads, l_max=4, e_width=16,
                                      *bargs, C.c_int(l_max), C.c_int(e_width), C.c_int(layers), C.c_int(n_radial),
                                      C.c_double(r_cut), C.c_uint64(seed), C.c_int(threads), _p(secs)))
     return float(secs[0]), float(secs[1])
+
+
+def read_extxyz(path):
+    """structures::read_extxyz_file: (positions, species, cell, pbc)."""
+    n = C.c_int64()
+    _ok(lib().ref_read_extxyz(path.encode(), C.byref(n), None, None, None, None))
+    pos = np.zeros((n.value, 3))
+    sp = np.zeros(n.value, np.int32)
+    cell = np.zeros((3, 3))
+    pbc = np.zeros(3, np.uint8)
+    _ok(lib().ref_read_extxyz(path.encode(), C.byref(n), _p(pos), _p(sp), _p(cell), _p(pbc)))
+    return pos, sp, cell, pbc
+
+
+def write_extxyz(path, pos, species, cell, pbc):
+    args = _struct_args(pos, species, cell, pbc)
+    _ok(lib().ref_write_extxyz(path.encode(), *args))

@@ -157,3 +157,4 @@ def test_facade_demo_host_only():
     out = subprocess.run([demo, "--host-only"], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "usage error mapped" in out.stdout and "out_len 160" in out.stdout
+    assert "extxyz round trip exact" in out.stdout
