@@ -33,10 +33,12 @@ using namespace tc;
 constexpr int TM = 128;                  // rows per tile (UMMA M, one per TMEM lane)
 constexpr int A_BYTES = TM * 128;        // one split of a 32-wide K chunk of A
 constexpr int B_MAX = 256 * 128;         // one split of a K chunk of B (N <= 256)
-// persistent warp-specialised GEMM: warps 0-3 epilogue, 4-11 A converters,
-// warp 12 MMA issuer, warp 13 loader (A by TMA, B by bulk copy); rings of A
+// persistent warp-specialised GEMM: warps 0-3 epilogue, 4-19 A converters,
+// warp 20 MMA issuer, warp 21 loader (A by TMA, B by bulk copy); rings of A
 // (3 stages) and B (2 stages)
-constexpr int EPI_WARPS = 4, PROD_WARPS = 8, MMA_WARP = EPI_WARPS + PROD_WARPS, LOAD_WARP = MMA_WARP + 1;
+constexpr int EPI_WARPS = 4, PROD_WARPS = 16, MMA_WARP = EPI_WARPS + PROD_WARPS, LOAD_WARP = MMA_WARP + 1;
+constexpr int PT = PROD_WARPS * 32, UPT = 1024 / PT;  // converter threads, 16-byte units each per A chunk
+static_assert(UPT * PT == 1024, "A chunk units split evenly");
 constexpr int THREADS = 32 * (LOAD_WARP + 1);
 constexpr int NA = 3, NB = 2;
 constexpr int A_STAGE = 2 * A_BYTES, B_STAGE = 2 * B_MAX;
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---- converters: the A box (raw fp32) split in place into tf32 hi and
     // the lo image at the same swizzled offsets.  Columns past the block's K
     // meet zero rows of the B image.
-    const int pt = tid - EPI_WARPS * 32;  // 0..255
+    const int pt = tid - EPI_WARPS * 32;  // 0..PT-1
     int sa = 0;
     uint32_t ka = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -180,11 +182,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       // 16-byte units of a chunk (fixed row, fixed logical columns), so its
       // 4 x 4 scales sigmoid(A[row][c]) (the row's first 2E values: l = 0,
       // m = 0) are loaded once per item
-      float4 gs[4];
+      float4 gs[UPT];
       if (gate_c2) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int u = pt + 256 * i, r = u >> 3, pos = u & 7;
+        for (int i = 0; i < UPT; ++i) {
+          const int u = pt + PT * i, r = u >> 3, pos = u & 7;
           const int64_t row = r0 + r;
           const int c0 = (((pos ^ (r & 7)) * 4)) % gate_c2;
           float4 h = row < n_rows ? __ldg(reinterpret_cast<const float4*>(A + row * lda + c0))
@@ -197,8 +199,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(bar(AL + sa), (ka / NA) & 1);
         const uint32_t sh = sA + sa * A_STAGE, sl = sh + A_BYTES;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t o = (uint32_t)(pt + 256 * i) * 16u;
+        for (int i = 0; i < UPT; ++i) {
+          const uint32_t o = (uint32_t)(pt + PT * i) * 16u;
           float4 v = lds4(sh + o);
           if (gate_c2) v = make_float4(v.x * gs[i].x, v.y * gs[i].y, v.z * gs[i].z, v.w * gs[i].w);
           const float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
