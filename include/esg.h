@@ -208,7 +208,10 @@ int esg_forward(esg_model* m, float* node_out /* n_owned*out_len */,
  * the output copies are queued; esg_forward_wait completes them (the buffers
  * must not be read or reused before).  A following forward runs while those
  * copies drain and waits for them only before its heads overwrite the device
- * outputs.  Pageable buffers: identical to esg_forward. */
+ * outputs.  With timing == NULL (and profiling off) the call returns as soon
+ * as the forward is queued -- the host can build the next structure's graph
+ * meanwhile -- and esg_forward_wait also waits for the forward.  Pageable
+ * buffers: identical to esg_forward. */
 int esg_forward_async(esg_model* m, float* node_out, float* edge_out, esg_timing* timing);
 int esg_forward_wait(esg_model* m);
 /* Per-category kernel timing with CUDA events on the launching stream.

@@ -292,6 +292,7 @@ int esg_ctx_destroy(esg_ctx* ctx) {
   if (ctx->zc) cudaFreeHost(ctx->zc);
   if (ctx->up) cudaFreeHost(ctx->up);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->build_stream) cudaStreamDestroy(ctx->build_stream);
   delete ctx;
   ESG_API_END
 }

@@ -148,6 +148,9 @@ struct DeviceModel {
   int64_t halo_bytes = 0;
   // optional per-category kernel timing (esg_profile_*): events around launches
   bool profile = false;
+  // esg_forward_async without timing: the host does not wait for the forward
+  // (its end event is synchronised by esg_forward_wait / the next call)
+  bool defer_sync = false;
   std::vector<cudaEvent_t> pool;
   std::vector<std::pair<int, int>> marks;  // (category, first event index)
   double prof_ms[ESG_PROF_NCAT] = {0};

@@ -162,6 +162,9 @@ struct esg_ctx {
   std::set<esg_graph*> graphs;
   std::set<esg_plan*> plans;
   cudaStream_t stream = nullptr;
+  // graph builds run on their own stream (created on first use), so the next
+  // structure's graph is built while an async forward still runs on `stream`
+  cudaStream_t build_stream = nullptr;
   ncclComm_t comm = nullptr;
   int64_t launches = 0;  // kernels launched by this library
   esg::BlockCache cache;
@@ -177,8 +180,9 @@ struct esg_ctx {
 };
 
 namespace esg {
-void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes);  // graph.cu; bytes % 4 == 0
-void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes);  // graph.cu; synchronous
+// graph.cu; synchronous on `st` (default: the context's stream); bytes % 4 == 0
+void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes, cudaStream_t st = nullptr);
+void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes, cudaStream_t st = nullptr);
 }
 
 struct esg_graph {

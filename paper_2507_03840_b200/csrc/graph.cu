@@ -195,7 +195,8 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
                            double r_cut) {
   if (!(r_cut > 0.0)) usage("cutoff must be positive");
   if (n < 1) usage("structure has no atoms");
-  cudaStream_t st = ctx->stream;
+  if (!ctx->build_stream) ESG_CUDA(cudaStreamCreateWithFlags(&ctx->build_stream, cudaStreamNonBlocking));
+  cudaStream_t st = ctx->build_stream;  // independent of an async forward in flight on ctx->stream
   const bool dbg = std::getenv("ESG_DEBUG_BUILD") != nullptr;
   auto tmark = std::chrono::steady_clock::now();
   auto mark = [&](const char* what) {
@@ -270,8 +271,8 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   int* d_cur = dalloc_c((int*)nullptr, nbins);
   int* d_atoms = dalloc_c((int*)nullptr, n);
   mark("host prologue");
-  h2d_staged(ctx, d_pos, pos.data(), sizeof(double) * 3 * n);
-  h2d_staged(ctx, d_img, off.data(), sizeof(double) * off.size());
+  h2d_staged(ctx, d_pos, pos.data(), sizeof(double) * 3 * n, st);
+  h2d_staged(ctx, d_img, off.data(), sizeof(double) * off.size(), st);
   ESG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int) * (nbins + 1), st));
   ESG_CUDA(cudaMemsetAsync(d_cur, 0, sizeof(int) * nbins, st));
   mark("uploads");
@@ -300,7 +301,7 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
   ctx->cache.release(d_tmp);
   int64_t E = 0;
   mark("count pass");
-  d2h_small(ctx, &E, G->d_off + n, sizeof(int64_t));
+  d2h_small(ctx, &E, G->d_off + n, sizeof(int64_t), st);
   mark("edge count readback");
   if (E > (int64_t)std::numeric_limits<int>::max() - 1) usage("graph exceeds 2^31 edges");
   G->E = E;
@@ -320,7 +321,7 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
     ESG_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
     k_max_segment<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(G->d_off, n, d_mx);
     unsigned long long max_seg = 0;
-    d2h_small(ctx, &max_seg, d_mx, sizeof(max_seg));
+    d2h_small(ctx, &max_seg, d_mx, sizeof(max_seg), st);
     ctx->cache.release(d_mx);
     int cap = SEG_SORT_CAP;  // ESG_SEG_SORT_CAP=0 forces the cub path (tests)
     if (const char* e = std::getenv("ESG_SEG_SORT_CAP")) cap = std::min(std::max(std::atoi(e), 0), SEG_SORT_CAP);
@@ -364,8 +365,9 @@ __global__ void k_copy_words(const uint32_t* __restrict__ src, uint32_t* __restr
 }
 }  // namespace
 
-void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes) {
+void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes, cudaStream_t st) {
   if (bytes == 0) return;
+  if (!st) st = ctx->stream;
   if (ctx->up_cap < bytes) {
     if (ctx->up) cudaFreeHost(ctx->up);
     ctx->up = nullptr;
@@ -373,14 +375,15 @@ void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes) {
     ESG_CUDA(cudaHostAlloc(&ctx->up, bytes, cudaHostAllocDefault));
     ctx->up_cap = bytes;
   }
-  ESG_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffer is free
+  // every staged copy is synchronous, so the staging buffer is free here
   std::memcpy(ctx->up, host, bytes);
-  ESG_CUDA(cudaMemcpyAsync(dev, ctx->up, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  ESG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ESG_CUDA(cudaMemcpyAsync(dev, ctx->up, bytes, cudaMemcpyHostToDevice, st));
+  ESG_CUDA(cudaStreamSynchronize(st));
 }
 
-void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes) {
+void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes, cudaStream_t st) {
   if (bytes == 0) return;
+  if (!st) st = ctx->stream;
   if (bytes % 4 != 0) usage("d2h_small copies whole 4-byte words");
   if (ctx->zc_cap < bytes) {
     if (ctx->zc) cudaFreeHost(ctx->zc);
@@ -392,11 +395,11 @@ void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes) {
   void* dptr = nullptr;
   ESG_CUDA(cudaHostGetDevicePointer(&dptr, ctx->zc, 0));
   const size_t n = bytes / 4;
-  k_copy_words<<<(unsigned)std::min<size_t>((n + 255) / 256, 1024), 256, 0, ctx->stream>>>(
+  k_copy_words<<<(unsigned)std::min<size_t>((n + 255) / 256, 1024), 256, 0, st>>>(
       static_cast<const uint32_t*>(dev), static_cast<uint32_t*>(dptr), n);
   ++ctx->launches;
   ESG_CUDA(cudaGetLastError());
-  ESG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ESG_CUDA(cudaStreamSynchronize(st));
   std::memcpy(host, ctx->zc, bytes);
 }
 

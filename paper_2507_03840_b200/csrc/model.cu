@@ -1101,6 +1101,7 @@ void forward_impl(esg_model* M, esg_timing* tm) {
   }
   ESG_CUDA(cudaEventRecord(D->ev[3], st));
   ESG_CUDA(cudaGetLastError());
+  if (D->defer_sync) return;  // async forward without timing: the host goes on
   ESG_CUDA(cudaEventSynchronize(D->ev[3]));
   prof_collect(D);
   if (tm) {
@@ -1263,6 +1264,7 @@ bool pinned(const void* p) {
 void model_outputs_wait(esg_model* M) {
   DeviceModel* D = M->dev;
   if (!D || !D->copies_pending) return;
+  ESG_CUDA(cudaEventSynchronize(D->ev[3]));  // the forward itself (a deferred one included)
   ESG_CUDA(cudaEventSynchronize(D->copies_done));
   D->copies_pending = false;
 }
@@ -1277,14 +1279,19 @@ void model_forward_to_host(esg_model* M, esg_timing* tm, float* node_out, float*
     if (!D->copies_done) ESG_CUDA(cudaEventCreateWithFlags(&D->copies_done, cudaEventDisableTiming));
     D->host_node_out = node_out;
     D->host_edge_out = edge_out;
+    // no timing asked for: the host does not wait for the forward either
+    D->defer_sync = async && !tm && !D->profile;
     try {
       model_forward(M, tm);
     } catch (...) {
       D->host_node_out = D->host_edge_out = nullptr;
+      D->defer_sync = false;
+      cudaStreamSynchronize(M->ctx->stream);
       cudaStreamSynchronize(D->copy_st);
       D->copies_pending = false;
       throw;
     }
+    D->defer_sync = false;
     D->host_node_out = D->host_edge_out = nullptr;
     ESG_CUDA(cudaEventRecord(D->copies_done, D->copy_st));
     D->copies_pending = true;

@@ -614,9 +614,14 @@ class Network:
         return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches, t.halo_skew_ms,
                       t.halo_exchange_ms, t.halo_bytes)
 
-    def forward_into_async(self, node_out: Optional[np.ndarray], edge_out: Optional[np.ndarray]) -> Timing:
+    def forward_into_async(self, node_out: Optional[np.ndarray], edge_out: Optional[np.ndarray],
+                           timing: bool = True) -> Optional[Timing]:
         """esg_forward_async: with pinned buffers returns once the copies are
-        queued; call wait_outputs() before reading or reusing the buffers."""
+        queued; call wait_outputs() before reading or reusing the buffers.
+        timing=False: returns as soon as the forward is queued (no Timing)."""
+        if not timing:
+            _check(lib().esg_forward_async(self._h, _p(node_out), _p(edge_out), None))
+            return None
         t = _Timing()
         _check(lib().esg_forward_async(self._h, _p(node_out), _p(edge_out), C.byref(t)))
         return Timing(t.forward_ms, t.message_ms, t.halo_ms, t.heads_ms, t.exchanges, t.gpu_launches, t.halo_skew_ms,

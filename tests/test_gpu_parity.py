@@ -325,6 +325,45 @@ def test_async_outputs_do_not_race(gpu_ctx):
     g.close()
 
 
+def test_async_pipeline_builds_next_graph(gpu_ctx):
+    """The e2e step pattern: an untimed esg_forward_async returns once the
+    forward is queued, the next structure's graph builds on the context's
+    build stream meanwhile, then prepare + forward on it.  Both outputs equal
+    the synchronous forwards bit for bit."""
+    import torch
+    sa = esg.make_jittered_lattice(3000, 2.2, 0.45, [72, 8, 8], 2)
+    sb = esg.make_jittered_lattice(3000, 2.2, 0.45, [72, 8, 8], 3)
+    r = 8.0
+    cfg = esg.ModelConfig(l_max=4, e_width=16, layers=2, n_radial=32, r_cut=r, seed=1,
+                          linear_precision=esg.LINEAR_FP32)
+    net = esg.Network(gpu_ctx, cfg, esg.BASIS_HFO2)
+    net.init_params()
+    want = []
+    for st in (sa, sb):
+        g = esg.build_graph(gpu_ctx, st, r)
+        net.prepare(g, st.species)
+        want.append(net.forward()[:2])
+        g.close()
+    ga = esg.build_graph(gpu_ctx, sa, r)
+    net.prepare(ga, sa.species)
+    bufs = []
+    for k, st in enumerate((sa, sb)):
+        if k:
+            gb = esg.build_graph(gpu_ctx, st, r)  # while forward 0 runs
+            net.prepare(gb, st.species)
+        bn = torch.empty((net.n_owned, net.out_len), dtype=torch.float32, pin_memory=True).numpy()
+        be = torch.empty((net.n_edges, net.out_len), dtype=torch.float32, pin_memory=True).numpy()
+        assert net.forward_into_async(bn, be, timing=False) is None
+        bufs.append((bn, be))
+    net.wait_outputs()
+    for (bn, be), (no, eo) in zip(bufs, want):
+        assert np.array_equal(bn.view(np.uint32), no.view(np.uint32))
+        assert np.array_equal(be.view(np.uint32), eo.view(np.uint32))
+    net.close()
+    ga.close()
+    gb.close()
+
+
 def test_forward_c3_golden_sample(gpu_ctx):
     """BASELINE config 3 (20,000-atom HfO2, 12.8M edges, 3 layers, seven
     edge chunks): the fp32 heads against the float oracle's on the committed
