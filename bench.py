@@ -551,7 +551,7 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--precision", default="fp32", choices=["bf16", "fp32"],
                     help="fp32: the fp32-faithful linears (the headline); bf16: throughput mode")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="0 skips the CPU baseline sample")
     ap.add_argument("--train-steps", type=int, default=2, help="C2 training steps after the forward (0: skip)")
     ap.add_argument("--bf16-steps", type=int, default=3, help="forwards timed in the bf16 side mode (0: skip)")
