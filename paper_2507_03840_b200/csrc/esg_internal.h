@@ -180,6 +180,11 @@ struct esg_ctx {
 };
 
 namespace esg {
+// the context's graph-side stream (graph build, Low-NN, comm plans; created on first use)
+inline cudaStream_t build_stream(esg_ctx* ctx) {
+  if (!ctx->build_stream) ESG_CUDA(cudaStreamCreateWithFlags(&ctx->build_stream, cudaStreamNonBlocking));
+  return ctx->build_stream;
+}
 // graph.cu; synchronous on `st` (default: the context's stream); bytes % 4 == 0
 void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes, cudaStream_t st = nullptr);
 void h2d_staged(esg_ctx* ctx, void* dev, const void* host, size_t bytes, cudaStream_t st = nullptr);

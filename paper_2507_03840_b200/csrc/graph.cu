@@ -195,8 +195,7 @@ esg_graph* build_graph_gpu(esg_ctx* ctx, int n, const double* pos_in, const M3& 
                            double r_cut) {
   if (!(r_cut > 0.0)) usage("cutoff must be positive");
   if (n < 1) usage("structure has no atoms");
-  if (!ctx->build_stream) ESG_CUDA(cudaStreamCreateWithFlags(&ctx->build_stream, cudaStreamNonBlocking));
-  cudaStream_t st = ctx->build_stream;  // independent of an async forward in flight on ctx->stream
+  cudaStream_t st = build_stream(ctx);  // independent of an async forward in flight on ctx->stream
   const bool dbg = std::getenv("ESG_DEBUG_BUILD") != nullptr;
   auto tmark = std::chrono::steady_clock::now();
   auto mark = [&](const char* what) {
@@ -408,7 +407,7 @@ void d2h_small(esg_ctx* ctx, void* host, const void* dev, size_t bytes, cudaStre
 void esg_graph::host_sync_offsets() const {
   if ((int64_t)h_off.size() == n + 1) return;
   h_off.resize(n + 1);
-  esg::d2h_small(ctx, h_off.data(), d_off, sizeof(int64_t) * (n + 1));
+  esg::d2h_small(ctx, h_off.data(), d_off, sizeof(int64_t) * (n + 1), esg::build_stream(ctx));
 }
 void esg_graph::host_sync() const {
   host_sync_offsets();

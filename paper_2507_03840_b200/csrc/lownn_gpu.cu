@@ -129,7 +129,7 @@ void lownn_gpu(esg_ctx* ctx, int n, const double* pos_h, const M3& cell, const b
   for (int64_t v : w) all_zero = all_zero && v == 0;
   if (all_zero) std::fill(w.begin(), w.end(), 1);
 
-  cudaStream_t st = ctx->stream;
+  cudaStream_t st = build_stream(ctx);  // graph-side work: beside an async forward
   auto& C = ctx->cache;
   const int S_max = 1 << (depth - 1);
   auto* pos = static_cast<double*>(C.alloc(sizeof(double) * 3 * (size_t)n));
@@ -147,8 +147,8 @@ void lownn_gpu(esg_ctx* ctx, int n, const double* pos_h, const M3& cell, const b
   auto* dim_d = static_cast<int*>(C.alloc(sizeof(int) * S_max));
   auto* off_d = static_cast<int64_t*>(C.alloc(sizeof(int64_t) * (S_max + 1)));
   auto* split_d = static_cast<int*>(C.alloc(sizeof(int) * S_max));
-  h2d_staged(ctx, pos, pos_h, sizeof(double) * 3 * (size_t)n);
-  h2d_staged(ctx, wd, w.data(), sizeof(int64_t) * n);
+  h2d_staged(ctx, pos, pos_h, sizeof(double) * 3 * (size_t)n, st);
+  h2d_staged(ctx, wd, w.data(), sizeof(int64_t) * n, st);
   ESG_CUDA(cudaMemsetAsync(seg, 0, sizeof(int) * n, st));
 
   size_t tmp_bytes = 0, b = 0;
@@ -172,7 +172,7 @@ void lownn_gpu(esg_ctx* ctx, int n, const double* pos_h, const M3& cell, const b
     ESG_CUDA(cudaMemsetAsync(ext + 3 * S_max, 0, sizeof(unsigned long long) * 3 * S, st));
     k_extent<<<nb, 256, 0, st>>>(pos, seg, n, ext, ext + 3 * S_max);
     ext_h.resize(6 * (size_t)S_max);
-    d2h_small(ctx, ext_h.data(), ext, sizeof(unsigned long long) * 6 * S_max);
+    d2h_small(ctx, ext_h.data(), ext, sizeof(unsigned long long) * 6 * S_max, st);
     std::vector<int> dim(S);
     for (int s = 0; s < S; ++s) {
       const auto& c = cuts[s];
@@ -204,7 +204,7 @@ void lownn_gpu(esg_ctx* ctx, int n, const double* pos_h, const M3& cell, const b
         if (nn[d] <= nn[best]) best = d;
       dim[s] = best;
     }
-    h2d_staged(ctx, dim_d, dim.data(), sizeof(int) * S);
+    h2d_staged(ctx, dim_d, dim.data(), sizeof(int) * S, st);
     // 3. order each segment by (coordinate, atom id) (lownn.cpp:72-76)
     k_sort_keys<<<nb, 256, 0, st>>>(pos, seg, dim_d, n, key_a, id_a);
     cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key_a, key_b, id_a, id_b, n, 0, 64, st);
@@ -215,11 +215,11 @@ void lownn_gpu(esg_ctx* ctx, int n, const double* pos_h, const M3& cell, const b
     // 4. first minimiser of |2 prefix - total| per segment (lownn.cpp:78-91)
     k_gather_w<<<nb, 256, 0, st>>>(wd, id_a, n, wv);
     cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, wv, pre, n, st);
-    h2d_staged(ctx, off_d, off.data(), sizeof(int64_t) * (S + 1));
+    h2d_staged(ctx, off_d, off.data(), sizeof(int64_t) * (S + 1), st);
     const int need = 1 << (level - 1);
     k_split<<<S, SPLIT_THREADS, 0, st>>>(pre, off_d, need, split_d);
     std::vector<int> split(S);
-    d2h_small(ctx, split.data(), split_d, sizeof(int) * S);
+    d2h_small(ctx, split.data(), split_d, sizeof(int) * S, st);
     // 5. children 2s (left) and 2s + 1 (right)
     k_relabel<<<nb, 256, 0, st>>>(seg_b, id_a, off_d, split_d, n, seg);
     ctx->launches += 6;
@@ -236,7 +236,7 @@ void lownn_gpu(esg_ctx* ctx, int n, const double* pos_h, const M3& cell, const b
     off.swap(off2);
     cuts.swap(cuts2);
   }
-  d2h_small(ctx, part_h, seg, sizeof(int) * n);
+  d2h_small(ctx, part_h, seg, sizeof(int) * n, st);
   ESG_CUDA(cudaStreamSynchronize(st));
   for (void* p : {(void*)pos, (void*)wd, (void*)wv, (void*)pre, (void*)seg, (void*)seg_a, (void*)seg_b, (void*)id_a,
                   (void*)id_b, (void*)key_a, (void*)key_b, (void*)ext, (void*)dim_d, (void*)off_d, (void*)split_d, tmp})

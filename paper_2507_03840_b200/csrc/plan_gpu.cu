@@ -114,7 +114,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   const int n = g->n;
   for (int i = 0; i < n; ++i)
     if (part_h[i] < 0 || part_h[i] >= n_parts) data("assignment part out of range");
-  cudaStream_t st = g->ctx->stream;
+  cudaStream_t st = build_stream(g->ctx);  // graph-side work: beside an async forward
   auto* P = new esg_plan();
   P->rank = rank;
   P->world = n_parts;
@@ -132,7 +132,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   uint64_t* keys = galloc_ctx<uint64_t>(g->ctx, n);
   uint64_t* keys_sorted = galloc_ctx<uint64_t>(g->ctx, n);
   uint8_t* sflags = galloc_ctx<uint8_t>(g->ctx, (size_t)n * n_parts);
-  h2d_staged(g->ctx, part, part_h, sizeof(int) * n);
+  h2d_staged(g->ctx, part, part_h, sizeof(int) * n, st);
   ESG_CUDA(cudaMemsetAsync(need, 0, n, st));
   ESG_CUDA(cudaMemsetAsync(halo_row, 0xff, sizeof(int) * n, st));
   ESG_CUDA(cudaMemsetAsync(sflags, 0, (size_t)n * n_parts, st));
@@ -156,7 +156,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   cub::DeviceScan::ExclusiveSum(tmp, need_b, flag, scan, n + 1, st);
   k_owned_rows<<<b1, 256, 0, st>>>(part, n, rank, scan, owned_row, row_global);
   int n_owned = 0;
-  d2h_small(g->ctx, &n_owned, scan + n, sizeof(int));
+  d2h_small(g->ctx, &n_owned, scan + n, sizeof(int), st);
   // halo rows, sorted by (owner, id)
   if (n) k_halo_need<<<bw, 256, 0, st>>>(g->d_off, g->d_src, part, n, rank, need, cnt);
   thrust::counting_iterator<int> it(0);
@@ -165,7 +165,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   ensure_tmp(need_b);
   cub::DeviceSelect::Flagged(tmp, need_b, it, need, ids, n_sel, n, st);
   int n_halo = 0;
-  d2h_small(g->ctx, &n_halo, n_sel, sizeof(int));
+  d2h_small(g->ctx, &n_halo, n_sel, sizeof(int), st);
   ESG_CUDA(cudaStreamSynchronize(st));
   if (n_halo) {
     k_halo_keys<<<(unsigned)((n_halo + 255) / 256), 256, 0, st>>>(ids, n_halo, part, keys);
@@ -182,7 +182,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   ensure_tmp(need_b);
   cub::DeviceScan::ExclusiveSum(tmp, need_b, cnt, base, n + 1, st);
   int64_t n_e = 0;
-  d2h_small(g->ctx, &n_e, base + n, sizeof(int64_t));
+  d2h_small(g->ctx, &n_e, base + n, sizeof(int64_t), st);
   ESG_CUDA(cudaStreamSynchronize(st));
   int* edge_index = galloc_ctx<int>(g->ctx, (size_t)std::max<int64_t>(n_e, 1));
   int* src_row = galloc_ctx<int>(g->ctx, (size_t)std::max<int64_t>(n_e, 1));
@@ -200,7 +200,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   P->row_global.resize(P->n_rows);
   std::vector<int> owned_h(n), halo_keys_owner;
   if (P->n_rows)
-    d2h_small(g->ctx, P->row_global.data(), row_global, sizeof(int) * P->n_rows);
+    d2h_small(g->ctx, P->row_global.data(), row_global, sizeof(int) * P->n_rows, st);
   // the per-edge arrays stay on the device (prepare copies them device to
   // device); the host copies are made only if the plan is exported
   P->ctx = g->ctx;
@@ -211,7 +211,7 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
   P->d_seg = galloc_ctx<int64_t>(g->ctx, (size_t)n_owned + 1);
   k_plan_seg<<<(unsigned)((n_owned + 256) / 256), 256, 0, st>>>(base, row_global, n_owned, n_e, P->d_seg);
   g->ctx->launches += 1;
-  if (n) d2h_small(g->ctx, owned_h.data(), owned_row, sizeof(int) * n);
+  if (n) d2h_small(g->ctx, owned_h.data(), owned_row, sizeof(int) * n, st);
   std::map<int, Neighbor> nb;
   for (int p = 0; p < n_parts; ++p) {
     if (p == rank) continue;
@@ -220,11 +220,11 @@ esg_plan* plan_build_gpu(const esg_graph* g, const int32_t* species, const int32
     ensure_tmp(need_b);
     cub::DeviceSelect::Flagged(tmp, need_b, it, sflags + (size_t)p * n, ids, n_sel, n, st);
     int m = 0;
-    d2h_small(g->ctx, &m, n_sel, sizeof(int));
+    d2h_small(g->ctx, &m, n_sel, sizeof(int), st);
     ESG_CUDA(cudaStreamSynchronize(st));
     if (!m) continue;
     std::vector<int> s(m);
-    d2h_small(g->ctx, s.data(), ids, sizeof(int) * m);
+    d2h_small(g->ctx, s.data(), ids, sizeof(int) * m, st);
     Neighbor& x = nb[p];
     x.peer = p;
     for (int id : s) x.send_rows.push_back(owned_h[id]);
@@ -261,9 +261,9 @@ void esg_plan::host_sync_edges() const {
   src_row.resize(n_edges);
   dst_row.resize(n_edges);
   if (n_edges) {
-    esg::d2h_small(ctx, edge_index.data(), d_edge_index, sizeof(int32_t) * n_edges);
-    esg::d2h_small(ctx, src_row.data(), d_src_row, sizeof(int32_t) * n_edges);
-    esg::d2h_small(ctx, dst_row.data(), d_dst_row, sizeof(int32_t) * n_edges);
+    esg::d2h_small(ctx, edge_index.data(), d_edge_index, sizeof(int32_t) * n_edges, esg::build_stream(ctx));
+    esg::d2h_small(ctx, src_row.data(), d_src_row, sizeof(int32_t) * n_edges, esg::build_stream(ctx));
+    esg::d2h_small(ctx, dst_row.data(), d_dst_row, sizeof(int32_t) * n_edges, esg::build_stream(ctx));
   }
 }
 
