@@ -42,8 +42,8 @@ constexpr int B_IMG = 8 * BOX;          // x: up to 256 channels
 constexpr int S_IMG = BOX;              // the chunk's gate scalars (<= 32 per edge)
 constexpr int STAGE = 2 * A_IMG + 2 * B_IMG + S_IMG;  // hi, lo images + gate scalars
 constexpr int NS = 4;                   // stage ring
-// warps 0-3 epilogue, 4-13 converters, 14 TMA loader, 15 MMA issuer
-constexpr int EPI_WARPS = 4, CONV_WARPS = 10, LOAD_WARP = EPI_WARPS + CONV_WARPS, MMA_WARP = LOAD_WARP + 1;
+// warps 0-3 epilogue, 4-15 converters, 16 TMA loader, 17 MMA issuer
+constexpr int EPI_WARPS = 4, CONV_WARPS = 12, LOAD_WARP = EPI_WARPS + CONV_WARPS, MMA_WARP = LOAD_WARP + 1;
 constexpr int CT = CONV_WARPS * 32;     // converter threads
 constexpr int THREADS = 32 * (MMA_WARP + 1);
 constexpr int BAR_OFF = NS * STAGE;
@@ -117,8 +117,8 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
       : "memory");
 }
 
-// persistent warp-specialised: warps 0-3 epilogue, 4-11 converters, 12 TMA
-// loader, 13 MMA issuer.  Items split-major (consecutive CTAs read the same
+// persistent warp-specialised: warps 0-3 epilogue, 4-15 converters, 16 TMA
+// loader, 17 MMA issuer.  Items split-major (consecutive CTAs read the same
 // edges: L2 reuse).
 __global__ void __launch_bounds__(THREADS, 1)
     k_dw_tf32x3(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x,
